@@ -1,0 +1,148 @@
+"""Pins for the oracle's branch-and-bound (§3.1-3.2) against what the
+paper fixes: the Fig. 3 / Eq. (8)-(11) indexing example, exact coverage of a
+parent by its subregions, the variable-cycling schedule (line 184), the
+invariant that no ruled-out subregion contains a point better than the
+incumbent, and enclosure of the known global minimum (Appendix A)."""
+from __future__ import annotations
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def test_partition_indexing_fig3():
+    g = json.load(open(os.path.join(GOLD, "partition_fig3.json")))
+    plo = np.array(g["selected"]["lo"])
+    phi = np.array(g["selected"]["hi"])
+    for r in range(g["m"] ** g["d"]):
+        lo, hi = oracle.child_box(plo, phi, 0, g["d"], g["m"], r)
+        assert list(lo) == [r % 4, r // 4]        # Eq. (8)-(9)
+        assert list(hi) == [r % 4 + 1, r // 4 + 1]  # Eq. (10)-(11)
+
+
+@pytest.mark.parametrize("m", [2, 3, 4, 5])
+def test_children_cover_parent_exactly(m):
+    rng = np.random.default_rng(m)
+    for _ in range(30):
+        n = int(rng.integers(1, 6))
+        d = int(rng.integers(1, n + 1))
+        cyc = int(rng.integers(0, n))
+        plo = rng.uniform(-10, 10, n)
+        phi = plo + 10.0 ** rng.uniform(-14, 1, n)
+        dims = [(cyc + j) % n for j in range(d)]
+        pieces = {dim: set() for dim in dims}
+        for c in range(m ** d):
+            lo, hi = oracle.child_box(plo, phi, cyc, d, m, c)
+            assert np.all(lo <= hi)
+            for i in range(n):
+                if i not in dims:
+                    assert lo[i] == plo[i] and hi[i] == phi[i]
+            for dim in dims:
+                pieces[dim].add((lo[dim], hi[dim]))
+        for dim in dims:
+            iv = sorted(pieces[dim])
+            assert iv[0][0] == plo[dim] and iv[-1][1] == phi[dim]  # end points exact
+            for a, b in zip(iv, iv[1:]):
+                assert a[1] == b[0]  # no gap, no overlap between neighbours
+
+
+def test_variable_cycling_dims_split():
+    # n = 25, d = 10: cycling index 20 splits x21..x25 and wraps to x1..x5
+    n, d, m = 25, 10, 2
+    plo, phi = np.zeros(n), np.ones(n)
+    split = set()
+    for c in range(m ** d):
+        lo, hi = oracle.child_box(plo, phi, 20, d, m, c)
+        split |= {i for i in range(n) if hi[i] - lo[i] < 1.0}
+    assert split == set(range(20, 25)) | set(range(0, 5))
+
+
+@pytest.mark.parametrize("fid", list(range(1, 11)))
+def test_branch_ruled_out_boxes_hold_no_better_point(fid):
+    n, d, m = 3, 3, 2
+    l, u = workloads.bounds(fid, n)
+    plo, phi = workloads.random_boxes(300 + fid, n, 6, l, u, mix=(0, 0, 0.2, 0.4, 0.4, 0))
+    cyc = np.array([0, 1, 2, 0, 1, 2], np.int32)
+    gub, par, code, lb, w = oracle.branch(fid, plo, phi, cyc, d, m, l, u, mono=True)
+    surv = set(zip(par.tolist(), code.tolist()))
+    # GUB is attained: it is the upper bound at some child midpoint
+    assert math.isfinite(gub)
+    rng = np.random.default_rng(fid)
+    for b in range(plo.shape[0]):
+        for c in range(m ** d):
+            clo, chi = oracle.child_box(plo[b], phi[b], int(cyc[b]), d, m, c)
+            e = oracle.eval_box(fid, clo, chi)
+            if (b, c) in surv:
+                assert e[0] <= gub
+                continue
+            pts = clo + rng.uniform(0, 1, (12, n)) * (chi - clo)
+            if e[0] > gub:
+                # ruled out by the bound: every point is worse than GUB
+                for p in pts:
+                    assert oracle.eval_point(fid, p)[0] > gub
+            else:
+                # ruled out by the first-order test: some split variable has a
+                # derivative of constant sign and the box is not on that edge
+                ok = False
+                for j in range(d):
+                    i = (int(cyc[b]) + j) % n
+                    g = oracle.grad_box(fid, clo, chi, i)
+                    if (g[0] > 0 and clo[i] != l[i]) or (g[1] < 0 and chi[i] != u[i]):
+                        ok = True
+                assert ok
+
+
+def _xstar(fid, n):
+    return np.full(n, {1: 0.0, 2: 5.0, 3: 0.0, 4: 0.9, 5: 0.0, 6: 1.0, 7: 0.0, 8: 0.0, 9: 0.0,
+                       10: 2 * math.pi / 3}[fid])
+
+
+def _fstar(fid, n):
+    return {1: 0.0, 2: -1.0, 3: -0.1 * n, 4: 1.0, 5: 0.0, 6: 0.0, 7: 0.0, 8: 0.0, 9: -4.0 * n,
+            10: -3.5}[fid]
+
+
+def test_config0_rastrigin_n2_encloses_global_minimum():
+    cfg = workloads.CONFIGS[0]
+    l, u = workloads.config_bounds(cfg)
+    r = oracle.solve(cfg["fid"], l, u, eps_f=cfg["eps"], eps_x=cfg["eps"], d=2, m=2)
+    assert r["status"] == 0
+    assert r["glb"] <= 0.0 <= r["gub"] and r["gub"] - r["glb"] <= 1e-6
+    assert np.all(r["hi"] - r["lo"] <= 1e-6)
+    assert any(np.all(lo <= 0) and np.all(0 <= hi) for lo, hi in zip(r["lo"], r["hi"]))
+
+
+@pytest.mark.parametrize("fid", list(range(1, 11)))
+def test_small_solves_enclose_known_minimum_paper_domains(fid):
+    n = 2
+    l, u = workloads.bounds(fid, n)
+    r = oracle.solve(fid, l, u, eps_f=1e-6, eps_x=1e-5, d=2, m=2, bmax=256, max_iter=4000)
+    assert r["status"] == 0, r["status"]
+    fs = _fstar(fid, n)
+    tol = 1e-12 * max(1, abs(fs)) * 10
+    assert r["glb"] - tol <= fs <= r["gub"] + tol
+    assert r["gub"] - r["glb"] <= 1e-6
+    xs = _xstar(fid, n)
+    assert any(np.all(lo <= xs + 1e-15) and np.all(xs - 1e-15 <= hi)
+               for lo, hi in zip(r["lo"], r["hi"])), "minimizer not in any surviving box"
+
+
+def test_incumbent_monotone_and_minimizer_kept_every_iteration():
+    fid, n = 6, 2
+    l, u = workloads.bounds(fid, n)
+    prev = math.inf
+    xs = _xstar(fid, n)
+    for k in range(1, 30, 3):
+        r = oracle.solve(fid, l, u, eps_f=0, eps_x=0, d=2, m=2, bmax=64, max_iter=k)
+        assert r["gub"] <= prev
+        prev = r["gub"]
+        assert r["glb"] <= 0.0 <= r["gub"]
+        assert any(np.all(lo <= xs) and np.all(xs <= hi) for lo, hi in zip(r["lo"], r["hi"]))

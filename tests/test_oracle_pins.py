@@ -1,0 +1,328 @@
+"""Pins for the CPU oracle against what the paper and mathematics fix
+(not against the oracle itself).  CPU only.
+
+* interval operations: Eq. (3)-(6) on exact operands, directed rounding
+  against exact rationals, transcendental enclosures against 50-digit Taylor
+  series (tests/hp.py), constants against 50-digit expansions;
+* the worked example of PAPER.md §2.1 (tests/golden/paper_example.json);
+* the global minima of Appendix A (tests/golden/paper_minima.json);
+* closed forms of every objective at special points where the trigonometric
+  arguments are exact multiples of pi/2 (values derived by hand below);
+* first-order partial derivatives against central differences of f;
+* inclusion of point evaluations in box enclosures (brute-force sampling).
+"""
+from __future__ import annotations
+
+import json
+import math
+import os
+from decimal import Decimal
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from tests import hp
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def load(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+# ----------------------------------------------------------------- constants
+def test_constants_tight_and_enclosing():
+    c = oracle.consts()
+    truth = {
+        "pi": hp.PI,
+        "e": hp.E,
+        "c0_02": Decimal("0.02"),
+        "c0_1": Decimal("0.1"),
+        "c0_9": Decimal("0.9"),
+    }
+    for k, v in truth.items():
+        lo, hi = c[k]
+        assert hp.contains((lo, hi), v), k
+        assert lo < hi and math.nextafter(lo, math.inf) == hi, k  # 1-ulp tight
+
+
+# ------------------------------------------------------- Eq. (3)-(6) exactly
+def test_interval_ops_eq3_to_eq6():
+    assert oracle.ia("ia_add", (1, 2), (3, 4)) == (4.0, 6.0)       # Eq. (3)
+    assert oracle.ia("ia_sub", (1, 2), (3, 4)) == (-3.0, -1.0)     # Eq. (4)
+    assert oracle.ia("ia_mul", (-1, 2), (3, 4)) == (-4.0, 8.0)     # Eq. (5)
+    assert oracle.ia("ia_mul", (-2, -1), (-4, 3)) == (-6.0, 8.0)
+    assert oracle.ia("ia_div", (1, 2), (4, 8)) == (0.125, 0.5)     # Eq. (6)
+    assert oracle.ia("ia_div", (-1, 2), (-8, -4)) == (-0.5, 0.25)
+    assert oracle.ia("ia_sqr", (-3, 2)) == (0.0, 9.0)
+    assert oracle.ia("ia_sqr", (-3, -2)) == (4.0, 9.0)
+    assert oracle.ia("ia_sqrt", (4, 9)) == (2.0, 3.0)
+
+
+def test_directed_rounding_against_rationals():
+    L = oracle.lib()
+    rng = np.random.default_rng(0)
+    ops = {
+        "add": (L.ia_add_dn, L.ia_add_up, lambda a, b: a + b),
+        "sub": (L.ia_sub_dn, L.ia_sub_up, lambda a, b: a - b),
+        "mul": (L.ia_mul_dn, L.ia_mul_up, lambda a, b: a * b),
+        "div": (L.ia_div_dn, L.ia_div_up, lambda a, b: a / b),
+    }
+    for _ in range(300):
+        a = float(rng.standard_normal() * 10.0 ** rng.integers(-5, 5))
+        b = float(rng.standard_normal() * 10.0 ** rng.integers(-5, 5))
+        for name, (dn, up, ex) in ops.items():
+            exact = ex(Fraction(a), Fraction(b))
+            lo, hi = dn(a, b), up(a, b)
+            assert Fraction(lo) <= exact <= Fraction(hi), name
+            # optimal outward rounding: adjacent or equal
+            assert hi == lo or math.nextafter(lo, math.inf) == hi, name
+            if Fraction(lo) == exact:
+                assert lo == hi
+
+
+@pytest.mark.parametrize("fn,ref", [("ia_cos", hp.dcos), ("ia_sin", hp.dsin)])
+def test_trig_enclosure_contains_true_range(fn, ref):
+    rng = np.random.default_rng(1)
+    pi = float(hp.PI)
+    for _ in range(400):
+        c = float(rng.uniform(-60, 60))
+        w = float(10 ** rng.uniform(-12, 0.9))
+        lo, hi = c - w / 2, c + w / 2
+        r = oracle.ia(fn, (lo, hi))
+        # endpoints (true values, 58 digits)
+        assert hp.contains(r, ref(lo)) and hp.contains(r, ref(hi))
+        # interior extrema: cos max at 2k pi, min at (2k+1) pi; sin shifted by pi/2
+        off = Fraction(0) if fn == "ia_cos" else Fraction(1, 2)
+        pf = Fraction(hp.PI)
+        k0 = math.floor(lo / pi) - 2
+        for k in range(k0, k0 + int(w / pi) + 6):
+            x = (k + off) * pf
+            if Fraction(lo) <= x <= Fraction(hi):
+                ext = 1.0 if k % 2 == 0 else -1.0
+                assert (r[1] if ext > 0 else r[0]) == ext
+        # tightness: no more than a few ulps beyond the true range
+        vals = [ref(lo), ref(hi)]
+        tlo, thi = min(vals), max(vals)
+        for k in range(k0, k0 + int(w / pi) + 6):
+            x = (k + off) * pf
+            if Fraction(lo) <= x <= Fraction(hi):
+                if k % 2 == 0:
+                    thi = Decimal(1)
+                else:
+                    tlo = Decimal(-1)
+        assert float(tlo) - r[0] <= 1e-14 and r[1] - float(thi) <= 1e-14
+
+
+def test_exp_sqrt_enclosures():
+    rng = np.random.default_rng(2)
+    for _ in range(200):
+        a = float(rng.uniform(-30, 30))
+        b = a + float(10 ** rng.uniform(-10, 1))
+        r = oracle.ia("ia_exp", (a, b))
+        assert hp.contains(r, hp.dexp(a)) and hp.contains(r, hp.dexp(b))
+        assert (r[1] - float(hp.dexp(b))) <= 1e-14 * float(hp.dexp(b))
+        a2, b2 = abs(a), abs(a) + abs(b)
+        s = oracle.ia("ia_sqrt", (a2, b2))
+        assert hp.contains(s, hp.dsqrt(a2)) and hp.contains(s, hp.dsqrt(b2))
+
+
+# ------------------------------------------------ §2.1 worked example (golden)
+def test_paper_example_natural_extension_and_splitting():
+    g = load("paper_example.json")
+    lo, hi = g["natural_extension"]["interval"]
+    assert oracle.eval_box(0, [lo], [hi]) == tuple(g["natural_extension"]["expected"])
+    k = g["splitting"]["subintervals"]
+    pts = [i / k for i in range(k + 1)]
+    pts[-1] = 1.0
+    encl = [oracle.eval_box(0, [pts[i]], [pts[i + 1]]) for i in range(k)]
+    ulo = min(e[0] for e in encl)
+    uhi = max(e[1] for e in encl)
+    elo, ehi = g["splitting"]["expected"]
+    assert abs(ulo - elo) < 1e-12 and abs(uhi - ehi) < 1e-12
+    xlo, xhi = g["exact_range"]["expected"]
+    assert ulo <= xlo and uhi >= xhi  # the union still encloses the exact range
+
+
+# ------------------------------------------------ Appendix A minima (golden)
+def _xstar(spec, n):
+    v = {"0": 0.0, "5": 5.0, "0.9": 0.9, "1": 1.0, "2pi/3": 2 * math.pi / 3}[spec]
+    return np.full(n, v)
+
+
+def _fstar(spec, n):
+    return {"0": 0.0, "-1": -1.0, "-0.1n": -0.1 * n, "1": 1.0, "-4n": -4.0 * n, "-3.5": -3.5}[spec]
+
+
+@pytest.mark.parametrize("n", [1, 2, 10, 100, 1000])
+def test_known_global_minima(n):
+    g = load("paper_minima.json")["functions"]
+    for fid_s, spec in g.items():
+        fid = int(fid_s)
+        x = _xstar(spec["xstar"], n)
+        lo, hi = oracle.eval_point(fid, x)
+        fstar = _fstar(spec["fstar"], n)
+        # 2pi/3 and 0.9 are rounded, so allow the first-order perturbation
+        slack = 1e-13 * max(1.0, abs(fstar)) * (n if spec["xstar"] in ("0.9", "2pi/3") else 1)
+        assert lo - slack <= fstar <= hi + slack, (spec["name"], n, lo, hi, fstar)
+        assert hi - lo <= 1e-12 * max(1.0, abs(fstar)) * n, (spec["name"], n, lo, hi)
+
+
+# ------------------------------------- closed forms at special points (pins)
+def _pt(fid, x):
+    lo, hi = oracle.eval_point(fid, np.asarray(x, np.float64))
+    return lo, hi
+
+
+PI = math.pi
+D_PI = float(hp.PI)
+
+
+def close(iv, value, tol):
+    return iv[0] - tol <= value <= iv[1] + tol
+
+
+def test_closed_forms_ackley_rastrigin_breiman():
+    rng = np.random.default_rng(3)
+    for n in (1, 3, 10):
+        k = rng.integers(-5, 6, n).astype(float)
+        # Ackley at integers: cos(2 pi k) = 1
+        r = math.sqrt(float(np.sum(k * k)) / n)
+        v = 20 - 20 * float(hp.dexp(Decimal(-0.02) * Decimal(r)))
+        assert close(_pt(1, k), v, 1e-13), (n, k)
+        # Ackley at half integers: cos = -1
+        h = k + 0.5
+        r = math.sqrt(float(np.sum(h * h)) / n)
+        v = float(-20 * hp.dexp(Decimal(-0.02) * Decimal(r)) - hp.dexp(-1) + 20 + hp.E)
+        assert close(_pt(1, h), v, 1e-13)
+        # Rastrigin at integers: 10n + sum(k^2 - 10) = sum k^2; half integers: 20n + sum x^2
+        assert close(_pt(7, k), float(np.sum(k * k)), 1e-12)
+        assert close(_pt(7, h), 20 * n + float(np.sum(h * h)), 1e-12)
+        # Breiman at integers: cos(5 pi j) = (-1)^j
+        v = -0.1 * float(np.sum((-1.0) ** np.abs(k))) + float(np.sum(k * k))
+        assert close(_pt(3, k), v, 1e-12)
+
+
+def test_closed_forms_fu():
+    # g^2 = pi/14: 7 g^2 = pi/2 -> sin^2 = 1;  14 g^2 = pi -> sin^2 = 0
+    g = math.sqrt(D_PI / 14)
+    assert close(_pt(4, [0.9 + g]), 1 + 8 + D_PI / 14, 2e-14 * 20)
+    # g^2 = pi/28: sin^2(pi/4) = 1/2, sin^2(pi/2) = 1 -> 1 + 4 + 6 + pi/28
+    g = math.sqrt(D_PI / 28)
+    assert close(_pt(4, [0.9 - g, 0.9]), 1 + 4 + 6 + D_PI / 28, 2e-14 * 20)
+
+
+def test_closed_forms_griewank():
+    n = 5
+    x = np.zeros(n)
+    x[0] = D_PI / 2  # kappa_1 = 1: cos(pi/2) = 0
+    assert close(_pt(5, x), 1 + (D_PI / 2) ** 2 / 4000, 1e-14)
+    x = np.zeros(n)
+    x[1] = D_PI * math.sqrt(2)  # kappa_2 = 1/sqrt(2): cos(pi) = -1
+    assert close(_pt(5, x), 2 + (D_PI * math.sqrt(2)) ** 2 / 4000, 1e-14)
+    x = np.zeros(n)
+    x[3] = D_PI * 2  # kappa_4 = 1/2: cos(pi) = -1  (pins the 1-based index)
+    assert close(_pt(5, x), 2 + (2 * D_PI) ** 2 / 4000, 1e-14)
+
+
+def test_closed_forms_levy():
+    n = 4
+    one = np.ones(n)
+    x = one.copy()
+    x[0] = 3.0  # y1 = 1.5: 10 sin^2(1.5 pi) = 10, u1 v2 = 0.25 * 1
+    assert close(_pt(6, x), D_PI / n * 10.25, 1e-14)
+    x = one.copy()
+    x[-1] = 5.0  # y_n = 2: u_n = 1, u_{n-1} v_n = 0 * ... = 0
+    assert close(_pt(6, x), D_PI / n * 1.0, 1e-14)
+    x = one.copy()
+    x[1] = 3.0  # y2 = 1.5: u1 v2 = 0 * 11, u2 v3 = 0.25 * 1
+    assert close(_pt(6, x), D_PI / n * 0.25, 1e-14)
+
+
+def test_closed_forms_salomon_styblinski_zabinsky_belegundu():
+    # Salomon: ||x|| = 1 -> 0.1 ; ||x|| = 0.5 -> 2.05
+    assert close(_pt(8, [1.0, 0.0, 0.0]), 0.1, 1e-14)
+    assert close(_pt(8, [0.0, 0.5]), 2.05, 1e-14)
+    # Styblinski: x1 = pi -> cos = -1: pi^2/(2n) + 4n
+    n = 3
+    x = np.zeros(n)
+    x[0] = D_PI
+    assert close(_pt(9, x), D_PI ** 2 / (2 * n) + 4 * n, 1e-12)
+    x[0] = D_PI / 2
+    assert close(_pt(9, x), (D_PI / 2) ** 2 / (2 * n), 1e-12)
+    # Zabinsky: x = pi/6 -> both products 0;  x = pi/6 + pi/10 ->
+    #   -2.5 ((sqrt5-1)/4)^n - 1
+    n = 3
+    assert close(_pt(10, np.full(n, D_PI / 6)), 0.0, 1e-14)
+    s = (math.sqrt(5) - 1) / 4
+    assert close(_pt(10, np.full(n, D_PI / 6 + D_PI / 10)), -2.5 * s ** n - 1.0, 1e-13)
+    # Belegundu: sqrt(S) = pi/5 -> cos(pi) = -1 ; pi/10 -> cos(pi/2) = 0
+    assert close(_pt(2, [5 + D_PI / 5, 5.0]), 0.1 * (D_PI / 5) ** 2 + 1, 1e-13)
+    assert close(_pt(2, [5.0, 5 + D_PI / 10]), 0.1 * (D_PI / 10) ** 2, 1e-13)
+
+
+# -------------------------------------- derivatives vs central differences
+@pytest.mark.parametrize("fid", list(range(0, 11)))
+def test_derivative_matches_central_difference(fid):
+    rng = np.random.default_rng(10 + fid)
+    for n in (1, 2, 5):
+        l, u = workloads.bounds(fid, n)
+        for _ in range(6):
+            x = rng.uniform(l + 0.05 * (u - l), u - 0.05 * (u - l))
+            if fid in (1, 8):
+                x = x + 0.5  # stay away from the non-differentiable r = 0
+            for i in range(n):
+                h = 1e-6 * max(1.0, abs(x[i]))
+                xp, xm = x.copy(), x.copy()
+                xp[i] += h
+                xm[i] -= h
+                fp = sum(_pt(fid, xp)) / 2
+                fm = sum(_pt(fid, xm)) / 2
+                fd = (fp - fm) / (2 * h)
+                w = 1e-9 * max(1.0, abs(x[i]))
+                lo = x.copy()
+                hi = x.copy()
+                lo[i] -= w
+                hi[i] += w
+                d = oracle.grad_box(fid, lo, hi, i)
+                scale = max(1.0, abs(fd))
+                assert d[0] - 1e-4 * scale <= fd <= d[1] + 1e-4 * scale, (fid, n, i, d, fd)
+                assert d[1] - d[0] <= 1e-3 * scale + 1e-6, (fid, d)
+
+
+# --------------------------------- inclusion of sampled points (brute force)
+@pytest.mark.parametrize("fid", list(range(0, 11)))
+def test_box_encloses_sampled_points(fid):
+    for n in (1, 2, 7):
+        l, u = workloads.bounds(fid, n)
+        lo, hi = workloads.random_boxes(100 + fid, n, 25, l, u)
+        pts = workloads.random_points_in(200 + fid, lo, hi, 8)
+        for b in range(lo.shape[0]):
+            e = oracle.eval_box(fid, lo[b], hi[b])
+            assert e[0] <= e[1]
+            for p in pts[b]:
+                v = oracle.eval_point(fid, p)
+                assert e[0] <= v[0] and v[1] <= e[1], (fid, n, b, e, v)
+            # corners too
+            for c in (lo[b], hi[b]):
+                v = oracle.eval_point(fid, c)
+                assert e[0] <= v[0] and v[1] <= e[1]
+            for i in range(n):
+                g = oracle.grad_box(fid, lo[b], hi[b], i)
+                for p in pts[b][:3]:
+                    gp = oracle.grad_box(fid, p, p, i)
+                    assert g[0] <= gp[0] and gp[1] <= g[1], (fid, i, g, gp)
+
+
+def test_tiny_box_enclosure_is_tight():
+    for fid in range(11):
+        n = 4
+        l, u = workloads.bounds(fid, n)
+        x = (l + u) / 2 + 0.123
+        w = 1e-10
+        e = oracle.eval_box(fid, x - w, x + w)
+        assert e[1] - e[0] < 1e-5, (fid, e)
