@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Benchmark of the interval branch-and-bound hot path (BASELINE.json metric:
+box-evaluations per second and time-to-enclose at eps = 1e-6).
+
+One step = one complete solve of the workload (every iteration of the hot
+path: select, partition, midpoint sampling + incumbent, bound + first-order
+test, compaction) from the root region to the eps-enclosure.  Default
+workload: BASELINE.json configs[1], Ackley n = 10 on [-32.768, 32.768]^10,
+eps = 1e-6 (it fits one GPU; configs[0] is the oracle-sized case).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): the domain is partitioned into N slabs along x_1, one per
+rank, and the incumbent GUB is all-reduced (MIN, NCCL) every iteration; the
+time is the max over ranks of the device time.  Prints ONE JSON line on
+rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+METRIC = "box-evals/sec"
+UNIT = "box-evals/s"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_PATH = os.path.join(ROOT, "profiles", "fp64_ops_per_child.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "traffic_r01.json")
+
+# B200: 148 SMs x 64 FP64 FMA lanes per SM per clock (half the FP32 rate; the
+# 37 TFLOP/s FP64 of the B200 datasheet) -- DESIGN.md "Roofline".
+SMS = 148
+FP64_LANES = 64
+
+# algorithmic HBM bytes per record of the list kernels
+BYTES_PER_RECORD = {"list_stats": 16, "radix_hist": 8, "partition": 48}
+
+
+def env_rank():
+    r = int(os.environ.get("RANK", "0"))
+    w = int(os.environ.get("WORLD_SIZE", "1"))
+    lr = int(os.environ.get("LOCAL_RANK", "0"))
+    return r, w, lr
+
+
+def load_json(p):
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 9:
+                rows.append(p)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ helpers
+def slab(l, u, rank, world):
+    """Partition of the domain along x_1 into `world` slabs (exact cover)."""
+    l = l.copy()
+    u = u.copy()
+    a, b = l[0], u[0]
+    edges = [a + (b - a) * k / world for k in range(world + 1)]
+    edges[0], edges[-1] = a, b
+    l[0], u[0] = edges[rank], edges[rank + 1]
+    return l, u
+
+
+def exchange_fn(dist):
+    def ex(x):
+        dist.all_reduce(x, op=dist.ReduceOp.MIN)
+
+    return ex
+
+
+def cpu_baseline(cfg, seconds=12.0):
+    """The CPU oracle, as it stands, on a bounded sample of the same workload:
+    or_branch on parents of the workload's first iterations (the root and its
+    level-1 children), timed on one host core."""
+    import oracle
+
+    fid, n = cfg["fid"], cfg["n"]
+    l, u = workloads.config_bounds(cfg)
+    d = min(n, 10)
+    kids = 2 ** d
+    parents = [(l, u)]
+    for c in range(0, kids, max(1, kids // 64)):
+        parents.append(oracle.child_box(l, u, 0, d, 2, c))
+    t0 = time.perf_counter()
+    evals = 0
+    k = 0
+    while time.perf_counter() - t0 < seconds and k < len(parents):
+        plo, phi = parents[k]
+        oracle.branch(fid, plo[None], phi[None], [0 if k == 0 else d % n], d, 2, l, u, mono=True)
+        evals += kids
+        k += 1
+    dt = time.perf_counter() - t0
+    return {"value": evals / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"or_branch on {k} parents of {cfg['name']} (root + level-1 regions), "
+                      f"{evals} child boxes, {dt:.1f} s"}
+
+
+def reference_arm(args, cfg):
+    r, world, _ = env_rank()
+    if r != 0:
+        return 0
+    import oracle
+
+    fid, n = cfg["fid"], cfg["n"]
+    l, u = workloads.config_bounds(cfg)
+    d = min(n, 10)
+    kids = 2 ** d
+    parent = (l, u)
+
+    def step():
+        oracle.branch(fid, parent[0][None], parent[1][None], [0], d, 2, l, u, mono=True)
+        return kids
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    ev = sum(step() for _ in range(args.steps))
+    dt = time.perf_counter() - t0
+    v = ev / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfg["name"], "fid": fid, "n": n, "domain": [cfg["lo"], cfg["hi"]],
+                   "eps": cfg["eps"], "step": "oracle or_branch of the root region (m^d children)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"{args.steps} x or_branch(root) = {ev} child boxes"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--bmax", type=int, default=0)
+    ap.add_argument("--no-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = workloads.CONFIGS[args.config]
+    if args.impl == "reference":
+        return reference_arm(args, cfg)
+
+    import torch
+
+    import paper_2507_01770_b200 as pb
+
+    rank, world, lrank = env_rank()
+    torch.cuda.set_device(lrank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", lrank))
+    dev = torch.device("cuda", lrank)
+    fid, n = cfg["fid"], cfg["n"]
+    L, U = workloads.config_bounds(cfg)
+    l, u = slab(L, U, rank, world)
+    ld = torch.tensor(l, device=dev)
+    ud = torch.tensor(u, device=dev)
+    opts = pb.options(d=min(n, 10), m=2, bmax=args.bmax or None, profile=1)
+    ws = pb.Workspace(pb.solve_workspace_bytes(fid, n, opts), device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    ex = exchange_fn(dist) if dist else None
+
+    def solve():
+        if ex:
+            return pb.ib_solve_dev_ex(fid, ld, ud, ex, cfg["eps"], cfg["eps"], opts, workspace=ws)
+        return pb.ib_solve_dev(fid, ld, ud, cfg["eps"], cfg["eps"], opts, workspace=ws)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        solve()
+    stream = torch.cuda.current_stream()
+    clk = ClockSampler(lrank)
+    total_ms = 0.0
+    res = []
+    barrier()
+    clk.start()
+    for _ in range(args.steps):
+        flush.fill_(1)  # L2 flush between steps (outside the timed events)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = solve()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        total_ms += e0.elapsed_time(e1)
+        res.append(r)
+    barrier()
+    clocks = clk.stop()
+    evals = sum(r.evals for r in res)
+    t = torch.tensor([total_ms, float(evals)], dtype=torch.float64, device=dev)
+    if dist:
+        tmax = t[:1].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tev = t[1:].clone()
+        dist.all_reduce(tev, op=dist.ReduceOp.SUM)
+        total_ms, evals = float(tmax.item()), float(tev.item())
+    value = evals / (total_ms / 1e3)
+    r0 = res[-1]
+    f_lo, f_hi = r0.f_lo, r0.f_hi
+    if dist:
+        enc = torch.tensor([f_lo, f_hi], dtype=torch.float64, device=dev)
+        dist.all_reduce(enc, op=dist.ReduceOp.MIN)
+        f_lo, f_hi = enc.tolist()
+
+    # ---- live roofline of the dominant kernel class (CUDA events inside the runtime)
+    prof = {}
+    for r in res:
+        for c, v in r.prof.items():
+            p = prof.setdefault(c, {"ms": 0.0, "launches": 0, "units": 0})
+            for k in p:
+                p[k] += v[k]
+    dom = max(prof, key=lambda c: prof[c]["ms"])
+    peaks = load_json(PEAKS_PATH) or {}
+    pd = prof[dom]
+    avg_s = pd["ms"] / 1e3 / max(1, pd["launches"])
+    units_per_launch = pd["units"] / max(1, pd["launches"])
+    traffic = (load_json(TRAFFIC_PATH) or {}).get(dom)
+    if dom in BYTES_PER_RECORD:
+        hbm = peaks.get("hbm_gbs", 6650.0)
+        ach = BYTES_PER_RECORD[dom] * units_per_launch / avg_s / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": traffic, "peak_source": "measured" if "hbm_gbs" in peaks else "fallback"}
+    else:
+        fp = load_json(FP64_PATH) or {}
+        per_unit = (fp.get(str(fid)) or {}).get(dom)
+        clock_ghz = (peaks.get("sm_max_mhz") or 1965.0) / 1e3
+        peak = SMS * FP64_LANES * 2 * clock_ghz / 1e3  # TFLOP/s
+        ach = per_unit * units_per_launch / avg_s / 1e12 if per_unit else None
+        roof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": peak, "unit": "TFLOP/s (FP64)",
+                "frac": (ach / peak) if ach else None, "traffic": traffic,
+                "per_unit_flops": per_unit, "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x sm_max_mhz"}
+    roof["share_of_step"] = pd["ms"] / max(1e-9, sum(p["ms"] for p in prof.values()))
+    roof["avg_launch_us"] = avg_s * 1e6
+    roof["units_per_launch"] = units_per_launch
+
+    # ---- e2e through the public host-buffer API (pinned host buffers)
+    e2e = None
+    if world == 1:
+        lh = torch.tensor(l, dtype=torch.float64).pin_memory()
+        uh = torch.tensor(u, dtype=torch.float64).pin_memory()
+        cap = 4096
+        so = torch.empty((cap, n), dtype=torch.float64).pin_memory()
+        sh = torch.empty((cap, n), dtype=torch.float64).pin_memory()
+        sl = torch.empty(cap, dtype=torch.float64).pin_memory()
+        import ctypes
+
+        ms = 0.0
+        ev2 = 0
+        d2h = 0
+        for _ in range(args.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            rr = pb.IbResult()
+            e0.record(stream)
+            rc = pb.lib().ib_solve(fid, n, ctypes.cast(lh.data_ptr(), pb._dp), ctypes.cast(uh.data_ptr(), pb._dp),
+                                   cfg["eps"], cfg["eps"], ctypes.byref(opts), ws.ptr(), ws.nbytes,
+                                   ctypes.byref(rr), ctypes.cast(so.data_ptr(), pb._dp),
+                                   ctypes.cast(sh.data_ptr(), pb._dp), ctypes.cast(sl.data_ptr(), pb._dp), cap,
+                                   ctypes.c_void_p(stream.cuda_stream))
+            e1.record(stream)
+            torch.cuda.synchronize()
+            pb._check(rc, "ib_solve")
+            ms += e0.elapsed_time(e1)
+            ev2 += rr.evals
+            d2h = min(rr.n_surv, cap) * (2 * n + 1) * 8 + 48
+        e2e = {"value": ev2 / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 2 * n * 8, "d2h_bytes_per_step": d2h}
+
+    base = None
+    if rank == 0 and world == 1 and not args.no_baseline:
+        try:
+            base = cpu_baseline(cfg)
+        except Exception as e:  # the baseline must never break the bench line
+            base = {"value": None, "error": repr(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": cfg["name"], "fid": fid, "n": n, "domain": [cfg["lo"], cfg["hi"]],
+                       "eps": cfg["eps"], "d": min(n, 10), "m": 2, "bmax": int(opts.bmax) or "auto",
+                       "step": "one full solve (root region -> eps-enclosure)",
+                       "l2": "flushed between steps (256 MiB write)",
+                       "parallelism": f"domain slabs x{world}, NCCL all-reduce(MIN) of GUB per iteration"},
+            "time_to_enclose_s": total_ms / args.steps / 1e3,
+            "enclosure": [f_lo, f_hi],
+            "iters": r0.iters, "evals_per_step": r0.evals, "peak_pool": r0.peak_pool,
+            "roofline": roof,
+            "kernel_ms": {c: round(p["ms"] / args.steps, 4) for c, p in prof.items()},
+            "cpu_baseline": base,
+            "e2e": e2e,
+            "clocks": clocks,
+            "gpu_launches": int(sum(r.n_kernels for r in res)),
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

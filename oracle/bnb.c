@@ -7,7 +7,7 @@
  * One iteration (paper order, Fig. 2):
  *   1. select the regions with the smallest lower bound from the list L
  *      (line 130; batched: the B smallest, ties broken by list position,
- *      DESIGN.md reading R1);
+ *      processed in list order, reading R1);
  *   2. partition each selected region into m^d subregions along the d
  *      variables given by its cycling index (lines 140, 176-184, Eq. 8-11);
  *   3. sample: evaluate f in interval arithmetic at the midpoint of every
@@ -236,12 +236,15 @@ int or_solve(int fid, int n, const double* l, const double* u, double eps_f, dou
         double* phi = (double*)malloc(sizeof(double) * (size_t)nb * n);
         int* pcyc = (int*)malloc(sizeof(int) * (size_t)nb);
         char* taken = (char*)calloc((size_t)pn, 1);
-        for (long b = 0; b < nb; ++b) {
-            rec_t* r = order[b];
-            memcpy(plo + b * n, r->box, sizeof(double) * (size_t)n);
-            memcpy(phi + b * n, r->box + n, sizeof(double) * (size_t)n);
-            pcyc[b] = r->cyc;
-            taken[r - pool] = 1;
+        for (long b = 0; b < nb; ++b) taken[order[b] - pool] = 1;
+        /* the selected regions are processed in list order (R1) */
+        long bb = 0;
+        for (long k = 0; k < pn; ++k) {
+            if (!taken[k]) continue;
+            memcpy(plo + bb * n, pool[k].box, sizeof(double) * (size_t)n);
+            memcpy(phi + bb * n, pool[k].box + n, sizeof(double) * (size_t)n);
+            pcyc[bb] = pool[k].cyc;
+            ++bb;
         }
         /* remove the selected regions from L, keeping the order of the rest */
         long keep = 0;

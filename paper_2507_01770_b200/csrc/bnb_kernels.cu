@@ -1,0 +1,961 @@
+// bnb_kernels.cu -- the CUDA kernels of one branch-and-bound iteration
+// (§3.1 flowchart, §3.2 partition / variable cycling) and of the
+// explicit-batch evaluators.  Host launchers at the bottom are called by
+// runtime.cu; nothing here knows about torch.
+//
+//   k_prep      : materialise the selected boxes (SPSD, Eq. 8-11), reduce
+//                 the per-variable terms of the unsplit variables (block-
+//                 cooperative interval sums/products, coalesced FP64 loads)
+//                 and tabulate the terms of the m pieces of the d split
+//                 variables
+//   k_child_ub  : midpoint sample of every child -> warp-shuffle min ->
+//                 ordered-int atomicMin on the incumbent GUB (line 134)
+//   k_child_lb  : lower bound + first-order test of every child, pruning
+//                 (lines 140-144) and stable decoupled-look-back compaction
+//                 of the survivors into the list L (line 146)
+//   k_pool_*    : statistics, radix-select histogram and 3-way partition of
+//                 L (select the B smallest lower bounds, line 130; drop
+//                 lb > GUB, line 136)
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.cuh"
+#include "objectives.cuh"
+#include "scan.cuh"
+
+namespace ib {
+
+// ------------------------------------------------------------ partition
+// Eq. (10)-(11) with m pieces, round-to-nearest, no FMA (bit-identical to
+// the oracle's part_point, reading R2).
+__device__ __forceinline__ double part_point(double a, double b, int m, int k) {
+  if (k <= 0) return a;
+  if (k >= m) return b;
+  double w = __ddiv_rn(__dsub_rn(b, a), (double)m);
+  double p = __dadd_rn(a, __dmul_rn(w, (double)k));
+  return p < b ? p : b;
+}
+__device__ __forceinline__ double midpt(double a, double b) {
+  double mid = __dadd_rn(a, __dmul_rn(__dsub_rn(b, a), 0.5));
+  return fmin(fmax(mid, a), b);
+}
+__device__ __forceinline__ int digit(uint32_t code, int j, int m) {
+  if (m == 2) return (code >> j) & 1u;
+  for (int t = 0; t < j; ++t) code /= (uint32_t)m;
+  return (int)(code % (uint32_t)m);
+}
+
+// ------------------------------------------------------------ reductions
+template <class F>
+__device__ __forceinline__ void warp_reduce_acc(Iv* a) {
+#pragma unroll
+  for (int k = 0; k < F::K; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      Iv t{__shfl_xor_sync(0xffffffffu, a[k].lo, o), __shfl_xor_sync(0xffffffffu, a[k].hi, o)};
+      a[k] = acc_comb<F>(k, a[k], t);
+    }
+  }
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// block reduction of K interval accumulators (result valid in thread 0)
+template <class F>
+__device__ __forceinline__ void block_reduce_acc(Iv* a) {
+  __shared__ Iv s_acc[TPB / 32][2];
+  warp_reduce_acc<F>(a);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0)
+    for (int k = 0; k < F::K; ++k) s_acc[wid][k] = a[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < TPB / 32; ++w)
+      for (int k = 0; k < F::K; ++k) a[k] = acc_comb<F>(k, a[k], s_acc[w][k]);
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ double block_max(double v) {
+  __shared__ double s_m[TPB / 32];
+  v = warp_max(v);
+  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int w = 1; w < TPB / 32; ++w) v = fmax(v, s_m[w]);
+  __syncthreads();
+  return v;
+}
+
+__device__ __forceinline__ void put(double* p, Iv v) {
+  p[0] = v.lo;
+  p[1] = v.hi;
+}
+__device__ __forceinline__ Iv get(const double* p) { return Iv{p[0], p[1]}; }
+
+// ------------------------------------------------------------ Levy helpers
+struct LevyChunk {
+  int c, d, n, L, R;
+  __device__ bool inJ(int t) const { return ((t - c + n) % n) < d; }
+  __device__ int local(int t) const {
+    int jj = (t - c + n) % n;
+    if (jj < d) return jj;
+    return t == L ? d : d + 1;
+  }
+};
+__device__ __forceinline__ LevyChunk levy_chunk(int c, int d, int n) {
+  LevyChunk q{c, d, n, -1, -1};
+  if (d < n) {
+    int L = c - 1;  // chain neighbour left of the chunk
+    if (c >= 1 && !q.inJ(L)) q.L = L;
+    int R = (c + d) % n;
+    if (R != 0 && !q.inJ(R)) q.R = R;
+  }
+  return q;
+}
+
+// ====================================================================== prep
+// One block per selected box b.  Source row: archive slot sel_slot[b] of
+// src_lo/src_hi with record code sel_code[b]; destination: slot new_slot[b]
+// of dst_lo/dst_hi.  src_sc / dst_sc hold each slot's chunk start.
+template <class F>
+__global__ void __launch_bounds__(TPB) k_prep(Problem P, int nb, const int32_t* __restrict__ sel_slot,
+                                              const uint32_t* __restrict__ sel_code,
+                                              const int32_t* __restrict__ new_slot,
+                                              const double* __restrict__ src_lo,
+                                              const double* __restrict__ src_hi,
+                                              const int32_t* __restrict__ src_sc, double* dst_lo,
+                                              double* dst_hi, int32_t* dst_sc, double* tab,
+                                              int tab_stride) {
+  const int b = blockIdx.x;
+  if (b >= nb) return;
+  const int n = P.n, d = P.d, m = P.m;
+  const int src = sel_slot[b];
+  const uint32_t code = sel_code[b];
+  const int dst = new_slot[b];
+  const int psc = src_sc[src];
+  const int c = (code == CODE_WHOLE) ? psc : (psc + d) % n;  // line 184
+  const double* slo = src_lo + (size_t)src * P.ld;
+  const double* shi = src_hi + (size_t)src * P.ld;
+  double* dlo = dst_lo + (size_t)dst * P.ld;
+  double* dhi = dst_hi + (size_t)dst * P.ld;
+  double* T = tab + (size_t)b * tab_stride;
+
+  Iv acc[2], accm[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) acc[k] = accm[k] = iv(0.0);
+  if constexpr (!F::CHAIN) {
+#pragma unroll
+    for (int k = 0; k < F::K; ++k) acc[k] = accm[k] = acc_ident<F>(k);
+  }
+  double wmax = 0.0;
+  for (int i = threadIdx.x; i < n; i += TPB) {
+    double a = slo[i], bb = shi[i];
+    if (code != CODE_WHOLE) {
+      int jj = (i - psc + n) % n;
+      if (jj < d) {
+        int p = digit(code, jj, m);
+        double a2 = part_point(a, bb, m, p), b2 = part_point(a, bb, m, p + 1);
+        a = a2;
+        bb = b2;
+      }
+    }
+    dlo[i] = a;
+    dhi[i] = bb;
+    if (((i - c + n) % n) >= d) {
+      wmax = fmax(wmax, __dsub_rn(bb, a));
+      if constexpr (!F::CHAIN) {
+        Iv t[2], tm[2];
+        F::terms(Iv{a, bb}, i, n, t);
+        double xm = midpt(a, bb);
+        F::terms(Iv{xm, xm}, i, n, tm);
+#pragma unroll
+        for (int k = 0; k < F::K; ++k) {
+          acc[k] = acc_comb<F>(k, acc[k], t[k]);
+          accm[k] = acc_comb<F>(k, accm[k], tm[k]);
+        }
+      }
+    }
+  }
+  __syncthreads();  // the destination row is complete (block-visible)
+
+  if constexpr (F::CHAIN) {
+    // Levy: rest = sum of chain terms that involve no split variable
+    LevyChunk q = levy_chunk(c, d, n);
+    Iv r = iv(0.0), rm = iv(0.0);
+    for (int i = threadIdx.x; i < n; i += TPB) {
+      bool ji = q.inJ(i);
+      Iv X{dlo[i], dhi[i]};
+      double xm = midpt(X.lo, X.hi);
+      LevyVals v = ObjLevy::vals(X), vm = ObjLevy::vals(Iv{xm, xm});
+      if (i == 0 && !ji) {
+        r = r + v.s0;
+        rm = rm + vm.s0;
+      }
+      if (i <= n - 2 && !ji && !q.inJ(i + 1)) {
+        Iv X1{dlo[i + 1], dhi[i + 1]};
+        double xm1 = midpt(X1.lo, X1.hi);
+        LevyVals w = ObjLevy::vals(X1), wm = ObjLevy::vals(Iv{xm1, xm1});
+        r = r + v.u * w.v;
+        rm = rm + vm.u * wm.v;
+      }
+      if (i == n - 1 && !ji) {
+        r = r + v.u;
+        rm = rm + vm.u;
+      }
+    }
+    Iv a2[2] = {r, iv(0.0)}, am2[2] = {rm, iv(0.0)};
+    block_reduce_acc<ObjRastrigin>(a2);  // any K=1 SUM reducer
+    block_reduce_acc<ObjRastrigin>(am2);
+    acc[0] = a2[0];
+    accm[0] = am2[0];
+    if (threadIdx.x == 0) {
+      // neighbour values and the list of affected chain terms
+      double* nb_ = T + H_LEVY_NB;
+      int nbv[2] = {q.L, q.R};
+      for (int s = 0; s < 2; ++s) {
+        Iv X = nbv[s] >= 0 ? Iv{dlo[nbv[s]], dhi[nbv[s]]} : iv(0.0);
+        double xm = midpt(X.lo, X.hi);
+        LevyVals v = ObjLevy::vals(X), vm = ObjLevy::vals(Iv{xm, xm});
+        put(nb_ + 8 * s + 0, v.u);
+        put(nb_ + 8 * s + 2, v.v);
+        put(nb_ + 8 * s + 4, vm.u);
+        put(nb_ + 8 * s + 6, vm.v);
+      }
+      int nt = 0;
+      double* td = T + H_LEVY_T;
+      if (q.inJ(0)) td[nt++] = (double)(0 * 65536 + q.local(0) * 256);
+      int ncand = d < n ? d + 1 : n;
+      for (int t = 0; t < ncand; ++t) {
+        int i = d < n ? (c - 1 + t + n) % n : t;
+        if (i > n - 2) continue;
+        if (q.inJ(i) || q.inJ(i + 1)) td[nt++] = (double)(1 * 65536 + q.local(i) * 256 + q.local(i + 1));
+      }
+      if (q.inJ(n - 1)) td[nt++] = (double)(2 * 65536 + q.local(n - 1) * 256);
+      T[H_LEVY_NT] = (double)nt;
+      T[H_LEVY_LR] = (double)q.L;
+      T[H_LEVY_LR + 1] = (double)q.R;
+    }
+  } else {
+    block_reduce_acc<F>(acc);
+    block_reduce_acc<F>(accm);
+  }
+  wmax = block_max(wmax);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 2; ++k) {
+      put(T + H_REST + 2 * k, acc[k]);
+      put(T + H_RESTM + 2 * k, accm[k]);
+    }
+    T[H_WREST] = wmax;
+    T[H_CHUNK] = (double)c;
+    dst_sc[dst] = c;
+  }
+  // tables of the m pieces of the d split variables
+  for (int t = threadIdx.x; t < d * m; t += TPB) {
+    int j = t / m, p = t % m;
+    int i = (c + j) % n;
+    double a = dlo[i], bb = dhi[i];
+    double pa = part_point(a, bb, m, p), pb = part_point(a, bb, m, p + 1);
+    double xm = midpt(pa, pb);
+    double* e = T + HDR + (size_t)t * ENT;
+    e[E_LO] = pa;
+    e[E_HI] = pb;
+    if constexpr (F::CHAIN) {
+      LevyVals v = ObjLevy::vals(Iv{pa, pb}), vm = ObjLevy::vals(Iv{xm, xm});
+      put(e + 2, v.u);
+      put(e + 4, v.v);
+      put(e + 6, v.s0);
+      put(e + 8, v.du);
+      put(e + 10, v.sg);
+      put(e + 12, vm.u);
+      put(e + 14, vm.v);
+      put(e + 16, vm.s0);
+    } else {
+      Iv tt[2], tm[2], g[2];
+      F::terms(Iv{pa, pb}, i, n, tt);
+      F::terms(Iv{xm, xm}, i, n, tm);
+      for (int k = 0; k < F::K; ++k) {
+        put(e + E_T + 2 * k, tt[k]);
+        put(e + E_T + 2 * F::K + 2 * k, tm[k]);
+      }
+      if constexpr (F::KG > 0) {
+        F::ding(Iv{pa, pb}, i, n, g);
+        for (int k = 0; k < F::KG; ++k) put(e + E_T + 4 * F::K + 2 * k, g[k]);
+      }
+      double flag = 0.0;
+      if constexpr (F::SEP) {
+        Iv D = F::dsep(Iv{pa, pb}, i, n);
+        if ((D.lo > 0.0 && pa != P.l[i]) || (D.hi < 0.0 && pb != P.u[i])) flag = 1.0;
+      }
+      e[E_T + 4 * F::K + 2 * F::KG] = flag;
+    }
+  }
+}
+
+// ================================================================ children
+struct ChildIdx {
+  int b;
+  uint32_t code;
+};
+__device__ __forceinline__ ChildIdx child_of(long g, int kids) {
+  return ChildIdx{(int)(g / kids), (uint32_t)(g % kids)};
+}
+
+// Levy accessors over (split pieces | neighbours)
+struct LevyView {
+  const double* T;
+  const int* e;  // entry index per split variable
+  int d;
+  __device__ Iv u(int li, bool mid) const {
+    if (li < d) return get(T + HDR + (size_t)e[li] * ENT + (mid ? 12 : 2));
+    return get(T + H_LEVY_NB + 8 * (li - d) + (mid ? 4 : 0));
+  }
+  __device__ Iv v(int li, bool mid) const {
+    if (li < d) return get(T + HDR + (size_t)e[li] * ENT + (mid ? 14 : 4));
+    return get(T + H_LEVY_NB + 8 * (li - d) + (mid ? 6 : 2));
+  }
+  __device__ Iv s0(int li, bool mid) const { return get(T + HDR + (size_t)e[li] * ENT + (mid ? 16 : 6)); }
+  __device__ Iv acc(bool mid) const {
+    Iv a = get(T + (mid ? H_RESTM : H_REST));
+    int nt = (int)T[H_LEVY_NT];
+    for (int t = 0; t < nt; ++t) {
+      int dsc = (int)T[H_LEVY_T + t];
+      int kind = dsc >> 16, li = (dsc >> 8) & 255, lj = dsc & 255;
+      if (kind == 0)
+        a = a + s0(li, mid);
+      else if (kind == 1)
+        a = a + u(li, mid) * v(lj, mid);
+      else
+        a = a + u(li, mid);
+    }
+    return a;
+  }
+};
+
+template <class F>
+__device__ __forceinline__ double child_ub(const Problem& P, const double* __restrict__ T, uint32_t code) {
+  const int d = P.d, m = P.m;
+  if constexpr (F::CHAIN) {
+    int e[D_MAX];
+    for (int j = 0; j < d; ++j) {
+      e[j] = j * m + (int)(code % (uint32_t)m);
+      code /= (uint32_t)m;
+    }
+    LevyView V{T, e, d};
+    return ObjLevy::outer(V.acc(true), P.n).hi;
+  } else {
+    Iv A[2];
+#pragma unroll
+    for (int k = 0; k < F::K; ++k) A[k] = get(T + H_RESTM + 2 * k);
+    for (int j = 0; j < d; ++j) {
+      int p = (int)(code % (uint32_t)m);
+      code /= (uint32_t)m;
+      const double* e = T + HDR + (size_t)(j * m + p) * ENT + E_T + 2 * F::K;
+#pragma unroll
+      for (int k = 0; k < F::K; ++k) A[k] = acc_comb<F>(k, A[k], get(e + 2 * k));
+    }
+    return F::outer(A, P.n).hi;
+  }
+}
+
+// lower bound, width and survival of one child (lines 140-144)
+template <class F>
+__device__ __forceinline__ bool child_lb(const Problem& P, const double* __restrict__ T, uint32_t code,
+                                         double gub, double& lb, double& w) {
+  const int d = P.d, m = P.m, n = P.n;
+  int e[D_MAX];
+  double wmax = T[H_WREST];
+  for (int j = 0; j < d; ++j) {
+    e[j] = j * m + (int)(code % (uint32_t)m);
+    code /= (uint32_t)m;
+    const double* ej = T + HDR + (size_t)e[j] * ENT;
+    wmax = fmax(wmax, __dsub_rn(ej[E_HI], ej[E_LO]));
+  }
+  w = wmax;
+  const int c = (int)T[H_CHUNK];
+  if constexpr (F::CHAIN) {
+    LevyView V{T, e, d};
+    lb = canon_lb(ObjLevy::outer(V.acc(false), n).lo);
+    if (!(lb <= gub)) return false;
+    if (!P.mono) return true;
+    LevyChunk q = levy_chunk(c, d, n);
+    for (int j = 0; j < d; ++j) {
+      int i = (c + j) % n;
+      const double* ej = T + HDR + (size_t)e[j] * ENT;
+      LevyVals me;
+      me.u = get(ej + 2);
+      me.v = get(ej + 4);
+      me.s0 = get(ej + 6);
+      me.du = get(ej + 8);
+      me.sg = get(ej + 10);
+      Iv up = i > 0 ? V.u(q.local(i - 1), false) : iv(0.0);
+      Iv vn = i < n - 1 ? V.v(q.local(i + 1), false) : iv(0.0);
+      Iv D = ObjLevy::deriv(me, up, vn, i, n);
+      if ((D.lo > 0.0 && ej[E_LO] != P.l[i]) || (D.hi < 0.0 && ej[E_HI] != P.u[i])) return false;
+    }
+    return true;
+  } else {
+    Iv A[2];
+#pragma unroll
+    for (int k = 0; k < F::K; ++k) A[k] = get(T + H_REST + 2 * k);
+    for (int j = 0; j < d; ++j) {
+      const double* ej = T + HDR + (size_t)e[j] * ENT + E_T;
+#pragma unroll
+      for (int k = 0; k < F::K; ++k) A[k] = acc_comb<F>(k, A[k], get(ej + 2 * k));
+    }
+    lb = canon_lb(F::outer(A, n).lo);
+    if (!(lb <= gub)) return false;
+    if (!P.mono) return true;
+    if constexpr (F::SEP) {
+      for (int j = 0; j < d; ++j)
+        if (T[HDR + (size_t)e[j] * ENT + E_T + 4 * F::K + 2 * F::KG] != 0.0) return false;
+      return true;
+    } else {
+      typename F::Ctx cx = F::ctx(A, n);
+      // products without variable i: prefix (running) x suffix (precomputed)
+      Iv suf[D_MAX + 1][2];
+      Iv pre[2];
+      if constexpr (F::HASPROD) {
+#pragma unroll
+        for (int k = 0; k < F::K; ++k) {
+          suf[d][k] = iv(1.0);
+          pre[k] = get(T + H_REST + 2 * k);
+        }
+        for (int j = d - 1; j >= 0; --j) {
+          const double* ej = T + HDR + (size_t)e[j] * ENT + E_T;
+#pragma unroll
+          for (int k = 0; k < F::K; ++k)
+            suf[j][k] = F::kind(k) == PROD ? get(ej + 2 * k) * suf[j + 1][k] : iv(0.0);
+        }
+      }
+      for (int j = 0; j < d; ++j) {
+        int i = (c + j) % n;
+        const double* ej = T + HDR + (size_t)e[j] * ENT;
+        Iv g[2], excl[2];
+#pragma unroll
+        for (int k = 0; k < F::KG; ++k) g[k] = get(ej + E_T + 4 * F::K + 2 * k);
+        if constexpr (F::HASPROD) {
+#pragma unroll
+          for (int k = 0; k < F::K; ++k) excl[k] = F::kind(k) == PROD ? pre[k] * suf[j + 1][k] : iv(0.0);
+        }
+        Iv X{ej[E_LO], ej[E_HI]};
+        Iv D = F::dfin(cx, g, X, i, n, excl);
+        if ((D.lo > 0.0 && X.lo != P.l[i]) || (D.hi < 0.0 && X.hi != P.u[i])) return false;
+        if constexpr (F::HASPROD) {
+#pragma unroll
+          for (int k = 0; k < F::K; ++k)
+            if (F::kind(k) == PROD) pre[k] = pre[k] * get(ej + E_T + 2 * k);
+        }
+      }
+      return true;
+    }
+  }
+}
+
+template <class F>
+__global__ void __launch_bounds__(TPB) k_child_ub(Problem P, const double* __restrict__ tab, int tab_stride,
+                                                  long total, unsigned long long* gub_key) {
+  double best = CUDART_INF;
+  for (long g = (long)blockIdx.x * TPB + threadIdx.x; g < total; g += (long)gridDim.x * TPB) {
+    ChildIdx ci = child_of(g, P.kids);
+    double ub = child_ub<F>(P, tab + (size_t)ci.b * tab_stride, ci.code);
+    best = fmin(best, ub);
+  }
+  __shared__ double s_m[TPB / 32];
+  best = warp_min(best);
+  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < TPB / 32; ++w) best = fmin(best, s_m[w]);
+    if (best < CUDART_INF) atomicMin(gub_key, (unsigned long long)okey(best));
+  }
+}
+
+template <class F>
+__global__ void __launch_bounds__(TPB) k_child_lb(Problem P, const double* __restrict__ tab, int tab_stride,
+                                                  long total, const unsigned long long* gub_key,
+                                                  const int32_t* __restrict__ new_slot, Pool out,
+                                                  const uint64_t* out_base, uint64_t* desc,
+                                                  uint32_t* tile_ctr, uint64_t* out_count, long ntiles) {
+  __shared__ uint32_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const double gub = okey_inv(*gub_key);
+  const long g0 = (long)tile * TILE + (long)threadIdx.x * IPT;
+  double lbv[IPT], wv[IPT];
+  uint32_t keep = 0;
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    long g = g0 + q;
+    lbv[q] = 0.0;
+    wv[q] = 0.0;
+    if (g < total) {
+      ChildIdx ci = child_of(g, P.kids);
+      if (child_lb<F>(P, tab + (size_t)ci.b * tab_stride, ci.code, gub, lbv[q], wv[q])) keep |= 1u << q;
+    }
+  }
+  uint32_t cnt[1] = {(uint32_t)__popc(keep)}, ex[1], tot[1];
+  block_exclusive_scan<1, TPB>(cnt, ex, tot);
+  uint64_t pfx[1];
+  dl_lookback<1>(desc, tile, tot, pfx);
+  uint64_t pos = *out_base + pfx[0] + ex[0];
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    if (keep & (1u << q)) {
+      ChildIdx ci = child_of(g0 + q, P.kids);
+      out.lb[pos] = lbv[q];
+      out.w[pos] = wv[q];
+      out.slot[pos] = new_slot[ci.b];
+      out.code[pos] = ci.code;
+      ++pos;
+    }
+  }
+  if (tile == (uint32_t)(ntiles - 1) && threadIdx.x == 0) *out_count = *out_base + pfx[0] + tot[0];
+}
+
+// ============================================================ list L kernels
+__global__ void __launch_bounds__(TPB) k_pool_stats(Pool p, const uint64_t* cnt_dev,
+                                                    const unsigned long long* gub_key, Stats* st) {
+  const double gub = okey_inv(*gub_key);
+  const long cnt = (long)*cnt_dev;
+  unsigned long long live = 0, mk = ~0ull;
+  double mw = 0.0;
+  for (long r = (long)blockIdx.x * TPB + threadIdx.x; r < cnt; r += (long)gridDim.x * TPB) {
+    double lb = p.lb[r];
+    if (lb <= gub) {
+      ++live;
+      unsigned long long k = okey(lb);
+      mk = k < mk ? k : mk;
+      mw = fmax(mw, p.w[r]);
+    }
+  }
+  __shared__ unsigned long long s_l[TPB / 32], s_k[TPB / 32];
+  __shared__ double s_w[TPB / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    live += __shfl_xor_sync(0xffffffffu, live, o);
+    unsigned long long t = __shfl_xor_sync(0xffffffffu, mk, o);
+    mk = t < mk ? t : mk;
+    mw = fmax(mw, __shfl_xor_sync(0xffffffffu, mw, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_l[threadIdx.x >> 5] = live;
+    s_k[threadIdx.x >> 5] = mk;
+    s_w[threadIdx.x >> 5] = mw;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < TPB / 32; ++w) {
+      live += s_l[w];
+      mk = s_k[w] < mk ? s_k[w] : mk;
+      mw = fmax(mw, s_w[w]);
+    }
+    if (live) atomicAdd(&st->live, live);
+    atomicMin(&st->min_lb_key, mk);
+    atomicMax(&st->max_w_bits, (unsigned long long)__double_as_longlong(mw));
+  }
+}
+
+// histogram of the next 8-bit digit of okey(lb) among live records whose
+// higher digits equal `prefix` (known = number of known high bits)
+__global__ void __launch_bounds__(TPB) k_radix_hist(Pool p, long cnt, const unsigned long long* gub_key,
+                                                    int known, unsigned long long prefix,
+                                                    unsigned int* hist) {
+  __shared__ unsigned int s_h[256];
+  for (int i = threadIdx.x; i < 256; i += TPB) s_h[i] = 0;
+  __syncthreads();
+  const double gub = okey_inv(*gub_key);
+  const int shift = 64 - known - 8;
+  for (long r = (long)blockIdx.x * TPB + threadIdx.x; r < cnt; r += (long)gridDim.x * TPB) {
+    double lb = p.lb[r];
+    if (!(lb <= gub)) continue;
+    unsigned long long k = okey(lb);
+    if (known > 0 && (k >> (64 - known)) != prefix) continue;
+    atomicAdd(&s_h[(k >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += TPB)
+    if (s_h[i]) atomicAdd(&hist[i], s_h[i]);
+}
+
+// Stable 3-way partition of L.  Live records (lb <= GUB) whose key's top
+// `known` bits are < prefix are selected; those equal to prefix are selected
+// while their rank among equals is < r_need; the rest of the live records are
+// kept.  known == 0 selects every live record.  counters: 0 lt, 1 eq, 2 gt.
+__global__ void __launch_bounds__(TPB) k_partition(Pool in, long cnt, const unsigned long long* gub_key,
+                                                   int known, unsigned long long prefix,
+                                                   unsigned long long r_need, int32_t* sel_slot,
+                                                   uint32_t* sel_code, double* sel_lb, Pool keep,
+                                                   uint64_t* desc, uint32_t* tile_ctr) {
+  __shared__ uint32_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const double gub = okey_inv(*gub_key);
+  const long r0 = (long)tile * TILE + (long)threadIdx.x * IPT;
+  uint8_t cls[IPT];  // 0 lt, 1 eq, 2 gt, 3 drop
+  uint32_t cnt3[3] = {0, 0, 0};
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    long r = r0 + q;
+    cls[q] = 3;
+    if (r < cnt) {
+      double lb = in.lb[r];
+      if (lb <= gub) {
+        if (known == 0) {
+          cls[q] = 0;
+        } else {
+          unsigned long long top = okey(lb) >> (64 - known);
+          cls[q] = top < prefix ? 0 : (top == prefix ? 1 : 2);
+        }
+        cnt3[cls[q]]++;
+      }
+    }
+  }
+  uint32_t ex[3], tot[3];
+  block_exclusive_scan<3, TPB>(cnt3, ex, tot);
+  uint64_t pfx[3];
+  dl_lookback<3>(desc, tile, tot, pfx);
+  uint64_t lt = pfx[0] + ex[0], eq = pfx[1] + ex[1], gt = pfx[2] + ex[2];
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    long r = r0 + q;
+    int k = cls[q];
+    if (k == 3) continue;
+    bool sel;
+    uint64_t pos;
+    if (k == 0) {
+      sel = true;
+      pos = lt + (eq < r_need ? eq : r_need);
+      ++lt;
+    } else if (k == 1) {
+      sel = eq < r_need;
+      pos = sel ? lt + eq : gt + (eq - r_need);
+      ++eq;
+    } else {
+      sel = false;
+      pos = gt + (eq > r_need ? eq - r_need : 0);
+      ++gt;
+    }
+    if (sel) {
+      sel_slot[pos] = in.slot[r];
+      sel_code[pos] = in.code[r];
+      sel_lb[pos] = in.lb[r];
+    } else {
+      keep.lb[pos] = in.lb[r];
+      keep.w[pos] = in.w[r];
+      keep.slot[pos] = in.slot[r];
+      keep.code[pos] = in.code[r];
+    }
+  }
+}
+
+// ---- archive slot garbage collection (mark from L and the batch, collect)
+__global__ void k_gc_mark(const int32_t* slot, long cnt, uint8_t* mark) {
+  for (long r = (long)blockIdx.x * blockDim.x + threadIdx.x; r < cnt; r += (long)gridDim.x * blockDim.x)
+    mark[slot[r]] = 1;
+}
+__global__ void __launch_bounds__(TPB) k_gc_collect(const uint8_t* mark, long cap, int32_t* free_list,
+                                                    uint64_t* desc, uint32_t* tile_ctr, uint64_t* out_count,
+                                                    long ntiles) {
+  __shared__ uint32_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const long s0 = (long)tile * TILE + (long)threadIdx.x * IPT;
+  uint32_t f = 0;
+#pragma unroll
+  for (int q = 0; q < IPT; ++q)
+    if (s0 + q < cap && !mark[s0 + q]) f |= 1u << q;
+  uint32_t cnt[1] = {(uint32_t)__popc(f)}, ex[1], tot[1];
+  block_exclusive_scan<1, TPB>(cnt, ex, tot);
+  uint64_t pfx[1];
+  dl_lookback<1>(desc, tile, tot, pfx);
+  uint64_t pos = pfx[0] + ex[0];
+#pragma unroll
+  for (int q = 0; q < IPT; ++q)
+    if (f & (1u << q)) free_list[pos++] = (int32_t)(s0 + q);
+  if (tile == (uint32_t)(ntiles - 1) && threadIdx.x == 0) *out_count = pfx[0] + tot[0];
+}
+__global__ void k_alloc(const int32_t* free_list, long top, int nb, int32_t* new_slot) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x)
+    new_slot[b] = free_list[top - 1 - b];
+}
+
+// generic stable compaction of indices with key <= threshold (ib_compact_le)
+__global__ void __launch_bounds__(TPB) k_compact_le(const double* keys, long cnt, double thr, int64_t* out_idx,
+                                                    uint64_t* desc, uint32_t* tile_ctr, uint64_t* out_count,
+                                                    long ntiles) {
+  __shared__ uint32_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const long s0 = (long)tile * TILE + (long)threadIdx.x * IPT;
+  uint32_t f = 0;
+#pragma unroll
+  for (int q = 0; q < IPT; ++q)
+    if (s0 + q < cnt && keys[s0 + q] <= thr) f |= 1u << q;
+  uint32_t c1[1] = {(uint32_t)__popc(f)}, ex[1], tot[1];
+  block_exclusive_scan<1, TPB>(c1, ex, tot);
+  uint64_t pfx[1];
+  dl_lookback<1>(desc, tile, tot, pfx);
+  uint64_t pos = pfx[0] + ex[0];
+#pragma unroll
+  for (int q = 0; q < IPT; ++q)
+    if (f & (1u << q)) out_idx[pos++] = s0 + q;
+  if (tile == (uint32_t)(ntiles - 1) && threadIdx.x == 0) *out_count = pfx[0] + tot[0];
+}
+
+// materialise records (slot, code) of L into explicit boxes
+__global__ void k_extract(Problem P, Pool p, long cnt, const double* A_lo, const double* A_hi,
+                          const int32_t* sc, double* out_lo, double* out_hi, double* out_lb) {
+  for (long r = blockIdx.x; r < cnt; r += gridDim.x) {
+    int s = p.slot[r];
+    uint32_t code = p.code[r];
+    int psc = sc[s];
+    for (int i = threadIdx.x; i < P.n; i += blockDim.x) {
+      double a = A_lo[(size_t)s * P.ld + i], b = A_hi[(size_t)s * P.ld + i];
+      if (code != CODE_WHOLE) {
+        int jj = (i - psc + P.n) % P.n;
+        if (jj < P.d) {
+          int q = digit(code, jj, P.m);
+          double a2 = part_point(a, b, P.m, q), b2 = part_point(a, b, P.m, q + 1);
+          a = a2;
+          b = b2;
+        }
+      }
+      out_lo[(size_t)r * P.n + i] = a;
+      out_hi[(size_t)r * P.n + i] = b;
+    }
+    if (threadIdx.x == 0 && out_lb) out_lb[r] = p.lb[r];
+  }
+}
+
+// ========================================================= explicit batches
+// f over explicit boxes: one warp per box, lanes stride over variables,
+// warp-shuffle interval reduction (the "warp-cooperative sum").
+template <class F>
+__global__ void __launch_bounds__(TPB) k_eval_boxes(int n, long nbox, const double* __restrict__ lo,
+                                                    const double* __restrict__ hi, long ld, double* out) {
+  const long wbox = ((long)blockIdx.x * TPB + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wbox >= nbox) return;
+  const double* bl = lo + wbox * ld;
+  const double* bh = hi + wbox * ld;
+  Iv acc[2];
+  if constexpr (F::CHAIN) {
+    acc[0] = iv(0.0);
+    for (int i = lane; i < n; i += 32) {
+      LevyVals v = ObjLevy::vals(Iv{bl[i], bh[i]});
+      if (i == 0) acc[0] = acc[0] + v.s0;
+      if (i <= n - 2) acc[0] = acc[0] + v.u * ObjLevy::vals(Iv{bl[i + 1], bh[i + 1]}).v;
+      if (i == n - 1) acc[0] = acc[0] + v.u;
+    }
+    warp_reduce_acc<ObjRastrigin>(acc);
+    if (lane == 0) {
+      Iv r = ObjLevy::outer(acc[0], n);
+      out[2 * wbox] = r.lo;
+      out[2 * wbox + 1] = r.hi;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < F::K; ++k) acc[k] = acc_ident<F>(k);
+    for (int i = lane; i < n; i += 32) {
+      Iv t[2];
+      F::terms(Iv{bl[i], bh[i]}, i, n, t);
+#pragma unroll
+      for (int k = 0; k < F::K; ++k) acc[k] = acc_comb<F>(k, acc[k], t[k]);
+    }
+    warp_reduce_acc<F>(acc);
+    if (lane == 0) {
+      Iv r = F::outer(acc, n);
+      out[2 * wbox] = r.lo;
+      out[2 * wbox + 1] = r.hi;
+    }
+  }
+}
+
+// partial derivative enclosures: one warp per request (box index, variable)
+template <class F>
+__global__ void __launch_bounds__(TPB) k_eval_grad(int n, long nreq, const double* __restrict__ lo,
+                                                   const double* __restrict__ hi, long ld,
+                                                   const int64_t* __restrict__ req_box,
+                                                   const int32_t* __restrict__ req_dim, double* out) {
+  const long w = ((long)blockIdx.x * TPB + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nreq) return;
+  const long bx = req_box[w];
+  const int i = req_dim[w];
+  const double* bl = lo + bx * ld;
+  const double* bh = hi + bx * ld;
+  Iv D;
+  if constexpr (F::CHAIN) {
+    LevyVals me = ObjLevy::vals(Iv{bl[i], bh[i]});
+    Iv up = i > 0 ? ObjLevy::vals(Iv{bl[i - 1], bh[i - 1]}).u : iv(0.0);
+    Iv vn = i < n - 1 ? ObjLevy::vals(Iv{bl[i + 1], bh[i + 1]}).v : iv(0.0);
+    D = ObjLevy::deriv(me, up, vn, i, n);
+  } else if constexpr (F::SEP) {
+    D = F::dsep(Iv{bl[i], bh[i]}, i, n);
+  } else {
+    Iv acc[2], excl[2];
+#pragma unroll
+    for (int k = 0; k < F::K; ++k) acc[k] = excl[k] = acc_ident<F>(k);
+    for (int j = lane; j < n; j += 32) {
+      Iv t[2];
+      F::terms(Iv{bl[j], bh[j]}, j, n, t);
+#pragma unroll
+      for (int k = 0; k < F::K; ++k) {
+        acc[k] = acc_comb<F>(k, acc[k], t[k]);
+        if (j != i) excl[k] = acc_comb<F>(k, excl[k], t[k]);
+      }
+    }
+    warp_reduce_acc<F>(acc);
+    warp_reduce_acc<F>(excl);
+    Iv g[2];
+    Iv X{bl[i], bh[i]};
+    F::ding(X, i, n, g);
+    typename F::Ctx cx = F::ctx(acc, n);
+    D = F::dfin(cx, g, X, i, n, excl);
+  }
+  if (lane == 0) {
+    out[2 * w] = D.lo;
+    out[2 * w + 1] = D.hi;
+  }
+}
+
+// ================================================================ launchers
+static inline unsigned grid_for(long items, int per_block, unsigned cap = 148u * 32u) {
+  long g = (items + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  return (unsigned)(g < (long)cap ? g : cap);
+}
+
+int launch_prep(const Problem& P, int nb, const int32_t* sel_slot, const uint32_t* sel_code,
+                const int32_t* new_slot, const double* src_lo, const double* src_hi, const int32_t* src_sc,
+                double* dst_lo, double* dst_hi, int32_t* dst_sc, double* tab, int tab_stride,
+                cudaStream_t st) {
+  if (nb <= 0) return 0;
+  IB_DISPATCH_FID(P.fid, k_prep<F><<<nb, TPB, 0, st>>>(P, nb, sel_slot, sel_code, new_slot, src_lo, src_hi,
+                                                       src_sc, dst_lo, dst_hi, dst_sc, tab, tab_stride));
+  return (int)cudaGetLastError();
+}
+
+int launch_child_ub(const Problem& P, const double* tab, int tab_stride, long total,
+                    unsigned long long* gub_key, cudaStream_t st) {
+  if (total <= 0) return 0;
+  unsigned g = grid_for(total, TPB);
+  IB_DISPATCH_FID(P.fid, k_child_ub<F><<<g, TPB, 0, st>>>(P, tab, tab_stride, total, gub_key));
+  return (int)cudaGetLastError();
+}
+
+int launch_child_lb(const Problem& P, const double* tab, int tab_stride, long total,
+                    const unsigned long long* gub_key, const int32_t* new_slot, Pool out,
+                    const uint64_t* out_base, uint64_t* desc, uint32_t* tile_ctr, uint64_t* out_count,
+                    cudaStream_t st) {
+  long ntiles = (total + TILE - 1) / TILE;
+  if (ntiles < 1) ntiles = 1;
+  cudaMemsetAsync(desc, 0, sizeof(uint64_t) * (size_t)ntiles, st);
+  cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t), st);
+  IB_DISPATCH_FID(P.fid, k_child_lb<F><<<(unsigned)ntiles, TPB, 0, st>>>(
+                             P, tab, tab_stride, total, gub_key, new_slot, out, out_base, desc, tile_ctr,
+                             out_count, ntiles));
+  return (int)cudaGetLastError();
+}
+
+__global__ void k_stats_init(Stats* s) {
+  s->live = 0ull;
+  s->min_lb_key = ~0ull;
+  s->max_w_bits = 0ull;
+}
+// cnt_dev: device record count; cnt_bound: host upper bound used for the grid
+int launch_pool_stats(Pool p, const uint64_t* cnt_dev, long cnt_bound, const unsigned long long* gub_key,
+                      Stats* st_dev, cudaStream_t st) {
+  k_stats_init<<<1, 1, 0, st>>>(st_dev);
+  if (cnt_bound > 0)
+    k_pool_stats<<<grid_for(cnt_bound, TPB, 148u * 8u), TPB, 0, st>>>(p, cnt_dev, gub_key, st_dev);
+  return (int)cudaGetLastError();
+}
+
+int launch_radix_hist(Pool p, long cnt, const unsigned long long* gub_key, int known,
+                      unsigned long long prefix, unsigned int* hist, cudaStream_t st) {
+  cudaMemsetAsync(hist, 0, 256 * sizeof(unsigned int), st);
+  if (cnt > 0)
+    k_radix_hist<<<grid_for(cnt, TPB * 8, 148u * 4u), TPB, 0, st>>>(p, cnt, gub_key, known, prefix, hist);
+  return (int)cudaGetLastError();
+}
+
+int launch_partition(Pool in, long cnt, const unsigned long long* gub_key, int known,
+                     unsigned long long prefix, unsigned long long r_need, int32_t* sel_slot,
+                     uint32_t* sel_code, double* sel_lb, Pool keep, uint64_t* desc, uint32_t* tile_ctr,
+                     cudaStream_t st) {
+  long ntiles = (cnt + TILE - 1) / TILE;
+  if (ntiles < 1) return 0;
+  cudaMemsetAsync(desc, 0, sizeof(uint64_t) * 3 * (size_t)ntiles, st);
+  cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t), st);
+  k_partition<<<(unsigned)ntiles, TPB, 0, st>>>(in, cnt, gub_key, known, prefix, r_need, sel_slot, sel_code,
+                                                sel_lb, keep, desc, tile_ctr);
+  return (int)cudaGetLastError();
+}
+
+int launch_gc(const int32_t* pool_slot, long pcnt, const int32_t* batch_slot, long nb, uint8_t* mark,
+              long cap, int32_t* free_list, uint64_t* desc, uint32_t* tile_ctr, uint64_t* out_count,
+              cudaStream_t st) {
+  cudaMemsetAsync(mark, 0, (size_t)cap, st);
+  if (pcnt > 0) k_gc_mark<<<grid_for(pcnt, TPB, 148u * 8u), TPB, 0, st>>>(pool_slot, pcnt, mark);
+  if (nb > 0) k_gc_mark<<<grid_for(nb, TPB, 148u * 8u), TPB, 0, st>>>(batch_slot, nb, mark);
+  long ntiles = (cap + TILE - 1) / TILE;
+  cudaMemsetAsync(desc, 0, sizeof(uint64_t) * (size_t)ntiles, st);
+  cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t), st);
+  k_gc_collect<<<(unsigned)ntiles, TPB, 0, st>>>(mark, cap, free_list, desc, tile_ctr, out_count, ntiles);
+  return (int)cudaGetLastError();
+}
+
+int launch_alloc(const int32_t* free_list, long top, int nb, int32_t* new_slot, cudaStream_t st) {
+  if (nb > 0) k_alloc<<<grid_for(nb, TPB), TPB, 0, st>>>(free_list, top, nb, new_slot);
+  return (int)cudaGetLastError();
+}
+
+int launch_compact_le(const double* keys, long cnt, double thr, int64_t* out_idx, uint64_t* desc,
+                      uint32_t* tile_ctr, uint64_t* out_count, cudaStream_t st) {
+  long ntiles = (cnt + TILE - 1) / TILE;
+  if (ntiles < 1) {
+    cudaMemsetAsync(out_count, 0, sizeof(uint64_t), st);
+    return (int)cudaGetLastError();
+  }
+  cudaMemsetAsync(desc, 0, sizeof(uint64_t) * (size_t)ntiles, st);
+  cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t), st);
+  k_compact_le<<<(unsigned)ntiles, TPB, 0, st>>>(keys, cnt, thr, out_idx, desc, tile_ctr, out_count, ntiles);
+  return (int)cudaGetLastError();
+}
+
+int launch_extract(const Problem& P, Pool p, long cnt, const double* A_lo, const double* A_hi,
+                   const int32_t* sc, double* out_lo, double* out_hi, double* out_lb, cudaStream_t st) {
+  if (cnt > 0) k_extract<<<grid_for(cnt, 1, 148u * 16u), 128, 0, st>>>(P, p, cnt, A_lo, A_hi, sc, out_lo, out_hi, out_lb);
+  return (int)cudaGetLastError();
+}
+
+int launch_eval_boxes(int fid, int n, long nbox, const double* lo, const double* hi, long ld, double* out,
+                      cudaStream_t st) {
+  if (nbox <= 0) return 0;
+  unsigned g = (unsigned)((nbox * 32 + TPB - 1) / TPB);
+  IB_DISPATCH_FID(fid, k_eval_boxes<F><<<g, TPB, 0, st>>>(n, nbox, lo, hi, ld, out));
+  return (int)cudaGetLastError();
+}
+
+int launch_eval_grad(int fid, int n, long nreq, const double* lo, const double* hi, long ld,
+                     const int64_t* req_box, const int32_t* req_dim, double* out, cudaStream_t st) {
+  if (nreq <= 0) return 0;
+  unsigned g = (unsigned)((nreq * 32 + TPB - 1) / TPB);
+  IB_DISPATCH_FID(fid, k_eval_grad<F><<<g, TPB, 0, st>>>(n, nreq, lo, hi, ld, req_box, req_dim, out));
+  return (int)cudaGetLastError();
+}
+
+}  // namespace ib

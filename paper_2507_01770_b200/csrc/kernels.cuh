@@ -1,0 +1,55 @@
+// kernels.cuh -- device data layout shared by the kernels and the host
+// runtime of the branch-and-bound hot path (no torch types anywhere).
+#pragma once
+#include <stdint.h>
+
+namespace ib {
+
+constexpr uint32_t CODE_WHOLE = 0xffffffffu;  // record = the archived box itself
+constexpr int D_MAX = 16;                       // split variables per iteration
+constexpr int M_MAX = 8;                        // pieces per split variable
+constexpr int DM_MAX = 64;                      // d * m table entries per parent
+constexpr int HDR = 48;                         // doubles of per-parent header
+constexpr int ENT = 24;                         // doubles per (variable, piece) entry
+constexpr int TPB = 256;                        // threads per block (all kernels)
+constexpr int IPT = 4;                          // items per thread in scans
+constexpr int TILE = TPB * IPT;
+
+// header offsets (doubles)
+constexpr int H_REST = 0;    // K intervals (K <= 2): rest accumulators
+constexpr int H_RESTM = 4;   // K intervals: rest accumulators at the midpoint
+constexpr int H_WREST = 8;   // max width over the unsplit variables
+constexpr int H_CHUNK = 9;   // first split variable c
+constexpr int H_LEVY_NB = 10;  // Levy: neighbour values [L: u v um vm][R: u v um vm]
+constexpr int H_LEVY_NT = 26;  // Levy: number of affected chain terms
+constexpr int H_LEVY_T = 27;   // Levy: term descriptors kind*65536 + li*256 + lj
+constexpr int H_LEVY_LR = 46;  // Levy: left / right neighbour variable (or -1)
+
+// entry offsets (doubles)
+constexpr int E_LO = 0, E_HI = 1, E_T = 2;  // then T[K] (2K), Tm[K] (2K), G[KG] (2KG), flag
+
+// pool of pending boxes (the paper's list L, §3.2): one record
+// = lower bound, max width, archive slot of the parent box, child code
+struct Pool {
+  double* lb;
+  double* w;
+  int32_t* slot;
+  uint32_t* code;
+};
+
+// statistics of the live part of L (lb <= GUB), one atomic update per block
+struct Stats {
+  unsigned long long live;
+  unsigned long long min_lb_key;
+  unsigned long long max_w_bits;  // w >= 0: bit pattern order == value order
+};
+
+struct Problem {
+  int fid, n, d, m, kids;  // kids = m^d
+  int ld;                  // archive row stride (doubles)
+  int mono;                // apply the first-order test
+  const double* l;         // device copies of the bounds
+  const double* u;
+};
+
+}  // namespace ib
