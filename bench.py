@@ -144,14 +144,15 @@ def cpu_baseline(cfg, seconds=12.0):
     t0 = time.perf_counter()
     evals = 0
     k = 0
-    while time.perf_counter() - t0 < seconds and k < len(parents):
-        plo, phi = parents[k]
-        oracle.branch(fid, plo[None], phi[None], [0 if k == 0 else d % n], d, 2, l, u, mono=True)
+    while time.perf_counter() - t0 < seconds:
+        j = k % len(parents)
+        plo, phi = parents[j]
+        oracle.branch(fid, plo[None], phi[None], [0 if j == 0 else d % n], d, 2, l, u, mono=True)
         evals += kids
         k += 1
     dt = time.perf_counter() - t0
     return {"value": evals / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"or_branch on {k} parents of {cfg['name']} (root + level-1 regions), "
+            "sample": f"or_branch on {k} parents (cycling the root + {len(parents) - 1} level-1 regions) of {cfg['name']}, "
                       f"{evals} child boxes, {dt:.1f} s"}
 
 

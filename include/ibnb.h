@@ -85,7 +85,7 @@ typedef struct {
     int status;       /* IB_STATUS_* */
     int n_kernels;    /* CUDA kernels this call launched */
     /* per kernel class, filled when opt.profile = 1 (else zero):
-     * 0 prep (units: parents), 1 child_ub (children), 2 child_lb (children),
+     * 0 prep (units: parents), 1 child_eval (children), 2 child_prune (children),
      * 3 list statistics (records), 4 radix histogram (records),
      * 5 partition of L (records) */
     double t_ms[IB_NPROF];

@@ -300,6 +300,8 @@ __global__ void __launch_bounds__(TPB) k_prep(Problem P, int nb, const int32_t* 
 }
 
 // ================================================================ children
+// Child g of the batch: parent b = g / m^d, code = g % m^d; digit j of the
+// code (base m) is the piece of split variable (c + j) mod n.
 struct ChildIdx {
   int b;
   uint32_t code;
@@ -339,52 +341,48 @@ struct LevyView {
   }
 };
 
-template <class F>
-__device__ __forceinline__ double child_ub(const Problem& P, const double* __restrict__ T, uint32_t code) {
-  const int d = P.d, m = P.m;
-  if constexpr (F::CHAIN) {
-    int e[D_MAX];
-    for (int j = 0; j < d; ++j) {
-      e[j] = j * m + (int)(code % (uint32_t)m);
-      code /= (uint32_t)m;
-    }
-    LevyView V{T, e, d};
-    return ObjLevy::outer(V.acc(true), P.n).hi;
-  } else {
-    Iv A[2];
-#pragma unroll
-    for (int k = 0; k < F::K; ++k) A[k] = get(T + H_RESTM + 2 * k);
-    for (int j = 0; j < d; ++j) {
-      int p = (int)(code % (uint32_t)m);
-      code /= (uint32_t)m;
-      const double* e = T + HDR + (size_t)(j * m + p) * ENT + E_T + 2 * F::K;
-#pragma unroll
-      for (int k = 0; k < F::K; ++k) A[k] = acc_comb<F>(k, A[k], get(e + 2 * k));
-    }
-    return F::outer(A, P.n).hi;
-  }
-}
-
-// lower bound, width and survival of one child (lines 140-144)
-template <class F>
-__device__ __forceinline__ bool child_lb(const Problem& P, const double* __restrict__ T, uint32_t code,
-                                         double gub, double& lb, double& w) {
-  const int d = P.d, m = P.m, n = P.n;
-  int e[D_MAX];
-  double wmax = T[H_WREST];
+__device__ __forceinline__ void entries_of(uint32_t code, int d, int m, int* e) {
   for (int j = 0; j < d; ++j) {
     e[j] = j * m + (int)(code % (uint32_t)m);
     code /= (uint32_t)m;
-    const double* ej = T + HDR + (size_t)e[j] * ENT;
-    wmax = fmax(wmax, __dsub_rn(ej[E_HI], ej[E_LO]));
   }
-  w = wmax;
+}
+
+// accumulators of the child box (rest combined with the d piece terms)
+template <class F>
+__device__ __forceinline__ void child_acc(const Problem& P, const double* __restrict__ T, uint32_t code, Iv* A) {
+#pragma unroll
+  for (int k = 0; k < F::K; ++k) A[k] = get(T + H_REST + 2 * k);
+  for (int j = 0; j < P.d; ++j) {
+    int p = (int)(code % (uint32_t)P.m);
+    code /= (uint32_t)P.m;
+    const double* e = T + HDR + (size_t)(j * P.m + p) * ENT + E_T;
+#pragma unroll
+    for (int k = 0; k < F::K; ++k) A[k] = acc_comb<F>(k, A[k], get(e + 2 * k));
+  }
+}
+
+__device__ __forceinline__ double child_width(const Problem& P, const double* __restrict__ T, uint32_t code) {
+  double w = T[H_WREST];
+  for (int j = 0; j < P.d; ++j) {
+    int p = (int)(code % (uint32_t)P.m);
+    code /= (uint32_t)P.m;
+    const double* e = T + HDR + (size_t)(j * P.m + p) * ENT;
+    w = fmax(w, __dsub_rn(e[E_HI], e[E_LO]));
+  }
+  return w;
+}
+
+// first-order test of PAPER.md lines 142-144 on the split variables of a
+// child whose lower bound already passed; true = the child survives
+template <class F>
+__device__ __noinline__ bool child_mono_ok(const Problem& P, const double* __restrict__ T, uint32_t code) {
+  const int d = P.d, m = P.m, n = P.n;
   const int c = (int)T[H_CHUNK];
+  int e[D_MAX];
+  entries_of(code, d, m, e);
   if constexpr (F::CHAIN) {
     LevyView V{T, e, d};
-    lb = canon_lb(ObjLevy::outer(V.acc(false), n).lo);
-    if (!(lb <= gub)) return false;
-    if (!P.mono) return true;
     LevyChunk q = levy_chunk(c, d, n);
     for (int j = 0; j < d; ++j) {
       int i = (c + j) % n;
@@ -401,6 +399,10 @@ __device__ __forceinline__ bool child_lb(const Problem& P, const double* __restr
       if ((D.lo > 0.0 && ej[E_LO] != P.l[i]) || (D.hi < 0.0 && ej[E_HI] != P.u[i])) return false;
     }
     return true;
+  } else if constexpr (F::SEP) {
+    for (int j = 0; j < d; ++j)
+      if (T[HDR + (size_t)e[j] * ENT + E_T + 4 * F::K + 2 * F::KG] != 0.0) return false;
+    return true;
   } else {
     Iv A[2];
 #pragma unroll
@@ -410,63 +412,111 @@ __device__ __forceinline__ bool child_lb(const Problem& P, const double* __restr
 #pragma unroll
       for (int k = 0; k < F::K; ++k) A[k] = acc_comb<F>(k, A[k], get(ej + 2 * k));
     }
-    lb = canon_lb(F::outer(A, n).lo);
-    if (!(lb <= gub)) return false;
-    if (!P.mono) return true;
-    if constexpr (F::SEP) {
-      for (int j = 0; j < d; ++j)
-        if (T[HDR + (size_t)e[j] * ENT + E_T + 4 * F::K + 2 * F::KG] != 0.0) return false;
-      return true;
-    } else {
-      typename F::Ctx cx = F::ctx(A, n);
-      // products without variable i: prefix (running) x suffix (precomputed)
-      Iv suf[D_MAX + 1][2];
-      Iv pre[2];
+    typename F::Ctx cx = F::ctx(A, n);
+    // products without variable i: running prefix x precomputed suffix
+    Iv suf[F::HASPROD ? D_MAX + 1 : 1][2];
+    Iv pre[2];
+    if constexpr (F::HASPROD) {
+#pragma unroll
+      for (int k = 0; k < F::K; ++k) {
+        suf[d][k] = iv(1.0);
+        pre[k] = get(T + H_REST + 2 * k);
+      }
+      for (int j = d - 1; j >= 0; --j) {
+        const double* ej = T + HDR + (size_t)e[j] * ENT + E_T;
+#pragma unroll
+        for (int k = 0; k < F::K; ++k)
+          suf[j][k] = F::kind(k) == PROD ? get(ej + 2 * k) * suf[j + 1][k] : iv(0.0);
+      }
+    }
+    for (int j = 0; j < d; ++j) {
+      int i = (c + j) % n;
+      const double* ej = T + HDR + (size_t)e[j] * ENT;
+      Iv g[2], excl[2] = {iv(0.0), iv(0.0)};
+#pragma unroll
+      for (int k = 0; k < F::KG; ++k) g[k] = get(ej + E_T + 4 * F::K + 2 * k);
       if constexpr (F::HASPROD) {
 #pragma unroll
-        for (int k = 0; k < F::K; ++k) {
-          suf[d][k] = iv(1.0);
-          pre[k] = get(T + H_REST + 2 * k);
-        }
-        for (int j = d - 1; j >= 0; --j) {
-          const double* ej = T + HDR + (size_t)e[j] * ENT + E_T;
-#pragma unroll
-          for (int k = 0; k < F::K; ++k)
-            suf[j][k] = F::kind(k) == PROD ? get(ej + 2 * k) * suf[j + 1][k] : iv(0.0);
-        }
+        for (int k = 0; k < F::K; ++k) excl[k] = F::kind(k) == PROD ? pre[k] * suf[j + 1][k] : iv(0.0);
       }
-      for (int j = 0; j < d; ++j) {
-        int i = (c + j) % n;
-        const double* ej = T + HDR + (size_t)e[j] * ENT;
-        Iv g[2], excl[2];
+      Iv X{ej[E_LO], ej[E_HI]};
+      Iv D = F::dfin(cx, g, X, i, n, excl);
+      if ((D.lo > 0.0 && X.lo != P.l[i]) || (D.hi < 0.0 && X.hi != P.u[i])) return false;
+      if constexpr (F::HASPROD) {
 #pragma unroll
-        for (int k = 0; k < F::KG; ++k) g[k] = get(ej + E_T + 4 * F::K + 2 * k);
-        if constexpr (F::HASPROD) {
-#pragma unroll
-          for (int k = 0; k < F::K; ++k) excl[k] = F::kind(k) == PROD ? pre[k] * suf[j + 1][k] : iv(0.0);
-        }
-        Iv X{ej[E_LO], ej[E_HI]};
-        Iv D = F::dfin(cx, g, X, i, n, excl);
-        if ((D.lo > 0.0 && X.lo != P.l[i]) || (D.hi < 0.0 && X.hi != P.u[i])) return false;
-        if constexpr (F::HASPROD) {
-#pragma unroll
-          for (int k = 0; k < F::K; ++k)
-            if (F::kind(k) == PROD) pre[k] = pre[k] * get(ej + E_T + 2 * k);
-        }
+        for (int k = 0; k < F::K; ++k)
+          if (F::kind(k) == PROD) pre[k] = pre[k] * get(ej + E_T + 2 * k);
       }
-      return true;
     }
+    return true;
   }
 }
 
+// Pass 1: upper bound at the midpoint and lower bound of every child.
+// A thread owns G = m^h consecutive children (all pieces of the h lowest
+// split variables): the terms of the d - h higher variables are combined
+// once per group.  Midpoint bounds are min-reduced (warp shuffle -> block ->
+// one ordered-int atomicMin per block into the incumbent, line 134); lower
+// bounds are stored per child for pass 2.
 template <class F>
-__global__ void __launch_bounds__(TPB) k_child_ub(Problem P, const double* __restrict__ tab, int tab_stride,
-                                                  long total, unsigned long long* gub_key) {
+__global__ void __launch_bounds__(TPB, 4) k_child_eval(Problem P, const double* __restrict__ tab, int tab_stride,
+                                                       long ngroups, unsigned long long* gub_key,
+                                                       double* __restrict__ clb) {
+  const int d = P.d, m = P.m, n = P.n, h = P.h, G = P.G;
+  const long gpp = P.kids / G;
   double best = CUDART_INF;
-  for (long g = (long)blockIdx.x * TPB + threadIdx.x; g < total; g += (long)gridDim.x * TPB) {
-    ChildIdx ci = child_of(g, P.kids);
-    double ub = child_ub<F>(P, tab + (size_t)ci.b * tab_stride, ci.code);
-    best = fmin(best, ub);
+  for (long gi = (long)blockIdx.x * TPB + threadIdx.x; gi < ngroups; gi += (long)gridDim.x * TPB) {
+    const int b = (int)(gi / gpp);
+    const uint32_t hcode = (uint32_t)(gi % gpp);
+    const double* __restrict__ T = tab + (size_t)b * tab_stride;
+    if constexpr (F::CHAIN) {
+      for (int q = 0; q < G; ++q) {
+        int e[D_MAX];
+        entries_of(hcode * (uint32_t)G + (uint32_t)q, d, m, e);
+        LevyView V{T, e, d};
+        best = fmin(best, ObjLevy::outer(V.acc(true), n).hi);
+        clb[gi * G + q] = canon_lb(ObjLevy::outer(V.acc(false), n).lo);
+      }
+    } else {
+      Iv A[2], Am[2];
+#pragma unroll
+      for (int k = 0; k < F::K; ++k) {
+        A[k] = get(T + H_REST + 2 * k);
+        Am[k] = get(T + H_RESTM + 2 * k);
+      }
+      uint32_t c = hcode;
+      for (int j = h; j < d; ++j) {
+        int p = (int)(c % (uint32_t)m);
+        c /= (uint32_t)m;
+        const double* e = T + HDR + (size_t)(j * m + p) * ENT + E_T;
+#pragma unroll
+        for (int k = 0; k < F::K; ++k) {
+          A[k] = acc_comb<F>(k, A[k], get(e + 2 * k));
+          Am[k] = acc_comb<F>(k, Am[k], get(e + 2 * F::K + 2 * k));
+        }
+      }
+      for (int q = 0; q < G; ++q) {
+        Iv B[2], Bm[2];
+#pragma unroll
+        for (int k = 0; k < F::K; ++k) {
+          B[k] = A[k];
+          Bm[k] = Am[k];
+        }
+        uint32_t lc = (uint32_t)q;
+        for (int j = 0; j < h; ++j) {
+          int p = (int)(lc % (uint32_t)m);
+          lc /= (uint32_t)m;
+          const double* e = T + HDR + (size_t)(j * m + p) * ENT + E_T;
+#pragma unroll
+          for (int k = 0; k < F::K; ++k) {
+            B[k] = acc_comb<F>(k, B[k], get(e + 2 * k));
+            Bm[k] = acc_comb<F>(k, Bm[k], get(e + 2 * F::K + 2 * k));
+          }
+        }
+        best = fmin(best, outer_hi<F>(Bm, n));
+        clb[gi * G + q] = canon_lb(outer_lo<F>(B, n));
+      }
+    }
   }
   __shared__ double s_m[TPB / 32];
   best = warp_min(best);
@@ -478,29 +528,56 @@ __global__ void __launch_bounds__(TPB) k_child_ub(Problem P, const double* __res
   }
 }
 
+// Pass 2: rule out children with lb > GUB (line 140) or failing the
+// first-order test (lines 142-144) and append the survivors to L in
+// (parent, code) order (line 146) with a decoupled-look-back compaction.
+// Candidates (lb <= GUB) are first densified in shared memory so that the
+// divergent first-order test runs on full warps.
 template <class F>
-__global__ void __launch_bounds__(TPB) k_child_lb(Problem P, const double* __restrict__ tab, int tab_stride,
-                                                  long total, const unsigned long long* gub_key,
-                                                  const int32_t* __restrict__ new_slot, Pool out,
-                                                  const uint64_t* out_base, uint64_t* desc,
-                                                  uint32_t* tile_ctr, uint64_t* out_count, long ntiles) {
+__global__ void __launch_bounds__(TPB, 2) k_child_prune(Problem P, const double* __restrict__ tab, int tab_stride,
+                                                        long total, const unsigned long long* gub_key,
+                                                        const double* __restrict__ clb,
+                                                        const int32_t* __restrict__ new_slot, Pool out,
+                                                        const uint64_t* out_base, uint64_t* desc, uint32_t* tile_ctr,
+                                                        uint64_t* out_count, long ntiles) {
   __shared__ uint32_t s_tile;
+  __shared__ uint16_t s_cand[TILE];
+  __shared__ uint8_t s_ok[TILE];
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
   const double gub = okey_inv(*gub_key);
-  const long g0 = (long)tile * TILE + (long)threadIdx.x * IPT;
-  double lbv[IPT], wv[IPT];
+  const long t0 = (long)tile * TILE;
+  const long g0 = t0 + (long)threadIdx.x * IPT;
+  double lbv[IPT];
   uint32_t keep = 0;
 #pragma unroll
   for (int q = 0; q < IPT; ++q) {
     long g = g0 + q;
-    lbv[q] = 0.0;
-    wv[q] = 0.0;
-    if (g < total) {
-      ChildIdx ci = child_of(g, P.kids);
-      if (child_lb<F>(P, tab + (size_t)ci.b * tab_stride, ci.code, gub, lbv[q], wv[q])) keep |= 1u << q;
+    lbv[q] = g < total ? clb[g] : CUDART_INF;
+    if (g < total && lbv[q] <= gub) keep |= 1u << q;
+  }
+  if (P.mono) {
+    uint32_t c1[1] = {(uint32_t)__popc(keep)}, ex[1], tot[1];
+    block_exclusive_scan<1, TPB>(c1, ex, tot);
+    uint32_t pos = ex[0];
+#pragma unroll
+    for (int q = 0; q < IPT; ++q)
+      if (keep & (1u << q)) s_cand[pos++] = (uint16_t)(threadIdx.x * IPT + q);
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < tot[0]; k += TPB) {
+      ChildIdx ci = child_of(t0 + s_cand[k], P.kids);
+      s_ok[k] = child_mono_ok<F>(P, tab + (size_t)ci.b * tab_stride, ci.code) ? 1 : 0;
     }
+    __syncthreads();
+    pos = ex[0];
+    uint32_t k2 = 0;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q)
+      if (keep & (1u << q)) {
+        if (s_ok[pos++]) k2 |= 1u << q;
+      }
+    keep = k2;
   }
   uint32_t cnt[1] = {(uint32_t)__popc(keep)}, ex[1], tot[1];
   block_exclusive_scan<1, TPB>(cnt, ex, tot);
@@ -512,7 +589,7 @@ __global__ void __launch_bounds__(TPB) k_child_lb(Problem P, const double* __res
     if (keep & (1u << q)) {
       ChildIdx ci = child_of(g0 + q, P.kids);
       out.lb[pos] = lbv[q];
-      out.w[pos] = wv[q];
+      out.w[pos] = child_width(P, tab + (size_t)ci.b * tab_stride, ci.code);
       out.slot[pos] = new_slot[ci.b];
       out.code[pos] = ci.code;
       ++pos;
@@ -848,24 +925,25 @@ int launch_prep(const Problem& P, int nb, const int32_t* sel_slot, const uint32_
   return (int)cudaGetLastError();
 }
 
-int launch_child_ub(const Problem& P, const double* tab, int tab_stride, long total,
-                    unsigned long long* gub_key, cudaStream_t st) {
+int launch_child_eval(const Problem& P, const double* tab, int tab_stride, long total,
+                      unsigned long long* gub_key, double* clb, cudaStream_t st) {
   if (total <= 0) return 0;
-  unsigned g = grid_for(total, TPB);
-  IB_DISPATCH_FID(P.fid, k_child_ub<F><<<g, TPB, 0, st>>>(P, tab, tab_stride, total, gub_key));
+  long ngroups = total / P.G;
+  unsigned g = grid_for(ngroups, TPB, 148u * 32u);
+  IB_DISPATCH_FID(P.fid, k_child_eval<F><<<g, TPB, 0, st>>>(P, tab, tab_stride, ngroups, gub_key, clb));
   return (int)cudaGetLastError();
 }
 
-int launch_child_lb(const Problem& P, const double* tab, int tab_stride, long total,
-                    const unsigned long long* gub_key, const int32_t* new_slot, Pool out,
-                    const uint64_t* out_base, uint64_t* desc, uint32_t* tile_ctr, uint64_t* out_count,
-                    cudaStream_t st) {
+int launch_child_prune(const Problem& P, const double* tab, int tab_stride, long total,
+                       const unsigned long long* gub_key, const double* clb, const int32_t* new_slot, Pool out,
+                       const uint64_t* out_base, uint64_t* desc, uint32_t* tile_ctr, uint64_t* out_count,
+                       cudaStream_t st) {
   long ntiles = (total + TILE - 1) / TILE;
   if (ntiles < 1) ntiles = 1;
   cudaMemsetAsync(desc, 0, sizeof(uint64_t) * (size_t)ntiles, st);
   cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t), st);
-  IB_DISPATCH_FID(P.fid, k_child_lb<F><<<(unsigned)ntiles, TPB, 0, st>>>(
-                             P, tab, tab_stride, total, gub_key, new_slot, out, out_base, desc, tile_ctr,
+  IB_DISPATCH_FID(P.fid, k_child_prune<F><<<(unsigned)ntiles, TPB, 0, st>>>(
+                             P, tab, tab_stride, total, gub_key, clb, new_slot, out, out_base, desc, tile_ctr,
                              out_count, ntiles));
   return (int)cudaGetLastError();
 }

@@ -46,6 +46,7 @@ struct Stats {
 
 struct Problem {
   int fid, n, d, m, kids;  // kids = m^d
+  int h, G;                // a child-eval thread owns G = m^h children
   int ld;                  // archive row stride (doubles)
   int mono;                // apply the first-order test
   const double* l;         // device copies of the bounds

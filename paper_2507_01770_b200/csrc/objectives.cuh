@@ -69,6 +69,22 @@ struct ObjAckley {
     Iv t2 = -iexp(divc(A[1], (double)n));
     return ((t1 + t2) + iv(20.0)) + c_e();
   }
+  // lower / upper endpoint of outer() alone: the same operations as outer()
+  // restricted to the endpoint they feed (bit-identical to outer().lo/.hi)
+  __device__ static double outer_lo(const Iv* A, int n) {
+    double rlo = __dsqrt_rd(fmax(__ddiv_rd(A[0].lo, (double)n), 0.0));
+    double e1 = widen_up<ULPS_EXP>(exp(__dmul_ru(-K::C0_02_LO, rlo)));
+    double t1 = __dmul_rd(-20.0, e1);
+    double t2 = -widen_up<ULPS_EXP>(exp(__ddiv_ru(A[1].hi, (double)n)));
+    return __dadd_rd(__dadd_rd(__dadd_rd(t1, t2), 20.0), K::E_LO);
+  }
+  __device__ static double outer_hi(const Iv* A, int n) {
+    double rhi = __dsqrt_ru(fmax(__ddiv_ru(A[0].hi, (double)n), 0.0));
+    double e1 = fmax(widen_dn<ULPS_EXP>(exp(__dmul_rd(-K::C0_02_HI, rhi))), 0.0);
+    double t1 = __dmul_ru(-20.0, e1);
+    double t2 = -fmax(widen_dn<ULPS_EXP>(exp(__ddiv_rd(A[1].lo, (double)n))), 0.0);
+    return __dadd_ru(__dadd_ru(__dadd_ru(t1, t2), 20.0), K::E_HI);
+  }
   // d f/d x_i = (0.4/n) e^{-0.02 r} x_i/r + (2 pi/n) e^{A1/n} sin(2 pi x_i)
   struct Ctx {
     Iv r, a, b;
@@ -331,6 +347,27 @@ struct ObjZabinsky {
   }
   __device__ static Iv dsep(Iv, int, int) { return Iv{-CUDART_INF, CUDART_INF}; }
 };
+
+// endpoint-only evaluation of outer(): F::outer_lo / F::outer_hi when the
+// objective provides them (cheaper), else the full interval's endpoint
+template <class F, class = void>
+struct HasOuterLo {
+  static constexpr bool value = false;
+};
+template <class F>
+struct HasOuterLo<F, decltype((void)F::outer_lo)> {
+  static constexpr bool value = true;
+};
+template <class F>
+__device__ __forceinline__ double outer_lo(const Iv* A, int n) {
+  if constexpr (HasOuterLo<F>::value) return F::outer_lo(A, n);
+  else return F::outer(A, n).lo;
+}
+template <class F>
+__device__ __forceinline__ double outer_hi(const Iv* A, int n) {
+  if constexpr (HasOuterLo<F>::value) return F::outer_hi(A, n);
+  else return F::outer(A, n).hi;
+}
 
 template <class F>
 __device__ __forceinline__ Iv acc_ident(int k) {

@@ -19,9 +19,20 @@
 namespace ib {
 int launch_prep(const Problem&, int, const int32_t*, const uint32_t*, const int32_t*, const double*,
                 const double*, const int32_t*, double*, double*, int32_t*, double*, int, cudaStream_t);
-int launch_child_ub(const Problem&, const double*, int, long, unsigned long long*, cudaStream_t);
-int launch_child_lb(const Problem&, const double*, int, long, const unsigned long long*, const int32_t*, Pool,
-                    const uint64_t*, uint64_t*, uint32_t*, uint64_t*, cudaStream_t);
+int launch_child_eval(const Problem&, const double*, int, long, unsigned long long*, double*, cudaStream_t);
+int launch_child_prune(const Problem&, const double*, int, long, const unsigned long long*, const double*,
+                       const int32_t*, Pool, const uint64_t*, uint64_t*, uint32_t*, uint64_t*, cudaStream_t);
+
+// children per child-eval thread: G = m^h <= 8 (h <= d)
+static Problem make_problem(int fid, int n, int d, int m, long kids, int ld, int mono, const double* l,
+                            const double* u) {
+  int h = 0, G = 1;
+  while (h < d && G * m <= 8) {
+    G *= m;
+    ++h;
+  }
+  return Problem{fid, n, d, m, (int)kids, h, G, ld, mono, l, u};
+}
 int launch_pool_stats(Pool, const uint64_t*, long, const unsigned long long*, Stats*, cudaStream_t);
 int launch_radix_hist(Pool, long, const unsigned long long*, int, unsigned long long, unsigned int*,
                       cudaStream_t);
@@ -166,7 +177,7 @@ struct SolveWs {
   Pool pa, pb;
   int32_t *sel_slot, *new_slot, *sc, *free_list;
   uint32_t* sel_code;
-  double *sel_lb, *alo, *ahi, *tab, *l, *u, *root_out;
+  double *sel_lb, *alo, *ahi, *tab, *l, *u, *root_out, *clb;
   uint64_t *desc, *cnt;  // cnt[0] out_count, cnt[1] out_base, cnt[2] gc count
   uint32_t* tile_ctr;
   unsigned long long* gub_key;
@@ -194,6 +205,7 @@ static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
   w.free_list = A.take<int32_t>(o.arch_cap);
   w.mark = A.take<uint8_t>(o.arch_cap);
   w.tab = A.take<double>((size_t)o.bmax * o.tab_stride);
+  w.clb = A.take<double>((size_t)o.bmax * o.kids);
   long tiles = std::max({o.pool_cap, o.bmax * o.kids, o.arch_cap}) / TILE + 2;
   w.desc = A.take<uint64_t>((size_t)tiles * 3);
   w.cnt = A.take<uint64_t>(4);
@@ -282,7 +294,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   SolveWs w;
   size_t need = layout(o, n, A, w);
   if (!ws || ws_bytes < need) return fail(IB_ENOSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
-  Problem P{fid, n, o.d, o.m, (int)o.kids, o.ld, o.mono, w.l, w.u};
+  Problem P = make_problem(fid, n, o.d, o.m, o.kids, o.ld, o.mono, w.l, w.u);
   Prof prof;
   prof.on = opt && opt->profile == 1;
   long nk = 0;  // kernels launched by this call
@@ -419,7 +431,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
         if (free_top < B) return fail(IB_ENOSPACE, "archive full (%ld slots)", o.arch_cap);
       }
       CKL(launch_alloc(w.free_list, free_top, (int)B, w.new_slot, st));
-      nk += 3;  // alloc + prep + child_ub
+      nk += 3;  // alloc + prep + child_eval
       free_top -= B;
       if (K + B * o.kids > o.pool_cap)
         return fail(IB_ENOSPACE, "list L capacity %ld exceeded (%ld kept + %ld children)", o.pool_cap, K,
@@ -430,7 +442,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
                       w.tab, o.tab_stride, st));
       prof.end(0, B, st);
       prof.begin(st);
-      CKL(launch_child_ub(P, w.tab, o.tab_stride, B * o.kids, w.gub_key, st));
+      CKL(launch_child_eval(P, w.tab, o.tab_stride, B * o.kids, w.gub_key, w.clb, st));
       prof.end(1, B * o.kids, st);
     }
     if (xfn) {
@@ -445,10 +457,10 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
     if (!done) {
       // steps 4-5: bound, rule out, insert survivors after the kept records
       k_set_u64<<<1, 1, 0, st>>>(w.cnt + 1, (uint64_t)K);
-      nk += 2;  // set + child_lb
+      nk += 2;  // set + child_prune
       prof.begin(st);
-      CKL(launch_child_lb(P, w.tab, o.tab_stride, B * o.kids, w.gub_key, w.new_slot, w.pb, w.cnt + 1, w.desc,
-                          w.tile_ctr, w.cnt, st));
+      CKL(launch_child_prune(P, w.tab, o.tab_stride, B * o.kids, w.gub_key, w.clb, w.new_slot, w.pb, w.cnt + 1,
+                             w.desc, w.tile_ctr, w.cnt, st));
       prof.end(2, B * o.kids, st);
       std::swap(w.pa, w.pb);
       ++iter;
@@ -562,7 +574,7 @@ int ib_eval_grad(int fid, int n, int64_t nreq, const double* lo, const double* h
 struct BranchWs {
   int32_t *iota, *dst_sc;
   uint32_t* whole;
-  double *dlo, *dhi, *tab;
+  double *dlo, *dhi, *tab, *clb;
   uint64_t *desc, *cnt;
   uint32_t* tile_ctr;
   unsigned long long* gub_key;
@@ -577,6 +589,7 @@ static size_t branch_layout(int n, int d, int m, long nb, Arena& A, BranchWs& w)
   w.dlo = A.take<double>((size_t)nb * ld);
   w.dhi = A.take<double>((size_t)nb * ld);
   w.tab = A.take<double>((size_t)nb * stride);
+  w.clb = A.take<double>((size_t)nb * kids);
   w.desc = A.take<uint64_t>((size_t)(nb * kids / TILE + 2));
   w.cnt = A.take<uint64_t>(2);
   w.tile_ctr = A.take<uint32_t>(1);
@@ -608,7 +621,7 @@ int ib_branch(int fid, int n, int d, int m, int mono, int64_t nb, const double* 
   size_t need = branch_layout(n, d, m, (long)nb, A, w);
   if (!ws || ws_bytes < need) return fail(IB_ENOSPACE, "ib_branch workspace %zu < %zu", ws_bytes, need);
   int ldi = (n + 1) & ~1;
-  Problem P{fid, n, d, m, (int)kids, ldi, mono ? 1 : 0, l, u};
+  Problem P = make_problem(fid, n, d, m, kids, ldi, mono ? 1 : 0, l, u);
   k_iota32<<<blocks_for(nb), 256, 0, st>>>(w.iota, nb, 0);
   k_fill_u32<<<blocks_for(nb), 256, 0, st>>>(w.whole, nb, CODE_WHOLE);
   k_gub_to_key<<<1, 1, 0, st>>>(gub, w.gub_key);
@@ -624,10 +637,10 @@ int ib_branch(int fid, int n, int d, int m, int mono, int64_t nb, const double* 
   }
   CKL(launch_prep(P, (int)nb, w.iota, w.whole, w.iota, plo, phi, pcyc, w.dlo, w.dhi, w.dst_sc, w.tab,
                   HDR + d * m * ENT, st));
-  CKL(launch_child_ub(P, w.tab, HDR + d * m * ENT, nb * kids, w.gub_key, st));
+  CKL(launch_child_eval(P, w.tab, HDR + d * m * ENT, nb * kids, w.gub_key, w.clb, st));
   Pool out{out_lb, out_w, out_parent, out_code};
-  CKL(launch_child_lb(P, w.tab, HDR + d * m * ENT, nb * kids, w.gub_key, w.iota, out, w.cnt + 1, w.desc,
-                      w.tile_ctr, (uint64_t*)out_count, st));
+  CKL(launch_child_prune(P, w.tab, HDR + d * m * ENT, nb * kids, w.gub_key, w.clb, w.iota, out, w.cnt + 1,
+                         w.desc, w.tile_ctr, (uint64_t*)out_count, st));
   k_key_to_gub<<<1, 1, 0, st>>>(w.gub_key, gub);
   CK(cudaGetLastError());
   return 0;
