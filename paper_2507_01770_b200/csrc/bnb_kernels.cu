@@ -203,8 +203,8 @@ __global__ void __launch_bounds__(TPB) k_prep(Problem P, int nb, const int32_t* 
         Iv X1{dlo[i + 1], dhi[i + 1]};
         double xm1 = midpt(X1.lo, X1.hi);
         LevyVals w = ObjLevy::vals(X1), wm = ObjLevy::vals(Iv{xm1, xm1});
-        r = r + v.u * w.v;
-        rm = rm + vm.u * wm.v;
+        r = r + mulpos(v.u, w.v);
+        rm = rm + mulpos(vm.u, wm.v);
       }
       if (i == n - 1 && !ji) {
         r = r + v.u;
@@ -333,7 +333,7 @@ struct LevyView {
       if (kind == 0)
         a = a + s0(li, mid);
       else if (kind == 1)
-        a = a + u(li, mid) * v(lj, mid);
+        a = a + mulpos(u(li, mid), v(lj, mid));  // u >= 0, v >= 1
       else
         a = a + u(li, mid);
     }
@@ -833,7 +833,7 @@ __global__ void __launch_bounds__(TPB) k_eval_boxes(int n, long nbox, const doub
     for (int i = lane; i < n; i += 32) {
       LevyVals v = ObjLevy::vals(Iv{bl[i], bh[i]});
       if (i == 0) acc[0] = acc[0] + v.s0;
-      if (i <= n - 2) acc[0] = acc[0] + v.u * ObjLevy::vals(Iv{bl[i + 1], bh[i + 1]}).v;
+      if (i <= n - 2) acc[0] = acc[0] + mulpos(v.u, ObjLevy::vals(Iv{bl[i + 1], bh[i + 1]}).v);
       if (i == n - 1) acc[0] = acc[0] + v.u;
     }
     warp_reduce_acc<ObjRastrigin>(acc);

@@ -22,10 +22,21 @@ namespace ib {
 
 enum { SUM = 0, PROD = 1 };
 
-// x_i / r over a box, with |x_i / r| <= s known a priori (R5)
-__device__ __forceinline__ Iv ratio_q(Iv x, Iv r, double s) {
+// x * p for an interval p with p.lo >= 0: exactly the two products Eq. (5)
+// selects (bit-identical to the general operator*, 2 DMUL instead of 8)
+__device__ __forceinline__ Iv mulpos(Iv x, Iv p) {
+  return Iv{x.lo >= 0.0 ? __dmul_rd(x.lo, p.lo) : __dmul_rd(x.lo, p.hi),
+            x.hi >= 0.0 ? __dmul_ru(x.hi, p.hi) : __dmul_ru(x.hi, p.lo)};
+}
+
+// outward reciprocal [1/r.hi, 1/r.lo] of an interval with r.lo > 0
+__device__ __forceinline__ Iv recip_pos(Iv r) { return Iv{__drcp_rd(r.hi), __drcp_ru(r.lo)}; }
+
+// x_i / r over a box, with |x_i / r| <= s known a priori (R5);
+// rinv = recip_pos(r) when r.lo > 0 (x * [1/r] encloses x / r)
+__device__ __forceinline__ Iv ratio_q(Iv x, Iv r, Iv rinv, double s) {
   if (r.lo > 0.0) {
-    Iv q = x / r;
+    Iv q = mulpos(x, rinv);
     return Iv{fmax(q.lo, -s), fmin(q.hi, s)};
   }
   return Iv{x.lo >= 0.0 ? 0.0 : -s, x.hi <= 0.0 ? 0.0 : s};
@@ -87,14 +98,15 @@ struct ObjAckley {
   }
   // d f/d x_i = (0.4/n) e^{-0.02 r} x_i/r + (2 pi/n) e^{A1/n} sin(2 pi x_i)
   struct Ctx {
-    Iv r, a, b;
+    Iv r, rinv, a, b;
     double s;
   };
   __device__ static Ctx ctx(const Iv* A, int n) {
     Ctx c;
     c.r = isqrt(divc(A[0], (double)n));
-    c.a = divc(scale(4.0, c_01()), (double)n) * iexp(-c_002() * c.r);
-    c.b = divc(c_pi_s(2.0), (double)n) * iexp(divc(A[1], (double)n));
+    c.rinv = c.r.lo > 0.0 ? recip_pos(c.r) : Iv{0.0, 0.0};
+    c.a = mulpos(iexp(-c_002() * c.r), divc(scale(4.0, c_01()), (double)n));  // both factors >= 0
+    c.b = mulpos(iexp(divc(A[1], (double)n)), divc(c_pi_s(2.0), (double)n));
     c.s = __dsqrt_ru((double)n);
     return c;
   }
@@ -103,7 +115,7 @@ struct ObjAckley {
     g[1] = isinpi(two_x(x));
   }
   __device__ static Iv dfin(const Ctx& c, const Iv* g, Iv, int, int, const Iv*) {
-    return c.a * ratio_q(g[0], c.r, c.s) + c.b * g[1];
+    return mulpos(ratio_q(g[0], c.r, c.rinv, c.s), c.a) + mulpos(g[1], c.b);
   }
   __device__ static Iv dsep(Iv, int, int) { return Iv{-CUDART_INF, CUDART_INF}; }
 };
@@ -199,7 +211,7 @@ struct ObjGriewank {
   __device__ static int kind(int k) { return k == 0 ? SUM : PROD; }
   __device__ static void terms(Iv x, int i, int, Iv* t) {
     t[0] = sqr(x);
-    t[1] = icos(griewank_kappa(i) * x);
+    t[1] = icos(mulpos(x, griewank_kappa(i)));
   }
   __device__ static Iv outer(const Iv* A, int) { return (iv(1.0) + divc(A[0], 4000.0)) - A[1]; }
   // x_i/2000 + k_i sin(k_i x_i) prod_{j != i} cos(k_j x_j)
@@ -208,7 +220,7 @@ struct ObjGriewank {
   __device__ static void ding(Iv x, int i, int, Iv* g) {
     Iv k = griewank_kappa(i);
     g[0] = divc(x, 2000.0);
-    g[1] = k * isin(k * x);
+    g[1] = mulpos(isin(mulpos(x, k)), k);
   }
   __device__ static Iv dfin(const Ctx&, const Iv* g, Iv, int, int, const Iv* excl) { return g[0] + g[1] * excl[1]; }
   __device__ static Iv dsep(Iv, int, int) { return Iv{-CUDART_INF, CUDART_INF}; }
@@ -239,15 +251,15 @@ struct ObjLevy {
     r.sg = c_pi_s(2.5) * isinpi(two_x(y));
     return r;
   }
-  __device__ static Iv outer(Iv acc, int n) { return divc(c_pi(), (double)n) * acc; }
+  __device__ static Iv outer(Iv acc, int n) { return mulpos(acc, divc(c_pi(), (double)n)); }
   // d f / d x_i (0-based i); uprev = u_{i-1}, vnext = v_{i+1}
   __device__ static Iv deriv(const LevyVals& me, Iv uprev, Iv vnext, int i, int n) {
     Iv acc = iv(0.0);
     if (i == 0) acc = acc + me.sg;
-    if (i < n - 1) acc = acc + me.du * vnext;
-    if (i > 0) acc = acc + uprev * me.sg;
+    if (i < n - 1) acc = acc + mulpos(me.du, vnext);  // v >= 1
+    if (i > 0) acc = acc + mulpos(me.sg, uprev);      // u >= 0
     if (i == n - 1) acc = acc + me.du;
-    return divc(c_pi(), (double)n) * acc;
+    return mulpos(acc, divc(c_pi(), (double)n));
   }
 };
 
@@ -282,16 +294,19 @@ struct ObjSalomon {
   }
   // (2 pi sin(2 pi r) + 0.1) x_i / r, |x_i/r| <= 1
   struct Ctx {
-    Iv r, t;
+    Iv r, rinv, t;
   };
   __device__ static Ctx ctx(const Iv* A, int) {
     Ctx c;
     c.r = isqrt(A[0]);
-    c.t = c_pi_s(2.0) * isinpi(two_x(c.r)) + c_01();
+    c.rinv = c.r.lo > 0.0 ? recip_pos(c.r) : Iv{0.0, 0.0};
+    c.t = mulpos(isinpi(two_x(c.r)), c_pi_s(2.0)) + c_01();
     return c;
   }
   __device__ static void ding(Iv x, int, int, Iv* g) { g[0] = x; }
-  __device__ static Iv dfin(const Ctx& c, const Iv* g, Iv, int, int, const Iv*) { return c.t * ratio_q(g[0], c.r, 1.0); }
+  __device__ static Iv dfin(const Ctx& c, const Iv* g, Iv, int, int, const Iv*) {
+    return c.t * ratio_q(g[0], c.r, c.rinv, 1.0);
+  }
   __device__ static Iv dsep(Iv, int, int) { return Iv{-CUDART_INF, CUDART_INF}; }
 };
 
@@ -307,14 +322,14 @@ struct ObjStyblinski {
     t[1] = icos(x);
   }
   __device__ static Iv outer(const Iv* A, int n) {
-    return divc(A[0], 2.0 * (double)n) - iv(4.0 * (double)n) * A[1];
+    return divc(A[0], 2.0 * (double)n) - mulpos(A[1], iv(4.0 * (double)n));
   }
   // x_i / n + 4 n sin(x_i) prod_{j != i} cos(x_j)
   using Ctx = NoCtx;
   __device__ static Ctx ctx(const Iv*, int) { return {}; }
   __device__ static void ding(Iv x, int, int n, Iv* g) {
     g[0] = divc(x, (double)n);
-    g[1] = iv(4.0 * (double)n) * isin(x);
+    g[1] = mulpos(isin(x), iv(4.0 * (double)n));
   }
   __device__ static Iv dfin(const Ctx&, const Iv* g, Iv, int, int, const Iv* excl) { return g[0] + g[1] * excl[1]; }
   __device__ static Iv dsep(Iv, int, int) { return Iv{-CUDART_INF, CUDART_INF}; }
