@@ -306,8 +306,15 @@ struct ChildIdx {
   int b;
   uint32_t code;
 };
-__device__ __forceinline__ ChildIdx child_of(long g, int kids) {
-  return ChildIdx{(int)(g / kids), (uint32_t)(g % kids)};
+__device__ __forceinline__ ChildIdx child_of(long g, const Problem& P) {
+  if (P.mbits) return ChildIdx{(int)(g >> P.kbits), (uint32_t)g & (uint32_t)(P.kids - 1)};
+  return ChildIdx{(int)(g / P.kids), (uint32_t)(g % P.kids)};
+}
+// piece of split variable j in child `code`
+__device__ __forceinline__ int piece(uint32_t code, int j, const Problem& P) {
+  if (P.mbits) return (int)((code >> (j * P.mbits)) & (uint32_t)(P.m - 1));
+  for (int t = 0; t < j; ++t) code /= (uint32_t)P.m;
+  return (int)(code % (uint32_t)P.m);
 }
 
 // Levy accessors over (split pieces | neighbours)
@@ -341,11 +348,8 @@ struct LevyView {
   }
 };
 
-__device__ __forceinline__ void entries_of(uint32_t code, int d, int m, int* e) {
-  for (int j = 0; j < d; ++j) {
-    e[j] = j * m + (int)(code % (uint32_t)m);
-    code /= (uint32_t)m;
-  }
+__device__ __forceinline__ void entries_of(uint32_t code, const Problem& P, int* e) {
+  for (int j = 0; j < P.d; ++j) e[j] = j * P.m + piece(code, j, P);
 }
 
 // accumulators of the child box (rest combined with the d piece terms)
@@ -354,9 +358,7 @@ __device__ __forceinline__ void child_acc(const Problem& P, const double* __rest
 #pragma unroll
   for (int k = 0; k < F::K; ++k) A[k] = get(T + H_REST + 2 * k);
   for (int j = 0; j < P.d; ++j) {
-    int p = (int)(code % (uint32_t)P.m);
-    code /= (uint32_t)P.m;
-    const double* e = T + HDR + (size_t)(j * P.m + p) * ENT + E_T;
+    const double* e = T + HDR + (size_t)(j * P.m + piece(code, j, P)) * ENT + E_T;
 #pragma unroll
     for (int k = 0; k < F::K; ++k) A[k] = acc_comb<F>(k, A[k], get(e + 2 * k));
   }
@@ -365,9 +367,7 @@ __device__ __forceinline__ void child_acc(const Problem& P, const double* __rest
 __device__ __forceinline__ double child_width(const Problem& P, const double* __restrict__ T, uint32_t code) {
   double w = T[H_WREST];
   for (int j = 0; j < P.d; ++j) {
-    int p = (int)(code % (uint32_t)P.m);
-    code /= (uint32_t)P.m;
-    const double* e = T + HDR + (size_t)(j * P.m + p) * ENT;
+    const double* e = T + HDR + (size_t)(j * P.m + piece(code, j, P)) * ENT;
     w = fmax(w, __dsub_rn(e[E_HI], e[E_LO]));
   }
   return w;
@@ -379,9 +379,9 @@ template <class F>
 __device__ __noinline__ bool child_mono_ok(const Problem& P, const double* __restrict__ T, uint32_t code) {
   const int d = P.d, m = P.m, n = P.n;
   const int c = (int)T[H_CHUNK];
-  int e[D_MAX];
-  entries_of(code, d, m, e);
   if constexpr (F::CHAIN) {
+    int e[D_MAX];
+    entries_of(code, P, e);
     LevyView V{T, e, d};
     LevyChunk q = levy_chunk(c, d, n);
     for (int j = 0; j < d; ++j) {
@@ -401,51 +401,52 @@ __device__ __noinline__ bool child_mono_ok(const Problem& P, const double* __res
     return true;
   } else if constexpr (F::SEP) {
     for (int j = 0; j < d; ++j)
-      if (T[HDR + (size_t)e[j] * ENT + E_T + 4 * F::K + 2 * F::KG] != 0.0) return false;
+      if (T[HDR + (size_t)(j * m + piece(code, j, P)) * ENT + E_T + 4 * F::K + 2 * F::KG] != 0.0) return false;
     return true;
   } else {
     Iv A[2];
-#pragma unroll
-    for (int k = 0; k < F::K; ++k) A[k] = get(T + H_REST + 2 * k);
-    for (int j = 0; j < d; ++j) {
-      const double* ej = T + HDR + (size_t)e[j] * ENT + E_T;
-#pragma unroll
-      for (int k = 0; k < F::K; ++k) A[k] = acc_comb<F>(k, A[k], get(ej + 2 * k));
-    }
+    child_acc<F>(P, T, code, A);
     typename F::Ctx cx = F::ctx(A, n);
-    // products without variable i: running prefix x precomputed suffix
-    Iv suf[F::HASPROD ? D_MAX + 1 : 1][2];
-    Iv pre[2];
     if constexpr (F::HASPROD) {
+      // products without variable i: running prefix x precomputed suffix
+      Iv suf[D_MAX + 1][2];
+      Iv pre[2];
 #pragma unroll
       for (int k = 0; k < F::K; ++k) {
         suf[d][k] = iv(1.0);
         pre[k] = get(T + H_REST + 2 * k);
       }
       for (int j = d - 1; j >= 0; --j) {
-        const double* ej = T + HDR + (size_t)e[j] * ENT + E_T;
+        const double* ej = T + HDR + (size_t)(j * m + piece(code, j, P)) * ENT + E_T;
 #pragma unroll
         for (int k = 0; k < F::K; ++k)
           suf[j][k] = F::kind(k) == PROD ? get(ej + 2 * k) * suf[j + 1][k] : iv(0.0);
       }
-    }
-    for (int j = 0; j < d; ++j) {
-      int i = (c + j) % n;
-      const double* ej = T + HDR + (size_t)e[j] * ENT;
-      Iv g[2], excl[2] = {iv(0.0), iv(0.0)};
+      for (int j = 0; j < d; ++j) {
+        int i = (c + j) % n;
+        const double* ej = T + HDR + (size_t)(j * m + piece(code, j, P)) * ENT;
+        Iv g[2], excl[2];
 #pragma unroll
-      for (int k = 0; k < F::KG; ++k) g[k] = get(ej + E_T + 4 * F::K + 2 * k);
-      if constexpr (F::HASPROD) {
+        for (int k = 0; k < F::KG; ++k) g[k] = get(ej + E_T + 4 * F::K + 2 * k);
 #pragma unroll
         for (int k = 0; k < F::K; ++k) excl[k] = F::kind(k) == PROD ? pre[k] * suf[j + 1][k] : iv(0.0);
-      }
-      Iv X{ej[E_LO], ej[E_HI]};
-      Iv D = F::dfin(cx, g, X, i, n, excl);
-      if ((D.lo > 0.0 && X.lo != P.l[i]) || (D.hi < 0.0 && X.hi != P.u[i])) return false;
-      if constexpr (F::HASPROD) {
+        Iv X{ej[E_LO], ej[E_HI]};
+        Iv D = F::dfin(cx, g, X, i, n, excl);
+        if ((D.lo > 0.0 && X.lo != P.l[i]) || (D.hi < 0.0 && X.hi != P.u[i])) return false;
 #pragma unroll
         for (int k = 0; k < F::K; ++k)
           if (F::kind(k) == PROD) pre[k] = pre[k] * get(ej + E_T + 2 * k);
+      }
+    } else {
+      for (int j = 0; j < d; ++j) {
+        int i = (c + j) % n;
+        const double* ej = T + HDR + (size_t)(j * m + piece(code, j, P)) * ENT;
+        Iv g[2], excl[2] = {iv(0.0), iv(0.0)};
+#pragma unroll
+        for (int k = 0; k < F::KG; ++k) g[k] = get(ej + E_T + 4 * F::K + 2 * k);
+        Iv X{ej[E_LO], ej[E_HI]};
+        Iv D = F::dfin(cx, g, X, i, n, excl);
+        if ((D.lo > 0.0 && X.lo != P.l[i]) || (D.hi < 0.0 && X.hi != P.u[i])) return false;
       }
     }
     return true;
@@ -466,13 +467,13 @@ __global__ void __launch_bounds__(TPB, 4) k_child_eval(Problem P, const double* 
   const long gpp = P.kids / G;
   double best = CUDART_INF;
   for (long gi = (long)blockIdx.x * TPB + threadIdx.x; gi < ngroups; gi += (long)gridDim.x * TPB) {
-    const int b = (int)(gi / gpp);
-    const uint32_t hcode = (uint32_t)(gi % gpp);
+    const int b = P.mbits ? (int)(gi >> (P.kbits - h * P.mbits)) : (int)(gi / gpp);
+    const uint32_t hcode = P.mbits ? (uint32_t)gi & (uint32_t)(gpp - 1) : (uint32_t)(gi % gpp);
     const double* __restrict__ T = tab + (size_t)b * tab_stride;
     if constexpr (F::CHAIN) {
       for (int q = 0; q < G; ++q) {
         int e[D_MAX];
-        entries_of(hcode * (uint32_t)G + (uint32_t)q, d, m, e);
+        entries_of(hcode * (uint32_t)G + (uint32_t)q, P, e);
         LevyView V{T, e, d};
         best = fmin(best, ObjLevy::outer(V.acc(true), n).hi);
         clb[gi * G + q] = canon_lb(ObjLevy::outer(V.acc(false), n).lo);
@@ -484,11 +485,9 @@ __global__ void __launch_bounds__(TPB, 4) k_child_eval(Problem P, const double* 
         A[k] = get(T + H_REST + 2 * k);
         Am[k] = get(T + H_RESTM + 2 * k);
       }
-      uint32_t c = hcode;
+      const uint32_t code0 = hcode * (uint32_t)G;
       for (int j = h; j < d; ++j) {
-        int p = (int)(c % (uint32_t)m);
-        c /= (uint32_t)m;
-        const double* e = T + HDR + (size_t)(j * m + p) * ENT + E_T;
+        const double* e = T + HDR + (size_t)(j * m + piece(code0, j, P)) * ENT + E_T;
 #pragma unroll
         for (int k = 0; k < F::K; ++k) {
           A[k] = acc_comb<F>(k, A[k], get(e + 2 * k));
@@ -502,11 +501,8 @@ __global__ void __launch_bounds__(TPB, 4) k_child_eval(Problem P, const double* 
           B[k] = A[k];
           Bm[k] = Am[k];
         }
-        uint32_t lc = (uint32_t)q;
         for (int j = 0; j < h; ++j) {
-          int p = (int)(lc % (uint32_t)m);
-          lc /= (uint32_t)m;
-          const double* e = T + HDR + (size_t)(j * m + p) * ENT + E_T;
+          const double* e = T + HDR + (size_t)(j * m + piece((uint32_t)q, j, P)) * ENT + E_T;
 #pragma unroll
           for (int k = 0; k < F::K; ++k) {
             B[k] = acc_comb<F>(k, B[k], get(e + 2 * k));
@@ -534,7 +530,7 @@ __global__ void __launch_bounds__(TPB, 4) k_child_eval(Problem P, const double* 
 // Candidates (lb <= GUB) are first densified in shared memory so that the
 // divergent first-order test runs on full warps.
 template <class F>
-__global__ void __launch_bounds__(TPB, 2) k_child_prune(Problem P, const double* __restrict__ tab, int tab_stride,
+__global__ void __launch_bounds__(TPB, 3) k_child_prune(Problem P, const double* __restrict__ tab, int tab_stride,
                                                         long total, const unsigned long long* gub_key,
                                                         const double* __restrict__ clb,
                                                         const int32_t* __restrict__ new_slot, Pool out,
@@ -566,7 +562,7 @@ __global__ void __launch_bounds__(TPB, 2) k_child_prune(Problem P, const double*
       if (keep & (1u << q)) s_cand[pos++] = (uint16_t)(threadIdx.x * IPT + q);
     __syncthreads();
     for (uint32_t k = threadIdx.x; k < tot[0]; k += TPB) {
-      ChildIdx ci = child_of(t0 + s_cand[k], P.kids);
+      ChildIdx ci = child_of(t0 + s_cand[k], P);
       s_ok[k] = child_mono_ok<F>(P, tab + (size_t)ci.b * tab_stride, ci.code) ? 1 : 0;
     }
     __syncthreads();
@@ -587,7 +583,7 @@ __global__ void __launch_bounds__(TPB, 2) k_child_prune(Problem P, const double*
 #pragma unroll
   for (int q = 0; q < IPT; ++q) {
     if (keep & (1u << q)) {
-      ChildIdx ci = child_of(g0 + q, P.kids);
+      ChildIdx ci = child_of(g0 + q, P);
       out.lb[pos] = lbv[q];
       out.w[pos] = child_width(P, tab + (size_t)ci.b * tab_stride, ci.code);
       out.slot[pos] = new_slot[ci.b];

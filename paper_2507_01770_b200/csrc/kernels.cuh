@@ -47,6 +47,8 @@ struct Stats {
 struct Problem {
   int fid, n, d, m, kids;  // kids = m^d
   int h, G;                // a child-eval thread owns G = m^h children
+  int mbits;               // log2(m) when m is a power of two, else 0
+  int kbits;               // log2(m^d) when m is a power of two, else 0
   int ld;                  // archive row stride (doubles)
   int mono;                // apply the first-order test
   const double* l;         // device copies of the bounds

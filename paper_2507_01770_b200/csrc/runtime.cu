@@ -31,7 +31,8 @@ static Problem make_problem(int fid, int n, int d, int m, long kids, int ld, int
     G *= m;
     ++h;
   }
-  return Problem{fid, n, d, m, (int)kids, h, G, ld, mono, l, u};
+  int mbits = (m & (m - 1)) == 0 ? __builtin_ctz((unsigned)m) : 0;
+  return Problem{fid, n, d, m, (int)kids, h, G, mbits, mbits * d, ld, mono, l, u};
 }
 int launch_pool_stats(Pool, const uint64_t*, long, const unsigned long long*, Stats*, cudaStream_t);
 int launch_radix_hist(Pool, long, const unsigned long long*, int, unsigned long long, unsigned int*,
