@@ -157,10 +157,12 @@ static int resolve_opts(int fid, int n, const ib_options* o, int64_t pool_cap_ar
   double kids = std::pow((double)r.m, (double)r.d);
   if (kids > (double)(1 << 24)) return fail(IB_EINVAL, "m^d too large");
   r.kids = (long)kids;
-  r.bmax = o->bmax > 0 ? o->bmax : std::max(1L, (1L << 22) / r.kids);
+  // default batch: ~4M children per iteration, fewer parents for large n
+  // (every unpruned child stays in L)
+  r.bmax = o->bmax > 0 ? o->bmax : std::max(1L, std::min((1L << 22) / r.kids, (1L << 17) / n));
   r.max_iter = o->max_iter > 0 ? o->max_iter : 1000000;
   long pc = o->pool_cap > 0 ? o->pool_cap : pool_cap_arg;
-  if (pc <= 0) pc = std::min(1L << 28, std::max(1L << 20, 8 * r.bmax * r.kids));
+  if (pc <= 0) pc = std::max(1L << 26, 4 * r.bmax * r.kids);
   r.pool_cap = pc;
   r.ld = (n + 1) & ~1;  // even row stride -> 16-byte aligned rows
   long ac = o->arch_cap;

@@ -21,10 +21,13 @@ ap.add_argument("--d", type=int, default=0)
 ap.add_argument("--eps", type=float, default=1e-6)
 a = ap.parse_args()
 for spec in a.runs.split(","):
+    m = a.m
     if ":" in spec:
         p = spec.split(":")
         fid, n = int(p[0]), int(p[1])
-        if len(p) > 2:
+        if len(p) > 4:
+            m = int(p[4])
+        if len(p) > 2 and p[2] != "":
             l, u = np.full(n, float(p[2])), np.full(n, float(p[3]))
         else:
             l, u = workloads.bounds(fid, n)
@@ -34,14 +37,14 @@ for spec in a.runs.split(","):
         fid, n = cfg["fid"], cfg["n"]
         l, u = workloads.config_bounds(cfg)
         name = cfg["name"]
-    o = pb.options(d=a.d or min(n, 10), m=a.m, bmax=a.bmax or None, max_iter=a.max_iter, profile=1)
+    o = pb.options(d=a.d or min(n, 10), m=m, bmax=a.bmax or None, max_iter=a.max_iter, profile=1)
     ws = pb.Workspace(pb.solve_workspace_bytes(fid, n, o))
     ld, ud = torch.tensor(l, device="cuda"), torch.tensor(u, device="cuda")
     t0 = time.time()
     try:
         r = pb.ib_solve_dev(fid, ld, ud, a.eps, a.eps, o, workspace=ws)
         dt = time.time() - t0
-        print(json.dumps({"run": name, "status": r.status, "iters": r.iters, "evals": r.evals, "f_lo": r.f_lo,
+        print(json.dumps({"run": name, "m": m, "status": r.status, "iters": r.iters, "evals": r.evals, "f_lo": r.f_lo,
                           "f_hi": r.f_hi, "n_surv": r.n_surv, "peak_pool": r.peak_pool, "max_width": r.max_width,
                           "wall_s": dt, "kernel_ms": {k: round(v["ms"], 2) for k, v in r.prof.items()}}), flush=True)
     except Exception as e:
