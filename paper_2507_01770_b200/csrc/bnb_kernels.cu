@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "objectives.cuh"
 #include "scan.cuh"
@@ -126,7 +128,7 @@ __device__ __forceinline__ LevyChunk levy_chunk(int c, int d, int n) {
 // src_lo/src_hi with record code sel_code[b]; destination: slot new_slot[b]
 // of dst_lo/dst_hi.  src_sc / dst_sc hold each slot's chunk start.
 template <class F>
-__global__ void __launch_bounds__(TPB) k_prep(Problem P, int nb, const int32_t* __restrict__ sel_slot,
+__global__ void __launch_bounds__(TPB) k_prep(Problem P, const Ctl* __restrict__ ctl, const int32_t* __restrict__ sel_slot,
                                               const uint32_t* __restrict__ sel_code,
                                               const int32_t* __restrict__ new_slot,
                                               const double* __restrict__ src_lo,
@@ -135,7 +137,7 @@ __global__ void __launch_bounds__(TPB) k_prep(Problem P, int nb, const int32_t* 
                                               double* dst_hi, int32_t* dst_sc, double* tab,
                                               int tab_stride) {
   const int b = blockIdx.x;
-  if (b >= nb) return;
+  if (ctl->done || b >= (int)ctl->B) return;
   const int n = P.n, d = P.d, m = P.m;
   const int src = sel_slot[b];
   const uint32_t code = sel_code[b];
@@ -460,11 +462,13 @@ __device__ __noinline__ bool child_mono_ok(const Problem& P, const double* __res
 // one ordered-int atomicMin per block into the incumbent, line 134); lower
 // bounds are stored per child for pass 2.
 template <class F>
-__global__ void __launch_bounds__(TPB, 4) k_child_eval(Problem P, const double* __restrict__ tab, int tab_stride,
-                                                       long ngroups, unsigned long long* gub_key,
+__global__ void __launch_bounds__(TPB, 4) k_child_eval(Problem P, Ctl* __restrict__ ctl,
+                                                       const double* __restrict__ tab, int tab_stride,
                                                        double* __restrict__ clb) {
+  if (ctl->done) return;
   const int d = P.d, m = P.m, n = P.n, h = P.h, G = P.G;
   const long gpp = P.kids / G;
+  const long ngroups = (long)ctl->B * gpp;
   double best = CUDART_INF;
   for (long gi = (long)blockIdx.x * TPB + threadIdx.x; gi < ngroups; gi += (long)gridDim.x * TPB) {
     const int b = P.mbits ? (int)(gi >> (P.kbits - h * P.mbits)) : (int)(gi / gpp);
@@ -520,85 +524,127 @@ __global__ void __launch_bounds__(TPB, 4) k_child_eval(Problem P, const double* 
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < TPB / 32; ++w) best = fmin(best, s_m[w]);
-    if (best < CUDART_INF) atomicMin(gub_key, (unsigned long long)okey(best));
+    if (best < CUDART_INF) atomicMin(&ctl->gub_key, (unsigned long long)okey(best));
   }
 }
 
-// Pass 2: rule out children with lb > GUB (line 140) or failing the
-// first-order test (lines 142-144) and append the survivors to L in
-// (parent, code) order (line 146) with a decoupled-look-back compaction.
-// Candidates (lb <= GUB) are first densified in shared memory so that the
-// divergent first-order test runs on full warps.
-template <class F>
-__global__ void __launch_bounds__(TPB, 3) k_child_prune(Problem P, const double* __restrict__ tab, int tab_stride,
-                                                        long total, const unsigned long long* gub_key,
-                                                        const double* __restrict__ clb,
-                                                        const int32_t* __restrict__ new_slot, Pool out,
-                                                        const uint64_t* out_base, uint64_t* desc, uint32_t* tile_ctr,
-                                                        uint64_t* out_count, long ntiles) {
+// Pass 2a: stable compaction of the candidates (children with lb <= GUB,
+// line 140) into cand[] (decoupled look-back).
+__global__ void __launch_bounds__(TPB) k_cand(const Problem P, Ctl* __restrict__ ctl, const double* __restrict__ clb,
+                                              uint32_t* __restrict__ cand, uint64_t* desc, uint32_t* tile_ctr) {
+  if (ctl->done) return;
   __shared__ uint32_t s_tile;
-  __shared__ uint16_t s_cand[TILE];
-  __shared__ uint8_t s_ok[TILE];
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
-  const double gub = okey_inv(*gub_key);
-  const long t0 = (long)tile * TILE;
-  const long g0 = t0 + (long)threadIdx.x * IPT;
-  double lbv[IPT];
-  uint32_t keep = 0;
+  const long total = (long)ctl->B * P.kids;
+  const long ntiles = (total + TILE - 1) / TILE;
+  if ((long)tile >= ntiles) return;  // tiles past the end: nobody waits on them
+  const double gub = okey_inv(ctl->gub_key);
+  const long g0 = (long)tile * TILE + (long)threadIdx.x * IPT;
+  uint32_t f = 0;
 #pragma unroll
-  for (int q = 0; q < IPT; ++q) {
-    long g = g0 + q;
-    lbv[q] = g < total ? clb[g] : CUDART_INF;
-    if (g < total && lbv[q] <= gub) keep |= 1u << q;
-  }
-  if (P.mono) {
-    uint32_t c1[1] = {(uint32_t)__popc(keep)}, ex[1], tot[1];
-    block_exclusive_scan<1, TPB>(c1, ex, tot);
-    uint32_t pos = ex[0];
-#pragma unroll
-    for (int q = 0; q < IPT; ++q)
-      if (keep & (1u << q)) s_cand[pos++] = (uint16_t)(threadIdx.x * IPT + q);
-    __syncthreads();
-    for (uint32_t k = threadIdx.x; k < tot[0]; k += TPB) {
-      ChildIdx ci = child_of(t0 + s_cand[k], P);
-      s_ok[k] = child_mono_ok<F>(P, tab + (size_t)ci.b * tab_stride, ci.code) ? 1 : 0;
-    }
-    __syncthreads();
-    pos = ex[0];
-    uint32_t k2 = 0;
-#pragma unroll
-    for (int q = 0; q < IPT; ++q)
-      if (keep & (1u << q)) {
-        if (s_ok[pos++]) k2 |= 1u << q;
-      }
-    keep = k2;
-  }
-  uint32_t cnt[1] = {(uint32_t)__popc(keep)}, ex[1], tot[1];
-  block_exclusive_scan<1, TPB>(cnt, ex, tot);
+  for (int q = 0; q < IPT; ++q)
+    if (g0 + q < total && clb[g0 + q] <= gub) f |= 1u << q;
+  uint32_t c1[1] = {(uint32_t)__popc(f)}, ex[1], tot[1];
+  block_exclusive_scan<1, TPB>(c1, ex, tot);
   uint64_t pfx[1];
   dl_lookback<1>(desc, tile, tot, pfx);
-  uint64_t pos = *out_base + pfx[0] + ex[0];
+  uint64_t pos = pfx[0] + ex[0];
+#pragma unroll
+  for (int q = 0; q < IPT; ++q)
+    if (f & (1u << q)) cand[pos++] = (uint32_t)(g0 + q);
+  if ((long)tile == ntiles - 1 && threadIdx.x == 0) ctl->ncand = pfx[0] + tot[0];
+}
+
+// Pass 2b: first-order test (lines 142-144) of every candidate, one thread
+// per candidate on a dense list (no divergence from pruned children).
+template <class F>
+__global__ void __launch_bounds__(TPB, 3) k_mono(Problem P, const Ctl* __restrict__ ctl, const double* __restrict__ tab,
+                                                 int tab_stride, const uint32_t* __restrict__ cand,
+                                                 uint8_t* __restrict__ ok) {
+  if (ctl->done) return;
+  const long nc = (long)ctl->ncand;
+  for (long k = (long)blockIdx.x * TPB + threadIdx.x; k < nc; k += (long)gridDim.x * TPB) {
+    ChildIdx ci = child_of(cand[k], P);
+    ok[k] = (!P.mono || child_mono_ok<F>(P, tab + (size_t)ci.b * tab_stride, ci.code)) ? 1 : 0;
+  }
+}
+
+// Pass 2c: insert the surviving candidates into L after its current end, in
+// (parent, code) order (line 146), stable decoupled-look-back compaction.
+__global__ void __launch_bounds__(TPB) k_emit(const Problem P, Ctl* __restrict__ ctl, const double* __restrict__ tab,
+                                              int tab_stride, const double* __restrict__ clb,
+                                              const uint32_t* __restrict__ cand, const uint8_t* __restrict__ ok,
+                                              const int32_t* __restrict__ new_slot, Pool out, uint64_t* desc,
+                                              uint32_t* tile_ctr) {
+  if (ctl->done) return;
+  __shared__ uint32_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const long nc = (long)ctl->ncand;
+  const long ntiles = (nc + TILE - 1) / TILE;
+  if (nc == 0) {
+    if (tile == 0 && threadIdx.x == 0) ctl->nsurv = 0;
+    return;
+  }
+  if ((long)tile >= ntiles) return;
+  const long k0 = (long)tile * TILE + (long)threadIdx.x * IPT;
+  uint32_t f = 0;
+#pragma unroll
+  for (int q = 0; q < IPT; ++q)
+    if (k0 + q < nc && ok[k0 + q]) f |= 1u << q;
+  uint32_t c1[1] = {(uint32_t)__popc(f)}, ex[1], tot[1];
+  block_exclusive_scan<1, TPB>(c1, ex, tot);
+  uint64_t pfx[1];
+  dl_lookback<1>(desc, tile, tot, pfx);
+  const uint64_t base = ctl->pcount, cap = ctl->pool_cap;
+  uint64_t pos = base + pfx[0] + ex[0];
 #pragma unroll
   for (int q = 0; q < IPT; ++q) {
-    if (keep & (1u << q)) {
-      ChildIdx ci = child_of(g0 + q, P);
-      out.lb[pos] = lbv[q];
-      out.w[pos] = child_width(P, tab + (size_t)ci.b * tab_stride, ci.code);
-      out.slot[pos] = new_slot[ci.b];
-      out.code[pos] = ci.code;
+    if (f & (1u << q)) {
+      if (pos < cap) {
+        uint32_t g = cand[k0 + q];
+        ChildIdx ci = child_of(g, P);
+        out.lb[pos] = clb[g];
+        out.w[pos] = child_width(P, tab + (size_t)ci.b * tab_stride, ci.code);
+        out.slot[pos] = new_slot[ci.b];
+        out.code[pos] = ci.code;
+      }
       ++pos;
     }
   }
-  if (tile == (uint32_t)(ntiles - 1) && threadIdx.x == 0) *out_count = *out_base + pfx[0] + tot[0];
+  if ((long)tile == ntiles - 1 && threadIdx.x == 0) {
+    ctl->nsurv = pfx[0] + tot[0];
+    if (base + pfx[0] + tot[0] > cap) {
+      ctl->err = -2;  // IB_ENOSPACE
+      ctl->done = 4;
+    }
+  }
 }
 
 // ============================================================ list L kernels
-__global__ void __launch_bounds__(TPB) k_pool_stats(Pool p, const uint64_t* cnt_dev,
-                                                    const unsigned long long* gub_key, Stats* st) {
-  const double gub = okey_inv(*gub_key);
-  const long cnt = (long)*cnt_dev;
+// iteration start: zero the statistics and the histogram
+__global__ void k_iter_begin(Ctl* ctl, unsigned int* hist) {
+  if (ctl->done) return;
+  if (threadIdx.x == 0) {
+    ctl->live = 0;
+    ctl->min_lb_key = ~0ull;
+    ctl->max_w_bits = 0;
+  }
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+}
+
+// statistics of the live part of L (lb <= GUB, lines 136 and 148-150) and
+// the histogram of the top 8 bits of the live lower bounds (radix pass 1)
+__global__ void __launch_bounds__(TPB) k_stats(Pool p, Ctl* ctl, unsigned int* hist) {
+  if (ctl->done) return;
+  __shared__ unsigned int s_h[256];
+  for (int i = threadIdx.x; i < 256; i += TPB) s_h[i] = 0;
+  __syncthreads();
+  const double gub = okey_inv(ctl->gub_key);
+  const long cnt = (long)ctl->pcount;
   unsigned long long live = 0, mk = ~0ull;
   double mw = 0.0;
   for (long r = (long)blockIdx.x * TPB + threadIdx.x; r < cnt; r += (long)gridDim.x * TPB) {
@@ -608,6 +654,7 @@ __global__ void __launch_bounds__(TPB) k_pool_stats(Pool p, const uint64_t* cnt_
       unsigned long long k = okey(lb);
       mk = k < mk ? k : mk;
       mw = fmax(mw, p.w[r]);
+      atomicAdd(&s_h[k >> 56], 1u);
     }
   }
   __shared__ unsigned long long s_l[TPB / 32], s_k[TPB / 32];
@@ -631,43 +678,204 @@ __global__ void __launch_bounds__(TPB) k_pool_stats(Pool p, const uint64_t* cnt_
       mk = s_k[w] < mk ? s_k[w] : mk;
       mw = fmax(mw, s_w[w]);
     }
-    if (live) atomicAdd(&st->live, live);
-    atomicMin(&st->min_lb_key, mk);
-    atomicMax(&st->max_w_bits, (unsigned long long)__double_as_longlong(mw));
+    if (live) atomicAdd(&ctl->live, live);
+    atomicMin(&ctl->min_lb_key, mk);
+    atomicMax(&ctl->max_w_bits, (unsigned long long)__double_as_longlong(mw));
+  }
+  for (int i = threadIdx.x; i < 256; i += TPB)
+    if (s_h[i]) atomicAdd(&hist[i], s_h[i]);
+}
+
+// pick the radix digit of the B-th smallest key from hist; zero hist
+__device__ void pick_digit(Ctl* ctl, unsigned int* hist) {
+  unsigned long long need = ctl->need, cum = 0;
+  int dig = 0;
+  for (; dig < 255; ++dig) {
+    if (cum + hist[dig] >= need) break;
+    cum += hist[dig];
+  }
+  unsigned int cnt = hist[dig];
+  ctl->need = need - cum;
+  ctl->prefix = (ctl->prefix << 8) | (unsigned long long)dig;
+  ctl->known += 8;
+  if (cnt == ctl->need || ctl->known >= 64) ctl->resolved = 1;
+  for (int i = 0; i < 256; ++i) hist[i] = 0;
+}
+
+// stop test (line 148: every region narrower than eps_x; line 150: GUB - GLB
+// <= eps_f) and batch size B = min(live, bmax) (line 130, reading R1)
+__global__ void k_control(Ctl* ctl, unsigned int* hist) {
+  if (ctl->done) return;
+  if (ctl->live == 0) {
+    ctl->done = 3;
+    return;
+  }
+  double glb = okey_inv(ctl->min_lb_key), gub = okey_inv(ctl->gub_key);
+  double maxw = __longlong_as_double((long long)ctl->max_w_bits);
+  if (maxw <= ctl->eps_x && __dsub_ru(gub, glb) <= ctl->eps_f) {
+    ctl->done = 1;
+    return;
+  }
+  if (ctl->iter >= ctl->max_iter) {
+    ctl->done = 2;
+    return;
+  }
+  unsigned long long B = ctl->live < ctl->bmax ? ctl->live : ctl->bmax;
+  ctl->B = B;
+  ctl->known = 0;
+  ctl->prefix = 0;
+  ctl->need = B;
+  ctl->resolved = 1;
+  if (ctl->live > ctl->bmax) {
+    ctl->resolved = 0;
+    pick_digit(ctl, hist);
   }
 }
 
-// histogram of the next 8-bit digit of okey(lb) among live records whose
-// higher digits equal `prefix` (known = number of known high bits)
-__global__ void __launch_bounds__(TPB) k_radix_hist(Pool p, long cnt, const unsigned long long* gub_key,
-                                                    int known, unsigned long long prefix,
-                                                    unsigned int* hist) {
+// radix pass: histogram of the next digit among live records matching prefix
+__global__ void __launch_bounds__(TPB) k_radix(Pool p, const Ctl* __restrict__ ctl, unsigned int* hist) {
+  if (ctl->done || ctl->resolved) return;
   __shared__ unsigned int s_h[256];
   for (int i = threadIdx.x; i < 256; i += TPB) s_h[i] = 0;
   __syncthreads();
-  const double gub = okey_inv(*gub_key);
+  const double gub = okey_inv(ctl->gub_key);
+  const int known = ctl->known;
+  const unsigned long long prefix = ctl->prefix;
   const int shift = 64 - known - 8;
+  const long cnt = (long)ctl->pcount;
   for (long r = (long)blockIdx.x * TPB + threadIdx.x; r < cnt; r += (long)gridDim.x * TPB) {
     double lb = p.lb[r];
     if (!(lb <= gub)) continue;
     unsigned long long k = okey(lb);
-    if (known > 0 && (k >> (64 - known)) != prefix) continue;
+    if ((k >> (64 - known)) != prefix) continue;
     atomicAdd(&s_h[(k >> shift) & 255u], 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 256; i += TPB)
     if (s_h[i]) atomicAdd(&hist[i], s_h[i]);
 }
+__global__ void k_pick(Ctl* ctl, unsigned int* hist) {
+  if (ctl->done || ctl->resolved) return;
+  ctl->sum_radix += ctl->pcount;
+  pick_digit(ctl, hist);
+}
 
-// Stable 3-way partition of L.  Live records (lb <= GUB) whose key's top
+// Selection (line 130): the B live records with the smallest (lb, position)
+// are copied, in list order, to the batch arrays and marked dead in L
+// (lb = +inf).  Kept records stay in place (lazy deletion).
+__global__ void __launch_bounds__(TPB) k_select(Pool p, Ctl* __restrict__ ctl, int32_t* sel_slot, uint32_t* sel_code,
+                                                uint64_t* desc, uint32_t* tile_ctr) {
+  if (ctl->done) return;
+  __shared__ uint32_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const long cnt = (long)ctl->pcount;
+  const long ntiles = (cnt + TILE - 1) / TILE;
+  if ((long)tile >= ntiles) return;
+  const double gub = okey_inv(ctl->gub_key);
+  const int known = ctl->known;
+  const unsigned long long prefix = ctl->prefix;
+  const unsigned long long r_need = ctl->need;
+  const bool all = known == 0;
+  const long r0 = (long)tile * TILE + (long)threadIdx.x * IPT;
+  uint8_t cls[IPT];  // 0 lt (selected), 1 eq (tie class), 2 not selected
+  uint32_t c2[2] = {0, 0};
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    long r = r0 + q;
+    cls[q] = 2;
+    if (r < cnt) {
+      double lb = p.lb[r];
+      if (lb <= gub) {
+        if (all) {
+          cls[q] = 0;
+        } else {
+          unsigned long long top = okey(lb) >> (64 - known);
+          cls[q] = top < prefix ? 0 : (top == prefix ? 1 : 2);
+        }
+        if (cls[q] < 2) c2[cls[q]]++;
+      }
+    }
+  }
+  uint32_t ex[2], tot[2];
+  block_exclusive_scan<2, TPB>(c2, ex, tot);
+  uint64_t pfx[2];
+  dl_lookback<2>(desc, tile, tot, pfx);
+  uint64_t lt = pfx[0] + ex[0], eq = pfx[1] + ex[1];
+#pragma unroll
+  for (int q = 0; q < IPT; ++q) {
+    long r = r0 + q;
+    int k = cls[q];
+    if (k == 2) continue;
+    bool sel;
+    uint64_t pos = 0;
+    if (k == 0) {
+      sel = true;
+      pos = lt + (eq < r_need ? eq : r_need);
+      ++lt;
+    } else {
+      sel = eq < r_need;
+      pos = lt + eq;
+      ++eq;
+    }
+    if (sel) {
+      sel_slot[pos] = p.slot[r];
+      sel_code[pos] = p.code[r];
+      p.lb[r] = CUDART_INF;  // removed from L
+    }
+  }
+}
+
+// archive slots for the B new parents, popped from the free list
+__global__ void k_alloc(Ctl* ctl, const int32_t* free_list, int32_t* new_slot) {
+  if (ctl->done) return;
+  const long B = (long)ctl->B, top = (long)ctl->free_top;
+  if (top < B) {
+    if (threadIdx.x == 0) {
+      ctl->err = -2;  // IB_ENOSPACE: archive full
+      ctl->done = 4;
+    }
+    return;
+  }
+  for (long b = threadIdx.x; b < B; b += blockDim.x) new_slot[b] = free_list[top - 1 - b];
+  __syncthreads();
+  if (threadIdx.x == 0) ctl->free_top = top - B;
+}
+
+// iteration end: the survivors become part of L
+__global__ void k_iter_end(Ctl* ctl, long kids) {
+  if (ctl->done) return;
+  ctl->sum_pool += ctl->pcount;
+  ctl->sum_B += ctl->B;
+  ctl->pcount += ctl->nsurv;
+  ctl->iter += 1;
+  ctl->evals += ctl->B * (unsigned long long)kids;
+}
+
+// multi-GPU exchange of the incumbent (2 doubles: GUB, finished flag)
+__global__ void k_xchg_put(const Ctl* ctl, double* xchg) {
+  xchg[0] = okey_inv(ctl->gub_key);
+  xchg[1] = ctl->done ? 0.0 : -1.0;
+}
+__global__ void k_xchg_take(Ctl* ctl, const double* xchg) {
+  unsigned long long k = okey(xchg[0]);
+  if (k < ctl->gub_key) ctl->gub_key = k;
+  ctl->gdone = xchg[1] == 0.0 ? 1 : 0;
+}
+
+// Stable 3-way partition of L with a host-given selection spec (ib_select,
+// compaction of L, final output).  Live records (lb <= GUB) whose key's top
 // `known` bits are < prefix are selected; those equal to prefix are selected
-// while their rank among equals is < r_need; the rest of the live records are
-// kept.  known == 0 selects every live record.  counters: 0 lt, 1 eq, 2 gt.
+// while their rank among equals is < r_need; the other live records are
+// kept.  known == 0 selects every live record; (known = 64, prefix = 0,
+// r_need = 0) keeps every live record.  counters: 0 lt, 1 eq, 2 gt.
 __global__ void __launch_bounds__(TPB) k_partition(Pool in, long cnt, const unsigned long long* gub_key,
                                                    int known, unsigned long long prefix,
                                                    unsigned long long r_need, int32_t* sel_slot,
                                                    uint32_t* sel_code, double* sel_lb, Pool keep,
-                                                   uint64_t* desc, uint32_t* tile_ctr) {
+                                                   uint64_t* desc, uint32_t* tile_ctr, uint64_t* keep_count,
+                                                   long ntiles) {
   __shared__ uint32_t s_tile;
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   __syncthreads();
@@ -719,9 +927,9 @@ __global__ void __launch_bounds__(TPB) k_partition(Pool in, long cnt, const unsi
       ++gt;
     }
     if (sel) {
-      sel_slot[pos] = in.slot[r];
-      sel_code[pos] = in.code[r];
-      sel_lb[pos] = in.lb[r];
+      if (sel_slot) sel_slot[pos] = in.slot[r];
+      if (sel_code) sel_code[pos] = in.code[r];
+      if (sel_lb) sel_lb[pos] = in.lb[r];
     } else {
       keep.lb[pos] = in.lb[r];
       keep.w[pos] = in.w[r];
@@ -729,16 +937,20 @@ __global__ void __launch_bounds__(TPB) k_partition(Pool in, long cnt, const unsi
       keep.code[pos] = in.code[r];
     }
   }
+  if (tile == (uint32_t)(ntiles - 1) && threadIdx.x == 0 && keep_count) {
+    uint64_t e = pfx[1] + tot[1];
+    *keep_count = pfx[2] + tot[2] + (e > r_need ? e - r_need : 0);
+  }
 }
 
-// ---- archive slot garbage collection (mark from L and the batch, collect)
-__global__ void k_gc_mark(const int32_t* slot, long cnt, uint8_t* mark) {
+// ---- archive slot garbage collection (mark from L, collect the unmarked)
+__global__ void k_gc_mark(const int32_t* slot, const Ctl* ctl, uint8_t* mark) {
+  const long cnt = (long)ctl->pcount;
   for (long r = (long)blockIdx.x * blockDim.x + threadIdx.x; r < cnt; r += (long)gridDim.x * blockDim.x)
     mark[slot[r]] = 1;
 }
 __global__ void __launch_bounds__(TPB) k_gc_collect(const uint8_t* mark, long cap, int32_t* free_list,
-                                                    uint64_t* desc, uint32_t* tile_ctr, uint64_t* out_count,
-                                                    long ntiles) {
+                                                    uint64_t* desc, uint32_t* tile_ctr, Ctl* ctl, long ntiles) {
   __shared__ uint32_t s_tile;
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   __syncthreads();
@@ -756,11 +968,7 @@ __global__ void __launch_bounds__(TPB) k_gc_collect(const uint8_t* mark, long ca
 #pragma unroll
   for (int q = 0; q < IPT; ++q)
     if (f & (1u << q)) free_list[pos++] = (int32_t)(s0 + q);
-  if (tile == (uint32_t)(ntiles - 1) && threadIdx.x == 0) *out_count = pfx[0] + tot[0];
-}
-__global__ void k_alloc(const int32_t* free_list, long top, int nb, int32_t* new_slot) {
-  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x)
-    new_slot[b] = free_list[top - 1 - b];
+  if (tile == (uint32_t)(ntiles - 1) && threadIdx.x == 0) ctl->free_top = pfx[0] + tot[0];
 }
 
 // generic stable compaction of indices with key <= threshold (ib_compact_le)
@@ -910,110 +1118,130 @@ static inline unsigned grid_for(long items, int per_block, unsigned cap = 148u *
   if (g < 1) g = 1;
   return (unsigned)(g < (long)cap ? g : cap);
 }
+static inline long tiles_for(long items) { return std::max(1L, (items + TILE - 1) / TILE); }
 
-int launch_prep(const Problem& P, int nb, const int32_t* sel_slot, const uint32_t* sel_code,
-                const int32_t* new_slot, const double* src_lo, const double* src_hi, const int32_t* src_sc,
-                double* dst_lo, double* dst_hi, int32_t* dst_sc, double* tab, int tab_stride,
-                cudaStream_t st) {
-  if (nb <= 0) return 0;
-  IB_DISPATCH_FID(P.fid, k_prep<F><<<nb, TPB, 0, st>>>(P, nb, sel_slot, sel_code, new_slot, src_lo, src_hi,
-                                                       src_sc, dst_lo, dst_hi, dst_sc, tab, tab_stride));
-  return (int)cudaGetLastError();
+#define LAUNCH_OK return (int)cudaGetLastError()
+
+// One iteration of the hot path, every kernel reading its sizes from ctl.
+// pool_bound / batch_bound: host upper bounds of |L| and B * m^d for grids.
+int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long bmax, cudaStream_t st,
+                     IterHook* hook) {
+  const long kids = P.kids;
+  // statistics + stop test + batch size + radix select (line 130)
+  if (hook) hook->begin(3, pool_bound, st);
+  k_iter_begin<<<1, 256, 0, st>>>(w.ctl, w.hist);
+  k_stats<<<grid_for(pool_bound, TPB, 148u * 8u), TPB, 0, st>>>(w.pool, w.ctl, w.hist);
+  k_control<<<1, 1, 0, st>>>(w.ctl, w.hist);
+  if (hook) hook->end(3, st);
+  if (hook) hook->begin(4, pool_bound, st);
+  for (int pass = 1; pass < 8; ++pass) {
+    k_radix<<<grid_for(pool_bound, TPB * 8, 148u * 4u), TPB, 0, st>>>(w.pool, w.ctl, w.hist);
+    k_pick<<<1, 1, 0, st>>>(w.ctl, w.hist);
+  }
+  if (hook) hook->end(4, st);
+  if (hook) hook->begin(5, pool_bound, st);
+  cudaMemsetAsync(w.desc, 0, sizeof(uint64_t) * 2 * (size_t)tiles_for(pool_bound), st);
+  cudaMemsetAsync(w.tile_ctr, 0, sizeof(uint32_t) * 4, st);
+  k_select<<<(unsigned)tiles_for(pool_bound), TPB, 0, st>>>(w.pool, w.ctl, w.sel_slot, w.sel_code, w.desc,
+                                                             w.tile_ctr);
+  k_alloc<<<1, 256, 0, st>>>(w.ctl, w.free_list, w.new_slot);
+  if (hook) hook->end(5, st);
+  // partition (SPSD) + tables (a2, a3)
+  if (hook) hook->begin(0, bmax, st);
+  IB_DISPATCH_FID(P.fid, k_prep<F><<<(unsigned)bmax, TPB, 0, st>>>(P, w.ctl, w.sel_slot, w.sel_code, w.new_slot,
+                                                                   w.src_lo, w.src_hi, w.src_sc, w.dst_lo,
+                                                                   w.dst_hi, w.dst_sc, w.tab, w.tab_stride));
+  if (hook) hook->end(0, st);
+  // bounds of every child + incumbent (a3, a4)
+  if (hook) hook->begin(1, bmax * kids, st);
+  IB_DISPATCH_FID(P.fid, k_child_eval<F><<<grid_for(bmax * kids / P.G, TPB, 148u * 16u), TPB, 0, st>>>(
+                             P, w.ctl, w.tab, w.tab_stride, w.clb));
+  if (hook) hook->end(1, st);
+  if (hook) hook->exchange(st);
+  // rule out + compact (a5, a6)
+  if (hook) hook->begin(2, bmax * kids, st);
+  cudaMemsetAsync(w.desc, 0, sizeof(uint64_t) * (size_t)tiles_for(bmax * kids), st);
+  cudaMemsetAsync(w.tile_ctr, 0, sizeof(uint32_t) * 4, st);
+  k_cand<<<(unsigned)tiles_for(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
+  IB_DISPATCH_FID(P.fid, k_mono<F><<<grid_for(bmax * kids, TPB, 148u * 12u), TPB, 0, st>>>(
+                             P, w.ctl, w.tab, w.tab_stride, w.cand, w.ok));
+  cudaMemsetAsync(w.desc2, 0, sizeof(uint64_t) * (size_t)tiles_for(bmax * kids), st);
+  k_emit<<<(unsigned)tiles_for(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok,
+                                                            w.new_slot, w.pool, w.desc2, w.tile_ctr + 1);
+  k_iter_end<<<1, 1, 0, st>>>(w.ctl, kids);
+  if (hook) hook->end(2, st);
+  LAUNCH_OK;
 }
 
-int launch_child_eval(const Problem& P, const double* tab, int tab_stride, long total,
-                      unsigned long long* gub_key, double* clb, cudaStream_t st) {
-  if (total <= 0) return 0;
-  long ngroups = total / P.G;
-  unsigned g = grid_for(ngroups, TPB, 148u * 32u);
-  IB_DISPATCH_FID(P.fid, k_child_eval<F><<<g, TPB, 0, st>>>(P, tab, tab_stride, ngroups, gub_key, clb));
-  return (int)cudaGetLastError();
+// steps a2-a6 only, for an explicit batch already in w (ib_branch): the
+// parents are selected, ctl->B = nb, ctl->pcount = 0
+int launch_branch(const Problem& P, const IterBufs& w, long nb, cudaStream_t st) {
+  const long kids = P.kids;
+  IB_DISPATCH_FID(P.fid, k_prep<F><<<(unsigned)nb, TPB, 0, st>>>(P, w.ctl, w.sel_slot, w.sel_code, w.new_slot,
+                                                                 w.src_lo, w.src_hi, w.src_sc, w.dst_lo, w.dst_hi,
+                                                                 w.dst_sc, w.tab, w.tab_stride));
+  IB_DISPATCH_FID(P.fid, k_child_eval<F><<<grid_for(nb * kids / P.G, TPB, 148u * 16u), TPB, 0, st>>>(
+                             P, w.ctl, w.tab, w.tab_stride, w.clb));
+  cudaMemsetAsync(w.desc, 0, sizeof(uint64_t) * (size_t)tiles_for(nb * kids), st);
+  cudaMemsetAsync(w.desc2, 0, sizeof(uint64_t) * (size_t)tiles_for(nb * kids), st);
+  cudaMemsetAsync(w.tile_ctr, 0, sizeof(uint32_t) * 4, st);
+  k_cand<<<(unsigned)tiles_for(nb * kids), TPB, 0, st>>>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
+  IB_DISPATCH_FID(P.fid, k_mono<F><<<grid_for(nb * kids, TPB, 148u * 12u), TPB, 0, st>>>(P, w.ctl, w.tab,
+                                                                                        w.tab_stride, w.cand, w.ok));
+  k_emit<<<(unsigned)tiles_for(nb * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok,
+                                                          w.new_slot, w.pool, w.desc2, w.tile_ctr + 1);
+  LAUNCH_OK;
 }
 
-int launch_child_prune(const Problem& P, const double* tab, int tab_stride, long total,
-                       const unsigned long long* gub_key, const double* clb, const int32_t* new_slot, Pool out,
-                       const uint64_t* out_base, uint64_t* desc, uint32_t* tile_ctr, uint64_t* out_count,
-                       cudaStream_t st) {
-  long ntiles = (total + TILE - 1) / TILE;
-  if (ntiles < 1) ntiles = 1;
-  cudaMemsetAsync(desc, 0, sizeof(uint64_t) * (size_t)ntiles, st);
-  cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t), st);
-  IB_DISPATCH_FID(P.fid, k_child_prune<F><<<(unsigned)ntiles, TPB, 0, st>>>(
-                             P, tab, tab_stride, total, gub_key, clb, new_slot, out, out_base, desc, tile_ctr,
-                             out_count, ntiles));
-  return (int)cudaGetLastError();
+int launch_xchg_put(const Ctl* ctl, double* x, cudaStream_t st) {
+  k_xchg_put<<<1, 1, 0, st>>>(ctl, x);
+  LAUNCH_OK;
+}
+int launch_xchg_take(Ctl* ctl, const double* x, cudaStream_t st) {
+  k_xchg_take<<<1, 1, 0, st>>>(ctl, x);
+  LAUNCH_OK;
 }
 
-__global__ void k_stats_init(Stats* s) {
-  s->live = 0ull;
-  s->min_lb_key = ~0ull;
-  s->max_w_bits = 0ull;
-}
-// cnt_dev: device record count; cnt_bound: host upper bound used for the grid
-int launch_pool_stats(Pool p, const uint64_t* cnt_dev, long cnt_bound, const unsigned long long* gub_key,
-                      Stats* st_dev, cudaStream_t st) {
-  k_stats_init<<<1, 1, 0, st>>>(st_dev);
-  if (cnt_bound > 0)
-    k_pool_stats<<<grid_for(cnt_bound, TPB, 148u * 8u), TPB, 0, st>>>(p, cnt_dev, gub_key, st_dev);
-  return (int)cudaGetLastError();
-}
-
-int launch_radix_hist(Pool p, long cnt, const unsigned long long* gub_key, int known,
-                      unsigned long long prefix, unsigned int* hist, cudaStream_t st) {
-  cudaMemsetAsync(hist, 0, 256 * sizeof(unsigned int), st);
-  if (cnt > 0)
-    k_radix_hist<<<grid_for(cnt, TPB * 8, 148u * 4u), TPB, 0, st>>>(p, cnt, gub_key, known, prefix, hist);
-  return (int)cudaGetLastError();
-}
-
-int launch_partition(Pool in, long cnt, const unsigned long long* gub_key, int known,
-                     unsigned long long prefix, unsigned long long r_need, int32_t* sel_slot,
-                     uint32_t* sel_code, double* sel_lb, Pool keep, uint64_t* desc, uint32_t* tile_ctr,
-                     cudaStream_t st) {
-  long ntiles = (cnt + TILE - 1) / TILE;
-  if (ntiles < 1) return 0;
+int launch_partition(Pool in, long cnt, const unsigned long long* gub_key, int known, unsigned long long prefix,
+                     unsigned long long r_need, int32_t* sel_slot, uint32_t* sel_code, double* sel_lb, Pool keep,
+                     uint64_t* desc, uint32_t* tile_ctr, uint64_t* keep_count, cudaStream_t st) {
+  long ntiles = tiles_for(cnt);
   cudaMemsetAsync(desc, 0, sizeof(uint64_t) * 3 * (size_t)ntiles, st);
   cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t), st);
-  k_partition<<<(unsigned)ntiles, TPB, 0, st>>>(in, cnt, gub_key, known, prefix, r_need, sel_slot, sel_code,
-                                                sel_lb, keep, desc, tile_ctr);
-  return (int)cudaGetLastError();
+  k_partition<<<(unsigned)ntiles, TPB, 0, st>>>(in, cnt, gub_key, known, prefix, r_need, sel_slot, sel_code, sel_lb,
+                                                keep, desc, tile_ctr, keep_count, ntiles);
+  LAUNCH_OK;
 }
 
-int launch_gc(const int32_t* pool_slot, long pcnt, const int32_t* batch_slot, long nb, uint8_t* mark,
-              long cap, int32_t* free_list, uint64_t* desc, uint32_t* tile_ctr, uint64_t* out_count,
-              cudaStream_t st) {
+int launch_gc(const int32_t* pool_slot, Ctl* ctl, long pool_bound, uint8_t* mark, long cap, int32_t* free_list,
+              uint64_t* desc, uint32_t* tile_ctr, cudaStream_t st) {
   cudaMemsetAsync(mark, 0, (size_t)cap, st);
-  if (pcnt > 0) k_gc_mark<<<grid_for(pcnt, TPB, 148u * 8u), TPB, 0, st>>>(pool_slot, pcnt, mark);
-  if (nb > 0) k_gc_mark<<<grid_for(nb, TPB, 148u * 8u), TPB, 0, st>>>(batch_slot, nb, mark);
-  long ntiles = (cap + TILE - 1) / TILE;
+  k_gc_mark<<<grid_for(pool_bound, TPB, 148u * 8u), TPB, 0, st>>>(pool_slot, ctl, mark);
+  long ntiles = tiles_for(cap);
   cudaMemsetAsync(desc, 0, sizeof(uint64_t) * (size_t)ntiles, st);
   cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t), st);
-  k_gc_collect<<<(unsigned)ntiles, TPB, 0, st>>>(mark, cap, free_list, desc, tile_ctr, out_count, ntiles);
-  return (int)cudaGetLastError();
-}
-
-int launch_alloc(const int32_t* free_list, long top, int nb, int32_t* new_slot, cudaStream_t st) {
-  if (nb > 0) k_alloc<<<grid_for(nb, TPB), TPB, 0, st>>>(free_list, top, nb, new_slot);
-  return (int)cudaGetLastError();
+  k_gc_collect<<<(unsigned)ntiles, TPB, 0, st>>>(mark, cap, free_list, desc, tile_ctr, ctl, ntiles);
+  LAUNCH_OK;
 }
 
 int launch_compact_le(const double* keys, long cnt, double thr, int64_t* out_idx, uint64_t* desc,
                       uint32_t* tile_ctr, uint64_t* out_count, cudaStream_t st) {
-  long ntiles = (cnt + TILE - 1) / TILE;
-  if (ntiles < 1) {
+  if (cnt <= 0) {
     cudaMemsetAsync(out_count, 0, sizeof(uint64_t), st);
-    return (int)cudaGetLastError();
+    LAUNCH_OK;
   }
+  long ntiles = tiles_for(cnt);
   cudaMemsetAsync(desc, 0, sizeof(uint64_t) * (size_t)ntiles, st);
   cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t), st);
   k_compact_le<<<(unsigned)ntiles, TPB, 0, st>>>(keys, cnt, thr, out_idx, desc, tile_ctr, out_count, ntiles);
-  return (int)cudaGetLastError();
+  LAUNCH_OK;
 }
 
-int launch_extract(const Problem& P, Pool p, long cnt, const double* A_lo, const double* A_hi,
-                   const int32_t* sc, double* out_lo, double* out_hi, double* out_lb, cudaStream_t st) {
-  if (cnt > 0) k_extract<<<grid_for(cnt, 1, 148u * 16u), 128, 0, st>>>(P, p, cnt, A_lo, A_hi, sc, out_lo, out_hi, out_lb);
-  return (int)cudaGetLastError();
+int launch_extract(const Problem& P, Pool p, long cnt, const double* A_lo, const double* A_hi, const int32_t* sc,
+                   double* out_lo, double* out_hi, double* out_lb, cudaStream_t st) {
+  if (cnt > 0)
+    k_extract<<<grid_for(cnt, 1, 148u * 16u), 128, 0, st>>>(P, p, cnt, A_lo, A_hi, sc, out_lo, out_hi, out_lb);
+  LAUNCH_OK;
 }
 
 int launch_eval_boxes(int fid, int n, long nbox, const double* lo, const double* hi, long ld, double* out,
@@ -1021,7 +1249,7 @@ int launch_eval_boxes(int fid, int n, long nbox, const double* lo, const double*
   if (nbox <= 0) return 0;
   unsigned g = (unsigned)((nbox * 32 + TPB - 1) / TPB);
   IB_DISPATCH_FID(fid, k_eval_boxes<F><<<g, TPB, 0, st>>>(n, nbox, lo, hi, ld, out));
-  return (int)cudaGetLastError();
+  LAUNCH_OK;
 }
 
 int launch_eval_grad(int fid, int n, long nreq, const double* lo, const double* hi, long ld,
@@ -1029,7 +1257,22 @@ int launch_eval_grad(int fid, int n, long nreq, const double* lo, const double* 
   if (nreq <= 0) return 0;
   unsigned g = (unsigned)((nreq * 32 + TPB - 1) / TPB);
   IB_DISPATCH_FID(fid, k_eval_grad<F><<<g, TPB, 0, st>>>(n, nreq, lo, hi, ld, req_box, req_dim, out));
-  return (int)cudaGetLastError();
+  LAUNCH_OK;
 }
 
+}  // namespace ib
+
+namespace ib {
+// statistics + control + radix passes of an iteration on an explicit list
+// (ib_select): leaves (known, prefix, need) of the B-th smallest key in ctl
+int launch_select_only(Pool p, Ctl* ctl, unsigned int* hist, long n, cudaStream_t st) {
+  k_iter_begin<<<1, 256, 0, st>>>(ctl, hist);
+  k_stats<<<grid_for(n, TPB, 148u * 8u), TPB, 0, st>>>(p, ctl, hist);
+  k_control<<<1, 1, 0, st>>>(ctl, hist);
+  for (int pass = 1; pass < 8; ++pass) {
+    k_radix<<<grid_for(n, TPB * 8, 148u * 4u), TPB, 0, st>>>(p, ctl, hist);
+    k_pick<<<1, 1, 0, st>>>(ctl, hist);
+  }
+  LAUNCH_OK;
+}
 }  // namespace ib

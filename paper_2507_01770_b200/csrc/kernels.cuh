@@ -1,6 +1,7 @@
 // kernels.cuh -- device data layout shared by the kernels and the host
 // runtime of the branch-and-bound hot path (no torch types anywhere).
 #pragma once
+#include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace ib {
@@ -44,6 +45,34 @@ struct Stats {
   unsigned long long max_w_bits;  // w >= 0: bit pattern order == value order
 };
 
+// Device-resident control block of a solve: every decision of the iteration
+// (stop test, batch size, radix-select digits, counts) is taken on the GPU,
+// so the host only synchronises once per chunk of iterations.  Kernels return
+// immediately once `done` is set.
+struct Ctl {
+  unsigned long long pcount;    // records in L, live and dead (appended order)
+  unsigned long long live;      // records with lb <= GUB (statistics pass)
+  unsigned long long min_lb_key;
+  unsigned long long max_w_bits;
+  unsigned long long gub_key;   // incumbent GUB, ordered-int encoded
+  unsigned long long B;         // regions selected this iteration
+  unsigned long long ncand;     // children with lb <= GUB
+  unsigned long long nsurv;     // children inserted into L
+  unsigned long long free_top;  // archive free list
+  unsigned long long iter, evals;
+  unsigned long long prefix, need;  // radix select state
+  int known, resolved;
+  int done;   // 0 running, 1 converged, 2 iteration limit, 3 L empty, 4 error
+  int err;    // IB_ENOSPACE when a capacity would be exceeded
+  int gdone;  // multi-GPU: every rank finished (from the exchange)
+  int xdone;  // multi-GPU: this rank stopped working (local decision)
+  double eps_f, eps_x;
+  unsigned long long bmax, max_iter, pool_cap;
+  unsigned long long sum_pool;   // records scanned by the statistics pass
+  unsigned long long sum_radix;  // records scanned by radix passes 2..8
+  unsigned long long sum_B;      // parents prepared
+};
+
 struct Problem {
   int fid, n, d, m, kids;  // kids = m^d
   int h, G;                // a child-eval thread owns G = m^h children
@@ -53,6 +82,36 @@ struct Problem {
   int mono;                // apply the first-order test
   const double* l;         // device copies of the bounds
   const double* u;
+};
+
+// device buffers one iteration reads / writes (all sizes come from Ctl)
+struct IterBufs {
+  Ctl* ctl;
+  unsigned int* hist;
+  Pool pool;
+  int32_t *sel_slot, *new_slot, *free_list;
+  uint32_t* sel_code;
+  const double *src_lo, *src_hi;
+  const int32_t* src_sc;
+  double *dst_lo, *dst_hi;
+  int32_t* dst_sc;
+  double* tab;
+  int tab_stride;
+  double* clb;
+  uint32_t* cand;
+  uint8_t* ok;
+  uint64_t *desc, *desc2;
+  uint32_t* tile_ctr;
+};
+
+// host callbacks around the kernel classes of an iteration: profiling
+// events (class 0 prep, 1 child_eval, 2 prune, 3 statistics, 4 radix,
+// 5 select) and the multi-GPU incumbent exchange
+struct IterHook {
+  virtual void begin(int cls, long units, cudaStream_t st) = 0;
+  virtual void end(int cls, cudaStream_t st) = 0;
+  virtual void exchange(cudaStream_t st) = 0;
+  virtual ~IterHook() {}
 };
 
 }  // namespace ib

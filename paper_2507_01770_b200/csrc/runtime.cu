@@ -1,9 +1,15 @@
-// runtime.cu -- host side of the B200 branch-and-bound: workspace arena,
-// the iteration driver of PAPER.md §3.1 (Fig. 2) and the extern "C" entry
-// points declared in include/ibnb.h.  The host never touches a box: it only
-// reads a 40-byte statistics block per iteration (and the 256-bin histogram
-// when the list L is larger than the batch) to decide the next launch.
+// runtime.cu -- host side of the B200 branch-and-bound: workspace arena, the
+// iteration driver of PAPER.md §3.1 (Fig. 2) and the extern "C" entry points
+// of include/ibnb.h.
+//
+// The host never touches a box and takes no per-iteration decision: every
+// iteration's stop test, batch size and radix-select digits are computed on
+// the GPU (Ctl, kernels.cuh), and iterations after the stop are no-ops.  The
+// host enqueues chunks of iterations (replaying one captured CUDA graph per
+// iteration when possible) and synchronises once per chunk to read the
+// control block, compact L and collect archive slots when needed.
 #include <cuda_runtime.h>
+#include <math_constants.h>
 
 #include <algorithm>
 #include <cmath>
@@ -17,31 +23,14 @@
 #include "kernels.cuh"
 
 namespace ib {
-int launch_prep(const Problem&, int, const int32_t*, const uint32_t*, const int32_t*, const double*,
-                const double*, const int32_t*, double*, double*, int32_t*, double*, int, cudaStream_t);
-int launch_child_eval(const Problem&, const double*, int, long, unsigned long long*, double*, cudaStream_t);
-int launch_child_prune(const Problem&, const double*, int, long, const unsigned long long*, const double*,
-                       const int32_t*, Pool, const uint64_t*, uint64_t*, uint32_t*, uint64_t*, cudaStream_t);
-
-// children per child-eval thread: G = m^h <= 8 (h <= d)
-static Problem make_problem(int fid, int n, int d, int m, long kids, int ld, int mono, const double* l,
-                            const double* u) {
-  int h = 0, G = 1;
-  while (h < d && G * m <= 8) {
-    G *= m;
-    ++h;
-  }
-  int mbits = (m & (m - 1)) == 0 ? __builtin_ctz((unsigned)m) : 0;
-  return Problem{fid, n, d, m, (int)kids, h, G, mbits, mbits * d, ld, mono, l, u};
-}
-int launch_pool_stats(Pool, const uint64_t*, long, const unsigned long long*, Stats*, cudaStream_t);
-int launch_radix_hist(Pool, long, const unsigned long long*, int, unsigned long long, unsigned int*,
-                      cudaStream_t);
-int launch_partition(Pool, long, const unsigned long long*, int, unsigned long long, unsigned long long,
-                     int32_t*, uint32_t*, double*, Pool, uint64_t*, uint32_t*, cudaStream_t);
-int launch_gc(const int32_t*, long, const int32_t*, long, uint8_t*, long, int32_t*, uint64_t*, uint32_t*,
-              uint64_t*, cudaStream_t);
-int launch_alloc(const int32_t*, long, int, int32_t*, cudaStream_t);
+int launch_iteration(const Problem&, const IterBufs&, long, long, cudaStream_t, IterHook*);
+int launch_branch(const Problem&, const IterBufs&, long, cudaStream_t);
+int launch_select_only(Pool, Ctl*, unsigned int*, long, cudaStream_t);
+int launch_xchg_put(const Ctl*, double*, cudaStream_t);
+int launch_xchg_take(Ctl*, const double*, cudaStream_t);
+int launch_partition(Pool, long, const unsigned long long*, int, unsigned long long, unsigned long long, int32_t*,
+                     uint32_t*, double*, Pool, uint64_t*, uint32_t*, uint64_t*, cudaStream_t);
+int launch_gc(const int32_t*, Ctl*, long, uint8_t*, long, int32_t*, uint64_t*, uint32_t*, cudaStream_t);
 int launch_compact_le(const double*, long, double, int64_t*, uint64_t*, uint32_t*, uint64_t*, cudaStream_t);
 int launch_extract(const Problem&, Pool, long, const double*, const double*, const int32_t*, double*, double*,
                    double*, cudaStream_t);
@@ -71,9 +60,28 @@ __device__ __forceinline__ double okey_inv_d(unsigned long long k) {
   unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
   return __longlong_as_double((long long)b);
 }
-__global__ void k_gub_to_key(const double* g, unsigned long long* k) { *k = okey_d(*g); }
-__global__ void k_key_to_gub(const unsigned long long* k, double* g) { *g = okey_inv_d(*k); }
-__global__ void k_set_u64(uint64_t* p, uint64_t v) { *p = v; }
+// root record of L (line 128) from the root bound computed by ib_eval
+__global__ void k_root(const double* root_out, double w0, Pool p, Ctl* ctl) {
+  double lb = root_out[0];
+  lb = lb != lb ? -CUDART_INF : (lb == 0.0 ? 0.0 : lb);
+  p.lb[0] = lb;
+  p.w[0] = w0;
+  p.slot[0] = 0;
+  p.code[0] = CODE_WHOLE;
+  ctl->pcount = 1;
+}
+__global__ void k_set_pcount(Ctl* ctl, const uint64_t* c) { ctl->pcount = *c; }
+__global__ void k_branch_ctl(Ctl* ctl, const double* gub, long nb, long cap) {
+  unsigned long long* z = reinterpret_cast<unsigned long long*>(ctl);
+  for (size_t i = 0; i < sizeof(Ctl) / 8; ++i) z[i] = 0ull;
+  ctl->gub_key = okey_d(*gub);
+  ctl->B = (unsigned long long)nb;
+  ctl->pool_cap = (unsigned long long)cap;
+}
+__global__ void k_branch_out(const Ctl* ctl, double* gub, int64_t* count) {
+  *gub = okey_inv_d(ctl->gub_key);
+  *count = (int64_t)ctl->nsurv;
+}
 
 static unsigned blocks_for(long n) {
   long g = (n + 255) / 256;
@@ -91,14 +99,6 @@ static double okey_inv_h(uint64_t k) {
   std::memcpy(&x, &b, 8);
   return x;
 }
-// a - b rounded upward, via TwoSum (host runs in round-to-nearest)
-static double sub_up(double a, double b) {
-  if (std::isinf(a) || std::isinf(b)) return a - b;
-  volatile double s = a - b;
-  volatile double bb = s - a;
-  volatile double err = (a - (s - bb)) + (-b - bb);
-  return err > 0.0 ? std::nextafter((double)s, INFINITY) : (double)s;
-}
 
 // ------------------------------------------------------------ errors
 static thread_local std::string g_err;
@@ -111,15 +111,15 @@ static int fail(int code, const char* fmt, ...) {
   g_err = buf;
   return code;
 }
-#define CK(x)                                                                       \
-  do {                                                                              \
-    cudaError_t e_ = (x);                                                           \
-    if (e_ != cudaSuccess) return fail((int)e_, "%s: %s", #x, cudaGetErrorString(e_)); \
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) return fail((int)e_, "%s: %s", #x, cudaGetErrorString(e_));     \
   } while (0)
-#define CKL(x)                                                                      \
-  do {                                                                              \
-    int e_ = (x);                                                                   \
-    if (e_ != 0) return fail(e_, "%s: %s", #x, cudaGetErrorString((cudaError_t)e_)); \
+#define CKL(x)                                                                             \
+  do {                                                                                     \
+    int e_ = (x);                                                                          \
+    if (e_ != 0) return fail(e_, "%s: %s", #x, cudaGetErrorString((cudaError_t)e_));       \
   } while (0)
 
 // ------------------------------------------------------------ arena
@@ -158,7 +158,7 @@ static int resolve_opts(int fid, int n, const ib_options* o, int64_t pool_cap_ar
   if (kids > (double)(1 << 24)) return fail(IB_EINVAL, "m^d too large");
   r.kids = (long)kids;
   // default batch: ~4M children per iteration, fewer parents for large n
-  // (every unpruned child stays in L)
+  // (every unpruned child stays in L; reading R1)
   r.bmax = o->bmax > 0 ? o->bmax : std::max(1L, std::min((1L << 22) / r.kids, (1L << 17) / n));
   r.max_iter = o->max_iter > 0 ? o->max_iter : 1000000;
   long pc = o->pool_cap > 0 ? o->pool_cap : pool_cap_arg;
@@ -176,17 +176,30 @@ static int resolve_opts(int fid, int n, const ib_options* o, int64_t pool_cap_ar
   return 0;
 }
 
+// children per child-eval thread: G = m^h <= 8 (h <= d)
+static Problem make_problem(int fid, int n, int d, int m, long kids, int ld, int mono, const double* l,
+                            const double* u) {
+  int h = 0, G = 1;
+  while (h < d && G * m <= 8) {
+    G *= m;
+    ++h;
+  }
+  int mbits = (m & (m - 1)) == 0 ? __builtin_ctz((unsigned)m) : 0;
+  return Problem{fid, n, d, m, (int)kids, h, G, mbits, mbits * d, ld, mono, l, u};
+}
+
+static long tiles_of(long n) { return std::max(1L, (n + TILE - 1) / TILE); }
+
 struct SolveWs {
   Pool pa, pb;
   int32_t *sel_slot, *new_slot, *sc, *free_list;
-  uint32_t* sel_code;
-  double *sel_lb, *alo, *ahi, *tab, *l, *u, *root_out, *clb;
-  uint64_t *desc, *cnt;  // cnt[0] out_count, cnt[1] out_base, cnt[2] gc count
+  uint32_t *sel_code, *cand;
+  uint8_t *ok, *mark;
+  double *alo, *ahi, *tab, *clb, *l, *u, *root_out;
+  uint64_t *desc, *desc2, *cnt;
   uint32_t* tile_ctr;
-  unsigned long long* gub_key;
-  Stats* stats;
+  Ctl* ctl;
   unsigned int* hist;
-  uint8_t* mark;
 };
 
 static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
@@ -198,9 +211,9 @@ static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
   };
   pool(w.pa);
   pool(w.pb);
+  const long kids_tot = o.bmax * o.kids;
   w.sel_slot = A.take<int32_t>(o.bmax);
   w.sel_code = A.take<uint32_t>(o.bmax);
-  w.sel_lb = A.take<double>(o.bmax);
   w.new_slot = A.take<int32_t>(o.bmax);
   w.alo = A.take<double>((size_t)o.arch_cap * o.ld);
   w.ahi = A.take<double>((size_t)o.arch_cap * o.ld);
@@ -208,13 +221,15 @@ static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
   w.free_list = A.take<int32_t>(o.arch_cap);
   w.mark = A.take<uint8_t>(o.arch_cap);
   w.tab = A.take<double>((size_t)o.bmax * o.tab_stride);
-  w.clb = A.take<double>((size_t)o.bmax * o.kids);
-  long tiles = std::max({o.pool_cap, o.bmax * o.kids, o.arch_cap}) / TILE + 2;
+  w.clb = A.take<double>((size_t)kids_tot);
+  w.cand = A.take<uint32_t>((size_t)kids_tot);
+  w.ok = A.take<uint8_t>((size_t)kids_tot);
+  long tiles = tiles_of(std::max({o.pool_cap, kids_tot, o.arch_cap})) + 2;
   w.desc = A.take<uint64_t>((size_t)tiles * 3);
+  w.desc2 = A.take<uint64_t>((size_t)tiles);
   w.cnt = A.take<uint64_t>(4);
   w.tile_ctr = A.take<uint32_t>(4);
-  w.gub_key = A.take<unsigned long long>(1);
-  w.stats = A.take<Stats>(1);
+  w.ctl = A.take<Ctl>(1);
   w.hist = A.take<unsigned int>(256);
   w.l = A.take<double>(n);
   w.u = A.take<double>(n);
@@ -222,17 +237,17 @@ static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
   return A.off + 256;
 }
 
-// per-launch CUDA-event timing of the kernel classes (opt.profile)
+// per-class CUDA-event timing (opt.profile)
 struct Prof {
   bool on = false;
   std::vector<cudaEvent_t> pool;
+  size_t next = 0;
   struct Rec {
     int cls;
-    long units;
     cudaEvent_t a, b;
   };
   std::vector<Rec> recs;
-  size_t next = 0;
+  cudaEvent_t cur[IB_NPROF] = {};
   cudaEvent_t ev() {
     if (next == pool.size()) {
       cudaEvent_t e;
@@ -241,31 +256,24 @@ struct Prof {
     }
     return pool[next++];
   }
-  cudaEvent_t cur_a = nullptr;
-  void begin(cudaStream_t st) {
-    if (!on || recs.size() > 20000) return;
-    cur_a = ev();
-    cudaEventRecord(cur_a, st);
+  void begin(int cls, cudaStream_t st) {
+    if (!on || recs.size() > 60000) return;
+    cur[cls] = ev();
+    cudaEventRecord(cur[cls], st);
   }
-  void end(int cls, long units, cudaStream_t st) {
-    if (!on || !cur_a) return;
+  void end(int cls, cudaStream_t st) {
+    if (!on || !cur[cls]) return;
     cudaEvent_t b = ev();
     cudaEventRecord(b, st);
-    recs.push_back(Rec{cls, units, cur_a, b});
-    cur_a = nullptr;
+    recs.push_back(Rec{cls, cur[cls], b});
+    cur[cls] = nullptr;
   }
   void collect(ib_result* res) {
-    for (int c = 0; c < IB_NPROF; ++c) {
-      res->t_ms[c] = 0.0;
-      res->launches[c] = 0;
-      res->units[c] = 0;
-    }
     for (auto& q : recs) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, q.a, q.b);
       res->t_ms[q.cls] += ms;
       res->launches[q.cls] += 1;
-      res->units[q.cls] += q.units;
     }
   }
   ~Prof() {
@@ -273,19 +281,26 @@ struct Prof {
   }
 };
 
-__global__ void k_xchg_put(const unsigned long long* gub_key, double* xchg, double done) {
-  xchg[0] = okey_inv_d(*gub_key);
-  xchg[1] = done;
-}
-__global__ void k_xchg_take(unsigned long long* gub_key, const double* xchg) {
-  unsigned long long k = okey_d(xchg[0]);
-  if (k < *gub_key) *gub_key = k;
-}
+struct Hook : IterHook {
+  Prof* prof = nullptr;
+  ib_exchange_fn xfn = nullptr;
+  void* xuser = nullptr;
+  double* xchg = nullptr;
+  Ctl* ctl = nullptr;
+  void begin(int cls, long, cudaStream_t st) override { prof->begin(cls, st); }
+  void end(int cls, cudaStream_t st) override { prof->end(cls, st); }
+  void exchange(cudaStream_t st) override {
+    if (!xfn) return;
+    launch_xchg_put(ctl, xchg, st);
+    xfn(xuser);
+    launch_xchg_take(ctl, xchg, st);
+  }
+};
 
 static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, const double* l_host,
                       const double* u_host, double eps_f, double eps_x, const ib_options* opt, void* ws,
                       size_t ws_bytes, ib_result* res, double* so_lo, double* so_hi, double* so_lb,
-                      int64_t surv_cap, bool host_out, cudaStream_t st, ib_exchange_fn xfn, void* xuser,
+                      int64_t surv_cap, bool host_out, cudaStream_t user_st, ib_exchange_fn xfn, void* xuser,
                       double* xchg) {
   Opts o;
   int rc = resolve_opts(fid, n, opt, 0, o);
@@ -300,6 +315,34 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   Problem P = make_problem(fid, n, o.d, o.m, o.kids, o.ld, o.mono, w.l, w.u);
   Prof prof;
   prof.on = opt && opt->profile == 1;
+  const bool use_graph = !prof.on && !xfn;
+  // graph capture needs a non-legacy stream: work on a private stream ordered
+  // after the caller's stream (the call is synchronous)
+  cudaStream_t st = user_st;
+  struct Cleanup {
+    cudaStream_t s = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    cudaGraph_t g = nullptr;
+    Ctl* host = nullptr;
+    ~Cleanup() {
+      if (s) cudaStreamSynchronize(s);
+      if (ge) cudaGraphExecDestroy(ge);
+      if (g) cudaGraphDestroy(g);
+      if (s) cudaStreamDestroy(s);
+      if (host) cudaFreeHost(host);
+    }
+  } cl;
+  if (use_graph) {
+    CK(cudaStreamCreateWithFlags(&cl.s, cudaStreamNonBlocking));
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventRecord(e, user_st));
+    CK(cudaStreamWaitEvent(cl.s, e, 0));
+    cudaEventDestroy(e);
+    st = cl.s;
+  }
+  CK(cudaMallocHost(&cl.host, sizeof(Ctl)));
+  Ctl* hctl = cl.host;
   long nk = 0;  // kernels launched by this call
 
   // bounds and the root region (line 128): archive slot 0, list L = {root}
@@ -322,166 +365,140 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
       return fail(IB_EINVAL, "bounds must be finite with l < u (variable %d)", i);
     w0 = std::max(w0, uh[i] - lh[i]);
   }
+  Ctl& hc = *hctl;
+  std::memset(&hc, 0, sizeof hc);
+  hc.gub_key = okey_h(INFINITY);
+  hc.free_top = (unsigned long long)(o.arch_cap - 1);
+  hc.eps_f = eps_f;
+  hc.eps_x = eps_x;
+  hc.bmax = (unsigned long long)o.bmax;
+  hc.max_iter = (unsigned long long)o.max_iter;
+  hc.pool_cap = (unsigned long long)o.pool_cap;
+  CK(cudaMemcpyAsync(w.ctl, &hc, sizeof hc, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(w.alo, w.l, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(w.ahi, w.u, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemsetAsync(w.sc, 0, sizeof(int32_t), st));
   CKL(launch_eval_boxes(fid, n, 1, w.alo, w.ahi, o.ld, w.root_out, st));
-  nk += 2;  // root bound + free-list iota
+  k_root<<<1, 1, 0, st>>>(w.root_out, w0, w.pa, w.ctl);
   // free list: slots 1 .. arch_cap-1
   k_iota32<<<blocks_for(o.arch_cap - 1), 256, 0, st>>>(w.free_list, o.arch_cap - 1, 1);
-  long free_top = o.arch_cap - 1;
-  double root[2];
-  CK(cudaMemcpyAsync(root, w.root_out, sizeof root, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  double lb0 = root[0] != root[0] ? -INFINITY : (root[0] == 0.0 ? 0.0 : root[0]);
-  uint32_t whole = CODE_WHOLE;
-  int32_t zero = 0;
-  unsigned long long inf_key = okey_h(INFINITY);
-  uint64_t one = 1;
-  CK(cudaMemcpyAsync(w.pa.lb, &lb0, 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(w.pa.w, &w0, 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(w.pa.slot, &zero, 4, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(w.pa.code, &whole, 4, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(w.gub_key, &inf_key, 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(w.cnt, &one, 8, cudaMemcpyHostToDevice, st));
+  nk += 3;
 
-  struct Rb {
-    Stats s;
-    unsigned long long gub_key;
-    uint64_t count;
-    double gdone;
-  } rb;
-  rb.gdone = -1.0;
-  long iter = 0, evals = 0, peak = 1, nx = 0;
-  int status = IB_STATUS_MAX_ITER;
-  double glb = INFINITY, gub = INFINITY, maxw = 0.0;
-  long pbound = 1, pcount = 1, live = 0;
+  IterBufs ib{};
+  ib.ctl = w.ctl;
+  ib.hist = w.hist;
+  ib.sel_slot = w.sel_slot;
+  ib.sel_code = w.sel_code;
+  ib.new_slot = w.new_slot;
+  ib.free_list = w.free_list;
+  ib.src_lo = w.alo;
+  ib.src_hi = w.ahi;
+  ib.src_sc = w.sc;
+  ib.dst_lo = w.alo;
+  ib.dst_hi = w.ahi;
+  ib.dst_sc = w.sc;
+  ib.tab = w.tab;
+  ib.tab_stride = o.tab_stride;
+  ib.clb = w.clb;
+  ib.cand = w.cand;
+  ib.ok = w.ok;
+  ib.desc = w.desc;
+  ib.desc2 = w.desc2;
+  ib.tile_ctr = w.tile_ctr;
+  Hook hook;
+  hook.prof = &prof;
+  hook.xfn = xfn;
+  hook.xuser = xuser;
+  hook.xchg = xchg;
+  hook.ctl = w.ctl;
+  const int kIterKernels = 24;  // kernels per iteration (launch_iteration)
+
+  unsigned long long pcount = 1, free_top = hc.free_top, peak = 1;
+  long chunk = 1, graph_bound = -1;
   for (;;) {
-    // steps 6-7: statistics of the live part of L (lb <= GUB): one sync
-    prof.begin(st);
-    CKL(launch_pool_stats(w.pa, w.cnt, pbound, w.gub_key, w.stats, st));
-    nk += 2;
-    prof.end(3, pbound, st);
-    CK(cudaMemcpyAsync(&rb.s, w.stats, sizeof(Stats), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&rb.gub_key, w.gub_key, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&rb.count, w.cnt, 8, cudaMemcpyDeviceToHost, st));
-    if (xfn) CK(cudaMemcpyAsync(&rb.gdone, xchg + 1, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    pcount = (long)rb.count;
-    peak = std::max(peak, pcount);
-    live = (long)rb.s.live;
-    gub = okey_inv_h(rb.gub_key);
-    glb = live ? okey_inv_h(rb.s.min_lb_key) : INFINITY;
-    std::memcpy(&maxw, &rb.s.max_w_bits, 8);
-    bool done = false;
-    if (live == 0) {
-      status = xfn ? IB_STATUS_EMPTY : IB_EEMPTY;
-      done = true;
-    } else if (maxw <= eps_x && sub_up(gub, glb) <= eps_f) {
-      status = IB_STATUS_CONVERGED;
-      done = true;
-    } else if (iter >= o.max_iter) {
-      status = IB_STATUS_MAX_ITER;
-      done = true;
-    }
-    if (!xfn && done) break;
-    if (xfn && nx > 0 && rb.gdone == 0.0) break;  // every rank finished
-    long B = 0, K = 0;
-    if (!done) {
-      // step 1: select the B smallest (lb, position) live records
-      B = std::min(live, o.bmax);
-      int known = 0;
-      unsigned long long prefix = 0, r_need = 0;
-      if (live > o.bmax) {
-        unsigned long long need = (unsigned long long)B;
-        unsigned int h[256];
-        while (known < 64) {
-          prof.begin(st);
-          CKL(launch_radix_hist(w.pa, pcount, w.gub_key, known, prefix, w.hist, st));
-          nk += 1;
-          prof.end(4, pcount, st);
-          CK(cudaMemcpyAsync(h, w.hist, sizeof h, cudaMemcpyDeviceToHost, st));
-          CK(cudaStreamSynchronize(st));
-          unsigned long long cum = 0;
-          int dig = 0;
-          for (; dig < 256; ++dig) {
-            if (cum + h[dig] >= need) break;
-            cum += h[dig];
-          }
-          if (dig == 256) return fail(IB_EINVAL, "radix select inconsistent");
-          need -= cum;
-          prefix = (prefix << 8) | (unsigned long long)dig;
-          known += 8;
-          if (h[dig] == need) break;
-        }
-        r_need = need;
-      }
-      K = live - B;
-      prof.begin(st);
-      CKL(launch_partition(w.pa, pcount, w.gub_key, known, prefix, r_need, w.sel_slot, w.sel_code, w.sel_lb,
-                           w.pb, w.desc, w.tile_ctr, st));
-      nk += 1;
-      prof.end(5, pcount, st);
-      // archive slots for the B new parents (mark-and-collect when short)
-      if (free_top < B) {
-        CKL(launch_gc(w.pb.slot, K, w.sel_slot, B, w.mark, o.arch_cap, w.free_list, w.desc, w.tile_ctr,
-                      w.cnt + 2, st));
-        nk += 3;
-        uint64_t fc;
-        CK(cudaMemcpyAsync(&fc, w.cnt + 2, 8, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        free_top = (long)fc;
-        if (free_top < B) return fail(IB_ENOSPACE, "archive full (%ld slots)", o.arch_cap);
-      }
-      CKL(launch_alloc(w.free_list, free_top, (int)B, w.new_slot, st));
-      nk += 3;  // alloc + prep + child_eval
-      free_top -= B;
-      if (K + B * o.kids > o.pool_cap)
-        return fail(IB_ENOSPACE, "list L capacity %ld exceeded (%ld kept + %ld children)", o.pool_cap, K,
-                    B * o.kids);
-      // steps 2-3: partition (SPSD) and midpoint sampling -> GUB
-      prof.begin(st);
-      CKL(launch_prep(P, (int)B, w.sel_slot, w.sel_code, w.new_slot, w.alo, w.ahi, w.sc, w.alo, w.ahi, w.sc,
-                      w.tab, o.tab_stride, st));
-      prof.end(0, B, st);
-      prof.begin(st);
-      CKL(launch_child_eval(P, w.tab, o.tab_stride, B * o.kids, w.gub_key, w.clb, st));
-      prof.end(1, B * o.kids, st);
-    }
-    if (xfn) {
-      // multi-GPU: GUB <- min over ranks (line 134 across the partition)
-      k_xchg_put<<<1, 1, 0, st>>>(w.gub_key, xchg, done ? 0.0 : -1.0);
+    const long per_it = o.bmax * o.kids;
+    // capacity planning for the chunk: compact L / collect archive slots
+    if ((long)pcount + chunk * per_it > o.pool_cap) {
+      // compact L: keep the live records (lb <= GUB), list order preserved
+      CKL(launch_partition(w.pa, (long)pcount, &w.ctl->gub_key, 64, 0ull, 0ull, nullptr, nullptr, nullptr, w.pb,
+                           w.desc, w.tile_ctr, w.cnt, st));
+      k_set_pcount<<<1, 1, 0, st>>>(w.ctl, w.cnt);
       nk += 2;
-      xfn(xuser);
-      ++nx;
-      k_xchg_take<<<1, 1, 0, st>>>(w.gub_key, xchg);
-      CK(cudaGetLastError());
-    }
-    if (!done) {
-      // steps 4-5: bound, rule out, insert survivors after the kept records
-      k_set_u64<<<1, 1, 0, st>>>(w.cnt + 1, (uint64_t)K);
-      nk += 2;  // set + child_prune
-      prof.begin(st);
-      CKL(launch_child_prune(P, w.tab, o.tab_stride, B * o.kids, w.gub_key, w.clb, w.new_slot, w.pb, w.cnt + 1,
-                             w.desc, w.tile_ctr, w.cnt, st));
-      prof.end(2, B * o.kids, st);
       std::swap(w.pa, w.pb);
-      ++iter;
-      evals += B * o.kids;
-      pbound = K + B * o.kids;
+      CK(cudaMemcpyAsync(&hc, w.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      pcount = hc.pcount;
+      graph_bound = -1;  // the list buffers swapped
+      if ((long)pcount + per_it > o.pool_cap)
+        return fail(IB_ENOSPACE, "list L capacity %ld exceeded (%llu live + %ld children)", o.pool_cap, pcount,
+                    per_it);
+      chunk = std::max(1L, std::min(chunk, (o.pool_cap - (long)pcount) / per_it));
     }
+    if ((long)free_top < chunk * o.bmax) {
+      CKL(launch_gc(w.pa.slot, w.ctl, (long)pcount, w.mark, o.arch_cap, w.free_list, w.desc, w.tile_ctr, st));
+      nk += 2;
+      CK(cudaMemcpyAsync(&hc, w.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      free_top = hc.free_top;
+      if ((long)free_top < o.bmax) return fail(IB_ENOSPACE, "archive full (%ld slots)", o.arch_cap);
+      chunk = std::max(1L, std::min(chunk, (long)free_top / o.bmax));
+    }
+    ib.pool = w.pa;
+    const long pool_bound = (long)pcount + chunk * per_it;
+    if (use_graph) {
+      // one captured iteration, replayed; re-captured when its grid bound is exceeded
+      if (graph_bound < pool_bound) {
+        if (cl.ge) {
+          cudaGraphExecDestroy(cl.ge);
+          cl.ge = nullptr;
+        }
+        if (cl.g) {
+          cudaGraphDestroy(cl.g);
+          cl.g = nullptr;
+        }
+        graph_bound = std::min(o.pool_cap, std::max(pool_bound, (long)(2 * pcount) + 8 * per_it));
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        int lr = launch_iteration(P, ib, graph_bound, o.bmax, st, nullptr);
+        cudaGraph_t g = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(st, &g);
+        if (lr) return fail(lr, "capture of the iteration failed");
+        CK(ce);
+        cl.g = g;
+        CK(cudaGraphInstantiate(&cl.ge, g, 0));
+      }
+      for (long c = 0; c < chunk; ++c) CK(cudaGraphLaunch(cl.ge, st));
+    } else {
+      for (long c = 0; c < chunk; ++c) CKL(launch_iteration(P, ib, pool_bound, o.bmax, st, &hook));
+    }
+    nk += chunk * kIterKernels;
+    CK(cudaMemcpyAsync(&hc, w.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    pcount = hc.pcount;
+    free_top = hc.free_top;
+    peak = std::max(peak, pcount);
+    if (hc.err) return fail(hc.err, "capacity exceeded on the device (L %ld, archive %ld)", o.pool_cap, o.arch_cap);
+    if (xfn ? hc.gdone : hc.done) break;
+    chunk = std::min(chunk * 2, 32L);
   }
-  if (status == IB_EEMPTY) return fail(IB_EEMPTY, "list L became empty after %ld iterations", iter);
+  const Ctl c = hc;
+  int status;
+  switch (c.done) {
+    case 1: status = IB_STATUS_CONVERGED; break;
+    case 2: status = IB_STATUS_MAX_ITER; break;
+    default: status = xfn ? IB_STATUS_EMPTY : IB_EEMPTY; break;
+  }
+  if (status == IB_EEMPTY) return fail(IB_EEMPTY, "list L became empty after %llu iterations", c.iter);
   // output (line 150): GLB, GUB and the live regions of L, in list order
-  CKL(launch_partition(w.pa, pcount, w.gub_key, 64, 0ull, 0ull, w.sel_slot, w.sel_code, w.sel_lb, w.pb, w.desc,
-                       w.tile_ctr, st));
+  CKL(launch_partition(w.pa, (long)pcount, &w.ctl->gub_key, 64, 0ull, 0ull, nullptr, nullptr, nullptr, w.pb, w.desc,
+                       w.tile_ctr, w.cnt, st));
   nk += 1;
-  long ncopy = std::min((long)surv_cap, live);
+  const long live = (long)c.live;
+  const long ncopy = std::min((long)surv_cap, live);
   if (so_lo && so_hi && ncopy > 0) {
     if (host_out) {
-      // stage through the (now unused) tables buffer, in chunks
-      long per = std::max(1L, (long)(((size_t)o.bmax * o.tab_stride) / (size_t)(2 * n + 1)));
-      double* tlo = w.tab;
+      // stage through the (unused) child-bound buffer, in chunks
+      long per = std::max(1L, (long)(((size_t)o.bmax * o.kids) / (size_t)(2 * n + 1)));
+      double* tlo = w.clb;
       for (long s = 0; s < ncopy; s += per) {
         long k = std::min(per, ncopy - s);
         double* thi = tlo + (size_t)k * n;
@@ -501,13 +518,19 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   }
   CK(cudaStreamSynchronize(st));
   prof.collect(res);
-  res->f_lo = glb;
-  res->f_hi = gub;
-  res->iters = iter;
-  res->evals = evals;
+  res->units[0] = (int64_t)c.sum_B;
+  res->units[1] = (int64_t)c.evals;
+  res->units[2] = (int64_t)c.evals;
+  res->units[3] = (int64_t)c.sum_pool;
+  res->units[4] = (int64_t)c.sum_radix;
+  res->units[5] = (int64_t)c.sum_pool;
+  res->f_lo = live ? okey_inv_h(c.min_lb_key) : INFINITY;
+  res->f_hi = okey_inv_h(c.gub_key);
+  res->iters = (int64_t)c.iter;
+  res->evals = (int64_t)c.evals;
   res->n_surv = live;
-  res->peak_pool = peak;
-  res->max_width = maxw;
+  res->peak_pool = (int64_t)peak;
+  std::memcpy(&res->max_width, &c.max_w_bits, 8);
   res->status = status;
   res->n_kernels = (int)std::min(nk, (long)INT32_MAX);
   return 0;
@@ -519,7 +542,7 @@ using namespace ib;
 
 extern "C" {
 
-const char* ib_version(void) { return "ibnb 0.1.0 (sm_100a, fp64 directed rounding)"; }
+const char* ib_version(void) { return "ibnb 0.2.0 (sm_100a, fp64 directed rounding, device-driven iteration)"; }
 const char* ib_last_error(void) { return g_err.c_str(); }
 int ib_num_functions(void) { return 11; }
 
@@ -531,32 +554,32 @@ size_t ib_solve_workspace_size(int fid, int n, const ib_options* opt, int64_t po
   return layout(o, n, A, w);
 }
 
-int ib_solve(int fid, int n, const double* l, const double* u, double eps_f, double eps_x,
-             const ib_options* opt, void* ws, size_t ws_bytes, ib_result* res, double* surv_lo,
-             double* surv_hi, double* surv_lb, int64_t surv_cap, void* stream) {
+int ib_solve(int fid, int n, const double* l, const double* u, double eps_f, double eps_x, const ib_options* opt,
+             void* ws, size_t ws_bytes, ib_result* res, double* surv_lo, double* surv_hi, double* surv_lb,
+             int64_t surv_cap, void* stream) {
   if (!l || !u) return fail(IB_EINVAL, "l/u NULL");
   g_err.clear();
-  return solve_impl(fid, n, nullptr, nullptr, l, u, eps_f, eps_x, opt, ws, ws_bytes, res, surv_lo, surv_hi,
-                    surv_lb, surv_cap, true, (cudaStream_t)stream, nullptr, nullptr, nullptr);
+  return solve_impl(fid, n, nullptr, nullptr, l, u, eps_f, eps_x, opt, ws, ws_bytes, res, surv_lo, surv_hi, surv_lb,
+                    surv_cap, true, (cudaStream_t)stream, nullptr, nullptr, nullptr);
 }
 
 int ib_solve_dev(int fid, int n, const double* l_dev, const double* u_dev, double eps_f, double eps_x,
-                 const ib_options* opt, void* ws, size_t ws_bytes, ib_result* res, double* surv_lo,
-                 double* surv_hi, double* surv_lb, int64_t surv_cap, void* stream) {
+                 const ib_options* opt, void* ws, size_t ws_bytes, ib_result* res, double* surv_lo, double* surv_hi,
+                 double* surv_lb, int64_t surv_cap, void* stream) {
   if (!l_dev || !u_dev) return fail(IB_EINVAL, "l/u NULL");
   g_err.clear();
-  return solve_impl(fid, n, l_dev, u_dev, nullptr, nullptr, eps_f, eps_x, opt, ws, ws_bytes, res, surv_lo,
-                    surv_hi, surv_lb, surv_cap, false, (cudaStream_t)stream, nullptr, nullptr, nullptr);
+  return solve_impl(fid, n, l_dev, u_dev, nullptr, nullptr, eps_f, eps_x, opt, ws, ws_bytes, res, surv_lo, surv_hi,
+                    surv_lb, surv_cap, false, (cudaStream_t)stream, nullptr, nullptr, nullptr);
 }
 
 int ib_solve_dev_ex(int fid, int n, const double* l_dev, const double* u_dev, double eps_f, double eps_x,
                     const ib_options* opt, void* ws, size_t ws_bytes, ib_result* res, double* surv_lo,
-                    double* surv_hi, double* surv_lb, int64_t surv_cap, void* stream, ib_exchange_fn fn,
-                    void* user, double* xchg) {
+                    double* surv_hi, double* surv_lb, int64_t surv_cap, void* stream, ib_exchange_fn fn, void* user,
+                    double* xchg) {
   if (!l_dev || !u_dev) return fail(IB_EINVAL, "l/u NULL");
   g_err.clear();
-  return solve_impl(fid, n, l_dev, u_dev, nullptr, nullptr, eps_f, eps_x, opt, ws, ws_bytes, res, surv_lo,
-                    surv_hi, surv_lb, surv_cap, false, (cudaStream_t)stream, fn, user, xchg);
+  return solve_impl(fid, n, l_dev, u_dev, nullptr, nullptr, eps_f, eps_x, opt, ws, ws_bytes, res, surv_lo, surv_hi,
+                    surv_lb, surv_cap, false, (cudaStream_t)stream, fn, user, xchg);
 }
 
 int ib_eval_boxes(int fid, int n, int64_t nbox, const double* lo, const double* hi, int64_t ld, double* out,
@@ -567,8 +590,8 @@ int ib_eval_boxes(int fid, int n, int64_t nbox, const double* lo, const double* 
   return 0;
 }
 
-int ib_eval_grad(int fid, int n, int64_t nreq, const double* lo, const double* hi, int64_t ld,
-                 const int64_t* req_box, const int32_t* req_dim, double* out, void* stream) {
+int ib_eval_grad(int fid, int n, int64_t nreq, const double* lo, const double* hi, int64_t ld, const int64_t* req_box,
+                 const int32_t* req_dim, double* out, void* stream) {
   if (fid < 0 || fid > 10 || n < 1 || nreq < 0 || ld < n) return fail(IB_EINVAL, "ib_eval_grad: bad arguments");
   CKL(launch_eval_grad(fid, n, (long)nreq, lo, hi, (long)ld, req_box, req_dim, out, (cudaStream_t)stream));
   return 0;
@@ -576,11 +599,12 @@ int ib_eval_grad(int fid, int n, int64_t nreq, const double* lo, const double* h
 
 struct BranchWs {
   int32_t *iota, *dst_sc;
-  uint32_t* whole;
+  uint32_t *whole, *cand;
+  uint8_t* ok;
   double *dlo, *dhi, *tab, *clb;
-  uint64_t *desc, *cnt;
+  uint64_t *desc, *desc2;
   uint32_t* tile_ctr;
-  unsigned long long* gub_key;
+  Ctl* ctl;
 };
 static size_t branch_layout(int n, int d, int m, long nb, Arena& A, BranchWs& w) {
   long kids = (long)std::pow((double)m, (double)d);
@@ -593,10 +617,12 @@ static size_t branch_layout(int n, int d, int m, long nb, Arena& A, BranchWs& w)
   w.dhi = A.take<double>((size_t)nb * ld);
   w.tab = A.take<double>((size_t)nb * stride);
   w.clb = A.take<double>((size_t)nb * kids);
-  w.desc = A.take<uint64_t>((size_t)(nb * kids / TILE + 2));
-  w.cnt = A.take<uint64_t>(2);
-  w.tile_ctr = A.take<uint32_t>(1);
-  w.gub_key = A.take<unsigned long long>(1);
+  w.cand = A.take<uint32_t>((size_t)nb * kids);
+  w.ok = A.take<uint8_t>((size_t)nb * kids);
+  w.desc = A.take<uint64_t>((size_t)tiles_of(nb * kids) + 2);
+  w.desc2 = A.take<uint64_t>((size_t)tiles_of(nb * kids) + 2);
+  w.tile_ctr = A.take<uint32_t>(4);
+  w.ctl = A.take<Ctl>(1);
   return A.off + 256;
 }
 
@@ -608,10 +634,10 @@ size_t ib_branch_workspace_size(int fid, int n, int d, int m, int64_t nb) {
   return branch_layout(n, d, m, (long)nb, A, w);
 }
 
-int ib_branch(int fid, int n, int d, int m, int mono, int64_t nb, const double* plo, const double* phi,
-              int64_t ld, const int32_t* pcyc, const double* l, const double* u, double* gub, void* ws,
-              size_t ws_bytes, int32_t* out_parent, uint32_t* out_code, double* out_lb, double* out_w,
-              int64_t* out_count, void* stream) {
+int ib_branch(int fid, int n, int d, int m, int mono, int64_t nb, const double* plo, const double* phi, int64_t ld,
+              const int32_t* pcyc, const double* l, const double* u, double* gub, void* ws, size_t ws_bytes,
+              int32_t* out_parent, uint32_t* out_code, double* out_lb, double* out_w, int64_t* out_count,
+              void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (fid < 0 || fid > 10 || n < 1 || d < 1 || d > n || d > D_MAX || m < 2 || m > M_MAX || d * m > DM_MAX ||
       nb < 1 || ld < n)
@@ -627,10 +653,9 @@ int ib_branch(int fid, int n, int d, int m, int mono, int64_t nb, const double* 
   Problem P = make_problem(fid, n, d, m, kids, ldi, mono ? 1 : 0, l, u);
   k_iota32<<<blocks_for(nb), 256, 0, st>>>(w.iota, nb, 0);
   k_fill_u32<<<blocks_for(nb), 256, 0, st>>>(w.whole, nb, CODE_WHOLE);
-  k_gub_to_key<<<1, 1, 0, st>>>(gub, w.gub_key);
-  k_set_u64<<<1, 1, 0, st>>>(w.cnt + 1, 0ull);
+  k_branch_ctl<<<1, 1, 0, st>>>(w.ctl, gub, nb, nb * kids);
   if ((int)ld != ldi) {
-    // copy the parents into our stride first (plain strided copy)
+    // bring the parents to our even row stride first
     CK(cudaMemcpy2DAsync(w.dlo, sizeof(double) * ldi, plo, sizeof(double) * ld, sizeof(double) * n, nb,
                          cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpy2DAsync(w.dhi, sizeof(double) * ldi, phi, sizeof(double) * ld, sizeof(double) * n, nb,
@@ -638,13 +663,28 @@ int ib_branch(int fid, int n, int d, int m, int mono, int64_t nb, const double* 
     plo = w.dlo;
     phi = w.dhi;
   }
-  CKL(launch_prep(P, (int)nb, w.iota, w.whole, w.iota, plo, phi, pcyc, w.dlo, w.dhi, w.dst_sc, w.tab,
-                  HDR + d * m * ENT, st));
-  CKL(launch_child_eval(P, w.tab, HDR + d * m * ENT, nb * kids, w.gub_key, w.clb, st));
-  Pool out{out_lb, out_w, out_parent, out_code};
-  CKL(launch_child_prune(P, w.tab, HDR + d * m * ENT, nb * kids, w.gub_key, w.clb, w.iota, out, w.cnt + 1,
-                         w.desc, w.tile_ctr, (uint64_t*)out_count, st));
-  k_key_to_gub<<<1, 1, 0, st>>>(w.gub_key, gub);
+  IterBufs ib{};
+  ib.ctl = w.ctl;
+  ib.pool = Pool{out_lb, out_w, out_parent, out_code};
+  ib.sel_slot = w.iota;
+  ib.sel_code = w.whole;
+  ib.new_slot = w.iota;
+  ib.src_lo = plo;
+  ib.src_hi = phi;
+  ib.src_sc = pcyc;
+  ib.dst_lo = w.dlo;
+  ib.dst_hi = w.dhi;
+  ib.dst_sc = w.dst_sc;
+  ib.tab = w.tab;
+  ib.tab_stride = HDR + d * m * ENT;
+  ib.clb = w.clb;
+  ib.cand = w.cand;
+  ib.ok = w.ok;
+  ib.desc = w.desc;
+  ib.desc2 = w.desc2;
+  ib.tile_ctr = w.tile_ctr;
+  CKL(launch_branch(P, ib, (long)nb, st));
+  k_branch_out<<<1, 1, 0, st>>>(w.ctl, gub, out_count);
   CK(cudaGetLastError());
   return 0;
 }
@@ -662,81 +702,62 @@ int ib_compact_le(const double* keys, int64_t n, double thr, int64_t* out_idx, i
 size_t ib_select_workspace_size(int64_t n) {
   if (n < 0) return 0;
   Arena A{nullptr, 0, 0, true};
-  A.take<double>(n);     // w
-  A.take<int32_t>(n);    // slot (iota)
-  A.take<uint32_t>(n);   // code
-  A.take<double>(n);     // keep lb
-  A.take<double>(n);     // keep w
-  A.take<int32_t>(n);    // keep slot
-  A.take<uint32_t>(n);   // keep code
-  A.take<int32_t>(n);    // sel slot
-  A.take<uint32_t>(n);   // sel code
-  A.take<double>(n);     // sel lb
+  A.take<double>(n);    // w
+  A.take<int32_t>(n);   // slot (iota)
+  A.take<uint32_t>(n);  // code
+  A.take<double>(n);    // keep lb
+  A.take<double>(n);    // keep w
+  A.take<int32_t>(n);   // keep slot
+  A.take<uint32_t>(n);  // keep code
+  A.take<int32_t>(n);   // sel slot
   A.take<uint64_t>((size_t)(n / TILE + 2) * 3);
   A.take<uint32_t>(4);
-  A.take<unsigned long long>(1);
-  A.take<Stats>(1);
+  A.take<Ctl>(1);
   A.take<unsigned int>(256);
+  A.take<uint64_t>(2);
   return A.off + 256;
 }
 
+// selection step alone, with the same device statistics / radix-select
+// kernels as a solve, then a stable partition with the resulting spec
 int ib_select(const double* lb, int64_t n, double gub, int64_t bmax, int64_t* sel_idx, int64_t* keep_idx,
               int64_t* n_sel, int64_t* n_keep, void* ws, size_t ws_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n < 0 || bmax < 1 || !n_sel || !n_keep) return fail(IB_EINVAL, "ib_select: bad arguments");
   if (!ws || ws_bytes < ib_select_workspace_size(n)) return fail(IB_ENOSPACE, "ib_select: workspace too small");
-  Arena A{(char*)ws, 0, ws_bytes, false};
-  Pool in{const_cast<double*>(lb), A.take<double>(n), A.take<int32_t>(n), A.take<uint32_t>(n)};
-  Pool keep{A.take<double>(n), A.take<double>(n), A.take<int32_t>(n), A.take<uint32_t>(n)};
-  int32_t* sel_slot = A.take<int32_t>(n);
-  uint32_t* sel_code = A.take<uint32_t>(n);
-  double* sel_lb = A.take<double>(n);
-  uint64_t* desc = A.take<uint64_t>((size_t)(n / TILE + 2) * 3);
-  uint32_t* tile_ctr = A.take<uint32_t>(4);
-  unsigned long long* gkey = A.take<unsigned long long>(1);
-  Stats* stats = A.take<Stats>(1);
-  unsigned int* hist = A.take<unsigned int>(256);
   if (n == 0) {
     *n_sel = *n_keep = 0;
     return 0;
   }
+  Arena A{(char*)ws, 0, ws_bytes, false};
+  Pool in{const_cast<double*>(lb), A.take<double>(n), A.take<int32_t>(n), A.take<uint32_t>(n)};
+  Pool keep{A.take<double>(n), A.take<double>(n), A.take<int32_t>(n), A.take<uint32_t>(n)};
+  int32_t* sel_slot = A.take<int32_t>(n);
+  uint64_t* desc = A.take<uint64_t>((size_t)(n / TILE + 2) * 3);
+  uint32_t* tile_ctr = A.take<uint32_t>(4);
+  Ctl* ctl = A.take<Ctl>(1);
+  unsigned int* hist = A.take<unsigned int>(256);
+  uint64_t* cnt = A.take<uint64_t>(2);
   k_fill_f64<<<blocks_for(n), 256, 0, st>>>(in.w, n, 0.0);
   k_iota32<<<blocks_for(n), 256, 0, st>>>(in.slot, n, 0);
   k_fill_u32<<<blocks_for(n), 256, 0, st>>>(in.code, n, 0u);
-  unsigned long long gk = okey_h(gub);
-  uint64_t nn = (uint64_t)n;
-  CK(cudaMemcpyAsync(gkey, &gk, 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(tile_ctr + 2, &nn, 8, cudaMemcpyHostToDevice, st));
-  CKL(launch_pool_stats(in, (const uint64_t*)(tile_ctr + 2), (long)n, gkey, stats, st));
-  Stats s;
-  CK(cudaMemcpyAsync(&s, stats, sizeof s, cudaMemcpyDeviceToHost, st));
+  Ctl hc;
+  std::memset(&hc, 0, sizeof hc);
+  hc.pcount = (unsigned long long)n;
+  hc.gub_key = okey_h(gub);
+  hc.eps_f = -1.0;  // never "converged"
+  hc.eps_x = -1.0;
+  hc.bmax = (unsigned long long)bmax;
+  hc.max_iter = ~0ull;
+  hc.pool_cap = (unsigned long long)n;
+  CK(cudaMemcpyAsync(ctl, &hc, sizeof hc, cudaMemcpyHostToDevice, st));
+  CKL(launch_select_only(in, ctl, hist, (long)n, st));
+  CK(cudaMemcpyAsync(&hc, ctl, sizeof hc, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  long live = (long)s.live;
+  long live = (long)hc.live;
   long B = std::min(live, (long)bmax);
-  int known = 0;
-  unsigned long long prefix = 0, r_need = 0;
-  if (live > bmax) {
-    unsigned long long need = (unsigned long long)B;
-    unsigned int h[256];
-    while (known < 64) {
-      CKL(launch_radix_hist(in, (long)n, gkey, known, prefix, hist, st));
-      CK(cudaMemcpyAsync(h, hist, sizeof h, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      unsigned long long cum = 0;
-      int dig = 0;
-      for (; dig < 256; ++dig) {
-        if (cum + h[dig] >= need) break;
-        cum += h[dig];
-      }
-      need -= cum;
-      prefix = (prefix << 8) | (unsigned long long)dig;
-      known += 8;
-      if (h[dig] == need) break;
-    }
-    r_need = need;
-  }
-  CKL(launch_partition(in, (long)n, gkey, known, prefix, r_need, sel_slot, sel_code, sel_lb, keep, desc, tile_ctr,
-                       st));
+  CKL(launch_partition(in, (long)n, &ctl->gub_key, hc.known, hc.prefix, hc.known == 0 ? 0ull : hc.need, sel_slot,
+                       nullptr, nullptr, keep, desc, tile_ctr, cnt, st));
   if (B > 0) k_i32_to_i64<<<blocks_for(B), 256, 0, st>>>(sel_slot, B, sel_idx);
   if (live - B > 0) k_i32_to_i64<<<blocks_for(live - B), 256, 0, st>>>(keep.slot, live - B, keep_idx);
   CK(cudaStreamSynchronize(st));
