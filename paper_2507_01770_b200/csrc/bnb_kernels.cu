@@ -534,12 +534,14 @@ __global__ void __launch_bounds__(TPB) k_cand(const Problem P, Ctl* __restrict__
                                               uint32_t* __restrict__ cand, uint64_t* desc, uint32_t* tile_ctr) {
   if (ctl->done) return;
   __shared__ uint32_t s_tile;
+  for (;;) {
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
+  __syncthreads();
   const long total = (long)ctl->B * P.kids;
   const long ntiles = (total + TILE - 1) / TILE;
-  if ((long)tile >= ntiles) return;  // tiles past the end: nobody waits on them
+  if ((long)tile >= ntiles) break;  // tiles past the end: nobody waits on them
   const double gub = okey_inv(ctl->gub_key);
   const long g0 = (long)tile * TILE + (long)threadIdx.x * IPT;
   uint32_t f = 0;
@@ -555,6 +557,7 @@ __global__ void __launch_bounds__(TPB) k_cand(const Problem P, Ctl* __restrict__
   for (int q = 0; q < IPT; ++q)
     if (f & (1u << q)) cand[pos++] = (uint32_t)(g0 + q);
   if ((long)tile == ntiles - 1 && threadIdx.x == 0) ctl->ncand = pfx[0] + tot[0];
+  }
 }
 
 // Pass 2b: first-order test (lines 142-144) of every candidate, one thread
@@ -580,16 +583,18 @@ __global__ void __launch_bounds__(TPB) k_emit(const Problem P, Ctl* __restrict__
                                               uint32_t* tile_ctr) {
   if (ctl->done) return;
   __shared__ uint32_t s_tile;
+  for (;;) {
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
+  __syncthreads();
   const long nc = (long)ctl->ncand;
   const long ntiles = (nc + TILE - 1) / TILE;
   if (nc == 0) {
     if (tile == 0 && threadIdx.x == 0) ctl->nsurv = 0;
-    return;
+    break;
   }
-  if ((long)tile >= ntiles) return;
+  if ((long)tile >= ntiles) break;
   const long k0 = (long)tile * TILE + (long)threadIdx.x * IPT;
   uint32_t f = 0;
 #pragma unroll
@@ -621,6 +626,7 @@ __global__ void __launch_bounds__(TPB) k_emit(const Problem P, Ctl* __restrict__
       ctl->err = -2;  // IB_ENOSPACE
       ctl->done = 4;
     }
+  }
   }
 }
 
@@ -767,12 +773,14 @@ __global__ void __launch_bounds__(TPB) k_select(Pool p, Ctl* __restrict__ ctl, i
                                                 uint64_t* desc, uint32_t* tile_ctr) {
   if (ctl->done) return;
   __shared__ uint32_t s_tile;
+  for (;;) {
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
+  __syncthreads();
   const long cnt = (long)ctl->pcount;
   const long ntiles = (cnt + TILE - 1) / TILE;
-  if ((long)tile >= ntiles) return;
+  if ((long)tile >= ntiles) break;
   const double gub = okey_inv(ctl->gub_key);
   const int known = ctl->known;
   const unsigned long long prefix = ctl->prefix;
@@ -824,6 +832,7 @@ __global__ void __launch_bounds__(TPB) k_select(Pool p, Ctl* __restrict__ ctl, i
       sel_code[pos] = p.code[r];
       p.lb[r] = CUDART_INF;  // removed from L
     }
+  }
   }
 }
 
@@ -877,9 +886,12 @@ __global__ void __launch_bounds__(TPB) k_partition(Pool in, long cnt, const unsi
                                                    uint64_t* desc, uint32_t* tile_ctr, uint64_t* keep_count,
                                                    long ntiles) {
   __shared__ uint32_t s_tile;
+  for (;;) {
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
+  __syncthreads();
+  if ((long)tile >= ntiles) break;
   const double gub = okey_inv(*gub_key);
   const long r0 = (long)tile * TILE + (long)threadIdx.x * IPT;
   uint8_t cls[IPT];  // 0 lt, 1 eq, 2 gt, 3 drop
@@ -941,6 +953,7 @@ __global__ void __launch_bounds__(TPB) k_partition(Pool in, long cnt, const unsi
     uint64_t e = pfx[1] + tot[1];
     *keep_count = pfx[2] + tot[2] + (e > r_need ? e - r_need : 0);
   }
+  }
 }
 
 // ---- archive slot garbage collection (mark from L, collect the unmarked)
@@ -952,9 +965,12 @@ __global__ void k_gc_mark(const int32_t* slot, const Ctl* ctl, uint8_t* mark) {
 __global__ void __launch_bounds__(TPB) k_gc_collect(const uint8_t* mark, long cap, int32_t* free_list,
                                                     uint64_t* desc, uint32_t* tile_ctr, Ctl* ctl, long ntiles) {
   __shared__ uint32_t s_tile;
+  for (;;) {
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
+  __syncthreads();
+  if ((long)tile >= ntiles) break;
   const long s0 = (long)tile * TILE + (long)threadIdx.x * IPT;
   uint32_t f = 0;
 #pragma unroll
@@ -969,6 +985,7 @@ __global__ void __launch_bounds__(TPB) k_gc_collect(const uint8_t* mark, long ca
   for (int q = 0; q < IPT; ++q)
     if (f & (1u << q)) free_list[pos++] = (int32_t)(s0 + q);
   if (tile == (uint32_t)(ntiles - 1) && threadIdx.x == 0) ctl->free_top = pfx[0] + tot[0];
+  }
 }
 
 // generic stable compaction of indices with key <= threshold (ib_compact_le)
@@ -976,9 +993,12 @@ __global__ void __launch_bounds__(TPB) k_compact_le(const double* keys, long cnt
                                                     uint64_t* desc, uint32_t* tile_ctr, uint64_t* out_count,
                                                     long ntiles) {
   __shared__ uint32_t s_tile;
+  for (;;) {
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
+  __syncthreads();
+  if ((long)tile >= ntiles) break;
   const long s0 = (long)tile * TILE + (long)threadIdx.x * IPT;
   uint32_t f = 0;
 #pragma unroll
@@ -993,6 +1013,7 @@ __global__ void __launch_bounds__(TPB) k_compact_le(const double* keys, long cnt
   for (int q = 0; q < IPT; ++q)
     if (f & (1u << q)) out_idx[pos++] = s0 + q;
   if (tile == (uint32_t)(ntiles - 1) && threadIdx.x == 0) *out_count = pfx[0] + tot[0];
+  }
 }
 
 // materialise records (slot, code) of L into explicit boxes
@@ -1119,6 +1140,8 @@ static inline unsigned grid_for(long items, int per_block, unsigned cap = 148u *
   return (unsigned)(g < (long)cap ? g : cap);
 }
 static inline long tiles_for(long items) { return std::max(1L, (items + TILE - 1) / TILE); }
+// persistent grid for the decoupled-look-back scans: blocks loop over tile tickets
+static inline unsigned scan_grid(long items) { return (unsigned)std::min(tiles_for(items), 148L * 6); }
 
 #define LAUNCH_OK return (int)cudaGetLastError()
 
@@ -1142,7 +1165,7 @@ int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long 
   if (hook) hook->begin(5, pool_bound, st);
   cudaMemsetAsync(w.desc, 0, sizeof(uint64_t) * 2 * (size_t)tiles_for(pool_bound), st);
   cudaMemsetAsync(w.tile_ctr, 0, sizeof(uint32_t) * 4, st);
-  k_select<<<(unsigned)tiles_for(pool_bound), TPB, 0, st>>>(w.pool, w.ctl, w.sel_slot, w.sel_code, w.desc,
+  k_select<<<scan_grid(pool_bound), TPB, 0, st>>>(w.pool, w.ctl, w.sel_slot, w.sel_code, w.desc,
                                                              w.tile_ctr);
   k_alloc<<<1, 256, 0, st>>>(w.ctl, w.free_list, w.new_slot);
   if (hook) hook->end(5, st);
@@ -1162,11 +1185,11 @@ int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long 
   if (hook) hook->begin(2, bmax * kids, st);
   cudaMemsetAsync(w.desc, 0, sizeof(uint64_t) * (size_t)tiles_for(bmax * kids), st);
   cudaMemsetAsync(w.tile_ctr, 0, sizeof(uint32_t) * 4, st);
-  k_cand<<<(unsigned)tiles_for(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
+  k_cand<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
   IB_DISPATCH_FID(P.fid, k_mono<F><<<grid_for(bmax * kids, TPB, 148u * 12u), TPB, 0, st>>>(
                              P, w.ctl, w.tab, w.tab_stride, w.cand, w.ok));
   cudaMemsetAsync(w.desc2, 0, sizeof(uint64_t) * (size_t)tiles_for(bmax * kids), st);
-  k_emit<<<(unsigned)tiles_for(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok,
+  k_emit<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok,
                                                             w.new_slot, w.pool, w.desc2, w.tile_ctr + 1);
   k_iter_end<<<1, 1, 0, st>>>(w.ctl, kids);
   if (hook) hook->end(2, st);
@@ -1185,10 +1208,10 @@ int launch_branch(const Problem& P, const IterBufs& w, long nb, cudaStream_t st)
   cudaMemsetAsync(w.desc, 0, sizeof(uint64_t) * (size_t)tiles_for(nb * kids), st);
   cudaMemsetAsync(w.desc2, 0, sizeof(uint64_t) * (size_t)tiles_for(nb * kids), st);
   cudaMemsetAsync(w.tile_ctr, 0, sizeof(uint32_t) * 4, st);
-  k_cand<<<(unsigned)tiles_for(nb * kids), TPB, 0, st>>>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
+  k_cand<<<scan_grid(nb * kids), TPB, 0, st>>>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
   IB_DISPATCH_FID(P.fid, k_mono<F><<<grid_for(nb * kids, TPB, 148u * 12u), TPB, 0, st>>>(P, w.ctl, w.tab,
                                                                                         w.tab_stride, w.cand, w.ok));
-  k_emit<<<(unsigned)tiles_for(nb * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok,
+  k_emit<<<scan_grid(nb * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok,
                                                           w.new_slot, w.pool, w.desc2, w.tile_ctr + 1);
   LAUNCH_OK;
 }
@@ -1208,7 +1231,7 @@ int launch_partition(Pool in, long cnt, const unsigned long long* gub_key, int k
   long ntiles = tiles_for(cnt);
   cudaMemsetAsync(desc, 0, sizeof(uint64_t) * 3 * (size_t)ntiles, st);
   cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t), st);
-  k_partition<<<(unsigned)ntiles, TPB, 0, st>>>(in, cnt, gub_key, known, prefix, r_need, sel_slot, sel_code, sel_lb,
+  k_partition<<<scan_grid(cnt), TPB, 0, st>>>(in, cnt, gub_key, known, prefix, r_need, sel_slot, sel_code, sel_lb,
                                                 keep, desc, tile_ctr, keep_count, ntiles);
   LAUNCH_OK;
 }
@@ -1220,7 +1243,7 @@ int launch_gc(const int32_t* pool_slot, Ctl* ctl, long pool_bound, uint8_t* mark
   long ntiles = tiles_for(cap);
   cudaMemsetAsync(desc, 0, sizeof(uint64_t) * (size_t)ntiles, st);
   cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t), st);
-  k_gc_collect<<<(unsigned)ntiles, TPB, 0, st>>>(mark, cap, free_list, desc, tile_ctr, ctl, ntiles);
+  k_gc_collect<<<scan_grid(cap), TPB, 0, st>>>(mark, cap, free_list, desc, tile_ctr, ctl, ntiles);
   LAUNCH_OK;
 }
 
@@ -1233,7 +1256,7 @@ int launch_compact_le(const double* keys, long cnt, double thr, int64_t* out_idx
   long ntiles = tiles_for(cnt);
   cudaMemsetAsync(desc, 0, sizeof(uint64_t) * (size_t)ntiles, st);
   cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t), st);
-  k_compact_le<<<(unsigned)ntiles, TPB, 0, st>>>(keys, cnt, thr, out_idx, desc, tile_ctr, out_count, ntiles);
+  k_compact_le<<<scan_grid(cnt), TPB, 0, st>>>(keys, cnt, thr, out_idx, desc, tile_ctr, out_count, ntiles);
   LAUNCH_OK;
 }
 

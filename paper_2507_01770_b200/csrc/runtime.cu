@@ -479,6 +479,21 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
     if (hc.err) return fail(hc.err, "capacity exceeded on the device (L %ld, archive %ld)", o.pool_cap, o.arch_cap);
     if (xfn ? hc.gdone : hc.done) break;
     chunk = std::min(chunk * 2, 32L);
+    // lazy deletion leaves selected / ruled-out records in L: compact when
+    // more than half of it is dead (list order preserved)
+    long live_now = (long)hc.live - (long)hc.B + (long)hc.nsurv;
+    long dead = (long)pcount - std::max(0L, live_now);
+    if (dead > std::max((long)pcount / 2, 1L << 18)) {
+      CKL(launch_partition(w.pa, (long)pcount, &w.ctl->gub_key, 64, 0ull, 0ull, nullptr, nullptr, nullptr, w.pb,
+                           w.desc, w.tile_ctr, w.cnt, st));
+      k_set_pcount<<<1, 1, 0, st>>>(w.ctl, w.cnt);
+      nk += 2;
+      std::swap(w.pa, w.pb);
+      CK(cudaMemcpyAsync(&hc, w.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      pcount = hc.pcount;
+      graph_bound = -1;  // the list buffers swapped
+    }
   }
   const Ctl c = hc;
   int status;
