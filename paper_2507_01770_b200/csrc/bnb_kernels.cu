@@ -71,28 +71,33 @@ __device__ __forceinline__ double warp_min(double v) {
 }
 
 // block reduction of K interval accumulators (result valid in thread 0)
-template <class F>
+template <class F, int BS = TPB>
 __device__ __forceinline__ void block_reduce_acc(Iv* a) {
-  __shared__ Iv s_acc[TPB / 32][2];
   warp_reduce_acc<F>(a);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0)
-    for (int k = 0; k < F::K; ++k) s_acc[wid][k] = a[k];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < TPB / 32; ++w)
-      for (int k = 0; k < F::K; ++k) a[k] = acc_comb<F>(k, a[k], s_acc[w][k]);
+  if constexpr (BS > 32) {
+    __shared__ Iv s_acc[BS / 32][2];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0)
+      for (int k = 0; k < F::K; ++k) s_acc[wid][k] = a[k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < BS / 32; ++w)
+        for (int k = 0; k < F::K; ++k) a[k] = acc_comb<F>(k, a[k], s_acc[w][k]);
+    }
+    __syncthreads();
   }
-  __syncthreads();
 }
+template <int BS = TPB>
 __device__ __forceinline__ double block_max(double v) {
-  __shared__ double s_m[TPB / 32];
   v = warp_max(v);
-  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x == 0)
-    for (int w = 1; w < TPB / 32; ++w) v = fmax(v, s_m[w]);
-  __syncthreads();
+  if constexpr (BS > 32) {
+    __shared__ double s_m[BS / 32];
+    if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int w = 1; w < BS / 32; ++w) v = fmax(v, s_m[w]);
+    __syncthreads();
+  }
   return v;
 }
 
@@ -127,10 +132,10 @@ __device__ __forceinline__ LevyChunk levy_chunk(int c, int d, int n) {
 // One block per selected box b.  Source row: archive slot sel_slot[b] of
 // src_lo/src_hi with record code sel_code[b]; destination: slot new_slot[b]
 // of dst_lo/dst_hi.  src_sc / dst_sc hold each slot's chunk start.
-template <class F>
-__global__ void __launch_bounds__(TPB) k_prep(Problem P, const Ctl* __restrict__ ctl, const int32_t* __restrict__ sel_slot,
-                                              const uint32_t* __restrict__ sel_code,
-                                              const int32_t* __restrict__ new_slot,
+template <class F, int BS>
+__global__ void __launch_bounds__(BS) k_prep(Problem P, const Ctl* __restrict__ ctl, const int32_t* __restrict__ sel_slot,
+                                             const uint32_t* __restrict__ sel_code, int32_t* __restrict__ new_slot,
+                                             const int32_t* __restrict__ free_list,
                                               const double* __restrict__ src_lo,
                                               const double* __restrict__ src_hi,
                                               const int32_t* __restrict__ src_sc, double* dst_lo,
@@ -141,7 +146,9 @@ __global__ void __launch_bounds__(TPB) k_prep(Problem P, const Ctl* __restrict__
   const int n = P.n, d = P.d, m = P.m;
   const int src = sel_slot[b];
   const uint32_t code = sel_code[b];
-  const int dst = new_slot[b];
+  // archive slot of the new parent: popped from the free list (solve) or given
+  const int dst = free_list ? free_list[ctl->free_top - 1 - b] : new_slot[b];
+  if (free_list && threadIdx.x == 0) new_slot[b] = dst;
   const int psc = src_sc[src];
   const int c = (code == CODE_WHOLE) ? psc : (psc + d) % n;  // line 184
   const double* slo = src_lo + (size_t)src * P.ld;
@@ -158,7 +165,7 @@ __global__ void __launch_bounds__(TPB) k_prep(Problem P, const Ctl* __restrict__
     for (int k = 0; k < F::K; ++k) acc[k] = accm[k] = acc_ident<F>(k);
   }
   double wmax = 0.0;
-  for (int i = threadIdx.x; i < n; i += TPB) {
+  for (int i = threadIdx.x; i < n; i += BS) {
     double a = slo[i], bb = shi[i];
     if (code != CODE_WHOLE) {
       int jj = (i - psc + n) % n;
@@ -192,7 +199,7 @@ __global__ void __launch_bounds__(TPB) k_prep(Problem P, const Ctl* __restrict__
     // Levy: rest = sum of chain terms that involve no split variable
     LevyChunk q = levy_chunk(c, d, n);
     Iv r = iv(0.0), rm = iv(0.0);
-    for (int i = threadIdx.x; i < n; i += TPB) {
+    for (int i = threadIdx.x; i < n; i += BS) {
       bool ji = q.inJ(i);
       Iv X{dlo[i], dhi[i]};
       double xm = midpt(X.lo, X.hi);
@@ -214,8 +221,8 @@ __global__ void __launch_bounds__(TPB) k_prep(Problem P, const Ctl* __restrict__
       }
     }
     Iv a2[2] = {r, iv(0.0)}, am2[2] = {rm, iv(0.0)};
-    block_reduce_acc<ObjRastrigin>(a2);  // any K=1 SUM reducer
-    block_reduce_acc<ObjRastrigin>(am2);
+    block_reduce_acc<ObjRastrigin, BS>(a2);  // any K=1 SUM reducer
+    block_reduce_acc<ObjRastrigin, BS>(am2);
     acc[0] = a2[0];
     accm[0] = am2[0];
     if (threadIdx.x == 0) {
@@ -246,10 +253,10 @@ __global__ void __launch_bounds__(TPB) k_prep(Problem P, const Ctl* __restrict__
       T[H_LEVY_LR + 1] = (double)q.R;
     }
   } else {
-    block_reduce_acc<F>(acc);
-    block_reduce_acc<F>(accm);
+    block_reduce_acc<F, BS>(acc);
+    block_reduce_acc<F, BS>(accm);
   }
-  wmax = block_max(wmax);
+  wmax = block_max<BS>(wmax);
   if (threadIdx.x == 0) {
     for (int k = 0; k < 2; ++k) {
       put(T + H_REST + 2 * k, acc[k]);
@@ -260,7 +267,7 @@ __global__ void __launch_bounds__(TPB) k_prep(Problem P, const Ctl* __restrict__
     dst_sc[dst] = c;
   }
   // tables of the m pieces of the d split variables
-  for (int t = threadIdx.x; t < d * m; t += TPB) {
+  for (int t = threadIdx.x; t < d * m; t += BS) {
     int j = t / m, p = t % m;
     int i = (c + j) % n;
     double a = dlo[i], bb = dhi[i];
@@ -461,12 +468,14 @@ __device__ __noinline__ bool child_mono_ok(const Problem& P, const double* __res
 // once per group.  Midpoint bounds are min-reduced (warp shuffle -> block ->
 // one ordered-int atomicMin per block into the incumbent, line 134); lower
 // bounds are stored per child for pass 2.
-template <class F>
-__global__ void __launch_bounds__(TPB, 4) k_child_eval(Problem P, Ctl* __restrict__ ctl,
+// GT = 8: bisection (m = 2, h = 3) with the group loop fully unrolled so the
+// outer functions of the 8 children interleave (ILP); GT = 0: runtime G
+template <class F, int GT>
+__global__ void __launch_bounds__(TPB, GT ? 3 : 4) k_child_eval(Problem P, Ctl* __restrict__ ctl,
                                                        const double* __restrict__ tab, int tab_stride,
                                                        double* __restrict__ clb) {
   if (ctl->done) return;
-  const int d = P.d, m = P.m, n = P.n, h = P.h, G = P.G;
+  const int d = P.d, m = GT ? 2 : P.m, n = P.n, h = GT ? 3 : P.h, G = GT ? GT : P.G;
   const long gpp = P.kids / G;
   const long ngroups = (long)ctl->B * gpp;
   double best = CUDART_INF;
@@ -498,6 +507,7 @@ __global__ void __launch_bounds__(TPB, 4) k_child_eval(Problem P, Ctl* __restric
           Am[k] = acc_comb<F>(k, Am[k], get(e + 2 * F::K + 2 * k));
         }
       }
+#pragma unroll(GT ? GT : 1)
       for (int q = 0; q < G; ++q) {
         Iv B[2], Bm[2];
 #pragma unroll
@@ -505,8 +515,10 @@ __global__ void __launch_bounds__(TPB, 4) k_child_eval(Problem P, Ctl* __restric
           B[k] = A[k];
           Bm[k] = Am[k];
         }
+#pragma unroll(GT ? 3 : 1)
         for (int j = 0; j < h; ++j) {
-          const double* e = T + HDR + (size_t)(j * m + piece((uint32_t)q, j, P)) * ENT + E_T;
+          const int p = GT ? ((q >> j) & 1) : piece((uint32_t)q, j, P);
+          const double* e = T + HDR + (size_t)(j * m + p) * ENT + E_T;
 #pragma unroll
           for (int k = 0; k < F::K; ++k) {
             B[k] = acc_comb<F>(k, B[k], get(e + 2 * k));
@@ -631,19 +643,58 @@ __global__ void __launch_bounds__(TPB) k_emit(const Problem P, Ctl* __restrict__
 }
 
 // ============================================================ list L kernels
-// iteration start: zero the statistics and the histogram
-__global__ void k_iter_begin(Ctl* ctl, unsigned int* hist) {
-  if (ctl->done) return;
-  if (threadIdx.x == 0) {
-    ctl->live = 0;
-    ctl->min_lb_key = ~0ull;
-    ctl->max_w_bits = 0;
+// Statistics of the live part of L (lb <= GUB, lines 136 and 148-150) and the
+// histogram of the top 8 bits of the live lower bounds (radix pass 1).  The
+// last block to finish (threadfence + ticket) takes the iteration's control
+// decisions: stop test (line 148: every region narrower than eps_x; line
+// 150: GUB - GLB <= eps_f), batch size B = min(live, bmax) (line 130, reading
+// R1) and the first radix digit of the B-th smallest key.
+
+// pick the radix digit of the B-th smallest key from hist with the whole
+// block (256 threads, one bin each); zero hist
+__device__ void block_pick_digit(Ctl* ctl, unsigned int* hist) {
+  __shared__ unsigned long long s_inc[256];
+  __shared__ int s_dig;
+  const int t = threadIdx.x;
+  unsigned long long h = t < 256 ? hist[t] : 0ull;
+  if (t < 256) s_inc[t] = h;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {  // Hillis-Steele inclusive scan
+    unsigned long long v = (t < 256 && t >= o) ? s_inc[t - o] : 0ull;
+    __syncthreads();
+    if (t < 256) s_inc[t] += v;
+    __syncthreads();
   }
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+  const unsigned long long need = ctl->need;
+  if (t == 0) s_dig = 255;
+  __syncthreads();
+  if (t < 256) {
+    unsigned long long before = t ? s_inc[t - 1] : 0ull;
+    if (before < need && s_inc[t] >= need) s_dig = t;
+  }
+  __syncthreads();
+  if (t == 0) {
+    int dig = s_dig;
+    unsigned long long before = dig ? s_inc[dig - 1] : 0ull;
+    unsigned long long cnt = s_inc[dig] - before;
+    ctl->need = need - before;
+    ctl->prefix = (ctl->prefix << 8) | (unsigned long long)dig;
+    ctl->known += 8;
+    if (cnt == ctl->need || ctl->known >= 64) ctl->resolved = 1;
+  }
+  if (t < 256) hist[t] = 0;
+  __syncthreads();
 }
 
-// statistics of the live part of L (lb <= GUB, lines 136 and 148-150) and
-// the histogram of the top 8 bits of the live lower bounds (radix pass 1)
+__device__ __forceinline__ bool last_block(Ctl* ctl) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&ctl->blocks_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  return s_last;
+}
+
 __global__ void __launch_bounds__(TPB) k_stats(Pool p, Ctl* ctl, unsigned int* hist) {
   if (ctl->done) return;
   __shared__ unsigned int s_h[256];
@@ -684,62 +735,60 @@ __global__ void __launch_bounds__(TPB) k_stats(Pool p, Ctl* ctl, unsigned int* h
       mk = s_k[w] < mk ? s_k[w] : mk;
       mw = fmax(mw, s_w[w]);
     }
-    if (live) atomicAdd(&ctl->live, live);
-    atomicMin(&ctl->min_lb_key, mk);
-    atomicMax(&ctl->max_w_bits, (unsigned long long)__double_as_longlong(mw));
+    if (live) atomicAdd(&ctl->acc_live, live);
+    atomicMin(&ctl->acc_min_key, mk);
+    atomicMax(&ctl->acc_max_w, (unsigned long long)__double_as_longlong(mw));
   }
   for (int i = threadIdx.x; i < 256; i += TPB)
     if (s_h[i]) atomicAdd(&hist[i], s_h[i]);
-}
-
-// pick the radix digit of the B-th smallest key from hist; zero hist
-__device__ void pick_digit(Ctl* ctl, unsigned int* hist) {
-  unsigned long long need = ctl->need, cum = 0;
-  int dig = 0;
-  for (; dig < 255; ++dig) {
-    if (cum + hist[dig] >= need) break;
-    cum += hist[dig];
+  if (!last_block(ctl)) return;
+  // ---- control (last block)
+  __shared__ int s_go;
+  if (threadIdx.x == 0) {
+    ctl->blocks_done = 0;
+    ctl->live = ctl->acc_live;
+    ctl->min_lb_key = ctl->acc_min_key;
+    ctl->max_w_bits = ctl->acc_max_w;
+    ctl->acc_live = 0;
+    ctl->acc_min_key = ~0ull;
+    ctl->acc_max_w = 0;
+    s_go = 0;
+    const unsigned long long L = ctl->live;
+    const double glb = okey_inv(ctl->min_lb_key);
+    const double maxw = __longlong_as_double((long long)ctl->max_w_bits);
+    if (L == 0) {
+      ctl->done = 3;
+    } else if (maxw <= ctl->eps_x && __dsub_ru(gub, glb) <= ctl->eps_f) {
+      ctl->done = 1;
+    } else if (ctl->iter >= ctl->max_iter) {
+      ctl->done = 2;
+    } else {
+      const unsigned long long B = L < ctl->bmax ? L : ctl->bmax;
+      ctl->B = B;
+      ctl->known = 0;
+      ctl->prefix = 0;
+      ctl->need = B;
+      ctl->resolved = 1;
+      if (ctl->free_top < B) {  // archive full
+        ctl->err = -2;
+        ctl->done = 4;
+      } else if (L > ctl->bmax) {
+        ctl->resolved = 0;
+        s_go = 1;
+      }
+    }
   }
-  unsigned int cnt = hist[dig];
-  ctl->need = need - cum;
-  ctl->prefix = (ctl->prefix << 8) | (unsigned long long)dig;
-  ctl->known += 8;
-  if (cnt == ctl->need || ctl->known >= 64) ctl->resolved = 1;
-  for (int i = 0; i < 256; ++i) hist[i] = 0;
-}
-
-// stop test (line 148: every region narrower than eps_x; line 150: GUB - GLB
-// <= eps_f) and batch size B = min(live, bmax) (line 130, reading R1)
-__global__ void k_control(Ctl* ctl, unsigned int* hist) {
-  if (ctl->done) return;
-  if (ctl->live == 0) {
-    ctl->done = 3;
-    return;
-  }
-  double glb = okey_inv(ctl->min_lb_key), gub = okey_inv(ctl->gub_key);
-  double maxw = __longlong_as_double((long long)ctl->max_w_bits);
-  if (maxw <= ctl->eps_x && __dsub_ru(gub, glb) <= ctl->eps_f) {
-    ctl->done = 1;
-    return;
-  }
-  if (ctl->iter >= ctl->max_iter) {
-    ctl->done = 2;
-    return;
-  }
-  unsigned long long B = ctl->live < ctl->bmax ? ctl->live : ctl->bmax;
-  ctl->B = B;
-  ctl->known = 0;
-  ctl->prefix = 0;
-  ctl->need = B;
-  ctl->resolved = 1;
-  if (ctl->live > ctl->bmax) {
-    ctl->resolved = 0;
-    pick_digit(ctl, hist);
+  __syncthreads();
+  if (s_go) {
+    block_pick_digit(ctl, hist);
+  } else {
+    for (int i = threadIdx.x; i < 256; i += TPB) hist[i] = 0;
   }
 }
 
-// radix pass: histogram of the next digit among live records matching prefix
-__global__ void __launch_bounds__(TPB) k_radix(Pool p, const Ctl* __restrict__ ctl, unsigned int* hist) {
+// radix pass: histogram of the next digit among live records matching the
+// known prefix; the last block picks the digit
+__global__ void __launch_bounds__(TPB) k_radix(Pool p, Ctl* __restrict__ ctl, unsigned int* hist) {
   if (ctl->done || ctl->resolved) return;
   __shared__ unsigned int s_h[256];
   for (int i = threadIdx.x; i < 256; i += TPB) s_h[i] = 0;
@@ -759,11 +808,12 @@ __global__ void __launch_bounds__(TPB) k_radix(Pool p, const Ctl* __restrict__ c
   __syncthreads();
   for (int i = threadIdx.x; i < 256; i += TPB)
     if (s_h[i]) atomicAdd(&hist[i], s_h[i]);
-}
-__global__ void k_pick(Ctl* ctl, unsigned int* hist) {
-  if (ctl->done || ctl->resolved) return;
-  ctl->sum_radix += ctl->pcount;
-  pick_digit(ctl, hist);
+  if (!last_block(ctl)) return;
+  if (threadIdx.x == 0) {
+    ctl->blocks_done = 0;
+    ctl->sum_radix += ctl->pcount;
+  }
+  block_pick_digit(ctl, hist);
 }
 
 // Selection (line 130): the B live records with the smallest (lb, position)
@@ -836,27 +886,12 @@ __global__ void __launch_bounds__(TPB) k_select(Pool p, Ctl* __restrict__ ctl, i
   }
 }
 
-// archive slots for the B new parents, popped from the free list
-__global__ void k_alloc(Ctl* ctl, const int32_t* free_list, int32_t* new_slot) {
-  if (ctl->done) return;
-  const long B = (long)ctl->B, top = (long)ctl->free_top;
-  if (top < B) {
-    if (threadIdx.x == 0) {
-      ctl->err = -2;  // IB_ENOSPACE: archive full
-      ctl->done = 4;
-    }
-    return;
-  }
-  for (long b = threadIdx.x; b < B; b += blockDim.x) new_slot[b] = free_list[top - 1 - b];
-  __syncthreads();
-  if (threadIdx.x == 0) ctl->free_top = top - B;
-}
-
 // iteration end: the survivors become part of L
 __global__ void k_iter_end(Ctl* ctl, long kids) {
   if (ctl->done) return;
   ctl->sum_pool += ctl->pcount;
   ctl->sum_B += ctl->B;
+  ctl->free_top -= ctl->B;  // archive slots taken by k_prep
   ctl->pcount += ctl->nsurv;
   ctl->iter += 1;
   ctl->evals += ctl->B * (unsigned long long)kids;
@@ -1147,50 +1182,63 @@ static inline unsigned scan_grid(long items) { return (unsigned)std::min(tiles_f
 
 // One iteration of the hot path, every kernel reading its sizes from ctl.
 // pool_bound / batch_bound: host upper bounds of |L| and B * m^d for grids.
+template <class F>
+static void launch_prep_t(const Problem& P, const IterBufs& w, long nb, const int32_t* free_list, cudaStream_t st) {
+  if (P.n <= 64)
+    k_prep<F, 32><<<(unsigned)nb, 32, 0, st>>>(P, w.ctl, w.sel_slot, w.sel_code, w.new_slot, free_list, w.src_lo,
+                                                w.src_hi, w.src_sc, w.dst_lo, w.dst_hi, w.dst_sc, w.tab, w.tab_stride);
+  else
+    k_prep<F, TPB><<<(unsigned)nb, TPB, 0, st>>>(P, w.ctl, w.sel_slot, w.sel_code, w.new_slot, free_list, w.src_lo,
+                                                  w.src_hi, w.src_sc, w.dst_lo, w.dst_hi, w.dst_sc, w.tab,
+                                                  w.tab_stride);
+}
+
+template <class F>
+static void launch_eval_t(const Problem& P, const IterBufs& w, long nkids, cudaStream_t st) {
+  unsigned g = grid_for(nkids / P.G, TPB, 148u * 16u);
+  if (P.m == 2 && P.G == 8 && !F::CHAIN)
+    k_child_eval<F, 8><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb);
+  else
+    k_child_eval<F, 0><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb);
+}
+
+// One iteration of the hot path (15 launches + 3 memsets), every kernel
+// reading its sizes and decisions from ctl.  pool_bound / bmax: host upper
+// bounds of |L| and B used only for grid sizes.
 int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long bmax, cudaStream_t st,
                      IterHook* hook) {
   const long kids = P.kids;
   // statistics + stop test + batch size + radix select (line 130)
   if (hook) hook->begin(3, pool_bound, st);
-  k_iter_begin<<<1, 256, 0, st>>>(w.ctl, w.hist);
   k_stats<<<grid_for(pool_bound, TPB, 148u * 8u), TPB, 0, st>>>(w.pool, w.ctl, w.hist);
-  k_control<<<1, 1, 0, st>>>(w.ctl, w.hist);
   if (hook) hook->end(3, st);
   if (hook) hook->begin(4, pool_bound, st);
-  for (int pass = 1; pass < 8; ++pass) {
+  for (int pass = 1; pass < 8; ++pass)
     k_radix<<<grid_for(pool_bound, TPB * 8, 148u * 4u), TPB, 0, st>>>(w.pool, w.ctl, w.hist);
-    k_pick<<<1, 1, 0, st>>>(w.ctl, w.hist);
-  }
   if (hook) hook->end(4, st);
   if (hook) hook->begin(5, pool_bound, st);
   cudaMemsetAsync(w.desc, 0, sizeof(uint64_t) * 2 * (size_t)tiles_for(pool_bound), st);
   cudaMemsetAsync(w.tile_ctr, 0, sizeof(uint32_t) * 4, st);
-  k_select<<<scan_grid(pool_bound), TPB, 0, st>>>(w.pool, w.ctl, w.sel_slot, w.sel_code, w.desc,
-                                                             w.tile_ctr);
-  k_alloc<<<1, 256, 0, st>>>(w.ctl, w.free_list, w.new_slot);
+  k_select<<<scan_grid(pool_bound), TPB, 0, st>>>(w.pool, w.ctl, w.sel_slot, w.sel_code, w.desc, w.tile_ctr);
   if (hook) hook->end(5, st);
   // partition (SPSD) + tables (a2, a3)
   if (hook) hook->begin(0, bmax, st);
-  IB_DISPATCH_FID(P.fid, k_prep<F><<<(unsigned)bmax, TPB, 0, st>>>(P, w.ctl, w.sel_slot, w.sel_code, w.new_slot,
-                                                                   w.src_lo, w.src_hi, w.src_sc, w.dst_lo,
-                                                                   w.dst_hi, w.dst_sc, w.tab, w.tab_stride));
+  IB_DISPATCH_FID(P.fid, launch_prep_t<F>(P, w, bmax, w.free_list, st));
   if (hook) hook->end(0, st);
   // bounds of every child + incumbent (a3, a4)
   if (hook) hook->begin(1, bmax * kids, st);
-  IB_DISPATCH_FID(P.fid, k_child_eval<F><<<grid_for(bmax * kids / P.G, TPB, 148u * 16u), TPB, 0, st>>>(
-                             P, w.ctl, w.tab, w.tab_stride, w.clb));
+  IB_DISPATCH_FID(P.fid, launch_eval_t<F>(P, w, bmax * kids, st));
   if (hook) hook->end(1, st);
   if (hook) hook->exchange(st);
   // rule out + compact (a5, a6)
   if (hook) hook->begin(2, bmax * kids, st);
   cudaMemsetAsync(w.desc, 0, sizeof(uint64_t) * (size_t)tiles_for(bmax * kids), st);
-  cudaMemsetAsync(w.tile_ctr, 0, sizeof(uint32_t) * 4, st);
+  cudaMemsetAsync(w.desc2, 0, sizeof(uint64_t) * (size_t)tiles_for(bmax * kids), st);
   k_cand<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
   IB_DISPATCH_FID(P.fid, k_mono<F><<<grid_for(bmax * kids, TPB, 148u * 12u), TPB, 0, st>>>(
                              P, w.ctl, w.tab, w.tab_stride, w.cand, w.ok));
-  cudaMemsetAsync(w.desc2, 0, sizeof(uint64_t) * (size_t)tiles_for(bmax * kids), st);
-  k_emit<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok,
-                                                            w.new_slot, w.pool, w.desc2, w.tile_ctr + 1);
+  k_emit<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok, w.new_slot,
+                                                  w.pool, w.desc2, w.tile_ctr + 1);
   k_iter_end<<<1, 1, 0, st>>>(w.ctl, kids);
   if (hook) hook->end(2, st);
   LAUNCH_OK;
@@ -1200,11 +1248,8 @@ int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long 
 // parents are selected, ctl->B = nb, ctl->pcount = 0
 int launch_branch(const Problem& P, const IterBufs& w, long nb, cudaStream_t st) {
   const long kids = P.kids;
-  IB_DISPATCH_FID(P.fid, k_prep<F><<<(unsigned)nb, TPB, 0, st>>>(P, w.ctl, w.sel_slot, w.sel_code, w.new_slot,
-                                                                 w.src_lo, w.src_hi, w.src_sc, w.dst_lo, w.dst_hi,
-                                                                 w.dst_sc, w.tab, w.tab_stride));
-  IB_DISPATCH_FID(P.fid, k_child_eval<F><<<grid_for(nb * kids / P.G, TPB, 148u * 16u), TPB, 0, st>>>(
-                             P, w.ctl, w.tab, w.tab_stride, w.clb));
+  IB_DISPATCH_FID(P.fid, launch_prep_t<F>(P, w, nb, nullptr, st));
+  IB_DISPATCH_FID(P.fid, launch_eval_t<F>(P, w, nb * kids, st));
   cudaMemsetAsync(w.desc, 0, sizeof(uint64_t) * (size_t)tiles_for(nb * kids), st);
   cudaMemsetAsync(w.desc2, 0, sizeof(uint64_t) * (size_t)tiles_for(nb * kids), st);
   cudaMemsetAsync(w.tile_ctr, 0, sizeof(uint32_t) * 4, st);
@@ -1289,13 +1334,9 @@ namespace ib {
 // statistics + control + radix passes of an iteration on an explicit list
 // (ib_select): leaves (known, prefix, need) of the B-th smallest key in ctl
 int launch_select_only(Pool p, Ctl* ctl, unsigned int* hist, long n, cudaStream_t st) {
-  k_iter_begin<<<1, 256, 0, st>>>(ctl, hist);
+  cudaMemsetAsync(hist, 0, 256 * sizeof(unsigned int), st);
   k_stats<<<grid_for(n, TPB, 148u * 8u), TPB, 0, st>>>(p, ctl, hist);
-  k_control<<<1, 1, 0, st>>>(ctl, hist);
-  for (int pass = 1; pass < 8; ++pass) {
-    k_radix<<<grid_for(n, TPB * 8, 148u * 4u), TPB, 0, st>>>(p, ctl, hist);
-    k_pick<<<1, 1, 0, st>>>(ctl, hist);
-  }
+  for (int pass = 1; pass < 8; ++pass) k_radix<<<grid_for(n, TPB * 8, 148u * 4u), TPB, 0, st>>>(p, ctl, hist);
   LAUNCH_OK;
 }
 }  // namespace ib

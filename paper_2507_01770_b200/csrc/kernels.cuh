@@ -68,6 +68,9 @@ struct Ctl {
   int xdone;  // multi-GPU: this rank stopped working (local decision)
   double eps_f, eps_x;
   unsigned long long bmax, max_iter, pool_cap;
+  unsigned long long acc_live, acc_min_key, acc_max_w;  // per-pass accumulators (statistics)
+  unsigned int blocks_done;      // last-block election counter
+  unsigned int pad2;
   unsigned long long sum_pool;   // records scanned by the statistics pass
   unsigned long long sum_radix;  // records scanned by radix passes 2..8
   unsigned long long sum_B;      // parents prepared

@@ -374,7 +374,9 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   hc.bmax = (unsigned long long)o.bmax;
   hc.max_iter = (unsigned long long)o.max_iter;
   hc.pool_cap = (unsigned long long)o.pool_cap;
+  hc.acc_min_key = ~0ull;
   CK(cudaMemcpyAsync(w.ctl, &hc, sizeof hc, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(w.hist, 0, 256 * sizeof(unsigned int), st));
   CK(cudaMemcpyAsync(w.alo, w.l, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(w.ahi, w.u, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemsetAsync(w.sc, 0, sizeof(int32_t), st));
@@ -411,7 +413,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   hook.xuser = xuser;
   hook.xchg = xchg;
   hook.ctl = w.ctl;
-  const int kIterKernels = 24;  // kernels per iteration (launch_iteration)
+  const int kIterKernels = 15;  // kernels per iteration (launch_iteration)
 
   unsigned long long pcount = 1, free_top = hc.free_top, peak = 1;
   long chunk = 1, graph_bound = -1;
@@ -765,6 +767,8 @@ int ib_select(const double* lb, int64_t n, double gub, int64_t bmax, int64_t* se
   hc.bmax = (unsigned long long)bmax;
   hc.max_iter = ~0ull;
   hc.pool_cap = (unsigned long long)n;
+  hc.acc_min_key = ~0ull;
+  hc.free_top = ~0ull;  // no archive in a bare selection
   CK(cudaMemcpyAsync(ctl, &hc, sizeof hc, cudaMemcpyHostToDevice, st));
   CKL(launch_select_only(in, ctl, hist, (long)n, st));
   CK(cudaMemcpyAsync(&hc, ctl, sizeof hc, cudaMemcpyDeviceToHost, st));
