@@ -1234,6 +1234,7 @@ int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long 
   if (hook) hook->begin(2, bmax * kids, st);
   cudaMemsetAsync(w.desc, 0, sizeof(uint64_t) * (size_t)tiles_for(bmax * kids), st);
   cudaMemsetAsync(w.desc2, 0, sizeof(uint64_t) * (size_t)tiles_for(bmax * kids), st);
+  cudaMemsetAsync(w.tile_ctr, 0, sizeof(uint32_t) * 4, st);  // tickets of k_cand / k_emit
   k_cand<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
   IB_DISPATCH_FID(P.fid, k_mono<F><<<grid_for(bmax * kids, TPB, 148u * 12u), TPB, 0, st>>>(
                              P, w.ctl, w.tab, w.tab_stride, w.cand, w.ok));
