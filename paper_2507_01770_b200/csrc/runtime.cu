@@ -12,7 +12,9 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -297,6 +299,55 @@ struct Hook : IterHook {
   }
 };
 
+// grid bound baked into a captured iteration: generous, so that one graph
+// serves the whole solve in the common case
+static long graph_bound_for(long pool_bound, unsigned long long pcount, long per_it, long cap) {
+  long b = std::max(pool_bound, (long)(2 * pcount) + 8 * per_it);
+  long p2 = 1;
+  while (p2 < b) p2 <<= 1;  // round up to a power of two: fewer distinct graphs
+  return std::min(p2, cap);
+}
+
+struct GraphKey {
+  Problem P;
+  const double* pool;
+  void* ws;
+  long bound;
+  long bmax, pool_cap, arch_cap;  // workspace layout
+};
+static bool same_problem(const Problem& a, const Problem& b) { return std::memcmp(&a, &b, sizeof(Problem)) == 0; }
+
+// per-thread reusable host resources: pinned control block, private stream,
+// instantiated iteration graphs
+struct ThreadCache {
+  Ctl* host = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev = nullptr;
+  struct Entry {
+    GraphKey k;
+    cudaGraphExec_t ge;
+  };
+  std::vector<Entry> graphs;
+  cudaGraphExec_t find(const GraphKey& k, long need_bound) {
+    for (auto& e : graphs)
+      if (same_problem(e.k.P, k.P) && e.k.pool == k.pool && e.k.ws == k.ws && e.k.bmax == k.bmax &&
+          e.k.pool_cap == k.pool_cap && e.k.arch_cap == k.arch_cap && e.k.bound >= need_bound)
+        return e.ge;
+    return nullptr;
+  }
+  void put(const GraphKey& k, cudaGraphExec_t ge) {
+    if (graphs.size() >= 8) {
+      cudaGraphExecDestroy(graphs.front().ge);
+      graphs.erase(graphs.begin());
+    }
+    graphs.push_back(Entry{k, ge});
+  }
+};
+static ThreadCache& thread_cache() {
+  static thread_local ThreadCache tc;
+  return tc;
+}
+
 static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, const double* l_host,
                       const double* u_host, double eps_f, double eps_x, const ib_options* opt, void* ws,
                       size_t ws_bytes, ib_result* res, double* so_lo, double* so_hi, double* so_lb,
@@ -316,33 +367,26 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   Prof prof;
   prof.on = opt && opt->profile == 1;
   const bool use_graph = !prof.on && !xfn;
-  // graph capture needs a non-legacy stream: work on a private stream ordered
-  // after the caller's stream (the call is synchronous)
+  // graph capture needs a non-legacy stream: work on a private stream (cached
+  // per thread) ordered after the caller's stream (the call is synchronous)
   cudaStream_t st = user_st;
-  struct Cleanup {
-    cudaStream_t s = nullptr;
-    cudaGraphExec_t ge = nullptr;
-    cudaGraph_t g = nullptr;
-    Ctl* host = nullptr;
-    ~Cleanup() {
-      if (s) cudaStreamSynchronize(s);
-      if (ge) cudaGraphExecDestroy(ge);
-      if (g) cudaGraphDestroy(g);
-      if (s) cudaStreamDestroy(s);
-      if (host) cudaFreeHost(host);
-    }
-  } cl;
+  ThreadCache& tc = thread_cache();
+  if (!tc.host) CK(cudaMallocHost(&tc.host, sizeof(Ctl)));
   if (use_graph) {
-    CK(cudaStreamCreateWithFlags(&cl.s, cudaStreamNonBlocking));
-    cudaEvent_t e;
-    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    CK(cudaEventRecord(e, user_st));
-    CK(cudaStreamWaitEvent(cl.s, e, 0));
-    cudaEventDestroy(e);
-    st = cl.s;
+    if (!tc.stream) CK(cudaStreamCreateWithFlags(&tc.stream, cudaStreamNonBlocking));
+    if (!tc.ev) CK(cudaEventCreateWithFlags(&tc.ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(tc.ev, user_st));
+    CK(cudaStreamWaitEvent(tc.stream, tc.ev, 0));
+    st = tc.stream;
   }
-  CK(cudaMallocHost(&cl.host, sizeof(Ctl)));
-  Ctl* hctl = cl.host;
+  struct SyncOnExit {
+    cudaStream_t s;
+    ~SyncOnExit() { cudaStreamSynchronize(s); }
+  } sync_on_exit{st};
+  Ctl* hctl = tc.host;
+  const bool trace = std::getenv("IBNB_TRACE") != nullptr;
+  auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  const double t_start = trace ? now() : 0.0;
   long nk = 0;  // kernels launched by this call
 
   // bounds and the root region (line 128): archive slot 0, list L = {root}
@@ -416,7 +460,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   const int kIterKernels = 15;  // kernels per iteration (launch_iteration)
 
   unsigned long long pcount = 1, free_top = hc.free_top, peak = 1;
-  long chunk = 1, graph_bound = -1;
+  long chunk = 1;
   for (;;) {
     const long per_it = o.bmax * o.kids;
     // capacity planning for the chunk: compact L / collect archive slots
@@ -430,7 +474,6 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
       CK(cudaMemcpyAsync(&hc, w.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       pcount = hc.pcount;
-      graph_bound = -1;  // the list buffers swapped
       if ((long)pcount + per_it > o.pool_cap)
         return fail(IB_ENOSPACE, "list L capacity %ld exceeded (%llu live + %ld children)", o.pool_cap, pcount,
                     per_it);
@@ -448,27 +491,24 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
     ib.pool = w.pa;
     const long pool_bound = (long)pcount + chunk * per_it;
     if (use_graph) {
-      // one captured iteration, replayed; re-captured when its grid bound is exceeded
-      if (graph_bound < pool_bound) {
-        if (cl.ge) {
-          cudaGraphExecDestroy(cl.ge);
-          cl.ge = nullptr;
-        }
-        if (cl.g) {
-          cudaGraphDestroy(cl.g);
-          cl.g = nullptr;
-        }
-        graph_bound = std::min(o.pool_cap, std::max(pool_bound, (long)(2 * pcount) + 8 * per_it));
+      // one captured iteration per (problem, buffers, grid bound), cached per
+      // thread and replayed; re-captured when its grid bound is exceeded
+      GraphKey key{P, ib.pool.lb, ws, graph_bound_for(pool_bound, pcount, per_it, o.pool_cap), o.bmax, o.pool_cap,
+                   o.arch_cap};
+      cudaGraphExec_t ge = tc.find(key, pool_bound);
+      if (!ge) {
         CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        int lr = launch_iteration(P, ib, graph_bound, o.bmax, st, nullptr);
+        int lr = launch_iteration(P, ib, key.bound, o.bmax, st, nullptr);
         cudaGraph_t g = nullptr;
         cudaError_t ce = cudaStreamEndCapture(st, &g);
         if (lr) return fail(lr, "capture of the iteration failed");
         CK(ce);
-        cl.g = g;
-        CK(cudaGraphInstantiate(&cl.ge, g, 0));
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        cudaGraphDestroy(g);
+        tc.put(key, ge);
+        if (trace) fprintf(stderr, "[ibnb] captured iteration graph, bound %ld\n", key.bound);
       }
-      for (long c = 0; c < chunk; ++c) CK(cudaGraphLaunch(cl.ge, st));
+      for (long c = 0; c < chunk; ++c) CK(cudaGraphLaunch(ge, st));
     } else {
       for (long c = 0; c < chunk; ++c) CKL(launch_iteration(P, ib, pool_bound, o.bmax, st, &hook));
     }
@@ -479,6 +519,9 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
     free_top = hc.free_top;
     peak = std::max(peak, pcount);
     if (hc.err) return fail(hc.err, "capacity exceeded on the device (L %ld, archive %ld)", o.pool_cap, o.arch_cap);
+    if (trace)
+      fprintf(stderr, "[ibnb] t=%.3f ms chunk=%ld iter=%llu |L|=%llu live=%llu B=%llu done=%d\n", now() - t_start,
+              chunk, hc.iter, hc.pcount, hc.live, hc.B, hc.done);
     if (xfn ? hc.gdone : hc.done) break;
     chunk = std::min(chunk * 2, 32L);
     // lazy deletion leaves selected / ruled-out records in L: compact when
@@ -494,7 +537,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
       CK(cudaMemcpyAsync(&hc, w.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       pcount = hc.pcount;
-      graph_bound = -1;  // the list buffers swapped
+      if (trace) fprintf(stderr, "[ibnb] compacted L -> %llu records\n", pcount);
     }
   }
   const Ctl c = hc;
