@@ -7,3 +7,4 @@ timeout 300 python bench.py --steps 5 --warmup 3 --no-baseline > gpurun_out/benc
 if [ -n "$2" ]; then timeout 1200 python scripts/explore.py --runs "$2" --max-iter 20000 > gpurun_out/explore_${TAG}.log 2>&1; echo explore rc=$?; cut -c1-400 gpurun_out/explore_${TAG}.log; fi
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
   python scripts/prof_solve.py --config 1 --solves 2 > gpurun_out/launches_${TAG}.log 2>&1; echo launches rc=$?
+IBNB_TRACE=1 timeout 300 python scripts/prof_solve.py --config 1 --solves 3 > gpurun_out/trace_${TAG}.log 2>&1; echo trace rc=$?
