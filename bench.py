@@ -46,7 +46,7 @@ SMS = 148
 FP64_LANES = 64
 
 # algorithmic HBM bytes per record of the list kernels
-BYTES_PER_RECORD = {"list_stats": 16, "radix_hist": 8, "partition": 48}
+BYTES_PER_RECORD = {"list": 24}  # statistics pass (lb, w: 16 B) + selection pass (lb: 8 B)
 
 
 def env_rank():
@@ -293,6 +293,7 @@ def main():
             p = prof.setdefault(c, {"ms": 0.0, "launches": 0, "units": 0})
             for k in p:
                 p[k] += v[k]
+    prof = {c: v for c, v in prof.items() if v["launches"]}
     dom = max(prof, key=lambda c: prof[c]["ms"])
     peaks = load_json(PEAKS_PATH) or {}
     pd = prof[dom]

@@ -85,9 +85,10 @@ typedef struct {
     int status;       /* IB_STATUS_* */
     int n_kernels;    /* CUDA kernels this call launched */
     /* per kernel class, filled when opt.profile = 1 (else zero):
-     * 0 prep (units: parents), 1 child_eval (children), 2 child_prune (children),
-     * 3 list statistics (records), 4 radix histogram (records),
-     * 5 partition of L (records) */
+     * 0 prep (units: parents), 1 child_eval (children), 2 child_prune
+     * (children), 3 list: statistics + radix select + selection (records of
+     * L scanned by the statistics pass), 4 radix passes (records, units
+     * only), 5 unused */
     double t_ms[IB_NPROF];
     int64_t launches[IB_NPROF];
     int64_t units[IB_NPROF];

@@ -26,7 +26,7 @@ CODE_WHOLE = 0xFFFFFFFF
 _lib = None
 
 NPROF = 6
-PROF_CLASSES = ("prep", "child_eval", "child_prune", "list_stats", "radix_hist", "partition")
+PROF_CLASSES = ("prep", "child_eval", "child_prune", "list", "unused4", "unused5")
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
 _dp = ctypes.POINTER(ctypes.c_double)

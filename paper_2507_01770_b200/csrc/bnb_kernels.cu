@@ -21,9 +21,13 @@
 
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
 #include "objectives.cuh"
 #include "scan.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ib {
 
@@ -542,9 +546,8 @@ __global__ void __launch_bounds__(TPB, GT ? 3 : 4) k_child_eval(Problem P, Ctl* 
 
 // Pass 2a: stable compaction of the candidates (children with lb <= GUB,
 // line 140) into cand[] (decoupled look-back).
-__global__ void __launch_bounds__(TPB) k_cand(const Problem P, Ctl* __restrict__ ctl, const double* __restrict__ clb,
-                                              uint32_t* __restrict__ cand, uint64_t* desc, uint32_t* tile_ctr) {
-  if (ctl->done) return;
+__device__ void cand_dev(const Problem& P, Ctl* __restrict__ ctl, const double* __restrict__ clb,
+                         uint32_t* __restrict__ cand, uint64_t* desc, uint32_t* tile_ctr) {
   __shared__ uint32_t s_tile;
   for (;;) {
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
@@ -575,10 +578,8 @@ __global__ void __launch_bounds__(TPB) k_cand(const Problem P, Ctl* __restrict__
 // Pass 2b: first-order test (lines 142-144) of every candidate, one thread
 // per candidate on a dense list (no divergence from pruned children).
 template <class F>
-__global__ void __launch_bounds__(TPB, 3) k_mono(Problem P, const Ctl* __restrict__ ctl, const double* __restrict__ tab,
-                                                 int tab_stride, const uint32_t* __restrict__ cand,
-                                                 uint8_t* __restrict__ ok) {
-  if (ctl->done) return;
+__device__ void mono_dev(const Problem& P, const Ctl* __restrict__ ctl, const double* __restrict__ tab,
+                         int tab_stride, const uint32_t* __restrict__ cand, uint8_t* __restrict__ ok) {
   const long nc = (long)ctl->ncand;
   for (long k = (long)blockIdx.x * TPB + threadIdx.x; k < nc; k += (long)gridDim.x * TPB) {
     ChildIdx ci = child_of(cand[k], P);
@@ -588,12 +589,10 @@ __global__ void __launch_bounds__(TPB, 3) k_mono(Problem P, const Ctl* __restric
 
 // Pass 2c: insert the surviving candidates into L after its current end, in
 // (parent, code) order (line 146), stable decoupled-look-back compaction.
-__global__ void __launch_bounds__(TPB) k_emit(const Problem P, Ctl* __restrict__ ctl, const double* __restrict__ tab,
-                                              int tab_stride, const double* __restrict__ clb,
-                                              const uint32_t* __restrict__ cand, const uint8_t* __restrict__ ok,
-                                              const int32_t* __restrict__ new_slot, Pool out, uint64_t* desc,
-                                              uint32_t* tile_ctr) {
-  if (ctl->done) return;
+__device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* __restrict__ tab, int tab_stride,
+                         const double* __restrict__ clb, const uint32_t* __restrict__ cand,
+                         const uint8_t* __restrict__ ok, const int32_t* __restrict__ new_slot, Pool out,
+                         uint64_t* desc, uint32_t* tile_ctr) {
   __shared__ uint32_t s_tile;
   for (;;) {
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
@@ -640,6 +639,27 @@ __global__ void __launch_bounds__(TPB) k_emit(const Problem P, Ctl* __restrict__
     }
   }
   }
+}
+
+__global__ void __launch_bounds__(TPB) k_cand(const Problem P, Ctl* __restrict__ ctl, const double* __restrict__ clb,
+                                              uint32_t* __restrict__ cand, uint64_t* desc, uint32_t* tile_ctr) {
+  if (ctl->done) return;
+  cand_dev(P, ctl, clb, cand, desc, tile_ctr);
+}
+template <class F>
+__global__ void __launch_bounds__(TPB, 3) k_mono(Problem P, const Ctl* __restrict__ ctl, const double* __restrict__ tab,
+                                                 int tab_stride, const uint32_t* __restrict__ cand,
+                                                 uint8_t* __restrict__ ok) {
+  if (ctl->done) return;
+  mono_dev<F>(P, ctl, tab, tab_stride, cand, ok);
+}
+__global__ void __launch_bounds__(TPB) k_emit(const Problem P, Ctl* __restrict__ ctl, const double* __restrict__ tab,
+                                              int tab_stride, const double* __restrict__ clb,
+                                              const uint32_t* __restrict__ cand, const uint8_t* __restrict__ ok,
+                                              const int32_t* __restrict__ new_slot, Pool out, uint64_t* desc,
+                                              uint32_t* tile_ctr) {
+  if (ctl->done) return;
+  emit_dev(P, ctl, tab, tab_stride, clb, cand, ok, new_slot, out, desc, tile_ctr);
 }
 
 // ============================================================ list L kernels
@@ -695,8 +715,9 @@ __device__ __forceinline__ bool last_block(Ctl* ctl) {
   return s_last;
 }
 
-__global__ void __launch_bounds__(TPB) k_stats(Pool p, Ctl* ctl, unsigned int* hist) {
-  if (ctl->done) return;
+// accumulate the statistics of this block's share of L into ctl->acc_* and
+// the top-8-bit histogram of the live keys
+__device__ void stats_accum_dev(const Pool& p, Ctl* ctl, unsigned int* hist) {
   __shared__ unsigned int s_h[256];
   for (int i = threadIdx.x; i < 256; i += TPB) s_h[i] = 0;
   __syncthreads();
@@ -741,10 +762,13 @@ __global__ void __launch_bounds__(TPB) k_stats(Pool p, Ctl* ctl, unsigned int* h
   }
   for (int i = threadIdx.x; i < 256; i += TPB)
     if (s_h[i]) atomicAdd(&hist[i], s_h[i]);
-  if (!last_block(ctl)) return;
-  // ---- control (last block)
+}
+
+// control decisions of an iteration, by one block after the statistics pass
+__device__ void stats_control_dev(Ctl* ctl, unsigned int* hist) {
   __shared__ int s_go;
   if (threadIdx.x == 0) {
+    const double gub = okey_inv(ctl->gub_key);
     ctl->blocks_done = 0;
     ctl->live = ctl->acc_live;
     ctl->min_lb_key = ctl->acc_min_key;
@@ -783,13 +807,20 @@ __global__ void __launch_bounds__(TPB) k_stats(Pool p, Ctl* ctl, unsigned int* h
     block_pick_digit(ctl, hist);
   } else {
     for (int i = threadIdx.x; i < 256; i += TPB) hist[i] = 0;
+    __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(TPB) k_stats(Pool p, Ctl* ctl, unsigned int* hist) {
+  if (ctl->done) return;
+  stats_accum_dev(p, ctl, hist);
+  if (!last_block(ctl)) return;
+  stats_control_dev(ctl, hist);
 }
 
 // radix pass: histogram of the next digit among live records matching the
 // known prefix; the last block picks the digit
-__global__ void __launch_bounds__(TPB) k_radix(Pool p, Ctl* __restrict__ ctl, unsigned int* hist) {
-  if (ctl->done || ctl->resolved) return;
+__device__ void radix_accum_dev(const Pool& p, const Ctl* __restrict__ ctl, unsigned int* hist) {
   __shared__ unsigned int s_h[256];
   for (int i = threadIdx.x; i < 256; i += TPB) s_h[i] = 0;
   __syncthreads();
@@ -808,6 +839,11 @@ __global__ void __launch_bounds__(TPB) k_radix(Pool p, Ctl* __restrict__ ctl, un
   __syncthreads();
   for (int i = threadIdx.x; i < 256; i += TPB)
     if (s_h[i]) atomicAdd(&hist[i], s_h[i]);
+}
+
+__global__ void __launch_bounds__(TPB) k_radix(Pool p, Ctl* __restrict__ ctl, unsigned int* hist) {
+  if (ctl->done || ctl->resolved) return;
+  radix_accum_dev(p, ctl, hist);
   if (!last_block(ctl)) return;
   if (threadIdx.x == 0) {
     ctl->blocks_done = 0;
@@ -819,9 +855,8 @@ __global__ void __launch_bounds__(TPB) k_radix(Pool p, Ctl* __restrict__ ctl, un
 // Selection (line 130): the B live records with the smallest (lb, position)
 // are copied, in list order, to the batch arrays and marked dead in L
 // (lb = +inf).  Kept records stay in place (lazy deletion).
-__global__ void __launch_bounds__(TPB) k_select(Pool p, Ctl* __restrict__ ctl, int32_t* sel_slot, uint32_t* sel_code,
-                                                uint64_t* desc, uint32_t* tile_ctr) {
-  if (ctl->done) return;
+__device__ void select_dev(const Pool& p, Ctl* __restrict__ ctl, int32_t* sel_slot, uint32_t* sel_code, uint64_t* desc,
+                           uint32_t* tile_ctr) {
   __shared__ uint32_t s_tile;
   for (;;) {
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
@@ -885,9 +920,14 @@ __global__ void __launch_bounds__(TPB) k_select(Pool p, Ctl* __restrict__ ctl, i
   }
   }
 }
+__global__ void __launch_bounds__(TPB) k_select(Pool p, Ctl* __restrict__ ctl, int32_t* sel_slot, uint32_t* sel_code,
+                                                uint64_t* desc, uint32_t* tile_ctr) {
+  if (ctl->done) return;
+  select_dev(p, ctl, sel_slot, sel_code, desc, tile_ctr);
+}
 
 // iteration end: the survivors become part of L
-__global__ void k_iter_end(Ctl* ctl, long kids) {
+__device__ void iter_end_dev(Ctl* ctl, long kids) {
   if (ctl->done) return;
   ctl->sum_pool += ctl->pcount;
   ctl->sum_B += ctl->B;
@@ -895,6 +935,68 @@ __global__ void k_iter_end(Ctl* ctl, long kids) {
   ctl->pcount += ctl->nsurv;
   ctl->iter += 1;
   ctl->evals += ctl->B * (unsigned long long)kids;
+}
+__global__ void k_iter_end(Ctl* ctl, long kids) { iter_end_dev(ctl, kids); }
+
+// ===================================================== fused cooperative kernels
+// One iteration = 4 launches: k_list (statistics, stop test, batch size,
+// radix select, selection), k_prep, k_child_eval, k_prune (candidates,
+// first-order test, insertion into L, iteration end).  The phases of k_list
+// and k_prune are separated by grid-wide barriers (cooperative launch, every
+// block resident); after a barrier the control block is re-read from L2.
+__device__ __forceinline__ int vload(const int* p) { return *(const volatile int*)p; }
+
+__global__ void __launch_bounds__(TPB) k_list(Pool p, Ctl* ctl, unsigned int* hist, int32_t* sel_slot,
+                                              uint32_t* sel_code, uint64_t* desc, uint32_t* tile_ctr) {
+  cg::grid_group grid = cg::this_grid();
+  if (ctl->done) return;  // uniform: read before any block writes it
+  const long gtid = (long)blockIdx.x * TPB + threadIdx.x, gsize = (long)gridDim.x * TPB;
+  const long ntiles = ((long)ctl->pcount + TILE - 1) / TILE + 1;
+  for (long i = gtid; i < 2 * ntiles + 2; i += gsize) desc[i] = 0;
+  if (gtid == 0) tile_ctr[0] = 0;
+  stats_accum_dev(p, ctl, hist);
+  grid.sync();
+  if (blockIdx.x == 0) stats_control_dev(ctl, hist);
+  grid.sync();
+  for (int pass = 1; pass < 8; ++pass) {
+    if (vload(&ctl->done) || vload(&ctl->resolved)) break;
+    radix_accum_dev(p, ctl, hist);
+    grid.sync();
+    if (blockIdx.x == 0) {
+      if (threadIdx.x == 0) ctl->sum_radix += ctl->pcount;
+      block_pick_digit(ctl, hist);
+    }
+    grid.sync();
+  }
+  if (vload(&ctl->done)) return;
+  select_dev(p, ctl, sel_slot, sel_code, desc, tile_ctr);
+}
+
+template <class F>
+__global__ void __launch_bounds__(TPB, 2) k_prune(Problem P, Ctl* ctl, const double* __restrict__ tab, int tab_stride,
+                                                  const double* __restrict__ clb, uint32_t* __restrict__ cand,
+                                                  uint8_t* __restrict__ ok, const int32_t* __restrict__ new_slot,
+                                                  Pool out, uint64_t* desc, uint64_t* desc2, uint32_t* tile_ctr) {
+  cg::grid_group grid = cg::this_grid();
+  if (ctl->done) return;
+  const long gtid = (long)blockIdx.x * TPB + threadIdx.x, gsize = (long)gridDim.x * TPB;
+  const long ntiles = ((long)ctl->B * P.kids + TILE - 1) / TILE + 1;
+  for (long i = gtid; i < ntiles + 1; i += gsize) {
+    desc[i] = 0;
+    desc2[i] = 0;
+  }
+  if (gtid == 0) {
+    tile_ctr[0] = 0;
+    tile_ctr[1] = 0;
+  }
+  grid.sync();
+  cand_dev(P, ctl, clb, cand, desc, tile_ctr);
+  grid.sync();
+  mono_dev<F>(P, ctl, tab, tab_stride, cand, ok);
+  grid.sync();
+  emit_dev(P, ctl, tab, tab_stride, clb, cand, ok, new_slot, out, desc2, tile_ctr + 1);
+  grid.sync();
+  if (gtid == 0) iter_end_dev(ctl, P.kids);
 }
 
 // multi-GPU exchange of the incumbent (2 doubles: GUB, finished flag)
@@ -1202,25 +1304,35 @@ static void launch_eval_t(const Problem& P, const IterBufs& w, long nkids, cudaS
     k_child_eval<F, 0><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb);
 }
 
-// One iteration of the hot path (15 launches + 3 memsets), every kernel
-// reading its sizes and decisions from ctl.  pool_bound / bmax: host upper
-// bounds of |L| and B used only for grid sizes.
+// co-resident grid of a cooperative kernel (all blocks active at once)
+static unsigned coop_grid(const void* fn, int per_sm_cap) {
+  int nb = 0, dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, TPB, 0);
+  nb = std::max(1, std::min(nb, per_sm_cap));
+  return (unsigned)(nb * sms);
+}
+template <class K, class... A>
+static cudaError_t coop_launch(K* fn, unsigned grid, cudaStream_t st, A... args) {
+  void* argv[] = {(void*)&args...};
+  return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(TPB), argv, 0, st);
+}
+
+// One iteration of the hot path: 4 launches (k_list, k_prep, k_child_eval,
+// k_prune), every kernel reading its sizes and decisions from ctl.
+// pool_bound / bmax: host upper bounds of |L| and B, used for grid sizes.
 int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long bmax, cudaStream_t st,
                      IterHook* hook) {
   const long kids = P.kids;
-  // statistics + stop test + batch size + radix select (line 130)
+  static unsigned g_list = 0;
+  if (!g_list) g_list = coop_grid((const void*)k_list, 4);
+  cudaError_t e;
+  // statistics + stop test + batch size + radix select + selection (a1, a7)
   if (hook) hook->begin(3, pool_bound, st);
-  k_stats<<<grid_for(pool_bound, TPB, 148u * 8u), TPB, 0, st>>>(w.pool, w.ctl, w.hist);
+  e = coop_launch(k_list, g_list, st, w.pool, w.ctl, w.hist, w.sel_slot, w.sel_code, w.desc, w.tile_ctr);
+  if (e != cudaSuccess) return (int)e;
   if (hook) hook->end(3, st);
-  if (hook) hook->begin(4, pool_bound, st);
-  for (int pass = 1; pass < 8; ++pass)
-    k_radix<<<grid_for(pool_bound, TPB * 8, 148u * 4u), TPB, 0, st>>>(w.pool, w.ctl, w.hist);
-  if (hook) hook->end(4, st);
-  if (hook) hook->begin(5, pool_bound, st);
-  cudaMemsetAsync(w.desc, 0, sizeof(uint64_t) * 2 * (size_t)tiles_for(pool_bound), st);
-  cudaMemsetAsync(w.tile_ctr, 0, sizeof(uint32_t) * 4, st);
-  k_select<<<scan_grid(pool_bound), TPB, 0, st>>>(w.pool, w.ctl, w.sel_slot, w.sel_code, w.desc, w.tile_ctr);
-  if (hook) hook->end(5, st);
   // partition (SPSD) + tables (a2, a3)
   if (hook) hook->begin(0, bmax, st);
   IB_DISPATCH_FID(P.fid, launch_prep_t<F>(P, w, bmax, w.free_list, st));
@@ -1230,17 +1342,15 @@ int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long 
   IB_DISPATCH_FID(P.fid, launch_eval_t<F>(P, w, bmax * kids, st));
   if (hook) hook->end(1, st);
   if (hook) hook->exchange(st);
-  // rule out + compact (a5, a6)
+  // rule out + compact + insert (a5, a6)
   if (hook) hook->begin(2, bmax * kids, st);
-  cudaMemsetAsync(w.desc, 0, sizeof(uint64_t) * (size_t)tiles_for(bmax * kids), st);
-  cudaMemsetAsync(w.desc2, 0, sizeof(uint64_t) * (size_t)tiles_for(bmax * kids), st);
-  cudaMemsetAsync(w.tile_ctr, 0, sizeof(uint32_t) * 4, st);  // tickets of k_cand / k_emit
-  k_cand<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
-  IB_DISPATCH_FID(P.fid, k_mono<F><<<grid_for(bmax * kids, TPB, 148u * 12u), TPB, 0, st>>>(
-                             P, w.ctl, w.tab, w.tab_stride, w.cand, w.ok));
-  k_emit<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok, w.new_slot,
-                                                  w.pool, w.desc2, w.tile_ctr + 1);
-  k_iter_end<<<1, 1, 0, st>>>(w.ctl, kids);
+  IB_DISPATCH_FID(P.fid, {
+    static unsigned g_prune = 0;
+    if (!g_prune) g_prune = coop_grid((const void*)k_prune<F>, 2);
+    e = coop_launch(k_prune<F>, g_prune, st, P, w.ctl, (const double*)w.tab, w.tab_stride, (const double*)w.clb,
+                    w.cand, w.ok, (const int32_t*)w.new_slot, w.pool, w.desc, w.desc2, w.tile_ctr);
+  });
+  if (e != cudaSuccess) return (int)e;
   if (hook) hook->end(2, st);
   LAUNCH_OK;
 }

@@ -457,7 +457,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   hook.xuser = xuser;
   hook.xchg = xchg;
   hook.ctl = w.ctl;
-  const int kIterKernels = 15;  // kernels per iteration (launch_iteration)
+  const int kIterKernels = 4;  // kernels per iteration (launch_iteration)
 
   unsigned long long pcount = 1, free_top = hc.free_top, peak = 1;
   long chunk = 1;
@@ -583,7 +583,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   res->units[2] = (int64_t)c.evals;
   res->units[3] = (int64_t)c.sum_pool;
   res->units[4] = (int64_t)c.sum_radix;
-  res->units[5] = (int64_t)c.sum_pool;
+  res->units[5] = 0;
   res->f_lo = live ? okey_inv_h(c.min_lb_key) : INFINITY;
   res->f_hi = okey_inv_h(c.gub_key);
   res->iters = (int64_t)c.iter;
