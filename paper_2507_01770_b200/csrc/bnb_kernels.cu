@@ -477,8 +477,16 @@ __device__ __noinline__ bool child_mono_ok(const Problem& P, const double* __res
 template <class F, int GT>
 __global__ void __launch_bounds__(TPB, GT ? 3 : 4) k_child_eval(Problem P, Ctl* __restrict__ ctl,
                                                        const double* __restrict__ tab, int tab_stride,
-                                                       double* __restrict__ clb) {
+                                                       double* __restrict__ clb, uint64_t* zero_a, uint64_t* zero_b,
+                                                       long nzero, uint32_t* zero_ctr) {
   if (ctl->done) return;
+  if (zero_a) {  // descriptors and tickets of the following k_cand / k_emit
+    for (long i = (long)blockIdx.x * TPB + threadIdx.x; i < nzero; i += (long)gridDim.x * TPB) {
+      zero_a[i] = 0;
+      zero_b[i] = 0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 4) zero_ctr[threadIdx.x] = 0;
+  }
   const int d = P.d, m = GT ? 2 : P.m, n = P.n, h = GT ? 3 : P.h, G = GT ? GT : P.G;
   const long gpp = P.kids / G;
   const long ngroups = (long)ctl->B * gpp;
@@ -589,10 +597,11 @@ __device__ void mono_dev(const Problem& P, const Ctl* __restrict__ ctl, const do
 
 // Pass 2c: insert the surviving candidates into L after its current end, in
 // (parent, code) order (line 146), stable decoupled-look-back compaction.
+__device__ void iter_end_dev(Ctl* ctl, long kids);
 __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* __restrict__ tab, int tab_stride,
                          const double* __restrict__ clb, const uint32_t* __restrict__ cand,
                          const uint8_t* __restrict__ ok, const int32_t* __restrict__ new_slot, Pool out,
-                         uint64_t* desc, uint32_t* tile_ctr) {
+                         uint64_t* desc, uint32_t* tile_ctr, bool finish) {
   __shared__ uint32_t s_tile;
   for (;;) {
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
@@ -602,7 +611,10 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
   const long nc = (long)ctl->ncand;
   const long ntiles = (nc + TILE - 1) / TILE;
   if (nc == 0) {
-    if (tile == 0 && threadIdx.x == 0) ctl->nsurv = 0;
+    if (tile == 0 && threadIdx.x == 0) {
+      ctl->nsurv = 0;
+      if (finish) iter_end_dev(ctl, P.kids);
+    }
     break;
   }
   if ((long)tile >= ntiles) break;
@@ -637,6 +649,7 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
       ctl->err = -2;  // IB_ENOSPACE
       ctl->done = 4;
     }
+    if (finish) iter_end_dev(ctl, P.kids);
   }
   }
 }
@@ -657,9 +670,9 @@ __global__ void __launch_bounds__(TPB) k_emit(const Problem P, Ctl* __restrict__
                                               int tab_stride, const double* __restrict__ clb,
                                               const uint32_t* __restrict__ cand, const uint8_t* __restrict__ ok,
                                               const int32_t* __restrict__ new_slot, Pool out, uint64_t* desc,
-                                              uint32_t* tile_ctr) {
+                                              uint32_t* tile_ctr, int finish) {
   if (ctl->done) return;
-  emit_dev(P, ctl, tab, tab_stride, clb, cand, ok, new_slot, out, desc, tile_ctr);
+  emit_dev(P, ctl, tab, tab_stride, clb, cand, ok, new_slot, out, desc, tile_ctr, finish != 0);
 }
 
 // ============================================================ list L kernels
@@ -994,7 +1007,7 @@ __global__ void __launch_bounds__(TPB, 2) k_prune(Problem P, Ctl* ctl, const dou
   grid.sync();
   mono_dev<F>(P, ctl, tab, tab_stride, cand, ok);
   grid.sync();
-  emit_dev(P, ctl, tab, tab_stride, clb, cand, ok, new_slot, out, desc2, tile_ctr + 1);
+  emit_dev(P, ctl, tab, tab_stride, clb, cand, ok, new_slot, out, desc2, tile_ctr + 1, false);
   grid.sync();
   if (gtid == 0) iter_end_dev(ctl, P.kids);
 }
@@ -1296,12 +1309,15 @@ static void launch_prep_t(const Problem& P, const IterBufs& w, long nb, const in
 }
 
 template <class F>
-static void launch_eval_t(const Problem& P, const IterBufs& w, long nkids, cudaStream_t st) {
+static void launch_eval_t(const Problem& P, const IterBufs& w, long nkids, cudaStream_t st, bool zero = false) {
   unsigned g = grid_for(nkids / P.G, TPB, 148u * 16u);
+  uint64_t* za = zero ? w.desc : nullptr;
+  uint64_t* zb = zero ? w.desc2 : nullptr;
+  long nz = tiles_for(nkids) + 1;
   if (P.m == 2 && P.G == 8 && !F::CHAIN)
-    k_child_eval<F, 8><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb);
+    k_child_eval<F, 8><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr);
   else
-    k_child_eval<F, 0><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb);
+    k_child_eval<F, 0><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr);
 }
 
 // co-resident grid of a cooperative kernel (all blocks active at once)
@@ -1319,14 +1335,14 @@ static cudaError_t coop_launch(K* fn, unsigned grid, cudaStream_t st, A... args)
   return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(TPB), argv, 0, st);
 }
 
-// One iteration of the hot path: 4 launches (k_list, k_prep, k_child_eval,
-// k_prune), every kernel reading its sizes and decisions from ctl.
+// One iteration of the hot path: 6 launches (k_list, k_prep, k_child_eval,
+// k_cand, k_mono, k_emit), every kernel reading its sizes and decisions from ctl.
 // pool_bound / bmax: host upper bounds of |L| and B, used for grid sizes.
 int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long bmax, cudaStream_t st,
                      IterHook* hook) {
   const long kids = P.kids;
   static unsigned g_list = 0;
-  if (!g_list) g_list = coop_grid((const void*)k_list, 4);
+  if (!g_list) g_list = coop_grid((const void*)k_list, 8);
   cudaError_t e;
   // statistics + stop test + batch size + radix select + selection (a1, a7)
   if (hook) hook->begin(3, pool_bound, st);
@@ -1339,18 +1355,16 @@ int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long 
   if (hook) hook->end(0, st);
   // bounds of every child + incumbent (a3, a4)
   if (hook) hook->begin(1, bmax * kids, st);
-  IB_DISPATCH_FID(P.fid, launch_eval_t<F>(P, w, bmax * kids, st));
+  IB_DISPATCH_FID(P.fid, launch_eval_t<F>(P, w, bmax * kids, st, true));
   if (hook) hook->end(1, st);
   if (hook) hook->exchange(st);
-  // rule out + compact + insert (a5, a6)
+  // rule out + compact + insert (a5, a6); descriptors zeroed by k_child_eval
   if (hook) hook->begin(2, bmax * kids, st);
-  IB_DISPATCH_FID(P.fid, {
-    static unsigned g_prune = 0;
-    if (!g_prune) g_prune = coop_grid((const void*)k_prune<F>, 2);
-    e = coop_launch(k_prune<F>, g_prune, st, P, w.ctl, (const double*)w.tab, w.tab_stride, (const double*)w.clb,
-                    w.cand, w.ok, (const int32_t*)w.new_slot, w.pool, w.desc, w.desc2, w.tile_ctr);
-  });
-  if (e != cudaSuccess) return (int)e;
+  k_cand<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
+  IB_DISPATCH_FID(P.fid, k_mono<F><<<grid_for(bmax * kids, TPB, 148u * 12u), TPB, 0, st>>>(
+                             P, w.ctl, w.tab, w.tab_stride, w.cand, w.ok));
+  k_emit<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok, w.new_slot,
+                                                  w.pool, w.desc2, w.tile_ctr + 1, 1);
   if (hook) hook->end(2, st);
   LAUNCH_OK;
 }
@@ -1368,7 +1382,7 @@ int launch_branch(const Problem& P, const IterBufs& w, long nb, cudaStream_t st)
   IB_DISPATCH_FID(P.fid, k_mono<F><<<grid_for(nb * kids, TPB, 148u * 12u), TPB, 0, st>>>(P, w.ctl, w.tab,
                                                                                         w.tab_stride, w.cand, w.ok));
   k_emit<<<scan_grid(nb * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok,
-                                                          w.new_slot, w.pool, w.desc2, w.tile_ctr + 1);
+                                                          w.new_slot, w.pool, w.desc2, w.tile_ctr + 1, 0);
   LAUNCH_OK;
 }
 

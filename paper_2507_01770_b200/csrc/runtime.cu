@@ -457,7 +457,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   hook.xuser = xuser;
   hook.xchg = xchg;
   hook.ctl = w.ctl;
-  const int kIterKernels = 4;  // kernels per iteration (launch_iteration)
+  const int kIterKernels = 6;  // kernels per iteration (launch_iteration)
 
   unsigned long long pcount = 1, free_top = hc.free_top, peak = 1;
   long chunk = 1;
