@@ -613,7 +613,7 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
   if (nc == 0) {
     if (tile == 0 && threadIdx.x == 0) {
       ctl->nsurv = 0;
-      if (finish) iter_end_dev(ctl, P.kids);
+      if (finish) ctl->pending_end = 1;
     }
     break;
   }
@@ -649,7 +649,9 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
       ctl->err = -2;  // IB_ENOSPACE
       ctl->done = 4;
     }
-    if (finish) iter_end_dev(ctl, P.kids);
+    // the iteration end is applied by the next k_list (other tiles may still
+    // be reading pcount as their base here)
+    if (finish) ctl->pending_end = 1;
   }
   }
 }
@@ -950,6 +952,12 @@ __device__ void iter_end_dev(Ctl* ctl, long kids) {
   ctl->evals += ctl->B * (unsigned long long)kids;
 }
 __global__ void k_iter_end(Ctl* ctl, long kids) { iter_end_dev(ctl, kids); }
+__global__ void k_apply_pending(Ctl* ctl, long kids) {
+  if (ctl->pending_end) {
+    ctl->pending_end = 0;
+    iter_end_dev(ctl, kids);
+  }
+}
 
 // ===================================================== fused cooperative kernels
 // One iteration = 4 launches: k_list (statistics, stop test, batch size,
@@ -960,10 +968,15 @@ __global__ void k_iter_end(Ctl* ctl, long kids) { iter_end_dev(ctl, kids); }
 __device__ __forceinline__ int vload(const int* p) { return *(const volatile int*)p; }
 
 __global__ void __launch_bounds__(TPB) k_list(Pool p, Ctl* ctl, unsigned int* hist, int32_t* sel_slot,
-                                              uint32_t* sel_code, uint64_t* desc, uint32_t* tile_ctr) {
+                                              uint32_t* sel_code, uint64_t* desc, uint32_t* tile_ctr, long kids) {
   cg::grid_group grid = cg::this_grid();
   if (ctl->done) return;  // uniform: read before any block writes it
   const long gtid = (long)blockIdx.x * TPB + threadIdx.x, gsize = (long)gridDim.x * TPB;
+  if (gtid == 0 && ctl->pending_end) {  // end of the previous iteration (k_emit)
+    ctl->pending_end = 0;
+    iter_end_dev(ctl, kids);
+  }
+  grid.sync();
   const long ntiles = ((long)ctl->pcount + TILE - 1) / TILE + 1;
   for (long i = gtid; i < 2 * ntiles + 2; i += gsize) desc[i] = 0;
   if (gtid == 0) tile_ctr[0] = 0;
@@ -1346,7 +1359,7 @@ int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long 
   cudaError_t e;
   // statistics + stop test + batch size + radix select + selection (a1, a7)
   if (hook) hook->begin(3, pool_bound, st);
-  e = coop_launch(k_list, g_list, st, w.pool, w.ctl, w.hist, w.sel_slot, w.sel_code, w.desc, w.tile_ctr);
+  e = coop_launch(k_list, g_list, st, w.pool, w.ctl, w.hist, w.sel_slot, w.sel_code, w.desc, w.tile_ctr, kids);
   if (e != cudaSuccess) return (int)e;
   if (hook) hook->end(3, st);
   // partition (SPSD) + tables (a2, a3)
@@ -1383,6 +1396,11 @@ int launch_branch(const Problem& P, const IterBufs& w, long nb, cudaStream_t st)
                                                                                         w.tab_stride, w.cand, w.ok));
   k_emit<<<scan_grid(nb * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok,
                                                           w.new_slot, w.pool, w.desc2, w.tile_ctr + 1, 0);
+  LAUNCH_OK;
+}
+
+int launch_apply_pending(Ctl* ctl, long kids, cudaStream_t st) {
+  k_apply_pending<<<1, 1, 0, st>>>(ctl, kids);
   LAUNCH_OK;
 }
 

@@ -70,7 +70,7 @@ struct Ctl {
   unsigned long long bmax, max_iter, pool_cap;
   unsigned long long acc_live, acc_min_key, acc_max_w;  // per-pass accumulators (statistics)
   unsigned int blocks_done;      // last-block election counter
-  unsigned int pad2;
+  unsigned int pending_end;      // the survivors of the last iteration are not yet counted in pcount
   unsigned long long sum_pool;   // records scanned by the statistics pass
   unsigned long long sum_radix;  // records scanned by radix passes 2..8
   unsigned long long sum_B;      // parents prepared

@@ -29,6 +29,7 @@ int launch_iteration(const Problem&, const IterBufs&, long, long, cudaStream_t, 
 int launch_branch(const Problem&, const IterBufs&, long, cudaStream_t);
 int launch_select_only(Pool, Ctl*, unsigned int*, long, cudaStream_t);
 int launch_xchg_put(const Ctl*, double*, cudaStream_t);
+int launch_apply_pending(Ctl*, long, cudaStream_t);
 int launch_xchg_take(Ctl*, const double*, cudaStream_t);
 int launch_partition(Pool, long, const unsigned long long*, int, unsigned long long, unsigned long long, int32_t*,
                      uint32_t*, double*, Pool, uint64_t*, uint32_t*, uint64_t*, cudaStream_t);
@@ -513,6 +514,10 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
       for (long c = 0; c < chunk; ++c) CKL(launch_iteration(P, ib, pool_bound, o.bmax, st, &hook));
     }
     nk += chunk * kIterKernels;
+    // count the survivors of the chunk's last iteration (normally done by the
+    // next iteration's k_list) before the host looks at L
+    CKL(launch_apply_pending(w.ctl, o.kids, st));
+    nk += 1;
     CK(cudaMemcpyAsync(&hc, w.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     pcount = hc.pcount;

@@ -226,3 +226,19 @@ def test_config1_ackley_n10_encloses_minimum(pb):
     for a, b, lb in list(zip(g.lo, g.hi, g.lb))[:64]:
         o = oracle.eval_box(cfg["fid"], a, b)
         assert abs(o[0] - lb) <= tol(cfg["fid"], a, b)
+
+
+@pytest.mark.parametrize("fid,n,lo,hi,m", [(1, 10, -32.768, 32.768, 2), (6, 200, -10.0, 10.0, 2)])
+def test_solve_is_deterministic_graph_and_eager(pb, fid, n, lo, hi, m):
+    """Same inputs -> bit-identical results: twice through the CUDA-graph
+    replay and once with eager launches (profiling), multi-tile lists."""
+    l, u = np.full(n, lo), np.full(n, hi)
+    res = []
+    for prof in (0, 0, 1):
+        r = pb.ib_solve(fid, l, u, 1e-6, 1e-6, pb.options(m=m, profile=prof), surv_cap=4096)
+        res.append(r)
+    for r in res[1:]:
+        assert (r.iters, r.evals, r.n_surv, r.status) == (res[0].iters, res[0].evals, res[0].n_surv, res[0].status)
+        assert r.f_lo == res[0].f_lo and r.f_hi == res[0].f_hi
+        np.testing.assert_array_equal(r.lo, res[0].lo)
+        np.testing.assert_array_equal(r.hi, res[0].hi)
