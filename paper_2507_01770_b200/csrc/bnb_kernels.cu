@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(TPB, GT ? 3 : 4) k_child_eval(Problem P, Ctl* 
   const int d = P.d, m = GT ? 2 : P.m, n = P.n, h = GT ? 3 : P.h, G = GT ? GT : P.G;
   const long gpp = P.kids / G;
   const long ngroups = (long)ctl->B * gpp;
+  const double gub0 = okey_inv(ctl->gub_key);  // incumbent before this iteration
   double best = CUDART_INF;
   for (long gi = (long)blockIdx.x * TPB + threadIdx.x; gi < ngroups; gi += (long)gridDim.x * TPB) {
     const int b = P.mbits ? (int)(gi >> (P.kbits - h * P.mbits)) : (int)(gi / gpp);
@@ -500,8 +501,9 @@ __global__ void __launch_bounds__(TPB, GT ? 3 : 4) k_child_eval(Problem P, Ctl* 
         int e[D_MAX];
         entries_of(hcode * (uint32_t)G + (uint32_t)q, P, e);
         LevyView V{T, e, d};
-        best = fmin(best, ObjLevy::outer(V.acc(true), n).hi);
-        clb[gi * G + q] = canon_lb(ObjLevy::outer(V.acc(false), n).lo);
+        const double lbq = canon_lb(ObjLevy::outer(V.acc(false), n).lo);
+        clb[gi * G + q] = lbq;
+        if (lbq <= gub0) best = fmin(best, ObjLevy::outer(V.acc(true), n).hi);
       }
     } else {
       Iv A[2], Am[2];
@@ -537,8 +539,10 @@ __global__ void __launch_bounds__(TPB, GT ? 3 : 4) k_child_eval(Problem P, Ctl* 
             Bm[k] = acc_comb<F>(k, Bm[k], get(e + 2 * F::K + 2 * k));
           }
         }
-        best = fmin(best, outer_hi<F>(Bm, n));
-        clb[gi * G + q] = canon_lb(outer_lo<F>(B, n));
+        // f(midpoint) >= lb: a child with lb > GUB_old cannot lower GUB
+        const double lbq = canon_lb(outer_lo<F>(B, n));
+        clb[gi * G + q] = lbq;
+        if (lbq <= gub0) best = fmin(best, outer_hi<F>(Bm, n));
       }
     }
   }
@@ -732,6 +736,7 @@ __device__ __forceinline__ bool last_block(Ctl* ctl) {
 
 // accumulate the statistics of this block's share of L into ctl->acc_* and
 // the top-8-bit histogram of the live keys
+template <bool WITH_W = true>
 __device__ void stats_accum_dev(const Pool& p, Ctl* ctl, unsigned int* hist) {
   __shared__ unsigned int s_h[256];
   for (int i = threadIdx.x; i < 256; i += TPB) s_h[i] = 0;
@@ -746,7 +751,7 @@ __device__ void stats_accum_dev(const Pool& p, Ctl* ctl, unsigned int* hist) {
       ++live;
       unsigned long long k = okey(lb);
       mk = k < mk ? k : mk;
-      mw = fmax(mw, p.w[r]);
+      if (WITH_W) mw = fmax(mw, p.w[r]);
       atomicAdd(&s_h[k >> 56], 1u);
     }
   }
@@ -779,25 +784,48 @@ __device__ void stats_accum_dev(const Pool& p, Ctl* ctl, unsigned int* hist) {
     if (s_h[i]) atomicAdd(&hist[i], s_h[i]);
 }
 
+// max width of the live records (only needed once the enclosure test passes)
+__device__ void maxw_accum_dev(const Pool& p, Ctl* ctl) {
+  const double gub = okey_inv(ctl->gub_key);
+  const long cnt = (long)ctl->pcount;
+  double mw = 0.0;
+  for (long r = (long)blockIdx.x * TPB + threadIdx.x; r < cnt; r += (long)gridDim.x * TPB)
+    if (p.lb[r] <= gub) mw = fmax(mw, p.w[r]);
+  mw = warp_max(mw);
+  if ((threadIdx.x & 31) == 0) atomicMax(&ctl->acc_max_w, (unsigned long long)__double_as_longlong(mw));
+}
+
 // control decisions of an iteration, by one block after the statistics pass
-__device__ void stats_control_dev(Ctl* ctl, unsigned int* hist) {
+// `wstage`: 0 = the max width was accumulated with the statistics (k_stats);
+// 1 = first call of the cooperative kernel, widths not read yet: if the
+// enclosure test GUB - GLB <= eps_f passes, ask for a width pass (returns
+// with ctl->need_w = 1); 2 = second call, after the width pass.
+__device__ void stats_control_dev(Ctl* ctl, unsigned int* hist, int wstage = 0) {
   __shared__ int s_go;
   if (threadIdx.x == 0) {
     const double gub = okey_inv(ctl->gub_key);
-    ctl->blocks_done = 0;
-    ctl->live = ctl->acc_live;
-    ctl->min_lb_key = ctl->acc_min_key;
-    ctl->max_w_bits = ctl->acc_max_w;
-    ctl->acc_live = 0;
-    ctl->acc_min_key = ~0ull;
-    ctl->acc_max_w = 0;
     s_go = 0;
+    if (wstage != 2) {
+      ctl->blocks_done = 0;
+      ctl->live = ctl->acc_live;
+      ctl->min_lb_key = ctl->acc_min_key;
+      ctl->acc_live = 0;
+      ctl->acc_min_key = ~0ull;
+    }
+    if (wstage != 1) {
+      ctl->max_w_bits = ctl->acc_max_w;
+      ctl->acc_max_w = 0;
+    }
+    ctl->need_w = 0;
     const unsigned long long L = ctl->live;
     const double glb = okey_inv(ctl->min_lb_key);
-    const double maxw = __longlong_as_double((long long)ctl->max_w_bits);
+    const bool encl = L > 0 && __dsub_ru(gub, glb) <= ctl->eps_f;
     if (L == 0) {
       ctl->done = 3;
-    } else if (maxw <= ctl->eps_x && __dsub_ru(gub, glb) <= ctl->eps_f) {
+    } else if (encl && wstage == 1) {
+      ctl->need_w = 1;  // the width test decides: run the width pass first
+      s_go = -1;
+    } else if (encl && __longlong_as_double((long long)ctl->max_w_bits) <= ctl->eps_x) {
       ctl->done = 1;
     } else if (ctl->iter >= ctl->max_iter) {
       ctl->done = 2;
@@ -818,9 +846,9 @@ __device__ void stats_control_dev(Ctl* ctl, unsigned int* hist) {
     }
   }
   __syncthreads();
-  if (s_go) {
+  if (s_go == 1) {
     block_pick_digit(ctl, hist);
-  } else {
+  } else if (s_go == 0) {
     for (int i = threadIdx.x; i < 256; i += TPB) hist[i] = 0;
     __syncthreads();
   }
@@ -980,10 +1008,16 @@ __global__ void __launch_bounds__(TPB) k_list(Pool p, Ctl* ctl, unsigned int* hi
   const long ntiles = ((long)ctl->pcount + TILE - 1) / TILE + 1;
   for (long i = gtid; i < 2 * ntiles + 2; i += gsize) desc[i] = 0;
   if (gtid == 0) tile_ctr[0] = 0;
-  stats_accum_dev(p, ctl, hist);
+  stats_accum_dev<false>(p, ctl, hist);
   grid.sync();
-  if (blockIdx.x == 0) stats_control_dev(ctl, hist);
+  if (blockIdx.x == 0) stats_control_dev(ctl, hist, 1);
   grid.sync();
+  if (vload(&ctl->need_w)) {  // enclosure narrow enough: the width test decides
+    maxw_accum_dev(p, ctl);
+    grid.sync();
+    if (blockIdx.x == 0) stats_control_dev(ctl, hist, 2);
+    grid.sync();
+  }
   for (int pass = 1; pass < 8; ++pass) {
     if (vload(&ctl->done) || vload(&ctl->resolved)) break;
     radix_accum_dev(p, ctl, hist);
@@ -1396,6 +1430,15 @@ int launch_branch(const Problem& P, const IterBufs& w, long nb, cudaStream_t st)
                                                                                         w.tab_stride, w.cand, w.ok));
   k_emit<<<scan_grid(nb * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok,
                                                           w.new_slot, w.pool, w.desc2, w.tile_ctr + 1, 0);
+  LAUNCH_OK;
+}
+
+__global__ void k_zero_w(Ctl* ctl) { ctl->acc_max_w = 0; }
+__global__ void __launch_bounds__(TPB) k_final_w(Pool p, Ctl* ctl) { maxw_accum_dev(p, ctl); }
+// max width of the live records into ctl->acc_max_w (final result)
+int launch_final_width(Pool p, Ctl* ctl, long pool_bound, cudaStream_t st) {
+  k_zero_w<<<1, 1, 0, st>>>(ctl);
+  k_final_w<<<grid_for(pool_bound, TPB, 148u * 8u), TPB, 0, st>>>(p, ctl);
   LAUNCH_OK;
 }
 

@@ -66,6 +66,8 @@ struct Ctl {
   int err;    // IB_ENOSPACE when a capacity would be exceeded
   int gdone;  // multi-GPU: every rank finished (from the exchange)
   int xdone;  // multi-GPU: this rank stopped working (local decision)
+  int need_w;  // the stop test needs the max width of L (width pass requested)
+  int pad3;
   double eps_f, eps_x;
   unsigned long long bmax, max_iter, pool_cap;
   unsigned long long acc_live, acc_min_key, acc_max_w;  // per-pass accumulators (statistics)

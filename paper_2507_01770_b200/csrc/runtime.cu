@@ -30,6 +30,7 @@ int launch_branch(const Problem&, const IterBufs&, long, cudaStream_t);
 int launch_select_only(Pool, Ctl*, unsigned int*, long, cudaStream_t);
 int launch_xchg_put(const Ctl*, double*, cudaStream_t);
 int launch_apply_pending(Ctl*, long, cudaStream_t);
+int launch_final_width(Pool, Ctl*, long, cudaStream_t);
 int launch_xchg_take(Ctl*, const double*, cudaStream_t);
 int launch_partition(Pool, long, const unsigned long long*, int, unsigned long long, unsigned long long, int32_t*,
                      uint32_t*, double*, Pool, uint64_t*, uint32_t*, uint64_t*, cudaStream_t);
@@ -545,6 +546,11 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
       if (trace) fprintf(stderr, "[ibnb] compacted L -> %llu records\n", pcount);
     }
   }
+  // exact max width of the remaining regions for the result
+  CKL(launch_final_width(w.pa, w.ctl, (long)pcount, st));
+  nk += 2;
+  CK(cudaMemcpyAsync(&hc, w.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
   const Ctl c = hc;
   int status;
   switch (c.done) {
@@ -595,7 +601,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   res->evals = (int64_t)c.evals;
   res->n_surv = live;
   res->peak_pool = (int64_t)peak;
-  std::memcpy(&res->max_width, &c.max_w_bits, 8);
+  std::memcpy(&res->max_width, &c.acc_max_w, 8);
   res->status = status;
   res->n_kernels = (int)std::min(nk, (long)INT32_MAX);
   return 0;
