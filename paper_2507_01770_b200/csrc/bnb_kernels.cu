@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(TPB) k_cand(const Problem P, Ctl* __restrict__
   cand_dev(P, ctl, clb, cand, desc, tile_ctr);
 }
 template <class F>
-__global__ void __launch_bounds__(TPB, 3) k_mono(Problem P, const Ctl* __restrict__ ctl, const double* __restrict__ tab,
+__global__ void __launch_bounds__(TPB, 4) k_mono(Problem P, const Ctl* __restrict__ ctl, const double* __restrict__ tab,
                                                  int tab_stride, const uint32_t* __restrict__ cand,
                                                  uint8_t* __restrict__ ok) {
   if (ctl->done) return;
@@ -725,6 +725,15 @@ __device__ void block_pick_digit(Ctl* ctl, unsigned int* hist) {
   __syncthreads();
 }
 
+// histogram increment aggregated over the lanes of a warp hitting the same bin
+// (lower bounds cluster, so most lanes of a warp share a bin)
+__device__ __forceinline__ void hist_add(unsigned int* s_h, unsigned bin, bool valid) {
+  const unsigned active = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
+  const unsigned peers = __match_any_sync(active, bin);
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&s_h[bin], (unsigned)__popc(peers));
+}
+
 __device__ __forceinline__ bool last_block(Ctl* ctl) {
   __shared__ bool s_last;
   __threadfence();
@@ -745,14 +754,22 @@ __device__ void stats_accum_dev(const Pool& p, Ctl* ctl, unsigned int* hist) {
   const long cnt = (long)ctl->pcount;
   unsigned long long live = 0, mk = ~0ull;
   double mw = 0.0;
-  for (long r = (long)blockIdx.x * TPB + threadIdx.x; r < cnt; r += (long)gridDim.x * TPB) {
-    double lb = p.lb[r];
-    if (lb <= gub) {
-      ++live;
-      unsigned long long k = okey(lb);
-      mk = k < mk ? k : mk;
-      if (WITH_W) mw = fmax(mw, p.w[r]);
-      atomicAdd(&s_h[k >> 56], 1u);
+  // 4 independent loads in flight per thread (memory-level parallelism)
+  const long gs = (long)gridDim.x * TPB;
+  for (long r0 = (long)blockIdx.x * TPB + threadIdx.x; r0 < cnt; r0 += 4 * gs) {
+    double lbv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) lbv[u] = r0 + u * gs < cnt ? p.lb[r0 + u * gs] : CUDART_INF;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool ok = lbv[u] <= gub;
+      unsigned long long k = okey(lbv[u]);
+      if (ok) {
+        ++live;
+        mk = k < mk ? k : mk;
+        if (WITH_W) mw = fmax(mw, p.w[r0 + u * gs]);
+      }
+      hist_add(s_h, (unsigned)(k >> 56), ok);
     }
   }
   __shared__ unsigned long long s_l[TPB / 32], s_k[TPB / 32];
@@ -789,8 +806,19 @@ __device__ void maxw_accum_dev(const Pool& p, Ctl* ctl) {
   const double gub = okey_inv(ctl->gub_key);
   const long cnt = (long)ctl->pcount;
   double mw = 0.0;
-  for (long r = (long)blockIdx.x * TPB + threadIdx.x; r < cnt; r += (long)gridDim.x * TPB)
-    if (p.lb[r] <= gub) mw = fmax(mw, p.w[r]);
+  const long gs = (long)gridDim.x * TPB;
+  for (long r0 = (long)blockIdx.x * TPB + threadIdx.x; r0 < cnt; r0 += 4 * gs) {
+    double lbv[4], wv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool in = r0 + u * gs < cnt;
+      lbv[u] = in ? p.lb[r0 + u * gs] : CUDART_INF;
+      wv[u] = in ? p.w[r0 + u * gs] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (lbv[u] <= gub) mw = fmax(mw, wv[u]);
+  }
   mw = warp_max(mw);
   if ((threadIdx.x & 31) == 0) atomicMax(&ctl->acc_max_w, (unsigned long long)__double_as_longlong(mw));
 }
@@ -872,12 +900,17 @@ __device__ void radix_accum_dev(const Pool& p, const Ctl* __restrict__ ctl, unsi
   const unsigned long long prefix = ctl->prefix;
   const int shift = 64 - known - 8;
   const long cnt = (long)ctl->pcount;
-  for (long r = (long)blockIdx.x * TPB + threadIdx.x; r < cnt; r += (long)gridDim.x * TPB) {
-    double lb = p.lb[r];
-    if (!(lb <= gub)) continue;
-    unsigned long long k = okey(lb);
-    if ((k >> (64 - known)) != prefix) continue;
-    atomicAdd(&s_h[(k >> shift) & 255u], 1u);
+  const long gs = (long)gridDim.x * TPB;
+  for (long r0 = (long)blockIdx.x * TPB + threadIdx.x; r0 < cnt; r0 += 4 * gs) {
+    double lbv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) lbv[u] = r0 + u * gs < cnt ? p.lb[r0 + u * gs] : CUDART_INF;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      unsigned long long k = okey(lbv[u]);
+      const bool ok = lbv[u] <= gub && (k >> (64 - known)) == prefix;
+      hist_add(s_h, (unsigned)((k >> shift) & 255u), ok);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 256; i += TPB)
