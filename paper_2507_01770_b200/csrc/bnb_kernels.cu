@@ -726,7 +726,8 @@ __device__ void block_pick_digit(Ctl* ctl, unsigned int* hist) {
 }
 
 // histogram increment aggregated over the lanes of a warp hitting the same bin
-// (lower bounds cluster, so most lanes of a warp share a bin)
+// (lower bounds cluster, so most lanes of a warp share a bin).  Must be
+// called by all 32 lanes (callers loop with a warp-uniform condition).
 __device__ __forceinline__ void hist_add(unsigned int* s_h, unsigned bin, bool valid) {
   const unsigned active = __ballot_sync(0xffffffffu, valid);
   if (!valid) return;
@@ -756,7 +757,7 @@ __device__ void stats_accum_dev(const Pool& p, Ctl* ctl, unsigned int* hist) {
   double mw = 0.0;
   // 4 independent loads in flight per thread (memory-level parallelism)
   const long gs = (long)gridDim.x * TPB;
-  for (long r0 = (long)blockIdx.x * TPB + threadIdx.x; r0 < cnt; r0 += 4 * gs) {
+  for (long r0 = (long)blockIdx.x * TPB + threadIdx.x; r0 - (long)(threadIdx.x & 31) < cnt; r0 += 4 * gs) {
     double lbv[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) lbv[u] = r0 + u * gs < cnt ? p.lb[r0 + u * gs] : CUDART_INF;
@@ -807,7 +808,7 @@ __device__ void maxw_accum_dev(const Pool& p, Ctl* ctl) {
   const long cnt = (long)ctl->pcount;
   double mw = 0.0;
   const long gs = (long)gridDim.x * TPB;
-  for (long r0 = (long)blockIdx.x * TPB + threadIdx.x; r0 < cnt; r0 += 4 * gs) {
+  for (long r0 = (long)blockIdx.x * TPB + threadIdx.x; r0 - (long)(threadIdx.x & 31) < cnt; r0 += 4 * gs) {
     double lbv[4], wv[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -901,7 +902,7 @@ __device__ void radix_accum_dev(const Pool& p, const Ctl* __restrict__ ctl, unsi
   const int shift = 64 - known - 8;
   const long cnt = (long)ctl->pcount;
   const long gs = (long)gridDim.x * TPB;
-  for (long r0 = (long)blockIdx.x * TPB + threadIdx.x; r0 < cnt; r0 += 4 * gs) {
+  for (long r0 = (long)blockIdx.x * TPB + threadIdx.x; r0 - (long)(threadIdx.x & 31) < cnt; r0 += 4 * gs) {
     double lbv[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) lbv[u] = r0 + u * gs < cnt ? p.lb[r0 + u * gs] : CUDART_INF;
