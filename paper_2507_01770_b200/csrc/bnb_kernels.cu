@@ -763,7 +763,7 @@ __device__ void stats_accum_dev(const Pool& p, Ctl* ctl, unsigned int* hist) {
     for (int u = 0; u < 4; ++u) lbv[u] = r0 + u * gs < cnt ? p.lb[r0 + u * gs] : CUDART_INF;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const bool ok = lbv[u] <= gub;
+      const bool ok = r0 + u * gs < cnt && lbv[u] <= gub;  // (GUB may be +inf)
       unsigned long long k = okey(lbv[u]);
       if (ok) {
         ++live;
@@ -818,7 +818,7 @@ __device__ void maxw_accum_dev(const Pool& p, Ctl* ctl) {
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (lbv[u] <= gub) mw = fmax(mw, wv[u]);
+      if (r0 + u * gs < cnt && lbv[u] <= gub) mw = fmax(mw, wv[u]);
   }
   mw = warp_max(mw);
   if ((threadIdx.x & 31) == 0) atomicMax(&ctl->acc_max_w, (unsigned long long)__double_as_longlong(mw));
@@ -909,7 +909,7 @@ __device__ void radix_accum_dev(const Pool& p, const Ctl* __restrict__ ctl, unsi
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       unsigned long long k = okey(lbv[u]);
-      const bool ok = lbv[u] <= gub && (k >> (64 - known)) == prefix;
+      const bool ok = r0 + u * gs < cnt && lbv[u] <= gub && (k >> (64 - known)) == prefix;
       hist_add(s_h, (unsigned)((k >> shift) & 255u), ok);
     }
   }
