@@ -45,8 +45,46 @@ TRAFFIC_PATH = os.path.join(ROOT, "profiles", "traffic_r01.json")
 SMS = 148
 FP64_LANES = 64
 
-# algorithmic HBM bytes per record of the list kernels
-BYTES_PER_RECORD = {"list": 24}  # statistics pass (lb, w: 16 B) + selection pass (lb: 8 B)
+# algorithmic HBM bytes of the memory-bound kernels:
+#   list: 8 B (lb, statistics pass) + 8 B (lb, selection pass) per record of L
+#         + 8 B per record of each radix pass 2..8;
+#   cand: 8 B (child lower bound) per child; emit: 1 + 4 + 8 B per candidate
+HBM_BYTES = {
+    "list": lambda p: 16 * p["units"] + 8 * p.get("radix_records", 0),
+    "cand": lambda p: 8 * p["units"],
+    "emit": lambda p: 13 * p["units"],
+}
+FP64_KERNELS = ("child_eval", "mono", "prep")
+
+
+def roofline(prof, prof_ms, fid):
+    """Roofline entry of the kernel with the largest device time."""
+    dom = max(prof, key=lambda c: prof[c]["ms"])
+    pd = prof[dom]
+    peaks = load_json(PEAKS_PATH) or {}
+    avg_s = pd["ms"] / 1e3 / max(1, pd["launches"])
+    traffic = (load_json(TRAFFIC_PATH) or {}).get(dom)
+    if dom in HBM_BYTES:
+        hbm = peaks.get("hbm_gbs", 6650.0)
+        per_launch = HBM_BYTES[dom](pd) / max(1, pd["launches"])
+        ach = per_launch / avg_s / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": traffic, "algorithmic_bytes_per_launch": per_launch,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s"}
+    else:
+        fp = load_json(FP64_PATH) or {}
+        per_unit = (fp.get(str(fid)) or {}).get(dom)
+        clock_ghz = (peaks.get("sm_max_mhz") or 1965.0) / 1e3
+        peak = SMS * FP64_LANES * 2 * clock_ghz / 1e3  # TFLOP/s
+        units = pd["units"] / max(1, pd["launches"])
+        ach = per_unit * units / avg_s / 1e12 if per_unit else None
+        roof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": peak, "unit": "TFLOP/s (FP64)",
+                "frac": (ach / peak) if ach else None, "traffic": traffic, "per_unit_flops": per_unit,
+                "units_per_launch": units,
+                "peak_source": "148 SM x 64 FP64 FMA/clk x 2 flop x sm_max_mhz (DESIGN.md)"}
+    roof["share_of_step"] = pd["ms"] / max(1e-9, prof_ms)
+    roof["avg_launch_us"] = avg_s * 1e6
+    return roof
 
 
 def env_rank():
@@ -286,38 +324,16 @@ def main():
         dist.all_reduce(enc, op=dist.ReduceOp.MIN)
         f_lo, f_hi = enc.tolist()
 
-    # ---- live roofline of the dominant kernel class (CUDA events inside the runtime)
+    # ---- live roofline of the dominant kernel (CUDA events inside the runtime)
     prof = {}
     for r in pres:
         for c, v in r.prof.items():
-            p = prof.setdefault(c, {"ms": 0.0, "launches": 0, "units": 0})
-            for k in p:
-                p[k] += v[k]
-    prof = {c: v for c, v in prof.items() if v["launches"]}
-    dom = max(prof, key=lambda c: prof[c]["ms"])
-    peaks = load_json(PEAKS_PATH) or {}
-    pd = prof[dom]
-    avg_s = pd["ms"] / 1e3 / max(1, pd["launches"])
-    units_per_launch = pd["units"] / max(1, pd["launches"])
-    traffic = (load_json(TRAFFIC_PATH) or {}).get(dom)
-    if dom in BYTES_PER_RECORD:
-        hbm = peaks.get("hbm_gbs", 6650.0)
-        ach = BYTES_PER_RECORD[dom] * units_per_launch / avg_s / 1e9
-        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "traffic": traffic, "peak_source": "measured" if "hbm_gbs" in peaks else "fallback"}
-    else:
-        fp = load_json(FP64_PATH) or {}
-        per_unit = (fp.get(str(fid)) or {}).get(dom)
-        clock_ghz = (peaks.get("sm_max_mhz") or 1965.0) / 1e3
-        peak = SMS * FP64_LANES * 2 * clock_ghz / 1e3  # TFLOP/s
-        ach = per_unit * units_per_launch / avg_s / 1e12 if per_unit else None
-        roof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": peak, "unit": "TFLOP/s (FP64)",
-                "frac": (ach / peak) if ach else None, "traffic": traffic,
-                "per_unit_flops": per_unit, "peak_source": "148 SM x 64 FP64 FMA/clk x 2 x sm_max_mhz"}
-    roof["share_of_step"] = pd["ms"] / max(1e-9, prof_ms)
-    roof["avg_launch_us"] = avg_s * 1e6
-    roof["units_per_launch"] = units_per_launch
-    roof["timing"] = "CUDA events per kernel class, second timed region (eager launches)"
+            p = prof.setdefault(c, {})
+            for k, x in v.items():
+                p[k] = p.get(k, 0) + x
+    prof = {c: v for c, v in prof.items() if v.get("launches")}
+    roof = roofline(prof, prof_ms, fid)
+    roof["timing"] = "CUDA events around each kernel, second timed region (eager launches)"
 
     # ---- e2e through the public host-buffer API (pinned host buffers)
     e2e = None
@@ -376,6 +392,7 @@ def main():
             "iters": r0.iters, "evals_per_step": r0.evals, "peak_pool": r0.peak_pool,
             "roofline": roof,
             "kernel_ms": {c: round(p["ms"] / len(pres), 4) for c, p in prof.items()},
+            "kernel_roofline": {c: roofline({c: p}, prof_ms, fid) for c, p in prof.items()},
             "profiled_ms_per_step": prof_ms / len(pres),
             "cpu_baseline": base,
             "e2e": e2e,

@@ -84,14 +84,15 @@ typedef struct {
     double max_width; /* widest remaining region (max over variables) */
     int status;       /* IB_STATUS_* */
     int n_kernels;    /* CUDA kernels this call launched */
-    /* per kernel class, filled when opt.profile = 1 (else zero):
-     * 0 prep (units: parents), 1 child_eval (children), 2 child_prune
-     * (children), 3 list: statistics + radix select + selection (records of
-     * L scanned by the statistics pass), 4 radix passes (records, units
-     * only), 5 unused */
+    /* per kernel, filled when opt.profile = 1 (else zero):
+     * 0 k_prep (units: parents), 1 k_child_eval (children), 2 k_cand
+     * (children), 3 k_list: statistics + radix select + selection (records
+     * of L at the statistics pass), 4 k_mono (candidates), 5 k_emit
+     * (candidates) */
     double t_ms[IB_NPROF];
     int64_t launches[IB_NPROF];
     int64_t units[IB_NPROF];
+    int64_t radix_records; /* records scanned by radix passes 2..8 */
 } ib_result;
 
 /* Multi-GPU incumbent exchange (GUB is the best sample

@@ -26,7 +26,7 @@ CODE_WHOLE = 0xFFFFFFFF
 _lib = None
 
 NPROF = 6
-PROF_CLASSES = ("prep", "child_eval", "child_prune", "list", "unused4", "unused5")
+PROF_CLASSES = ("prep", "child_eval", "cand", "list", "mono", "emit")
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -45,6 +45,7 @@ class IbResult(ctypes.Structure):
         ("n_surv", _i64), ("peak_pool", _i64), ("max_width", ctypes.c_double),
         ("status", ctypes.c_int), ("n_kernels", ctypes.c_int),
         ("t_ms", ctypes.c_double * NPROF), ("launches", _i64 * NPROF), ("units", _i64 * NPROF),
+        ("radix_records", _i64),
     ]
 
 
@@ -154,6 +155,7 @@ class SolveResult:
 def _res(r: IbResult, lo=None, hi=None, lb=None) -> SolveResult:
     prof = {c: {"ms": r.t_ms[i], "launches": r.launches[i], "units": r.units[i]}
             for i, c in enumerate(PROF_CLASSES)}
+    prof["list"]["radix_records"] = r.radix_records
     return SolveResult(r.f_lo, r.f_hi, r.iters, r.evals, r.n_surv, r.peak_pool, r.max_width, r.status,
                        lo, hi, lb, prof, r.n_kernels)
 

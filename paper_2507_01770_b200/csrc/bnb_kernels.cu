@@ -1006,6 +1006,7 @@ __global__ void __launch_bounds__(TPB) k_select(Pool p, Ctl* __restrict__ ctl, i
 // iteration end: the survivors become part of L
 __device__ void iter_end_dev(Ctl* ctl, long kids) {
   if (ctl->done) return;
+  ctl->sum_cand += ctl->ncand;
   ctl->sum_pool += ctl->pcount;
   ctl->sum_B += ctl->B;
   ctl->free_top -= ctl->B;  // archive slots taken by k_prep
@@ -1434,19 +1435,24 @@ int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long 
   if (hook) hook->begin(0, bmax, st);
   IB_DISPATCH_FID(P.fid, launch_prep_t<F>(P, w, bmax, w.free_list, st));
   if (hook) hook->end(0, st);
-  // bounds of every child + incumbent (a3, a4)
+  // bounds of every child + incumbent (a3, a4); zeroes the scan descriptors
   if (hook) hook->begin(1, bmax * kids, st);
   IB_DISPATCH_FID(P.fid, launch_eval_t<F>(P, w, bmax * kids, st, true));
   if (hook) hook->end(1, st);
   if (hook) hook->exchange(st);
-  // rule out + compact + insert (a5, a6); descriptors zeroed by k_child_eval
+  // rule out (a5): candidates lb <= GUB, then the first-order test
   if (hook) hook->begin(2, bmax * kids, st);
   k_cand<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
+  if (hook) hook->end(2, st);
+  if (hook) hook->begin(4, bmax * kids, st);
   IB_DISPATCH_FID(P.fid, k_mono<F><<<grid_for(bmax * kids, TPB, 148u * 12u), TPB, 0, st>>>(
                              P, w.ctl, w.tab, w.tab_stride, w.cand, w.ok));
+  if (hook) hook->end(4, st);
+  // insert the survivors into L (a6)
+  if (hook) hook->begin(5, bmax * kids, st);
   k_emit<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok, w.new_slot,
                                                   w.pool, w.desc2, w.tile_ctr + 1, 1);
-  if (hook) hook->end(2, st);
+  if (hook) hook->end(5, st);
   LAUNCH_OK;
 }
 

@@ -76,6 +76,7 @@ struct Ctl {
   unsigned long long sum_pool;   // records scanned by the statistics pass
   unsigned long long sum_radix;  // records scanned by radix passes 2..8
   unsigned long long sum_B;      // parents prepared
+  unsigned long long sum_cand;   // children that passed the lower-bound test
 };
 
 struct Problem {

@@ -589,12 +589,13 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   }
   CK(cudaStreamSynchronize(st));
   prof.collect(res);
-  res->units[0] = (int64_t)c.sum_B;
-  res->units[1] = (int64_t)c.evals;
-  res->units[2] = (int64_t)c.evals;
-  res->units[3] = (int64_t)c.sum_pool;
-  res->units[4] = (int64_t)c.sum_radix;
-  res->units[5] = 0;
+  res->units[0] = (int64_t)c.sum_B;      // prep: parents
+  res->units[1] = (int64_t)c.evals;      // child_eval: children
+  res->units[2] = (int64_t)c.evals;      // cand: children scanned
+  res->units[3] = (int64_t)c.sum_pool;   // list: records of L (statistics pass)
+  res->units[4] = (int64_t)c.sum_cand;   // mono: candidates tested
+  res->units[5] = (int64_t)c.sum_cand;   // emit: candidates scanned
+  res->radix_records = (int64_t)c.sum_radix;
   res->f_lo = live ? okey_inv_h(c.min_lb_key) : INFINITY;
   res->f_hi = okey_inv_h(c.gub_key);
   res->iters = (int64_t)c.iter;

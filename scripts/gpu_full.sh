@@ -3,7 +3,7 @@ TAG=${1:-f}
 CFG=${2:-1}
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()"
-for K in k_mono k_child_eval k_list; do
+for K in k_list; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 8 -c 1 \
     -o gpurun_out/full_${K}_${TAG} -f python scripts/prof_solve.py --config $CFG --solves 1 > gpurun_out/full_${K}_${TAG}.log 2>&1; echo $K rc=$?
 done
