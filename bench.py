@@ -46,11 +46,11 @@ SMS = 148
 FP64_LANES = 64
 
 # algorithmic HBM bytes of the memory-bound kernels:
-#   list: 8 B (lb, statistics pass) + 8 B (lb, selection pass) per record of L
-#         + 8 B per record of each radix pass 2..8;
+#   list: 12 B (index + lb) per hot entry per pass over the hot index, 8 B per
+#         record of L per refill pass, 16 B per record for a width pass;
 #   cand: 8 B (child lower bound) per child; emit: 1 + 4 + 8 B per candidate
 HBM_BYTES = {
-    "list": lambda p: 16 * p["units"] + 8 * p.get("radix_records", 0),
+    "list": lambda p: p["units"],  # counted by the kernel (hot-index scans, refills)
     "cand": lambda p: 8 * p["units"],
     "emit": lambda p: 13 * p["units"],
 }

@@ -86,8 +86,9 @@ typedef struct {
     int n_kernels;    /* CUDA kernels this call launched */
     /* per kernel, filled when opt.profile = 1 (else zero):
      * 0 k_prep (units: parents), 1 k_child_eval (children), 2 k_cand
-     * (children), 3 k_list: statistics + radix select + selection (records
-     * of L at the statistics pass), 4 k_mono (candidates), 5 k_emit
+     * (children), 3 k_list: statistics + radix select + selection on the
+     * hot index, refills (units: algorithmic bytes read), 4 k_mono
+     * (candidates), 5 k_emit
      * (candidates) */
     double t_ms[IB_NPROF];
     int64_t launches[IB_NPROF];

@@ -478,14 +478,21 @@ template <class F, int GT>
 __global__ void __launch_bounds__(TPB, GT ? 3 : 4) k_child_eval(Problem P, Ctl* __restrict__ ctl,
                                                        const double* __restrict__ tab, int tab_stride,
                                                        double* __restrict__ clb, uint64_t* zero_a, uint64_t* zero_b,
-                                                       long nzero, uint32_t* zero_ctr) {
+                                                       long nzero, uint32_t* zero_ctr, unsigned int* zero_hist) {
   if (ctl->done) return;
-  if (zero_a) {  // descriptors and tickets of the following k_cand / k_emit
-    for (long i = (long)blockIdx.x * TPB + threadIdx.x; i < nzero; i += (long)gridDim.x * TPB) {
-      zero_a[i] = 0;
+  if (zero_a) {  // descriptors and tickets of the following k_cand / k_emit,
+                 // histograms and accumulators of the next k_list
+    for (long i = (long)blockIdx.x * TPB + threadIdx.x; i < 2 * nzero; i += (long)gridDim.x * TPB) {
+      if (i < nzero) zero_a[i] = 0;
       zero_b[i] = 0;
     }
+    for (long i = (long)blockIdx.x * TPB + threadIdx.x; i < 16 * 256; i += (long)gridDim.x * TPB) zero_hist[i] = 0;
     if (blockIdx.x == 0 && threadIdx.x < 4) zero_ctr[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ctl->acc_live = ctl->acc_live2 = ctl->acc_live3 = 0;
+      ctl->acc_min_key = ctl->acc_min_key2 = ctl->acc_min_key3 = ~0ull;
+      ctl->acc_max_w = 0;
+    }
   }
   const int d = P.d, m = GT ? 2 : P.m, n = P.n, h = GT ? 3 : P.h, G = GT ? GT : P.G;
   const long gpp = P.kids / G;
@@ -605,8 +612,11 @@ __device__ void iter_end_dev(Ctl* ctl, long kids);
 __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* __restrict__ tab, int tab_stride,
                          const double* __restrict__ clb, const uint32_t* __restrict__ cand,
                          const uint8_t* __restrict__ ok, const int32_t* __restrict__ new_slot, Pool out,
-                         uint64_t* desc, uint32_t* tile_ctr, bool finish) {
+                         uint64_t* desc, uint32_t* tile_ctr, bool finish, uint32_t* hot0, uint32_t* hot1) {
+  // counters: 0 every survivor (-> L), 1 survivors with key < tau (-> hot index)
   __shared__ uint32_t s_tile;
+  uint32_t* hot = hot0 ? (ctl->hsel ? hot1 : hot0) : nullptr;
+  const unsigned long long tau = ctl->tau_key;
   for (;;) {
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
   __syncthreads();
@@ -617,22 +627,26 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
   if (nc == 0) {
     if (tile == 0 && threadIdx.x == 0) {
       ctl->nsurv = 0;
+      ctl->nsurv_hot = 0;
       if (finish) ctl->pending_end = 1;
     }
     break;
   }
   if ((long)tile >= ntiles) break;
   const long k0 = (long)tile * TILE + (long)threadIdx.x * IPT;
-  uint32_t f = 0;
+  uint32_t f = 0, fh = 0;
 #pragma unroll
   for (int q = 0; q < IPT; ++q)
-    if (k0 + q < nc && ok[k0 + q]) f |= 1u << q;
-  uint32_t c1[1] = {(uint32_t)__popc(f)}, ex[1], tot[1];
-  block_exclusive_scan<1, TPB>(c1, ex, tot);
-  uint64_t pfx[1];
-  dl_lookback<1>(desc, tile, tot, pfx);
-  const uint64_t base = ctl->pcount, cap = ctl->pool_cap;
-  uint64_t pos = base + pfx[0] + ex[0];
+    if (k0 + q < nc && ok[k0 + q]) {
+      f |= 1u << q;
+      if (hot && okey(clb[cand[k0 + q]]) < tau) fh |= 1u << q;
+    }
+  uint32_t c2[2] = {(uint32_t)__popc(f), (uint32_t)__popc(fh)}, ex[2], tot[2];
+  block_exclusive_scan<2, TPB>(c2, ex, tot);
+  uint64_t pfx[2];
+  dl_lookback<2>(desc, tile, tot, pfx);
+  const uint64_t base = ctl->pcount, cap = ctl->pool_cap, hbase = ctl->nhot;
+  uint64_t pos = base + pfx[0] + ex[0], hpos = hbase + pfx[1] + ex[1];
 #pragma unroll
   for (int q = 0; q < IPT; ++q) {
     if (f & (1u << q)) {
@@ -643,12 +657,14 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
         out.w[pos] = child_width(P, tab + (size_t)ci.b * tab_stride, ci.code);
         out.slot[pos] = new_slot[ci.b];
         out.code[pos] = ci.code;
+        if (fh & (1u << q)) hot[hpos++] = (uint32_t)pos;
       }
       ++pos;
     }
   }
   if ((long)tile == ntiles - 1 && threadIdx.x == 0) {
     ctl->nsurv = pfx[0] + tot[0];
+    ctl->nsurv_hot = pfx[1] + tot[1];
     if (base + pfx[0] + tot[0] > cap) {
       ctl->err = -2;  // IB_ENOSPACE
       ctl->done = 4;
@@ -676,9 +692,9 @@ __global__ void __launch_bounds__(TPB) k_emit(const Problem P, Ctl* __restrict__
                                               int tab_stride, const double* __restrict__ clb,
                                               const uint32_t* __restrict__ cand, const uint8_t* __restrict__ ok,
                                               const int32_t* __restrict__ new_slot, Pool out, uint64_t* desc,
-                                              uint32_t* tile_ctr, int finish) {
+                                              uint32_t* tile_ctr, int finish, uint32_t* hot0, uint32_t* hot1) {
   if (ctl->done) return;
-  emit_dev(P, ctl, tab, tab_stride, clb, cand, ok, new_slot, out, desc, tile_ctr, finish != 0);
+  emit_dev(P, ctl, tab, tab_stride, clb, cand, ok, new_slot, out, desc, tile_ctr, finish != 0, hot0, hot1);
 }
 
 // ============================================================ list L kernels
@@ -1011,6 +1027,7 @@ __device__ void iter_end_dev(Ctl* ctl, long kids) {
   ctl->sum_B += ctl->B;
   ctl->free_top -= ctl->B;  // archive slots taken by k_prep
   ctl->pcount += ctl->nsurv;
+  ctl->nhot += ctl->nsurv_hot;
   ctl->iter += 1;
   ctl->evals += ctl->B * (unsigned long long)kids;
 }
@@ -1030,41 +1047,364 @@ __global__ void k_apply_pending(Ctl* ctl, long kids) {
 // block resident); after a barrier the control block is re-read from L2.
 __device__ __forceinline__ int vload(const int* p) { return *(const volatile int*)p; }
 
-__global__ void __launch_bounds__(TPB) k_list(Pool p, Ctl* ctl, unsigned int* hist, int32_t* sel_slot,
-                                              uint32_t* sel_code, uint64_t* desc, uint32_t* tile_ctr, long kids) {
+// ------------------------------------------------------------ hot index of L
+// The selection (line 130) only ever needs the smallest lower bounds: a
+// position-ordered index of the live records with key < tau ("hot") is kept
+// next to L, and statistics / radix select / selection run on it; it is
+// rebuilt from a full pass over L (a "refill") only when it holds fewer than
+// bmax live records.  Positions in L are insertion order, so selecting the B
+// smallest (key, position) entries of the hot index is exactly the oracle's
+// rule on the whole list (every cold key >= tau > every hot key).
+
+// block-wide pick over a 256-bin histogram: smallest digit whose cumulative
+// count reaches need; every thread gets (dig, before, cnt)
+struct Pick {
+  int dig;
+  unsigned long long before, cnt, total;
+};
+__device__ Pick block_pick(const unsigned int* hist, unsigned long long need) {
+  __shared__ unsigned long long s_inc[256];
+  __shared__ Pick s_p;
+  const int t = threadIdx.x;
+  unsigned long long h = __ldcg(&hist[t]);
+  s_inc[t] = h;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {
+    unsigned long long v = t >= o ? s_inc[t - o] : 0ull;
+    __syncthreads();
+    s_inc[t] += v;
+    __syncthreads();
+  }
+  if (t == 0) s_p.dig = 255;
+  __syncthreads();
+  unsigned long long before = t ? s_inc[t - 1] : 0ull;
+  if (before < need && s_inc[t] >= need) s_p.dig = t;
+  __syncthreads();
+  if (t == 0) {
+    int d = s_p.dig;
+    s_p.before = d ? s_inc[d - 1] : 0ull;
+    s_p.cnt = s_inc[d] - s_p.before;
+    s_p.total = s_inc[255];
+  }
+  __syncthreads();
+  Pick r = s_p;
+  __syncthreads();
+  return r;
+}
+
+// accumulate (live count, min key) of a set of records of L and the
+// histogram of digit (64 - known - 8 .. 64 - known) of the live keys whose
+// top `known` bits equal prefix.  idx == nullptr: records [0, n) of L.
+__device__ void scan_keys_dev(const Pool& p, const uint32_t* __restrict__ idx, long n, double gub, int known,
+                              unsigned long long prefix, unsigned int* hist, unsigned long long* acc_live,
+                              unsigned long long* acc_min) {
+  __shared__ unsigned int s_h[256];
+  for (int i = threadIdx.x; i < 256; i += TPB) s_h[i] = 0;
+  __syncthreads();
+  const int shift = 64 - known - 8;
+  unsigned long long live = 0, mk = ~0ull;
+  const long gs = (long)gridDim.x * TPB;
+  for (long r0 = (long)blockIdx.x * TPB + threadIdx.x; r0 - (long)(threadIdx.x & 31) < n; r0 += 4 * gs) {
+    double lbv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long i = r0 + u * gs;
+      lbv[u] = i < n ? p.lb[idx ? (long)idx[i] : i] : CUDART_INF;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const unsigned long long k = okey(lbv[u]);
+      const bool ok = r0 + u * gs < n && lbv[u] <= gub && (known == 0 || (k >> (64 - known)) == prefix);
+      if (ok) {
+        ++live;
+        mk = k < mk ? k : mk;
+      }
+      hist_add(s_h, (unsigned)((k >> shift) & 255u), ok);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += TPB)
+    if (s_h[i]) atomicAdd(&hist[i], s_h[i]);
+  if (acc_live) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      live += __shfl_xor_sync(0xffffffffu, live, o);
+      unsigned long long t = __shfl_xor_sync(0xffffffffu, mk, o);
+      mk = t < mk ? t : mk;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      if (live) atomicAdd(acc_live, live);
+      atomicMin(acc_min, mk);
+    }
+  }
+}
+
+// refill: positions of the live records of L with key < tau, in order
+__device__ void hot_collect_dev(const Pool& p, long n, double gub, unsigned long long tau, uint32_t* out,
+                                unsigned long long* out_count, uint64_t* desc, uint32_t* tile_ctr) {
+  __shared__ uint32_t s_tile;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    __syncthreads();
+    const long ntiles = (n + TILE - 1) / TILE;
+    if ((long)tile >= ntiles) break;
+    const long r0 = (long)tile * TILE + (long)threadIdx.x * IPT;
+    uint32_t f = 0;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      if (r0 + q < n) {
+        const double lb = p.lb[r0 + q];
+        if (lb <= gub && okey(lb) < tau) f |= 1u << q;
+      }
+    }
+    uint32_t c1[1] = {(uint32_t)__popc(f)}, ex[1], tot[1];
+    block_exclusive_scan<1, TPB>(c1, ex, tot);
+    uint64_t pfx[1];
+    dl_lookback<1>(desc, tile, tot, pfx);
+    uint64_t pos = pfx[0] + ex[0];
+#pragma unroll
+    for (int q = 0; q < IPT; ++q)
+      if (f & (1u << q)) out[pos++] = (uint32_t)(r0 + q);
+    if ((long)tile == ntiles - 1 && threadIdx.x == 0) *out_count = pfx[0] + tot[0];
+  }
+}
+
+// selection (line 130) over the hot index: the B entries with the smallest
+// (key, position) go to the batch and are removed from L (lb = +inf); the
+// other live hot entries are kept, in order, in `hout`.  counters: 0 lt
+// (selected), 1 eq (tie class), 2 gt (kept).  known == 0 selects all.
+__device__ void hot_select_dev(const Pool& p, const uint32_t* __restrict__ hin, long n, uint32_t* hout, double gub,
+                               int known, unsigned long long prefix, unsigned long long r_need, int32_t* sel_slot,
+                               uint32_t* sel_code, unsigned long long* keep_count, uint64_t* desc,
+                               uint32_t* tile_ctr) {
+  __shared__ uint32_t s_tile;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    __syncthreads();
+    const long ntiles = (n + TILE - 1) / TILE;
+    if ((long)tile >= ntiles) break;
+    const long i0 = (long)tile * TILE + (long)threadIdx.x * IPT;
+    uint8_t cls[IPT];  // 0 lt, 1 eq, 2 gt, 3 dead
+    uint32_t rr[IPT];
+    uint32_t c3[3] = {0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      cls[q] = 3;
+      rr[q] = 0;
+      if (i0 + q < n) {
+        rr[q] = hin[i0 + q];
+        const double lb = p.lb[rr[q]];
+        if (lb <= gub) {
+          if (known == 0) {
+            cls[q] = 0;
+          } else {
+            const unsigned long long top = okey(lb) >> (64 - known);
+            cls[q] = top < prefix ? 0 : (top == prefix ? 1 : 2);
+          }
+          c3[cls[q]]++;
+        }
+      }
+    }
+    uint32_t ex[3], tot[3];
+    block_exclusive_scan<3, TPB>(c3, ex, tot);
+    uint64_t pfx[3];
+    dl_lookback<3>(desc, tile, tot, pfx);
+    uint64_t lt = pfx[0] + ex[0], eq = pfx[1] + ex[1], gt = pfx[2] + ex[2];
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      const int k = cls[q];
+      if (k == 3) continue;
+      bool sel;
+      uint64_t pos;
+      if (k == 0) {
+        sel = true;
+        pos = lt + (eq < r_need ? eq : r_need);
+        ++lt;
+      } else if (k == 1) {
+        sel = eq < r_need;
+        pos = sel ? lt + eq : gt + (eq - r_need);
+        ++eq;
+      } else {
+        sel = false;
+        pos = gt + (eq > r_need ? eq - r_need : 0);
+        ++gt;
+      }
+      if (sel) {
+        sel_slot[pos] = p.slot[rr[q]];
+        sel_code[pos] = p.code[rr[q]];
+        p.lb[rr[q]] = CUDART_INF;  // removed from L
+      } else {
+        hout[pos] = rr[q];
+      }
+    }
+    if ((long)tile == ntiles - 1 && threadIdx.x == 0) {
+      const uint64_t e = pfx[1] + tot[1];
+      *keep_count = pfx[2] + tot[2] + (e > r_need ? e - r_need : 0);
+    }
+  }
+}
+
+// One cooperative kernel per iteration for the list L (a1, a7): iteration
+// end of the previous one, hot statistics (refill when short), stop test,
+// batch size, radix select and selection.  Every block takes the same
+// decisions from the same global values after each grid barrier; thread 0
+// of block 0 records them in ctl.  hists: 16 x 256 zeroed counters (zeroed
+// again by k_child_eval); the acc_* fields likewise.
+__global__ void __launch_bounds__(TPB) k_list(Pool p, Ctl* ctl, unsigned int* hists, int32_t* sel_slot,
+                                              uint32_t* sel_code, uint64_t* desc, uint64_t* desc2, uint32_t* tile_ctr,
+                                              uint32_t* hot0, uint32_t* hot1, long kids) {
   cg::grid_group grid = cg::this_grid();
   if (ctl->done) return;  // uniform: read before any block writes it
   const long gtid = (long)blockIdx.x * TPB + threadIdx.x, gsize = (long)gridDim.x * TPB;
-  if (gtid == 0 && ctl->pending_end) {  // end of the previous iteration (k_emit)
+  const bool lead = gtid == 0;
+  if (lead && ctl->pending_end) {  // end of the previous iteration (k_emit)
     ctl->pending_end = 0;
     iter_end_dev(ctl, kids);
   }
   grid.sync();
-  const long ntiles = ((long)ctl->pcount + TILE - 1) / TILE + 1;
-  for (long i = gtid; i < 2 * ntiles + 2; i += gsize) desc[i] = 0;
-  if (gtid == 0) tile_ctr[0] = 0;
-  stats_accum_dev<false>(p, ctl, hist);
-  grid.sync();
-  if (blockIdx.x == 0) stats_control_dev(ctl, hist, 1);
-  grid.sync();
-  if (vload(&ctl->need_w)) {  // enclosure narrow enough: the width test decides
-    maxw_accum_dev(p, ctl);
-    grid.sync();
-    if (blockIdx.x == 0) stats_control_dev(ctl, hist, 2);
-    grid.sync();
-  }
-  for (int pass = 1; pass < 8; ++pass) {
-    if (vload(&ctl->done) || vload(&ctl->resolved)) break;
-    radix_accum_dev(p, ctl, hist);
-    grid.sync();
-    if (blockIdx.x == 0) {
-      if (threadIdx.x == 0) ctl->sum_radix += ctl->pcount;
-      block_pick_digit(ctl, hist);
+  const double gub = okey_inv(ctl->gub_key);
+  const long pc = (long)ctl->pcount;
+  const unsigned long long bmax = ctl->bmax;
+  int hsel = ctl->hsel;
+  long nh = (long)ctl->nhot;
+  unsigned long long tau = ctl->tau_key;
+  const bool valid = ctl->hot_valid != 0;
+  unsigned long long bytes = 0;
+  {
+    const long tl = (pc + TILE - 1) / TILE + 1;
+    for (long i = gtid; i < 3 * tl; i += gsize) {
+      desc2[i] = 0;
+      if (i < tl) desc[i] = 0;
     }
-    grid.sync();
+    if (lead) {
+      tile_ctr[0] = 0;
+      tile_ctr[1] = 0;
+    }
   }
-  if (vload(&ctl->done)) return;
-  select_dev(p, ctl, sel_slot, sel_code, desc, tile_ctr);
+  // statistics of the hot entries + histogram of their top 8 key bits
+  unsigned long long live = 0, minkey = ~0ull;
+  const unsigned int* hh = hists;
+  if (valid) {
+    scan_keys_dev(p, hsel ? hot1 : hot0, nh, gub, 0, 0, hists, &ctl->acc_live, &ctl->acc_min_key);
+    bytes += 12ull * nh;
+  }
+  grid.sync();
+  if (valid) {
+    live = __ldcg(&ctl->acc_live);
+    minkey = __ldcg(&ctl->acc_min_key);
+  }
+  if (!valid || (live < bmax && tau != ~0ull)) {
+    // refill: histogram of all live keys of L, threshold tau for ~hot_target entries
+    scan_keys_dev(p, nullptr, pc, gub, 0, 0, hists + 256, &ctl->acc_live2, &ctl->acc_min_key2);
+    bytes += 8ull * pc;
+    grid.sync();
+    const unsigned long long total = __ldcg(&ctl->acc_live2), target = ctl->hot_target;
+    unsigned long long new_tau = ~0ull;
+    if (total > target) {
+      Pick a = block_pick(hists + 256, target);
+      if (a.before + a.cnt > 2 * target) {  // refine inside the boundary bucket
+        scan_keys_dev(p, nullptr, pc, gub, 8, (unsigned long long)a.dig, hists + 512, nullptr, nullptr);
+        bytes += 8ull * pc;
+        grid.sync();
+        Pick b2 = block_pick(hists + 512, target - a.before);
+        const unsigned long long t16 = ((unsigned long long)a.dig << 8) | (unsigned long long)b2.dig;
+        new_tau = t16 == 0xffffull ? ~0ull : (t16 + 1) << 48;
+      } else {
+        new_tau = a.dig == 255 ? ~0ull : ((unsigned long long)a.dig + 1) << 56;
+      }
+    }
+    uint32_t* hout = hsel ? hot0 : hot1;
+    hot_collect_dev(p, pc, gub, new_tau, hout, &ctl->nhot_keep, desc, tile_ctr);
+    bytes += 8ull * pc;
+    grid.sync();
+    hsel ^= 1;
+    nh = (long)__ldcg(&ctl->nhot_keep);
+    tau = new_tau;
+    if (lead) {
+      ctl->hsel = hsel;
+      ctl->nhot = (unsigned long long)nh;
+      ctl->tau_key = tau;
+      ctl->hot_valid = 1;
+      ctl->live_total = total;
+      ctl->sum_refill += (unsigned long long)pc;
+      ctl->compact_hint = total < (unsigned long long)pc / 2;
+      tile_ctr[1] = 0;
+    }
+    // statistics of the rebuilt hot index
+    scan_keys_dev(p, hsel ? hot1 : hot0, nh, gub, 0, 0, hists + 2560, &ctl->acc_live3, &ctl->acc_min_key3);
+    bytes += 12ull * nh;
+    grid.sync();
+    live = __ldcg(&ctl->acc_live3);
+    minkey = __ldcg(&ctl->acc_min_key3);
+    hh = hists + 2560;
+  }
+  // stop test (line 148: every region narrower than eps_x; line 150:
+  // GUB - GLB <= eps_f); GLB = smallest hot key (all cold keys are larger)
+  int done = 0;
+  if (live == 0) {
+    done = 3;  // the refill found no live record: L is empty
+  } else if (__dsub_ru(gub, okey_inv(minkey)) <= ctl->eps_f) {
+    maxw_accum_dev(p, ctl);  // the width test decides: max width of all of L
+    bytes += 16ull * pc;
+    grid.sync();
+    if (__longlong_as_double((long long)__ldcg(&ctl->acc_max_w)) <= ctl->eps_x) done = 1;
+  }
+  if (!done && ctl->iter >= ctl->max_iter) done = 2;
+  const unsigned long long B = live < bmax ? live : bmax;
+  if (!done && ctl->free_top < B) done = 4;  // archive full
+  if (done) {
+    if (lead) {
+      ctl->live = live;
+      ctl->min_lb_key = minkey;
+      ctl->max_w_bits = ctl->acc_max_w;
+      if (done == 4) ctl->err = -2;
+      ctl->list_bytes += bytes;
+      ctl->done = done;
+    }
+    return;
+  }
+  // radix select of the B-th smallest hot key (line 130, reading R1)
+  int known = 0;
+  unsigned long long prefix = 0, need = B;
+  bool resolved = live <= bmax;
+  if (!resolved) {
+    Pick a = block_pick(hh, need);
+    need -= a.before;
+    prefix = (unsigned long long)a.dig;
+    known = 8;
+    resolved = a.cnt == need;
+  }
+  for (int pass = 1; pass < 8 && !resolved; ++pass) {
+    unsigned int* hp = hists + (2 + pass) * 256;
+    scan_keys_dev(p, hsel ? hot1 : hot0, nh, gub, known, prefix, hp, nullptr, nullptr);
+    bytes += 12ull * nh;
+    grid.sync();
+    Pick a = block_pick(hp, need);
+    need -= a.before;
+    prefix = (prefix << 8) | (unsigned long long)a.dig;
+    known += 8;
+    resolved = a.cnt == need || known >= 64;
+  }
+  // selection + compaction of the hot index into the other buffer
+  hot_select_dev(p, hsel ? hot1 : hot0, nh, hsel ? hot0 : hot1, gub, resolved && known == 0 ? 0 : known, prefix,
+                 known == 0 ? 0ull : need, sel_slot, sel_code, &ctl->nhot_keep, desc2, tile_ctr + 1);
+  bytes += 16ull * nh;
+  grid.sync();
+  if (lead) {
+    ctl->hsel = hsel ^ 1;
+    ctl->nhot = __ldcg(&ctl->nhot_keep);
+    ctl->B = B;
+    ctl->live = live;
+    ctl->min_lb_key = minkey;
+    ctl->known = known;
+    ctl->prefix = prefix;
+    ctl->need = need;
+    ctl->list_bytes += bytes;
+  }
 }
 
 template <class F>
@@ -1089,7 +1429,7 @@ __global__ void __launch_bounds__(TPB, 2) k_prune(Problem P, Ctl* ctl, const dou
   grid.sync();
   mono_dev<F>(P, ctl, tab, tab_stride, cand, ok);
   grid.sync();
-  emit_dev(P, ctl, tab, tab_stride, clb, cand, ok, new_slot, out, desc2, tile_ctr + 1, false);
+  emit_dev(P, ctl, tab, tab_stride, clb, cand, ok, new_slot, out, desc2, tile_ctr + 1, false, nullptr, nullptr);
   grid.sync();
   if (gtid == 0) iter_end_dev(ctl, P.kids);
 }
@@ -1397,9 +1737,9 @@ static void launch_eval_t(const Problem& P, const IterBufs& w, long nkids, cudaS
   uint64_t* zb = zero ? w.desc2 : nullptr;
   long nz = tiles_for(nkids) + 1;
   if (P.m == 2 && P.G == 8 && !F::CHAIN)
-    k_child_eval<F, 8><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr);
+    k_child_eval<F, 8><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr, w.hist);
   else
-    k_child_eval<F, 0><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr);
+    k_child_eval<F, 0><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr, w.hist);
 }
 
 // co-resident grid of a cooperative kernel (all blocks active at once)
@@ -1428,7 +1768,8 @@ int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long 
   cudaError_t e;
   // statistics + stop test + batch size + radix select + selection (a1, a7)
   if (hook) hook->begin(3, pool_bound, st);
-  e = coop_launch(k_list, g_list, st, w.pool, w.ctl, w.hist, w.sel_slot, w.sel_code, w.desc, w.tile_ctr, kids);
+  e = coop_launch(k_list, g_list, st, w.pool, w.ctl, w.hist, w.sel_slot, w.sel_code, w.desc, w.desc2, w.tile_ctr,
+                  w.hot0, w.hot1, kids);
   if (e != cudaSuccess) return (int)e;
   if (hook) hook->end(3, st);
   // partition (SPSD) + tables (a2, a3)
@@ -1451,7 +1792,7 @@ int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long 
   // insert the survivors into L (a6)
   if (hook) hook->begin(5, bmax * kids, st);
   k_emit<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok, w.new_slot,
-                                                  w.pool, w.desc2, w.tile_ctr + 1, 1);
+                                                  w.pool, w.desc2, w.tile_ctr + 1, 1, w.hot0, w.hot1);
   if (hook) hook->end(5, st);
   LAUNCH_OK;
 }
@@ -1463,13 +1804,13 @@ int launch_branch(const Problem& P, const IterBufs& w, long nb, cudaStream_t st)
   IB_DISPATCH_FID(P.fid, launch_prep_t<F>(P, w, nb, nullptr, st));
   IB_DISPATCH_FID(P.fid, launch_eval_t<F>(P, w, nb * kids, st));
   cudaMemsetAsync(w.desc, 0, sizeof(uint64_t) * (size_t)tiles_for(nb * kids), st);
-  cudaMemsetAsync(w.desc2, 0, sizeof(uint64_t) * (size_t)tiles_for(nb * kids), st);
+  cudaMemsetAsync(w.desc2, 0, sizeof(uint64_t) * 2 * (size_t)tiles_for(nb * kids), st);
   cudaMemsetAsync(w.tile_ctr, 0, sizeof(uint32_t) * 4, st);
   k_cand<<<scan_grid(nb * kids), TPB, 0, st>>>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
   IB_DISPATCH_FID(P.fid, k_mono<F><<<grid_for(nb * kids, TPB, 148u * 12u), TPB, 0, st>>>(P, w.ctl, w.tab,
                                                                                         w.tab_stride, w.cand, w.ok));
   k_emit<<<scan_grid(nb * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok,
-                                                          w.new_slot, w.pool, w.desc2, w.tile_ctr + 1, 0);
+                                                          w.new_slot, w.pool, w.desc2, w.tile_ctr + 1, 0, nullptr, nullptr);
   LAUNCH_OK;
 }
 

@@ -71,12 +71,27 @@ struct Ctl {
   double eps_f, eps_x;
   unsigned long long bmax, max_iter, pool_cap;
   unsigned long long acc_live, acc_min_key, acc_max_w;  // per-pass accumulators (statistics)
+  unsigned long long acc_live2, acc_min_key2;           // refill pass
+  unsigned long long acc_live3, acc_min_key3;           // rebuilt hot index
+  unsigned long long list_bytes;                        // algorithmic bytes of k_list
   unsigned int blocks_done;      // last-block election counter
   unsigned int pending_end;      // the survivors of the last iteration are not yet counted in pcount
   unsigned long long sum_pool;   // records scanned by the statistics pass
   unsigned long long sum_radix;  // records scanned by radix passes 2..8
   unsigned long long sum_B;      // parents prepared
   unsigned long long sum_cand;   // children that passed the lower-bound test
+  // hot index of L: positions (increasing) of the records with key < tau_key
+  unsigned long long tau_key;    // ~0: every record is hot
+  unsigned long long nhot;       // entries of the current hot buffer
+  unsigned long long nsurv_hot;  // survivors of this iteration appended to it
+  unsigned long long nhot_keep;  // entries kept by the selection
+  unsigned long long hot_target; // hot index size aimed at by a refill
+  unsigned long long sum_refill; // records of L scanned by refills
+  unsigned long long live_total; // live records of L at the last refill
+  int hsel;       // current hot buffer (0 / 1)
+  int hot_valid;  // 0: the hot index must be rebuilt (start, after compaction)
+  int compact_hint;  // a refill found L more than half dead
+  int pad4;
 };
 
 struct Problem {
@@ -108,6 +123,7 @@ struct IterBufs {
   uint8_t* ok;
   uint64_t *desc, *desc2;
   uint32_t* tile_ctr;
+  uint32_t *hot0, *hot1;  // hot index double buffer
 };
 
 // host callbacks around the kernel classes of an iteration: profiling

@@ -74,7 +74,13 @@ __global__ void k_root(const double* root_out, double w0, Pool p, Ctl* ctl) {
   p.code[0] = CODE_WHOLE;
   ctl->pcount = 1;
 }
-__global__ void k_set_pcount(Ctl* ctl, const uint64_t* c) { ctl->pcount = *c; }
+// after a compaction of L: new record count, positions changed -> rebuild the hot index
+__global__ void k_set_pcount(Ctl* ctl, const uint64_t* c) {
+  ctl->pcount = *c;
+  ctl->hot_valid = 0;
+  ctl->nhot = 0;
+  ctl->compact_hint = 0;
+}
 __global__ void k_branch_ctl(Ctl* ctl, const double* gub, long nb, long cap) {
   unsigned long long* z = reinterpret_cast<unsigned long long*>(ctl);
   for (size_t i = 0; i < sizeof(Ctl) / 8; ++i) z[i] = 0ull;
@@ -197,7 +203,7 @@ static long tiles_of(long n) { return std::max(1L, (n + TILE - 1) / TILE); }
 struct SolveWs {
   Pool pa, pb;
   int32_t *sel_slot, *new_slot, *sc, *free_list;
-  uint32_t *sel_code, *cand;
+  uint32_t *sel_code, *cand, *hot0, *hot1;
   uint8_t *ok, *mark;
   double *alo, *ahi, *tab, *clb, *l, *u, *root_out;
   uint64_t *desc, *desc2, *cnt;
@@ -230,11 +236,13 @@ static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
   w.ok = A.take<uint8_t>((size_t)kids_tot);
   long tiles = tiles_of(std::max({o.pool_cap, kids_tot, o.arch_cap})) + 2;
   w.desc = A.take<uint64_t>((size_t)tiles * 3);
-  w.desc2 = A.take<uint64_t>((size_t)tiles);
+  w.desc2 = A.take<uint64_t>((size_t)tiles * 3);
+  w.hot0 = A.take<uint32_t>(o.pool_cap);
+  w.hot1 = A.take<uint32_t>(o.pool_cap);
   w.cnt = A.take<uint64_t>(4);
   w.tile_ctr = A.take<uint32_t>(4);
   w.ctl = A.take<Ctl>(1);
-  w.hist = A.take<unsigned int>(256);
+  w.hist = A.take<unsigned int>(16 * 256);
   w.l = A.take<double>(n);
   w.u = A.take<double>(n);
   w.root_out = A.take<double>(2);
@@ -420,9 +428,12 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   hc.bmax = (unsigned long long)o.bmax;
   hc.max_iter = (unsigned long long)o.max_iter;
   hc.pool_cap = (unsigned long long)o.pool_cap;
-  hc.acc_min_key = ~0ull;
+  hc.acc_min_key = hc.acc_min_key2 = hc.acc_min_key3 = ~0ull;
+  hc.tau_key = ~0ull;
+  hc.hot_valid = 0;  // built by the first iteration's refill
+  hc.hot_target = (unsigned long long)(8 * o.bmax + 16384);
   CK(cudaMemcpyAsync(w.ctl, &hc, sizeof hc, cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(w.hist, 0, 256 * sizeof(unsigned int), st));
+  CK(cudaMemsetAsync(w.hist, 0, 16 * 256 * sizeof(unsigned int), st));
   CK(cudaMemcpyAsync(w.alo, w.l, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(w.ahi, w.u, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemsetAsync(w.sc, 0, sizeof(int32_t), st));
@@ -453,6 +464,8 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   ib.desc = w.desc;
   ib.desc2 = w.desc2;
   ib.tile_ctr = w.tile_ctr;
+  ib.hot0 = w.hot0;
+  ib.hot1 = w.hot1;
   Hook hook;
   hook.prof = &prof;
   hook.xfn = xfn;
@@ -530,11 +543,9 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
               chunk, hc.iter, hc.pcount, hc.live, hc.B, hc.done);
     if (xfn ? hc.gdone : hc.done) break;
     chunk = std::min(chunk * 2, 32L);
-    // lazy deletion leaves selected / ruled-out records in L: compact when
-    // more than half of it is dead (list order preserved)
-    long live_now = (long)hc.live - (long)hc.B + (long)hc.nsurv;
-    long dead = (long)pcount - std::max(0L, live_now);
-    if (dead > std::max((long)pcount / 2, 1L << 18)) {
+    // lazy deletion leaves selected / ruled-out records in L: compact when a
+    // refill of the hot index found it more than half dead
+    if (hc.compact_hint && (long)pcount > (1L << 18)) {
       CKL(launch_partition(w.pa, (long)pcount, &w.ctl->gub_key, 64, 0ull, 0ull, nullptr, nullptr, nullptr, w.pb,
                            w.desc, w.tile_ctr, w.cnt, st));
       k_set_pcount<<<1, 1, 0, st>>>(w.ctl, w.cnt);
@@ -563,7 +574,10 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   CKL(launch_partition(w.pa, (long)pcount, &w.ctl->gub_key, 64, 0ull, 0ull, nullptr, nullptr, nullptr, w.pb, w.desc,
                        w.tile_ctr, w.cnt, st));
   nk += 1;
-  const long live = (long)c.live;
+  uint64_t live_all = 0;  // every live region of L (hot and cold)
+  CK(cudaMemcpyAsync(&live_all, w.cnt, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const long live = (long)live_all;
   const long ncopy = std::min((long)surv_cap, live);
   if (so_lo && so_hi && ncopy > 0) {
     if (host_out) {
@@ -592,7 +606,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   res->units[0] = (int64_t)c.sum_B;      // prep: parents
   res->units[1] = (int64_t)c.evals;      // child_eval: children
   res->units[2] = (int64_t)c.evals;      // cand: children scanned
-  res->units[3] = (int64_t)c.sum_pool;   // list: records of L (statistics pass)
+  res->units[3] = (int64_t)c.list_bytes;  // list: algorithmic bytes (hot scans, refills, width passes)
   res->units[4] = (int64_t)c.sum_cand;   // mono: candidates tested
   res->units[5] = (int64_t)c.sum_cand;   // emit: candidates scanned
   res->radix_records = (int64_t)c.sum_radix;
@@ -692,7 +706,7 @@ static size_t branch_layout(int n, int d, int m, long nb, Arena& A, BranchWs& w)
   w.cand = A.take<uint32_t>((size_t)nb * kids);
   w.ok = A.take<uint8_t>((size_t)nb * kids);
   w.desc = A.take<uint64_t>((size_t)tiles_of(nb * kids) + 2);
-  w.desc2 = A.take<uint64_t>((size_t)tiles_of(nb * kids) + 2);
+  w.desc2 = A.take<uint64_t>((size_t)2 * tiles_of(nb * kids) + 4);
   w.tile_ctr = A.take<uint32_t>(4);
   w.ctl = A.take<Ctl>(1);
   return A.off + 256;
