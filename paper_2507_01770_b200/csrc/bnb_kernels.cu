@@ -1331,6 +1331,7 @@ __global__ void __launch_bounds__(TPB) k_list(Pool p, Ctl* ctl, unsigned int* hi
       ctl->hot_valid = 1;
       ctl->live_total = total;
       ctl->sum_refill += (unsigned long long)pc;
+      ctl->nrefill += 1;
       ctl->compact_hint = total < (unsigned long long)pc / 2;
       tile_ctr[1] = 0;
     }
@@ -1350,6 +1351,7 @@ __global__ void __launch_bounds__(TPB) k_list(Pool p, Ctl* ctl, unsigned int* hi
   } else if (__dsub_ru(gub, okey_inv(minkey)) <= ctl->eps_f) {
     maxw_accum_dev(p, ctl);  // the width test decides: max width of all of L
     bytes += 16ull * pc;
+    if (lead) ctl->nwidth += 1;
     grid.sync();
     if (__longlong_as_double((long long)__ldcg(&ctl->acc_max_w)) <= ctl->eps_x) done = 1;
   }

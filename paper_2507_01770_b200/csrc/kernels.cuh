@@ -88,6 +88,8 @@ struct Ctl {
   unsigned long long hot_target; // hot index size aimed at by a refill
   unsigned long long sum_refill; // records of L scanned by refills
   unsigned long long live_total; // live records of L at the last refill
+  unsigned long long nrefill;    // refills so far
+  unsigned long long nwidth;     // width passes so far
   int hsel;       // current hot buffer (0 / 1)
   int hot_valid;  // 0: the hot index must be rebuilt (start, after compaction)
   int compact_hint;  // a refill found L more than half dead

@@ -539,8 +539,9 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
     peak = std::max(peak, pcount);
     if (hc.err) return fail(hc.err, "capacity exceeded on the device (L %ld, archive %ld)", o.pool_cap, o.arch_cap);
     if (trace)
-      fprintf(stderr, "[ibnb] t=%.3f ms chunk=%ld iter=%llu |L|=%llu live=%llu B=%llu done=%d\n", now() - t_start,
-              chunk, hc.iter, hc.pcount, hc.live, hc.B, hc.done);
+      fprintf(stderr, "[ibnb] t=%.3f ms chunk=%ld iter=%llu |L|=%llu live_hot=%llu nhot=%llu B=%llu refills=%llu "
+              "width_passes=%llu done=%d\n", now() - t_start, chunk, hc.iter, hc.pcount, hc.live, hc.nhot, hc.B,
+              hc.nrefill, hc.nwidth, hc.done);
     if (xfn ? hc.gdone : hc.done) break;
     chunk = std::min(chunk * 2, 32L);
     // lazy deletion leaves selected / ruled-out records in L: compact when a
