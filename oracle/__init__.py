@@ -60,7 +60,7 @@ class SolveResult(ctypes.Structure):
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (make)."""
-    srcs = [os.path.join(_HERE, f) for f in ("ia.c", "fns.c", "bnb.c", "ia.h", "oracle.h")]
+    srcs = [os.path.join(_HERE, f) for f in ("ia.c", "fns.c", "bnb.c", "search.c", "ia.h", "oracle.h")]
     if (
         not force
         and os.path.exists(_LIB_PATH)
@@ -89,8 +89,14 @@ def lib():
                                     _lp]
             L.or_solve.argtypes = [ctypes.c_int, ctypes.c_int, _dp, _dp, ctypes.c_double,
                                    ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_long,
-                                   ctypes.c_int, ctypes.c_long, ctypes.c_long, _dp, _dp, _dp,
-                                   ctypes.POINTER(SolveResult)]
+                                   ctypes.c_int, ctypes.c_long, ctypes.c_long, ctypes.c_int,
+                                   _dp, _dp, _dp, ctypes.POINTER(SolveResult)]
+            L.or_search_candidate.argtypes = [ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                              ctypes.c_int, _dp]
+            L.or_search_propose.argtypes = [ctypes.c_int, ctypes.c_int, _dp, _dp, _dp,
+                                            ctypes.c_double, _dp, _dp]
+            L.or_search.argtypes = [ctypes.c_int, ctypes.c_int, _dp, _dp, ctypes.c_int, _dp, _dp,
+                                    _ip]
             for fn in ("ia_add_dn", "ia_add_up", "ia_sub_dn", "ia_sub_up", "ia_mul_dn",
                        "ia_mul_up", "ia_div_dn", "ia_div_up"):
                 getattr(L, fn).argtypes = [ctypes.c_double, ctypes.c_double]
@@ -201,7 +207,7 @@ def branch(fid, plo, phi, pcyc, d, m, l, u, mono=True, gub_in=float("inf")):
 
 
 def solve(fid, l, u, eps_f=1e-6, eps_x=1e-6, d=10, m=2, bmax=4096, mono=True,
-          max_iter=10_000, cap=1 << 16):
+          max_iter=10_000, cap=1 << 16, search=0):
     l, u = _f64(l), _f64(u)
     n = l.size
     slo = np.zeros((cap, n))
@@ -209,7 +215,8 @@ def solve(fid, l, u, eps_f=1e-6, eps_x=1e-6, d=10, m=2, bmax=4096, mono=True,
     slb = np.zeros(cap)
     res = SolveResult()
     rc = lib().or_solve(fid, n, _d(l), _d(u), float(eps_f), float(eps_x), int(d), int(m),
-                        int(bmax), int(bool(mono)), int(max_iter), int(cap), _d(slo), _d(shi),
+                        int(bmax), int(bool(mono)), int(max_iter), int(cap), int(search),
+                        _d(slo), _d(shi),
                         _d(slb), ctypes.byref(res))
     if rc < 0:
         raise ValueError(f"or_solve rc={rc}")
@@ -225,3 +232,34 @@ def solve(fid, l, u, eps_f=1e-6, eps_x=1e-6, d=10, m=2, bmax=4096, mono=True,
         "hi": shi[:k],
         "lb": slb[:k],
     }
+
+
+# ---------------------------------------------------------------- search (R9)
+SEARCH_GRID, SEARCH_SCALES, SEARCH_ALPHAS = 32, 48, 8
+SEARCH_CANDS = SEARCH_GRID + 2 * SEARCH_SCALES
+
+
+def search_candidate(xi: float, li: float, ui: float, c: int):
+    """Candidate c of one variable (reading R9), None when outside [li, ui]."""
+    p = ctypes.c_double()
+    ok = lib().or_search_candidate(float(xi), float(li), float(ui), int(c), ctypes.byref(p))
+    return p.value if ok else None
+
+
+def search_propose(fid, x, l, u, fcur):
+    """One proposal step of the R9 search: (xs, fb)."""
+    x, l, u = _f64(x), _f64(l), _f64(u)
+    xs = np.zeros_like(x)
+    fb = np.zeros_like(x)
+    lib().or_search_propose(fid, x.size, _d(x), _d(l), _d(u), float(fcur), _d(xs), _d(fb))
+    return xs, fb
+
+
+def search(fid, l, u, rounds=32):
+    """R9 coordinate pattern search from the midpoint: (x, f_upper, rounds)."""
+    l, u = _f64(l), _f64(u)
+    x = np.zeros_like(l)
+    f = ctypes.c_double()
+    r = ctypes.c_int()
+    lib().or_search(fid, l.size, _d(l), _d(u), int(rounds), _d(x), ctypes.byref(f), ctypes.byref(r))
+    return x, f.value, r.value

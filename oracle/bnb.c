@@ -173,7 +173,7 @@ static int rec_cmp(const void* a, const void* b) {
 }
 
 int or_solve(int fid, int n, const double* l, const double* u, double eps_f, double eps_x, int d,
-             int m, long bmax, int mono, long max_iter, long cap, double* surv_lo,
+             int m, long bmax, int mono, long max_iter, long cap, int search, double* surv_lo,
              double* surv_hi, double* surv_lb, or_result_t* res) {
     if (d > n) d = n;
     if (d < 1 || m < 2 || bmax < 1) return -1;
@@ -194,6 +194,15 @@ int or_solve(int fid, int n, const double* l, const double* u, double eps_f, dou
     pn = 1;
 
     double gub = INFINITY;
+    /* initial incumbent from the coordinate pattern search (reading R9,
+     * oracle/search.c); search = its round limit, 0 = no search */
+    if (search > 0) {
+        double* xs0 = (double*)malloc(sizeof(double) * (size_t)n);
+        double fs = INFINITY;
+        or_search(fid, n, l, u, search, xs0, &fs, NULL);
+        if (fs < gub) gub = fs;
+        free(xs0);
+    }
     long iter = 0, evals = 0;
     int status = 1;
     double* clo = (double*)malloc(sizeof(double) * (size_t)n);

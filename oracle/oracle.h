@@ -34,8 +34,14 @@ typedef struct {
     int status; /* 0 converged, 1 max_iter, 2 pool empty, <0 error */
 } or_result_t;
 
+int or_search_candidate(double xi, double li, double ui, int c, double* p);
+int or_search_propose(int fid, int n, const double* x, const double* l, const double* u,
+                      double fcur, double* xs, double* fb);
+int or_search(int fid, int n, const double* l, const double* u, int rmax, double* x_out,
+              double* f_out, int* rounds_out);
+
 int or_solve(int fid, int n, const double* l, const double* u, double eps_f, double eps_x, int d,
-             int m, long bmax, int mono, long max_iter, long cap, double* surv_lo,
+             int m, long bmax, int mono, long max_iter, long cap, int search, double* surv_lo,
              double* surv_hi, double* surv_lb, or_result_t* res);
 
 #endif
