@@ -67,6 +67,11 @@ typedef struct {
                          1 on [default], -1 off */
     int profile;      /* 1: time every kernel launch with CUDA events on the
                          solve stream (ib_result.t_ms / launches / units) */
+    int search;       /* rounds of the coordinate pattern search that supplies
+                         the initial incumbent GUB before the first iteration
+                         (sampling, §3.1; reading R9;
+                         see ib_search) [32]; -1 = no search */
+    int reserved;     /* must be 0 */
     int64_t bmax;     /* regions selected per iteration (smallest lower bounds,
                          line 130, batched) [max(1, 2^22 / m^d)] */
     int64_t max_iter; /* iteration limit [1,000,000] */
@@ -94,6 +99,8 @@ typedef struct {
     int64_t launches[IB_NPROF];
     int64_t units[IB_NPROF];
     int64_t radix_records; /* records scanned by radix passes 2..8 */
+    double f_search;       /* GUB supplied by the initial search (+inf: none) */
+    int64_t search_rounds; /* accepted moves of that search */
 } ib_result;
 
 /* Multi-GPU incumbent exchange (GUB is the best sample
@@ -165,6 +172,25 @@ int ib_branch(int fid, int n, int d, int m, int mono, int64_t nb, const double* 
               int64_t ld, const int32_t* pcyc, const double* l, const double* u, double* gub,
               void* ws, size_t ws_bytes, int32_t* out_parent, uint32_t* out_code, double* out_lb,
               double* out_w, int64_t* out_count, void* stream);
+
+/* Coordinate pattern search of DESIGN.md reading R9 (the sampling step
+ * that supplies the initial incumbent, §3.1): from the
+ * midpoint of [l, u], at most `rounds` improving moves, each the best of
+ *   - the 8 joint moves x + 2^-a (xs - x), a = 0..7, where xs_i is the best
+ *     of 128 candidates for variable i with the others fixed (32 grid points
+ *     of [l_i, u_i], x_i +- (u_i - l_i) 2^-j for j = 1..48), and
+ *   - the single best coordinate move;
+ * every compared value is the upper end of an interval enclosure of f at a
+ * point of [l, u], so *f_out is a rigorous upper bound of the global minimum.
+ *   l, u        device, n doubles, l < u
+ *   x_out       device, n doubles (may be NULL): the final point
+ *   f_out       device, 1 double (may be NULL): upper bound of f(x_out)
+ *   rounds_out  device, 1 int32 (may be NULL): accepted moves
+ *   ws          device workspace >= ib_search_workspace_size(n)
+ * One cooperative kernel launch; asynchronous on `stream`. */
+size_t ib_search_workspace_size(int n);
+int ib_search(int fid, int n, const double* l, const double* u, int rounds, double* x_out, double* f_out,
+              int32_t* rounds_out, void* ws, size_t ws_bytes, void* stream);
 
 /* Stable compaction: indices i < n with keys[i] <= thr, in increasing order
  * (device out_idx, capacity n; *out_count device).  ws: >= 8 * (n/1024 + 2)

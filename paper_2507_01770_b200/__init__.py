@@ -18,7 +18,7 @@ from . import build as _build
 
 __all__ = [
     "ib_version", "ib_last_error", "ib_num_functions", "IbOptions", "ib_solve", "ib_solve_dev", "ib_solve_dev_ex",
-    "ib_eval_boxes", "ib_eval_grad", "ib_branch", "ib_compact_le", "ib_select", "lib", "LIB_PATH",
+    "ib_eval_boxes", "ib_eval_grad", "ib_branch", "ib_search", "ib_compact_le", "ib_select", "lib", "LIB_PATH",
 ]
 
 LIB_PATH = _build.LIB
@@ -35,7 +35,7 @@ _dp = ctypes.POINTER(ctypes.c_double)
 class IbOptions(ctypes.Structure):
     _fields_ = [
         ("d", ctypes.c_int), ("m", ctypes.c_int), ("mono", ctypes.c_int), ("profile", ctypes.c_int),
-        ("bmax", _i64), ("max_iter", _i64), ("pool_cap", _i64), ("arch_cap", _i64),
+        ("search", ctypes.c_int), ("reserved", ctypes.c_int), ("bmax", _i64), ("max_iter", _i64), ("pool_cap", _i64), ("arch_cap", _i64),
     ]
 
 
@@ -45,7 +45,7 @@ class IbResult(ctypes.Structure):
         ("n_surv", _i64), ("peak_pool", _i64), ("max_width", ctypes.c_double),
         ("status", ctypes.c_int), ("n_kernels", ctypes.c_int),
         ("t_ms", ctypes.c_double * NPROF), ("launches", _i64 * NPROF), ("units", _i64 * NPROF),
-        ("radix_records", _i64),
+        ("radix_records", _i64), ("f_search", ctypes.c_double), ("search_rounds", _i64),
     ]
 
 
@@ -69,6 +69,9 @@ EXPORTS = {
     "ib_branch": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64,
                                  _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp, _vp, _vp,
                                  _vp, _vp, _vp]),
+    "ib_search_workspace_size": (ctypes.c_size_t, [ctypes.c_int]),
+    "ib_search": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, _vp,
+                                 ctypes.c_size_t, _vp]),
     "ib_compact_le": (ctypes.c_int, [_vp, _i64, ctypes.c_double, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "ib_select_workspace_size": (ctypes.c_size_t, [_i64]),
     "ib_select": (ctypes.c_int, [_vp, _i64, ctypes.c_double, _i64, _vp, _vp, ctypes.POINTER(_i64),
@@ -150,6 +153,8 @@ class SolveResult:
     lb: object = None
     prof: dict = None
     n_kernels: int = 0
+    f_search: float = float("inf")
+    search_rounds: int = 0
 
 
 def _res(r: IbResult, lo=None, hi=None, lb=None) -> SolveResult:
@@ -157,7 +162,7 @@ def _res(r: IbResult, lo=None, hi=None, lb=None) -> SolveResult:
             for i, c in enumerate(PROF_CLASSES)}
     prof["list"]["radix_records"] = r.radix_records
     return SolveResult(r.f_lo, r.f_hi, r.iters, r.evals, r.n_surv, r.peak_pool, r.max_width, r.status,
-                       lo, hi, lb, prof, r.n_kernels)
+                       lo, hi, lb, prof, r.n_kernels, r.f_search, r.search_rounds)
 
 
 EXCHANGE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p)
@@ -313,6 +318,23 @@ def ib_branch(fid: int, plo, phi, pcyc, d: int, m: int, l, u, gub: float = float
         "lb": out_lb[:k],
         "w": out_w[:k],
     }
+
+
+def ib_search(fid: int, l, u, rounds: int = 32, stream=None):
+    """Coordinate pattern search (reading R9) on device bounds l, u (cuda
+    float64).  Returns (x: cuda tensor, f_upper: float, rounds: int)."""
+    torch = _torch()
+    n = l.numel()
+    x = torch.empty(n, dtype=torch.float64, device=l.device)
+    f = torch.empty(1, dtype=torch.float64, device=l.device)
+    r = torch.zeros(1, dtype=torch.int32, device=l.device)
+    wsb = lib().ib_search_workspace_size(n)
+    if wsb == 0:
+        _check(-1, "ib_search_workspace_size")
+    ws = torch.empty(int(wsb), dtype=torch.uint8, device=l.device)
+    _check(lib().ib_search(fid, n, _ptr(l.contiguous()), _ptr(u.contiguous()), int(rounds), _ptr(x), _ptr(f), _ptr(r),
+                           _ptr(ws), int(wsb), _stream(stream)), "ib_search")
+    return x, float(f.item()), int(r.item())
 
 
 def ib_compact_le(keys, thr: float, stream=None):

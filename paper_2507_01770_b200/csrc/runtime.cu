@@ -41,6 +41,10 @@ int launch_extract(const Problem&, Pool, long, const double*, const double*, con
 int launch_eval_boxes(int, int, long, const double*, const double*, long, double*, cudaStream_t);
 int launch_eval_grad(int, int, long, const double*, const double*, long, const int64_t*, const int32_t*,
                      double*, cudaStream_t);
+size_t search_ws_bytes(int n, int grid);
+int search_grid_max();
+int launch_search(int fid, int n, const double* l, const double* u, int rounds, void* ws, size_t ws_bytes,
+                  unsigned long long* gub_key, double* x_out, double* f_out, int32_t* rounds_out, cudaStream_t st);
 
 // ------------------------------------------------------------ small kernels
 __global__ void k_iota32(int32_t* a, long n, int32_t base) {
@@ -147,7 +151,7 @@ struct Arena {
 };
 
 struct Opts {
-  int d, m, mono;
+  int d, m, mono, search;
   long kids, bmax, max_iter, pool_cap, arch_cap;
   int ld, tab_stride;
 };
@@ -162,6 +166,7 @@ static int resolve_opts(int fid, int n, const ib_options* o, int64_t pool_cap_ar
   if (r.d > n) r.d = n;
   r.m = o->m > 0 ? o->m : 2;
   r.mono = o->mono < 0 ? 0 : 1;
+  r.search = o->search < 0 ? 0 : (o->search > 0 ? o->search : 32);
   if (r.d > D_MAX || r.m < 2 || r.m > M_MAX || r.d * r.m > DM_MAX)
     return fail(IB_EINVAL, "unsupported d=%d m=%d", r.d, r.m);
   double kids = std::pow((double)r.m, (double)r.d);
@@ -205,7 +210,10 @@ struct SolveWs {
   int32_t *sel_slot, *new_slot, *sc, *free_list;
   uint32_t *sel_code, *cand, *hot0, *hot1;
   uint8_t *ok, *mark;
-  double *alo, *ahi, *tab, *clb, *l, *u, *root_out;
+  double *alo, *ahi, *tab, *clb, *l, *u, *root_out, *f_search;
+  int32_t* search_rounds;
+  char* search_ws;
+  size_t search_bytes;
   uint64_t *desc, *desc2, *cnt;
   uint32_t* tile_ctr;
   Ctl* ctl;
@@ -246,6 +254,10 @@ static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
   w.l = A.take<double>(n);
   w.u = A.take<double>(n);
   w.root_out = A.take<double>(2);
+  w.f_search = A.take<double>(1);
+  w.search_rounds = A.take<int32_t>(1);
+  w.search_bytes = search_ws_bytes(n, search_grid_max());
+  w.search_ws = A.take<char>(w.search_bytes);
   return A.off + 256;
 }
 
@@ -442,6 +454,17 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   // free list: slots 1 .. arch_cap-1
   k_iota32<<<blocks_for(o.arch_cap - 1), 256, 0, st>>>(w.free_list, o.arch_cap - 1, 1);
   nk += 3;
+  // sampling (line 134, reading R9): the coordinate pattern search supplies
+  // the initial incumbent GUB (ordered-int atomicMin into ctl->gub_key)
+  double f_search = INFINITY;
+  int32_t search_rounds = 0;
+  if (o.search > 0) {
+    CKL(launch_search(fid, n, w.l, w.u, o.search, w.search_ws, w.search_bytes, &w.ctl->gub_key, nullptr, w.f_search,
+                      w.search_rounds, st));
+    CK(cudaMemcpyAsync(&f_search, w.f_search, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&search_rounds, w.search_rounds, 4, cudaMemcpyDeviceToHost, st));
+    nk += 1;
+  }
 
   IterBufs ib{};
   ib.ctl = w.ctl;
@@ -620,6 +643,8 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   std::memcpy(&res->max_width, &c.acc_max_w, 8);
   res->status = status;
   res->n_kernels = (int)std::min(nk, (long)INT32_MAX);
+  res->f_search = f_search;
+  res->search_rounds = search_rounds;
   return 0;
 }
 
@@ -773,6 +798,19 @@ int ib_branch(int fid, int n, int d, int m, int mono, int64_t nb, const double* 
   CKL(launch_branch(P, ib, (long)nb, st));
   k_branch_out<<<1, 1, 0, st>>>(w.ctl, gub, out_count);
   CK(cudaGetLastError());
+  return 0;
+}
+
+size_t ib_search_workspace_size(int n) {
+  if (n < 1) return 0;
+  return search_ws_bytes(n, search_grid_max());
+}
+
+int ib_search(int fid, int n, const double* l, const double* u, int rounds, double* x_out, double* f_out,
+              int32_t* rounds_out, void* ws, size_t ws_bytes, void* stream) {
+  if (fid < 0 || fid > 10 || n < 1 || rounds < 0 || !l || !u || !ws) return fail(IB_EINVAL, "ib_search: bad arguments");
+  if (ws_bytes < ib_search_workspace_size(n)) return fail(IB_ENOSPACE, "ib_search: workspace too small");
+  CKL(launch_search(fid, n, l, u, rounds, ws, ws_bytes, nullptr, x_out, f_out, rounds_out, (cudaStream_t)stream));
   return 0;
 }
 

@@ -1,0 +1,462 @@
+// search.cu -- the sampling step that supplies the initial incumbent GUB
+// (§3.1: any sampling strategy is acceptable; GUB is
+// the smallest upper bound of f over the sampled points).  DESIGN.md reading
+// R9: a coordinate pattern search from the midpoint of [l, u] in which every
+// compared value is the upper end of an interval enclosure of f at a feasible
+// point, so the value it returns is a rigorous GUB.
+//
+// One persistent cooperative kernel runs the whole search; a round is three
+// grid-wide phases separated by grid barriers:
+//   A  (thread per variable) apply the previous round's move (double-
+//      buffered x, so neighbours are read race-free), interval terms at x,
+//      block partial accumulators; every block then reduces the partials in
+//      the same fixed order -> A_k and fcur = upper(outer(A));
+//   B  (warp per variable) the 128 candidates of the variable, 4 per lane:
+//      the accumulators without variable i (sum: A - t_i, product: A / t_i)
+//      combined with the candidate's terms -> upper(outer), warp argmin
+//      (value, candidate index) -> proposal xs_i, fb_i; block min of fb;
+//   C  (thread per variable) terms of the 8 joint moves
+//      y_a = x + 2^-a (xs - x), block partials; block 0 reduces them, takes
+//      the best of the 8 moves and of the single best coordinate move, and
+//      publishes the decision (or stop).
+// No floating-point atomics: every reduction has a fixed order for a given
+// grid, so the search is deterministic.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include <cooperative_groups.h>
+
+#include "kernels.cuh"
+#include "objectives.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace ib {
+
+constexpr int S_GRID = 32, S_SCALES = 48, S_CANDS = S_GRID + 2 * S_SCALES, S_ALPHAS = 8;
+constexpr int S_TPB = 256;
+constexpr int S_NONE = -1, S_SINGLE = S_ALPHAS;
+
+struct SearchCtl {
+  double fcur;   // upper bound of f at the current x
+  int dec;       // move of the round: S_NONE, alpha index, or S_SINGLE
+  int istar;     // variable of the single move
+  int stop;      // no improving move: the search ended
+  int rounds;    // accepted moves
+};
+
+struct SearchWs {
+  double *xa, *xb, *xs, *fb;
+  Iv *partA, *partC;
+  double* partB;  // per block: fb min, variable index (as double)
+  SearchCtl* sc;
+};
+
+__device__ __forceinline__ double s_clamp(double v, double lo, double hi) { return fmin(fmax(v, lo), hi); }
+
+// candidate c of variable i (reading R9; same rule as oracle/search.c)
+__device__ __forceinline__ bool s_candidate(double xi, double li, double ui, int c, double& p) {
+  const double span = __dsub_rn(ui, li);
+  if (c < S_GRID) {
+    if (c == S_GRID - 1) {
+      p = ui;
+      return true;
+    }
+    double w = __ddiv_rn(span, (double)(S_GRID - 1));
+    double q = __dadd_rn(li, __dmul_rn(w, (double)c));
+    p = q < ui ? q : ui;
+    return true;
+  }
+  const int j = (c - S_GRID) / 2 + 1;
+  const double h = scalbn(span, -j);
+  const double q = (c & 1) ? __dadd_rn(xi, h) : __dsub_rn(xi, h);
+  if (q < li || q > ui) return false;
+  p = q;
+  return true;
+}
+
+__device__ __forceinline__ double s_alpha(int a) { return scalbn(1.0, -a); }
+__device__ __forceinline__ double s_move(double x, double xs, int a, double li, double ui) {
+  return s_clamp(__dadd_rn(x, __dmul_rn(s_alpha(a), __dsub_rn(xs, x))), li, ui);
+}
+// x after the decision of the previous round
+__device__ __forceinline__ double s_apply(double x, double xs, int dec, int istar, int i, double li, double ui) {
+  if (dec == S_NONE) return x;
+  if (dec == S_SINGLE) return i == istar ? xs : x;
+  return s_move(x, xs, dec, li, ui);
+}
+
+// Levy chain (A11): the chain term owned by variable i, t_i = [s0(y_0) if
+// i = 0] + (i < n-1 ? u_i v_{i+1} : u_{n-1})
+__device__ __forceinline__ Iv levy_own(const LevyVals& me, const LevyVals* nxt, int i, int n) {
+  Iv t = i == 0 ? me.s0 : iv(0.0);
+  return i < n - 1 ? t + mulpos(me.u, nxt->v) : t + me.u;
+}
+// every chain term that contains variable i
+__device__ __forceinline__ Iv levy_touch(const LevyVals& me, const LevyVals* prv, const LevyVals* nxt, int i, int n) {
+  Iv t = i == 0 ? me.s0 : iv(0.0);
+  if (i > 0) t = t + mulpos(prv->u, me.v);
+  return i < n - 1 ? t + mulpos(me.u, nxt->v) : t + me.u;
+}
+
+// accumulators without variable i: sum A - t_i; product A / t_i (every
+// product accumulator of Appendix A is a product of sines / cosines, so
+// [-1, 1] encloses it when t_i may vanish)
+template <class F>
+__device__ __forceinline__ Iv s_excl(int k, Iv A, Iv t) {
+  if (F::kind(k) == SUM) return A - t;
+  if (t.lo > 0.0 || t.hi < 0.0) return A / t;
+  return Iv{-1.0, 1.0};
+}
+
+// accumulator algebra that also covers the Levy chain (one sum)
+template <class F>
+__device__ __forceinline__ Iv s_ident(int k) {
+  if constexpr (F::CHAIN) return iv(0.0);
+  else return acc_ident<F>(k);
+}
+template <class F>
+__device__ __forceinline__ Iv s_comb(int k, Iv a, Iv b) {
+  if constexpr (F::CHAIN) return a + b;
+  else return acc_comb<F>(k, a, b);
+}
+template <class F>
+__device__ __forceinline__ double s_outer_hi(const Iv* A, int n) {
+  if constexpr (F::CHAIN) return ObjLevy::outer(A[0], n).hi;
+  else return F::outer(A, n).hi;
+}
+// block reduction of K accumulators (result valid in thread 0)
+template <class F>
+__device__ __forceinline__ void block_reduce_acc_s(Iv* a) {
+  constexpr int K = F::K;
+  __shared__ Iv s_acc[S_TPB / 32][2];
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      Iv t{__shfl_xor_sync(0xffffffffu, a[k].lo, o), __shfl_xor_sync(0xffffffffu, a[k].hi, o)};
+      a[k] = s_comb<F>(k, a[k], t);
+    }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0)
+    for (int k = 0; k < K; ++k) s_acc[wid][k] = a[k];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int w = 1; w < S_TPB / 32; ++w)
+      for (int k = 0; k < K; ++k) a[k] = s_comb<F>(k, a[k], s_acc[w][k]);
+  __syncthreads();
+}
+
+template <class F>
+__device__ __forceinline__ void s_block_partial(Iv* acc, Iv* out) {
+  block_reduce_acc_s<F>(acc);
+  if (threadIdx.x == 0)
+    for (int k = 0; k < F::K; ++k) out[k] = acc[k];
+}
+
+template <class F>
+__global__ void __launch_bounds__(S_TPB) k_search(int n, const double* __restrict__ l, const double* __restrict__ u,
+                                                  SearchWs w, int rmax, unsigned long long* gub_key,
+                                                  double* x_out, double* f_out, int32_t* rounds_out) {
+  cg::grid_group grid = cg::this_grid();
+  constexpr bool CH = F::CHAIN;
+  constexpr int K = CH ? 1 : F::K;
+  const int G = gridDim.x;
+  const long T = (long)G * S_TPB;
+  const long gt = (long)blockIdx.x * S_TPB + threadIdx.x;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  __shared__ Iv s_A[2];
+  __shared__ double s_fcur;
+  __shared__ double s_wmin[S_TPB / 32];
+  __shared__ int s_wi[S_TPB / 32];
+
+  double* xo = w.xa;  // x of the previous round (read-only in phase A)
+  double* xn = w.xb;  // x of this round
+  int dec = S_NONE, istar = -1, r = 0;
+  bool first = true;  // phase A of round 0 starts from the midpoint of [l, u]
+  double fcur = 0.0;
+  auto x_of = [&](long j) -> double {
+    if (first) return s_clamp(__dadd_rn(l[j], __dmul_rn(__dsub_rn(u[j], l[j]), 0.5)), l[j], u[j]);
+    return s_apply(xo[j], w.xs[j], dec, istar, (int)j, l[j], u[j]);
+  };
+  for (;;) {
+    // ---------------------------------------------------------- phase A
+    Iv acc[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) acc[k] = s_ident<F>(k < K ? k : 0);
+    for (long i = gt; i < n; i += T) {
+      const double xi = x_of(i);
+      xn[i] = xi;
+      if constexpr (CH) {
+        LevyVals me = ObjLevy::vals(iv(xi));
+        LevyVals nx;
+        if (i < n - 1) nx = ObjLevy::vals(iv(x_of(i + 1)));
+        acc[0] = acc[0] + levy_own(me, &nx, (int)i, n);
+      } else {
+        Iv t[2];
+        F::terms(iv(xi), (int)i, n, t);
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[k] = acc_comb<F>(k, acc[k], t[k]);
+      }
+    }
+    s_block_partial<F>(acc, w.partA + (size_t)blockIdx.x * 2);
+    grid.sync();
+    // every block reduces the partials in the same order
+#pragma unroll
+    for (int k = 0; k < 2; ++k) acc[k] = s_ident<F>(k < K ? k : 0);
+    for (int b = threadIdx.x; b < G; b += S_TPB)
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc[k] = s_comb<F>(k, acc[k], w.partA[(size_t)b * 2 + k]);
+    block_reduce_acc_s<F>(acc);
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < K; ++k) s_A[k] = acc[k];
+      s_fcur = s_outer_hi<F>(acc, n);
+    }
+    __syncthreads();
+    fcur = s_fcur;
+    first = false;
+    Iv A[2] = {s_A[0], s_A[1]};
+    if (r == rmax) break;
+
+    // ---------------------------------------------------------- phase B
+    double wmin = CUDART_INF;
+    int wi = 0x7fffffff;
+    const long gw = gt >> 5, TW = T >> 5;
+    for (long i = gw; i < n; i += TW) {
+      const double xi = xn[i], li = l[i], ui = u[i];
+      Iv ex[2];
+      Iv Lprev_u = iv(0.0), Rnext_v = iv(0.0), touch = iv(0.0);
+      if constexpr (CH) {
+        LevyVals me = ObjLevy::vals(iv(xi)), pv, nx;
+        if (i > 0) pv = ObjLevy::vals(iv(xn[i - 1]));
+        if (i < n - 1) nx = ObjLevy::vals(iv(xn[i + 1]));
+        Lprev_u = i > 0 ? pv.u : iv(0.0);
+        Rnext_v = i < n - 1 ? nx.v : iv(0.0);
+        touch = levy_touch(me, &pv, &nx, (int)i, n);
+        ex[0] = A[0] - touch;
+      } else {
+        Iv t[2];
+        F::terms(iv(xi), (int)i, n, t);
+#pragma unroll
+        for (int k = 0; k < K; ++k) ex[k] = s_excl<F>(k, A[k], t[k]);
+      }
+      double bv = CUDART_INF;
+      int bc = S_CANDS;
+#pragma unroll
+      for (int q = 0; q < S_CANDS / 32; ++q) {
+        const int c = lane + 32 * q;
+        double p;
+        if (!s_candidate(xi, li, ui, c, p)) continue;
+        double v;
+        if constexpr (CH) {
+          LevyVals me = ObjLevy::vals(iv(p));
+          LevyVals pv, nx;
+          pv.u = Lprev_u;
+          nx.v = Rnext_v;
+          Iv tt = i == 0 ? me.s0 : iv(0.0);
+          if (i > 0) tt = tt + mulpos(pv.u, me.v);
+          tt = i < n - 1 ? tt + mulpos(me.u, nx.v) : tt + me.u;
+          v = ObjLevy::outer(ex[0] + tt, n).hi;
+        } else {
+          Iv t[2], Ac[2];
+          F::terms(iv(p), (int)i, n, t);
+#pragma unroll
+          for (int k = 0; k < K; ++k) Ac[k] = acc_comb<F>(k, ex[k], t[k]);
+          v = F::outer(Ac, n).hi;
+        }
+        if (v < bv) {  // q ascending: ties keep the smaller candidate index
+          bv = v;
+          bc = c;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        if (ov < bv || (ov == bv && oc < bc)) {
+          bv = ov;
+          bc = oc;
+        }
+      }
+      double xsi = xi, fbi = fcur;
+      if (bv < fcur) {
+        double p;
+        s_candidate(xi, li, ui, bc, p);
+        xsi = p;
+        fbi = bv;
+      }
+      if (lane == 0) {
+        w.xs[i] = xsi;
+        w.fb[i] = fbi;
+      }
+      if (fbi < wmin) {  // i ascending within the warp: ties keep the smaller i
+        wmin = fbi;
+        wi = (int)i;
+      }
+    }
+    if (lane == 0) {
+      s_wmin[wib] = wmin;
+      s_wi[wib] = wi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double bm = s_wmin[0];
+      int bi = s_wi[0];
+      for (int k = 1; k < S_TPB / 32; ++k)
+        if (s_wmin[k] < bm || (s_wmin[k] == bm && s_wi[k] < bi)) {
+          bm = s_wmin[k];
+          bi = s_wi[k];
+        }
+      w.partB[2 * blockIdx.x] = bm;
+      w.partB[2 * blockIdx.x + 1] = (double)bi;
+    }
+    grid.sync();
+
+    // ---------------------------------------------------------- phase C
+    Iv ac[S_ALPHAS][2];
+#pragma unroll
+    for (int a = 0; a < S_ALPHAS; ++a)
+#pragma unroll
+      for (int k = 0; k < 2; ++k) ac[a][k] = s_ident<F>(k < K ? k : 0);
+    for (long i = gt; i < n; i += T) {
+      const double xi = xn[i], xsi = w.xs[i], li = l[i], ui = u[i];
+#pragma unroll
+      for (int a = 0; a < S_ALPHAS; ++a) {
+        const double y = s_move(xi, xsi, a, li, ui);
+        if constexpr (CH) {
+          LevyVals me = ObjLevy::vals(iv(y)), nx;
+          if (i < n - 1) nx = ObjLevy::vals(iv(s_move(xn[i + 1], w.xs[i + 1], a, l[i + 1], u[i + 1])));
+          ac[a][0] = ac[a][0] + levy_own(me, &nx, (int)i, n);
+        } else {
+          Iv t[2];
+          F::terms(iv(y), (int)i, n, t);
+#pragma unroll
+          for (int k = 0; k < K; ++k) ac[a][k] = acc_comb<F>(k, ac[a][k], t[k]);
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < S_ALPHAS; ++a) s_block_partial<F>(ac[a], w.partC + ((size_t)blockIdx.x * S_ALPHAS + a) * 2);
+    grid.sync();
+    if (blockIdx.x == 0) {
+      // the 8 joint moves: reduce their partials over the blocks (fixed order)
+      double vbest = CUDART_INF;
+      int abest = S_NONE;
+      for (int a = 0; a < S_ALPHAS; ++a) {
+        Iv q[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) q[k] = s_ident<F>(k < K ? k : 0);
+        for (int b = threadIdx.x; b < G; b += S_TPB)
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            Iv pv = w.partC[((size_t)b * S_ALPHAS + a) * 2 + k];
+            q[k] = s_comb<F>(k, q[k], pv);
+          }
+        block_reduce_acc_s<F>(q);
+        if (threadIdx.x == 0) {
+          double v = s_outer_hi<F>(q, n);
+          if (v < vbest) {
+            vbest = v;
+            abest = a;
+          }
+        }
+      }
+      if (threadIdx.x == 0) {
+        double bm = CUDART_INF;
+        int bi = 0x7fffffff;
+        for (int b = 0; b < G; ++b) {
+          double m = w.partB[2 * b];
+          int ii = (int)w.partB[2 * b + 1];
+          if (m < bm || (m == bm && ii < bi)) {
+            bm = m;
+            bi = ii;
+          }
+        }
+        int d = abest;
+        if (bm < vbest) {
+          vbest = bm;
+          d = S_SINGLE;
+        }
+        SearchCtl* sc = w.sc;
+        if (d != S_NONE && vbest < fcur) {
+          sc->dec = d;
+          sc->istar = bi;
+          sc->stop = 0;
+        } else {
+          sc->dec = S_NONE;
+          sc->stop = 1;
+        }
+      }
+    }
+    grid.sync();
+    if (w.sc->stop) break;
+    dec = w.sc->dec;
+    istar = w.sc->istar;
+    ++r;
+    double* t = xo;
+    xo = xn;
+    xn = t;
+  }
+  // result: x of the last phase A and its upper bound
+  if (x_out)
+    for (long i = gt; i < n; i += T) x_out[i] = xn[i];
+  if (gt == 0) {
+    w.sc->fcur = fcur;
+    w.sc->rounds = r;
+    if (f_out) *f_out = fcur;
+    if (rounds_out) *rounds_out = r;
+    if (gub_key) atomicMin(gub_key, (unsigned long long)okey(fcur));
+  }
+}
+
+size_t search_ws_bytes(int n, int grid) {
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  return 4 * al(sizeof(double) * (size_t)n) + al(sizeof(Iv) * 2 * (size_t)grid) +
+         al(sizeof(Iv) * 2 * S_ALPHAS * (size_t)grid) + al(sizeof(double) * 2 * (size_t)grid) + al(sizeof(SearchCtl)) +
+         256;
+}
+
+int search_grid_max() { return 256; }
+int search_grid(int n) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // one warp per variable in phase B, at most one resident block per SM
+  int want = (n + S_TPB / 32 - 1) / (S_TPB / 32);
+  return std::max(1, std::min(std::min(want, sms), search_grid_max()));
+}
+
+// run the search (rounds = round limit, 0 = evaluate the midpoint only)
+int launch_search(int fid, int n, const double* l, const double* u, int rounds, void* ws, size_t ws_bytes,
+                  unsigned long long* gub_key, double* x_out, double* f_out, int32_t* rounds_out, cudaStream_t st) {
+  const int grid = search_grid(n);
+  if (ws_bytes < search_ws_bytes(n, grid)) return -2;
+  char* p = (char*)ws;
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    off = (off + 255) & ~(size_t)255;
+    void* r = p + off;
+    off += b;
+    return r;
+  };
+  SearchWs w;
+  w.xa = (double*)take(sizeof(double) * n);
+  w.xb = (double*)take(sizeof(double) * n);
+  w.xs = (double*)take(sizeof(double) * n);
+  w.fb = (double*)take(sizeof(double) * n);
+  w.partA = (Iv*)take(sizeof(Iv) * 2 * grid);
+  w.partC = (Iv*)take(sizeof(Iv) * 2 * S_ALPHAS * grid);
+  w.partB = (double*)take(sizeof(double) * 2 * grid);
+  w.sc = (SearchCtl*)take(sizeof(SearchCtl));
+  cudaError_t e = cudaErrorInvalidValue;
+  IB_DISPATCH_FID(fid, {
+    void* argv[] = {(void*)&n, (void*)&l, (void*)&u, (void*)&w, (void*)&rounds, (void*)&gub_key, (void*)&x_out,
+                    (void*)&f_out, (void*)&rounds_out};
+    e = cudaLaunchCooperativeKernel((const void*)k_search<F>, dim3(grid), dim3(S_TPB), argv, 0, st);
+  });
+  return (int)e;
+}
+
+}  // namespace ib

@@ -36,7 +36,7 @@ def declared_functions():
 def test_header_declares_the_boundary():
     names = declared_functions()
     for must in ("ib_solve", "ib_solve_dev", "ib_eval_boxes", "ib_eval_grad", "ib_branch", "ib_compact_le",
-                 "ib_select", "ib_version", "ib_last_error", "ib_solve_workspace_size"):
+                 "ib_select", "ib_search", "ib_version", "ib_last_error", "ib_solve_workspace_size"):
         assert must in names
 
 

@@ -172,9 +172,11 @@ def test_select_bit_exact(pb):
 
 
 # ------------------------------------------------------------ full solves
-def _solve_parity(pb, fid, l, u, eps_f, eps_x, d, m, bmax, max_iter=100_000):
-    o = oracle.solve(fid, l, u, eps_f=eps_f, eps_x=eps_x, d=d, m=m, bmax=bmax, max_iter=max_iter)
-    g = pb.ib_solve(fid, l, u, eps_f, eps_x, pb.options(d=d, m=m, bmax=bmax, max_iter=max_iter))
+def _solve_parity(pb, fid, l, u, eps_f, eps_x, d, m, bmax, max_iter=100_000, search=0):
+    """search = rounds of the R9 search on both sides (0: none)"""
+    o = oracle.solve(fid, l, u, eps_f=eps_f, eps_x=eps_x, d=d, m=m, bmax=bmax, max_iter=max_iter, search=search)
+    g = pb.ib_solve(fid, l, u, eps_f, eps_x, pb.options(d=d, m=m, bmax=bmax, max_iter=max_iter,
+                                                       search=search if search > 0 else -1))
     t = tol(fid, l, u)
     assert g.status == o["status"]
     assert g.iters == o["iters"] and g.evals == o["evals"]
@@ -198,6 +200,16 @@ def test_small_solves_match_oracle_paper_domains(pb, fid):
     l, u = workloads.bounds(fid, 2)
     g, o = _solve_parity(pb, fid, l, u, 1e-6, 1e-5, 2, 2, 256, 4000)
     assert g.status == 0
+
+
+@pytest.mark.parametrize("fid", list(range(1, 11)))
+def test_small_solves_with_search_match_oracle(pb, fid):
+    """R9 search on both sides: same incumbent (to the tolerance), same run."""
+    l, u = workloads.bounds(fid, 2)
+    g, o = _solve_parity(pb, fid, l, u, 1e-6, 1e-5, 2, 2, 256, 4000, search=32)
+    assert g.status == 0
+    xo, fo, _ = oracle.search(fid, l, u, 32)
+    assert abs(g.f_search - fo) <= tol(fid, l, u)
 
 
 @pytest.mark.parametrize("bmax", [1, 7, 64])
@@ -242,3 +254,55 @@ def test_solve_is_deterministic_graph_and_eager(pb, fid, n, lo, hi, m):
         assert r.f_lo == res[0].f_lo and r.f_hi == res[0].f_hi
         np.testing.assert_array_equal(r.lo, res[0].lo)
         np.testing.assert_array_equal(r.hi, res[0].hi)
+
+
+# ------------------------------------------------------------ search (R9)
+@pytest.mark.parametrize("fid", list(range(0, 11)))
+@pytest.mark.parametrize("n", [1, 2, 5, 9])
+def test_search_matches_oracle(pb, fid, n):
+    l, u = workloads.bounds(fid, n)
+    x, f, r = pb.ib_search(fid, cuda(l), cuda(u), 32)
+    xo, fo, ro = oracle.search(fid, l, u, 32)
+    t = tol(fid, l, u)
+    assert abs(f - fo) <= t, (f, fo)
+    x = x.cpu().numpy()
+    assert np.all(x >= l) and np.all(x <= u)
+    # rigorous: the GPU's value bounds f at its own point (oracle enclosure)
+    ev = oracle.eval_point(fid, x)
+    assert ev[0] <= f + t and f <= ev[1] + t
+    if r == ro:
+        assert np.max(np.abs(x - xo)) <= 1e-9 * (1 + np.max(np.abs(u - l)))
+
+
+@pytest.mark.parametrize("rounds", [0, 1, 3])
+def test_search_round_limit(pb, rounds):
+    l, u = workloads.bounds(7, 6)
+    x, f, r = pb.ib_search(7, cuda(l), cuda(u), rounds)
+    xo, fo, ro = oracle.search(7, l, u, rounds)
+    assert r == ro <= rounds
+    assert abs(f - fo) <= tol(7, l, u)
+
+
+@pytest.mark.parametrize("fid", list(range(1, 11)))
+def test_search_is_rigorous_at_n1000(pb, fid):
+    n = 1000
+    l, u = workloads.bounds(fid, n)
+    x, f, r = pb.ib_search(fid, cuda(l), cuda(u), 32)
+    x = x.cpu().numpy()
+    ev = oracle.eval_point(fid, x)
+    t = tol(fid, l, u)
+    assert ev[0] <= f + t and f <= ev[1] + t
+    mid = oracle.eval_point(fid, l + (u - l) * 0.5)
+    assert f <= mid[1] + t
+
+
+STAR = {1: 0.0, 2: -1.0, 3: None, 4: 1.0, 6: 0.0, 7: 0.0, 9: None}
+
+
+@pytest.mark.parametrize("fid", [1, 2, 3, 4, 6, 7, 9])
+def test_search_reaches_minimum_n10000(pb, fid):
+    n = 10_000
+    l, u = workloads.bounds(fid, n)
+    _, f, _ = pb.ib_search(fid, cuda(l), cuda(u), 64)
+    fs = {3: -0.1 * n, 9: -4.0 * n}.get(fid, STAR[fid])
+    assert fs - 1e-9 * (1 + abs(fs)) <= f <= fs + 1e-6 * (1 + abs(fs)), (fid, f, fs)
