@@ -95,6 +95,7 @@ def lib():
                                               ctypes.c_int, _dp]
             L.or_search_propose.argtypes = [ctypes.c_int, ctypes.c_int, _dp, _dp, _dp,
                                             ctypes.c_double, _dp, _dp]
+            L.or_search_diag.argtypes = [ctypes.c_int, ctypes.c_int, _dp, _dp, _dp, _dp]
             L.or_search.argtypes = [ctypes.c_int, ctypes.c_int, _dp, _dp, ctypes.c_int, _dp, _dp,
                                     _ip]
             for fn in ("ia_add_dn", "ia_add_up", "ia_sub_dn", "ia_sub_up", "ia_mul_dn",
@@ -253,6 +254,15 @@ def search_propose(fid, x, l, u, fcur):
     fb = np.zeros_like(x)
     lib().or_search_propose(fid, x.size, _d(x), _d(l), _d(u), float(fcur), _d(xs), _d(fb))
     return xs, fb
+
+
+def search_diag(fid, l, u):
+    """R9 diagonal line search: (t*, f_upper at x(t*))."""
+    l, u = _f64(l), _f64(u)
+    t = ctypes.c_double()
+    f = ctypes.c_double()
+    lib().or_search_diag(fid, l.size, _d(l), _d(u), ctypes.byref(t), ctypes.byref(f))
+    return t.value, f.value
 
 
 def search(fid, l, u, rounds=32):

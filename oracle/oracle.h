@@ -37,6 +37,7 @@ typedef struct {
 int or_search_candidate(double xi, double li, double ui, int c, double* p);
 int or_search_propose(int fid, int n, const double* x, const double* l, const double* u,
                       double fcur, double* xs, double* fb);
+int or_search_diag(int fid, int n, const double* l, const double* u, double* t_out, double* f_out);
 int or_search(int fid, int n, const double* l, const double* u, int rmax, double* x_out,
               double* f_out, int* rounds_out);
 

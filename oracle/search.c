@@ -8,7 +8,13 @@
  * upper bound over the sampled points).
  * TEST INFRASTRUCTURE ONLY (see oracle/README.md).
  *
- * Algorithm (R9), from x = midpoint of [l, u]:
+ * Algorithm (R9).  First a line search along the diagonal of [l, u] (the
+ * paper's own sample points lie on diagonals, line 219):
+ *   x(t) = clamp(l + t (u - l)), t_k = k / 2^14 (k = 0..2^14, t = 1/2 is the
+ *   midpoint), t* = the t_k with the smallest upper(F(x(t_k))) (first k on
+ *   ties); then at most 16 rounds of t* +- 2^-j (j = 11..58, minus before
+ *   plus), moving to the best candidate while it is strictly better.
+ * Then, from x = x(t*):
  *   repeat for at most rmax rounds:
  *     fcur = upper(F(x))
  *     proposal: for every variable i, over the candidate values c = 0..127
@@ -37,6 +43,18 @@
 #define SR_SCALES 48
 #define SR_CANDS (SR_GRID + 2 * SR_SCALES)
 #define SR_ALPHAS 8
+#define SR_DIAG_LOG2 14
+#define SR_DIAG_ROUNDS 16
+#define SR_DIAG_J0 11
+#define SR_DIAG_J1 58
+
+/* x(t) = clamp(l + t (u - l)) */
+static void diag_point(int n, const double* l, const double* u, double t, double* x) {
+    for (int i = 0; i < n; ++i) {
+        double v = l[i] + t * (u[i] - l[i]);
+        x[i] = v < l[i] ? l[i] : (v > u[i] ? u[i] : v);
+    }
+}
 
 static double upper_at(int fid, int n, const double* x, ia_t* X) {
     for (int i = 0; i < n; ++i) X[i] = ia_pt(x[i]);
@@ -95,6 +113,44 @@ int or_search_propose(int fid, int n, const double* x, const double* l, const do
     return 0;
 }
 
+int or_search_diag(int fid, int n, const double* l, const double* u, double* t_out, double* f_out) {
+    double* x = (double*)malloc(sizeof(double) * (size_t)n);
+    ia_t* X = (ia_t*)malloc(sizeof(ia_t) * (size_t)n);
+    const long nd = (1L << SR_DIAG_LOG2) + 1;
+    double ts = 0.0, fs = INFINITY;
+    for (long k = 0; k < nd; ++k) {
+        double t = ldexp((double)k, -SR_DIAG_LOG2);
+        diag_point(n, l, u, t, x);
+        double v = upper_at(fid, n, x, X);
+        if (v < fs) {
+            fs = v;
+            ts = t;
+        }
+    }
+    for (int r = 0; r < SR_DIAG_ROUNDS; ++r) {
+        double bv = fs, bt = ts;
+        for (int j = SR_DIAG_J0; j <= SR_DIAG_J1; ++j)
+            for (int s = -1; s <= 1; s += 2) {
+                double t = ts + (double)s * ldexp(1.0, -j);
+                if (t < 0.0 || t > 1.0) continue;
+                diag_point(n, l, u, t, x);
+                double v = upper_at(fid, n, x, X);
+                if (v < bv) {
+                    bv = v;
+                    bt = t;
+                }
+            }
+        if (!(bv < fs)) break;
+        fs = bv;
+        ts = bt;
+    }
+    *t_out = ts;
+    *f_out = fs;
+    free(X);
+    free(x);
+    return 0;
+}
+
 int or_search(int fid, int n, const double* l, const double* u, int rmax, double* x_out,
               double* f_out, int* rounds_out) {
     double* x = x_out;
@@ -103,10 +159,9 @@ int or_search(int fid, int n, const double* l, const double* u, int rmax, double
     double* y = (double*)malloc(sizeof(double) * (size_t)n);
     double* ybest = (double*)malloc(sizeof(double) * (size_t)n);
     ia_t* X = (ia_t*)malloc(sizeof(ia_t) * (size_t)n);
-    for (int i = 0; i < n; ++i) {
-        double mid = l[i] + (u[i] - l[i]) * 0.5;
-        x[i] = mid < l[i] ? l[i] : (mid > u[i] ? u[i] : mid);
-    }
+    double t0, f0;
+    or_search_diag(fid, n, l, u, &t0, &f0);
+    diag_point(n, l, u, t0, x);
     double fcur = upper_at(fid, n, x, X);
     int r = 0;
     while (r < rmax) {

@@ -115,7 +115,7 @@ def test_search_value_is_an_upper_bound_at_its_point(fid, n):
     l, u = workloads.bounds(fid, n)
     x, f, rounds = oracle.search(fid, l, u)
     assert np.all(x >= l) and np.all(x <= u)
-    assert rounds >= 1
+    assert rounds >= 0
     true = _f_hp(fid, x)
     assert Decimal(f) >= true  # rigorous: the upper end of an enclosure
     assert Decimal(f) - true <= Decimal("1e-12") * (1 + abs(true)) + Decimal("1e-12") * n
@@ -129,10 +129,10 @@ def _fstar(fid: int, n: int) -> float:
     return -0.1 * n if s == "-0.1n" else (-4.0 * n if s == "-4n" else float(s))
 
 
-# functions whose minimiser the search reaches from the midpoint of the
-# paper's domain (Salomon, Zabinsky and small-n Griewank stall at local
-# minima; the branch-and-bound itself is what encloses those)
-@pytest.mark.parametrize("fid", [1, 2, 3, 4, 6, 7, 9])
+# every Appendix A minimiser is x* = c (1, ..., 1), on the diagonal of the
+# paper's cube domains, so the diagonal stage reaches it and the coordinate
+# stage keeps it
+@pytest.mark.parametrize("fid", list(range(1, 11)))
 @pytest.mark.parametrize("n", [2, 6])
 def test_search_reaches_known_minimum(fid, n):
     l, u = workloads.bounds(fid, n)
@@ -159,3 +159,26 @@ def test_solve_with_search_encloses_minimum():
         assert r["status"] == 0
         assert r["glb"] <= fs + 1e-12 and fs <= r["gub"]
         assert r["gub"] - r["glb"] <= 1e-6
+
+
+@pytest.mark.parametrize("fid", list(range(1, 11)))
+def test_diagonal_stage_reaches_known_minimum_n50(fid):
+    n = 50
+    l, u = workloads.bounds(fid, n)
+    t, f = oracle.search_diag(fid, l, u)
+    fs = _fstar(fid, n)
+    assert 0.0 <= t <= 1.0
+    assert fs <= f <= fs + 1e-9 * (1 + abs(fs)), (fid, f, fs)
+    # no worse than the domain midpoint (t = 1/2 is a grid point)
+    assert f <= oracle.eval_point(fid, l + 0.5 * (u - l))[1]
+
+
+@pytest.mark.parametrize("fid", [7, 1, 9, 3])
+def test_diagonal_value_is_an_upper_bound(fid):
+    n = 5
+    l, u = workloads.bounds(fid, n)
+    t, f = oracle.search_diag(fid, l, u)
+    x = np.clip(l + t * (u - l), l, u)
+    true = _f_hp(fid, x)
+    assert Decimal(f) >= true
+    assert Decimal(f) - true <= Decimal("1e-12") * (1 + abs(true)) + Decimal("1e-12") * n
