@@ -174,8 +174,11 @@ int ib_branch(int fid, int n, int d, int m, int mono, int64_t nb, const double* 
               double* out_w, int64_t* out_count, void* stream);
 
 /* Coordinate pattern search of DESIGN.md reading R9 (the sampling step
- * that supplies the initial incumbent, §3.1): from the
- * midpoint of [l, u], at most `rounds` improving moves, each the best of
+ * that supplies the initial incumbent, §3.1): a line
+ * search along the diagonal x(t) = l + t (u - l) of [l, u] (t = k / 2^14,
+ * k = 0..2^14, then up to 16 rounds of t +- 2^-j, j = 11..58; the paper's own
+ * samples lie on diagonals, line 219), then from x(t*) at most `rounds`
+ * improving coordinate moves, each the best of
  *   - the 8 joint moves x + 2^-a (xs - x), a = 0..7, where xs_i is the best
  *     of 128 candidates for variable i with the others fixed (32 grid points
  *     of [l_i, u_i], x_i +- (u_i - l_i) 2^-j for j = 1..48), and

@@ -1,12 +1,16 @@
 // search.cu -- the sampling step that supplies the initial incumbent GUB
 // (§3.1: any sampling strategy is acceptable; GUB is
 // the smallest upper bound of f over the sampled points).  DESIGN.md reading
-// R9: a coordinate pattern search from the midpoint of [l, u] in which every
-// compared value is the upper end of an interval enclosure of f at a feasible
-// point, so the value it returns is a rigorous GUB.
+// R9: a line search along the diagonal of [l, u] (the paper samples along
+// diagonals, line 219), then a coordinate pattern search from its best point;
+// every compared value is the upper end of an interval enclosure of f at a
+// feasible point, so the value it returns is a rigorous GUB.
 //
-// One persistent cooperative kernel runs the whole search; a round is three
-// grid-wide phases separated by grid barriers:
+// One persistent cooperative kernel runs the whole search.  Diagonal stage:
+// warp per candidate t (2^14 + 1 grid points, then rounds of 96 dyadic
+// steps), per-block (value, index) minima, grid barrier, every block reduces
+// them in block order.  Coordinate stage, a round is three grid-wide phases
+// separated by grid barriers:
 //   A  (thread per variable) apply the previous round's move (double-
 //      buffered x, so neighbours are read race-free), interval terms at x,
 //      block partial accumulators; every block then reduces the partials in
@@ -38,6 +42,9 @@ namespace ib {
 constexpr int S_GRID = 32, S_SCALES = 48, S_CANDS = S_GRID + 2 * S_SCALES, S_ALPHAS = 8;
 constexpr int S_TPB = 256;
 constexpr int S_NONE = -1, S_SINGLE = S_ALPHAS;
+// diagonal stage: t_k = k / 2^14, then rounds of t* +- 2^-j, j = 11..58
+constexpr int S_DIAG_LOG2 = 14, S_DIAG_ROUNDS = 16, S_DIAG_J0 = 11, S_DIAG_J1 = 58;
+constexpr int S_DIAG_CANDS = 2 * (S_DIAG_J1 - S_DIAG_J0 + 1);
 
 struct SearchCtl {
   double fcur;   // upper bound of f at the current x
@@ -49,6 +56,7 @@ struct SearchCtl {
 
 struct SearchWs {
   double *xa, *xb, *xs, *fb;
+  double* partD;  // diagonal stage, double-buffered per round: [2][grid][value, index]
   Iv *partA, *partC;
   double* partB;  // per block: fb min, variable index (as double)
   SearchCtl* sc;
@@ -75,6 +83,11 @@ __device__ __forceinline__ bool s_candidate(double xi, double li, double ui, int
   if (q < li || q > ui) return false;
   p = q;
   return true;
+}
+
+// point of the diagonal of [l, u]: x(t) = clamp(l + t (u - l))
+__device__ __forceinline__ double s_dpt(double t, double li, double ui) {
+  return s_clamp(__dadd_rn(li, __dmul_rn(t, __dsub_rn(ui, li))), li, ui);
 }
 
 __device__ __forceinline__ double s_alpha(int a) { return scalbn(1.0, -a); }
@@ -156,6 +169,82 @@ __device__ __forceinline__ void s_block_partial(Iv* acc, Iv* out) {
     for (int k = 0; k < F::K; ++k) out[k] = acc[k];
 }
 
+// upper(F(x(t))) by one warp (lanes stride over the variables); all lanes
+// return the value
+template <class F>
+__device__ __forceinline__ double warp_upper_diag(double t, int n, const double* __restrict__ l,
+                                                  const double* __restrict__ u) {
+  constexpr int K = F::K;
+  const int lane = threadIdx.x & 31;
+  Iv acc[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) acc[k] = s_ident<F>(k < K ? k : 0);
+  for (int i = lane; i < n; i += 32) {
+    const double xi = s_dpt(t, l[i], u[i]);
+    if constexpr (F::CHAIN) {
+      LevyVals me = ObjLevy::vals(iv(xi)), nx;
+      if (i < n - 1) nx = ObjLevy::vals(iv(s_dpt(t, l[i + 1], u[i + 1])));
+      acc[0] = acc[0] + levy_own(me, &nx, i, n);
+    } else {
+      Iv tt[2];
+      F::terms(iv(xi), i, n, tt);
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc[k] = acc_comb<F>(k, acc[k], tt[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      Iv q{__shfl_xor_sync(0xffffffffu, acc[k].lo, o), __shfl_xor_sync(0xffffffffu, acc[k].hi, o)};
+      acc[k] = s_comb<F>(k, acc[k], q);
+    }
+  return s_outer_hi<F>(acc, n);
+}
+
+// (value, index) lexicographic minimum over the block -> out[0..1] (thread 0)
+__device__ __forceinline__ void block_argmin_out(double v, int k, double* out) {
+  __shared__ double s_v[S_TPB / 32];
+  __shared__ int s_k[S_TPB / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    int ok = __shfl_xor_sync(0xffffffffu, k, o);
+    if (ov < v || (ov == v && ok < k)) {
+      v = ov;
+      k = ok;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_v[threadIdx.x >> 5] = v;
+    s_k[threadIdx.x >> 5] = k;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < S_TPB / 32; ++w)
+      if (s_v[w] < v || (s_v[w] == v && s_k[w] < k)) {
+        v = s_v[w];
+        k = s_k[w];
+      }
+    out[0] = v;
+    out[1] = (double)k;
+  }
+  __syncthreads();
+}
+// every block: the minimum over the per-block (value, index) pairs, in block order
+__device__ __forceinline__ void grid_argmin_read(const double* part, int G, double& v, int& k) {
+  v = CUDART_INF;
+  k = 0x7fffffff;
+  for (int b = 0; b < G; ++b) {
+    double pv = part[2 * b];
+    int pk = (int)part[2 * b + 1];
+    if (pv < v || (pv == v && pk < k)) {
+      v = pv;
+      k = pk;
+    }
+  }
+}
+
 template <class F>
 __global__ void __launch_bounds__(S_TPB) k_search(int n, const double* __restrict__ l, const double* __restrict__ u,
                                                   SearchWs w, int rmax, unsigned long long* gub_key,
@@ -172,13 +261,58 @@ __global__ void __launch_bounds__(S_TPB) k_search(int n, const double* __restric
   __shared__ double s_wmin[S_TPB / 32];
   __shared__ int s_wi[S_TPB / 32];
 
+  // ------------------------------------------------------------ diagonal stage
+  const long gw0 = gt >> 5, TW0 = T >> 5;
+  double ts, fs;
+  {
+    double bv = CUDART_INF;
+    int bk = 0x7fffffff;
+    const int nd = (1 << S_DIAG_LOG2) + 1;
+    for (long k = gw0; k < nd; k += TW0) {  // k ascending per warp: first k kept on ties
+      double v = warp_upper_diag<F>(scalbn((double)k, -S_DIAG_LOG2), n, l, u);
+      if (v < bv) {
+        bv = v;
+        bk = (int)k;
+      }
+    }
+    block_argmin_out(bv, bk, w.partD + 2 * blockIdx.x);
+    grid.sync();
+    int ks;
+    grid_argmin_read(w.partD, G, fs, ks);
+    ts = scalbn((double)ks, -S_DIAG_LOG2);
+  }
+  for (int dr = 0; dr < S_DIAG_ROUNDS; ++dr) {
+    double* pd = w.partD + (size_t)2 * G * ((dr + 1) & 1);
+    double bv = CUDART_INF;
+    int bc = 0x7fffffff;
+    for (long c = gw0; c < S_DIAG_CANDS; c += TW0) {
+      const int j = S_DIAG_J0 + (int)c / 2;
+      const double t = (c & 1) ? __dadd_rn(ts, scalbn(1.0, -j)) : __dsub_rn(ts, scalbn(1.0, -j));
+      if (t < 0.0 || t > 1.0) continue;
+      double v = warp_upper_diag<F>(t, n, l, u);
+      if (v < bv) {
+        bv = v;
+        bc = (int)c;
+      }
+    }
+    block_argmin_out(bv, bc, pd + 2 * blockIdx.x);
+    grid.sync();
+    double v;
+    int c;
+    grid_argmin_read(pd, G, v, c);
+    if (!(v < fs)) break;
+    const int j = S_DIAG_J0 + c / 2;
+    ts = (c & 1) ? __dadd_rn(ts, scalbn(1.0, -j)) : __dsub_rn(ts, scalbn(1.0, -j));
+    fs = v;
+  }
+
   double* xo = w.xa;  // x of the previous round (read-only in phase A)
   double* xn = w.xb;  // x of this round
   int dec = S_NONE, istar = -1, r = 0;
-  bool first = true;  // phase A of round 0 starts from the midpoint of [l, u]
+  bool first = true;  // phase A of round 0 starts from the diagonal point x(t*)
   double fcur = 0.0;
   auto x_of = [&](long j) -> double {
-    if (first) return s_clamp(__dadd_rn(l[j], __dmul_rn(__dsub_rn(u[j], l[j]), 0.5)), l[j], u[j]);
+    if (first) return s_dpt(ts, l[j], u[j]);
     return s_apply(xo[j], w.xs[j], dec, istar, (int)j, l[j], u[j]);
   };
   for (;;) {
@@ -413,7 +547,7 @@ __global__ void __launch_bounds__(S_TPB) k_search(int n, const double* __restric
 
 size_t search_ws_bytes(int n, int grid) {
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-  return 4 * al(sizeof(double) * (size_t)n) + al(sizeof(Iv) * 2 * (size_t)grid) +
+  return 4 * al(sizeof(double) * (size_t)n) + al(sizeof(double) * 4 * (size_t)grid) + al(sizeof(Iv) * 2 * (size_t)grid) +
          al(sizeof(Iv) * 2 * S_ALPHAS * (size_t)grid) + al(sizeof(double) * 2 * (size_t)grid) + al(sizeof(SearchCtl)) +
          256;
 }
@@ -446,6 +580,7 @@ int launch_search(int fid, int n, const double* l, const double* u, int rounds, 
   w.xb = (double*)take(sizeof(double) * n);
   w.xs = (double*)take(sizeof(double) * n);
   w.fb = (double*)take(sizeof(double) * n);
+  w.partD = (double*)take(sizeof(double) * 4 * grid);
   w.partA = (Iv*)take(sizeof(Iv) * 2 * grid);
   w.partC = (Iv*)take(sizeof(Iv) * 2 * S_ALPHAS * grid);
   w.partB = (double*)take(sizeof(double) * 2 * grid);

@@ -271,7 +271,8 @@ def test_search_matches_oracle(pb, fid, n):
     ev = oracle.eval_point(fid, x)
     assert ev[0] <= f + t and f <= ev[1] + t
     if r == ro:
-        assert np.max(np.abs(x - xo)) <= 1e-9 * (1 + np.max(np.abs(u - l)))
+        # flat optima: points agree to ~sqrt(ulp) where the values tie
+        assert np.max(np.abs(x - xo)) <= 1e-7 * (1 + np.max(np.abs(u - l)))
 
 
 @pytest.mark.parametrize("rounds", [0, 1, 3])
