@@ -20,6 +20,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -133,26 +134,32 @@ __device__ __forceinline__ LevyChunk levy_chunk(int c, int d, int n) {
 }
 
 // ====================================================================== prep
-// One block per selected box b.  Source row: archive slot sel_slot[b] of
-// src_lo/src_hi with record code sel_code[b]; destination: slot new_slot[b]
-// of dst_lo/dst_hi.  src_sc / dst_sc hold each slot's chunk start.
+// Parent b of the batch is handled by P.pslices blocks (one block when the
+// batch is large; for large n and small batches the n variables are cut into
+// slices so that the O(n) reduction spreads over the SMs).  Block (b, s):
+// materialises its slice of the new parent (source row: archive slot
+// sel_slot[b] of src_lo/src_hi with record code sel_code[b]; destination:
+// slot new_slot[b] of dst_lo/dst_hi) and reduces the terms of its unsplit
+// variables; the partial results go to ppart, and the last block of the
+// parent to finish (threadfence + ticket) combines them in slice order and
+// writes the header and the piece tables.  src_sc / dst_sc hold each slot's
+// chunk start.
 template <class F, int BS>
-__global__ void __launch_bounds__(BS) k_prep(Problem P, const Ctl* __restrict__ ctl, const int32_t* __restrict__ sel_slot,
-                                             const uint32_t* __restrict__ sel_code, int32_t* __restrict__ new_slot,
-                                             const int32_t* __restrict__ free_list,
-                                              const double* __restrict__ src_lo,
-                                              const double* __restrict__ src_hi,
-                                              const int32_t* __restrict__ src_sc, double* dst_lo,
-                                              double* dst_hi, int32_t* dst_sc, double* tab,
-                                              int tab_stride) {
-  const int b = blockIdx.x;
+__device__ __forceinline__ void prep_item(const Problem& P, const Ctl* __restrict__ ctl,
+                                          const int32_t* __restrict__ sel_slot, const uint32_t* __restrict__ sel_code,
+                                          int32_t* __restrict__ new_slot, const int32_t* __restrict__ free_list,
+                                          const double* __restrict__ src_lo, const double* __restrict__ src_hi,
+                                          const int32_t* __restrict__ src_sc, double* dst_lo, double* dst_hi,
+                                          int32_t* dst_sc, double* tab, int tab_stride, double* __restrict__ ppart,
+                                          unsigned int* __restrict__ pticket, const int b, const int s) {
+  const int S = P.pslices;
   if (ctl->done || b >= (int)ctl->B) return;
   const int n = P.n, d = P.d, m = P.m;
   const int src = sel_slot[b];
   const uint32_t code = sel_code[b];
   // archive slot of the new parent: popped from the free list (solve) or given
   const int dst = free_list ? free_list[ctl->free_top - 1 - b] : new_slot[b];
-  if (free_list && threadIdx.x == 0) new_slot[b] = dst;
+  if (free_list && s == 0 && threadIdx.x == 0) new_slot[b] = dst;
   const int psc = src_sc[src];
   const int c = (code == CODE_WHOLE) ? psc : (psc + d) % n;  // line 184
   const double* slo = src_lo + (size_t)src * P.ld;
@@ -160,17 +167,10 @@ __global__ void __launch_bounds__(BS) k_prep(Problem P, const Ctl* __restrict__ 
   double* dlo = dst_lo + (size_t)dst * P.ld;
   double* dhi = dst_hi + (size_t)dst * P.ld;
   double* T = tab + (size_t)b * tab_stride;
-
-  Iv acc[2], accm[2];
-#pragma unroll
-  for (int k = 0; k < 2; ++k) acc[k] = accm[k] = iv(0.0);
-  if constexpr (!F::CHAIN) {
-#pragma unroll
-    for (int k = 0; k < F::K; ++k) acc[k] = accm[k] = acc_ident<F>(k);
-  }
-  double wmax = 0.0;
-  for (int i = threadIdx.x; i < n; i += BS) {
-    double a = slo[i], bb = shi[i];
+  // variable i of the new parent (Eq. 8-11 applied to the selected record)
+  auto mat = [&](int i, double& a, double& bb) {
+    a = slo[i];
+    bb = shi[i];
     if (code != CODE_WHOLE) {
       int jj = (i - psc + n) % n;
       if (jj < d) {
@@ -180,6 +180,22 @@ __global__ void __launch_bounds__(BS) k_prep(Problem P, const Ctl* __restrict__ 
         bb = b2;
       }
     }
+  };
+  const int per = (n + S - 1) / S;
+  const int i0 = s * per, i1 = min(n, i0 + per);
+
+  Iv acc[2], accm[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) acc[k] = accm[k] = iv(0.0);
+  if constexpr (!F::CHAIN) {
+#pragma unroll
+    for (int k = 0; k < F::K; ++k) acc[k] = accm[k] = acc_ident<F>(k);
+  }
+  double wmax = 0.0;
+  LevyChunk q = levy_chunk(c, d, n);
+  for (int i = i0 + threadIdx.x; i < i1; i += BS) {
+    double a, bb;
+    mat(i, a, bb);
     dlo[i] = a;
     dhi[i] = bb;
     if (((i - c + n) % n) >= d) {
@@ -196,51 +212,121 @@ __global__ void __launch_bounds__(BS) k_prep(Problem P, const Ctl* __restrict__ 
         }
       }
     }
-  }
-  __syncthreads();  // the destination row is complete (block-visible)
-
-  if constexpr (F::CHAIN) {
-    // Levy: rest = sum of chain terms that involve no split variable
-    LevyChunk q = levy_chunk(c, d, n);
-    Iv r = iv(0.0), rm = iv(0.0);
-    for (int i = threadIdx.x; i < n; i += BS) {
-      bool ji = q.inJ(i);
-      Iv X{dlo[i], dhi[i]};
-      double xm = midpt(X.lo, X.hi);
+    if constexpr (F::CHAIN) {
+      // Levy: rest = sum of chain terms that involve no split variable
+      const bool ji = q.inJ(i);
+      Iv X{a, bb};
+      double xm = midpt(a, bb);
       LevyVals v = ObjLevy::vals(X), vm = ObjLevy::vals(Iv{xm, xm});
       if (i == 0 && !ji) {
-        r = r + v.s0;
-        rm = rm + vm.s0;
+        acc[0] = acc[0] + v.s0;
+        accm[0] = accm[0] + vm.s0;
       }
       if (i <= n - 2 && !ji && !q.inJ(i + 1)) {
-        Iv X1{dlo[i + 1], dhi[i + 1]};
-        double xm1 = midpt(X1.lo, X1.hi);
-        LevyVals w = ObjLevy::vals(X1), wm = ObjLevy::vals(Iv{xm1, xm1});
-        r = r + mulpos(v.u, w.v);
-        rm = rm + mulpos(vm.u, wm.v);
+        double a1, b1;
+        mat(i + 1, a1, b1);
+        double xm1 = midpt(a1, b1);
+        LevyVals w = ObjLevy::vals(Iv{a1, b1}), wm = ObjLevy::vals(Iv{xm1, xm1});
+        acc[0] = acc[0] + mulpos(v.u, w.v);
+        accm[0] = accm[0] + mulpos(vm.u, wm.v);
       }
       if (i == n - 1 && !ji) {
-        r = r + v.u;
-        rm = rm + vm.u;
+        acc[0] = acc[0] + v.u;
+        accm[0] = accm[0] + vm.u;
       }
     }
-    Iv a2[2] = {r, iv(0.0)}, am2[2] = {rm, iv(0.0)};
+  }
+  if constexpr (F::CHAIN) {
+    Iv a2[2] = {acc[0], iv(0.0)}, am2[2] = {accm[0], iv(0.0)};
     block_reduce_acc<ObjRastrigin, BS>(a2);  // any K=1 SUM reducer
     block_reduce_acc<ObjRastrigin, BS>(am2);
     acc[0] = a2[0];
     accm[0] = am2[0];
+  } else {
+    block_reduce_acc<F, BS>(acc);
+    block_reduce_acc<F, BS>(accm);
+  }
+  wmax = block_max<BS>(wmax);
+  if (S > 1) {
+    // publish this slice's partial; the last slice block of parent b goes on
+    __shared__ int s_last;
     if (threadIdx.x == 0) {
+      double* pp = ppart + ((size_t)b * S + s) * 10;
+      for (int k = 0; k < 2; ++k) {
+        put(pp + 2 * k, acc[k]);
+        put(pp + 4 + 2 * k, accm[k]);
+      }
+      pp[8] = wmax;
+      __threadfence();
+      s_last = atomicAdd(&pticket[b], 1u) == (unsigned)(S - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    {
+      // combine the S partials in a fixed tree order (deterministic)
+      const double* pp = ppart + (size_t)b * S * 10;
+      Iv ra[2], rm[2];
+      double rw = 0.0;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) ra[k] = rm[k] = iv(0.0);
+      if constexpr (!F::CHAIN) {
+#pragma unroll
+        for (int k = 0; k < F::K; ++k) ra[k] = rm[k] = acc_ident<F>(k);
+      }
+      for (int t = threadIdx.x; t < S; t += BS) {
+        const double* pt = pp + (size_t)t * 10;
+        if constexpr (F::CHAIN) {
+          ra[0] = ra[0] + get(pt);
+          rm[0] = rm[0] + get(pt + 4);
+        } else {
+#pragma unroll
+          for (int k = 0; k < F::K; ++k) {
+            ra[k] = acc_comb<F>(k, ra[k], get(pt + 2 * k));
+            rm[k] = acc_comb<F>(k, rm[k], get(pt + 4 + 2 * k));
+          }
+        }
+        rw = fmax(rw, pt[8]);
+      }
+      if constexpr (F::CHAIN) {
+        block_reduce_acc<ObjRastrigin, BS>(ra);
+        block_reduce_acc<ObjRastrigin, BS>(rm);
+      } else {
+        block_reduce_acc<F, BS>(ra);
+        block_reduce_acc<F, BS>(rm);
+      }
+      rw = block_max<BS>(rw);
+      for (int k = 0; k < 2; ++k) {
+        acc[k] = ra[k];
+        accm[k] = rm[k];
+      }
+      wmax = rw;
+    }
+    if (threadIdx.x == 0) {
+      pticket[b] = 0u;  // every slice block of b has arrived: reset for the next launch
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 2; ++k) {
+      put(T + H_REST + 2 * k, acc[k]);
+      put(T + H_RESTM + 2 * k, accm[k]);
+    }
+    T[H_WREST] = wmax;
+    T[H_CHUNK] = (double)c;
+    dst_sc[dst] = c;
+    if constexpr (F::CHAIN) {
       // neighbour values and the list of affected chain terms
       double* nb_ = T + H_LEVY_NB;
       int nbv[2] = {q.L, q.R};
-      for (int s = 0; s < 2; ++s) {
-        Iv X = nbv[s] >= 0 ? Iv{dlo[nbv[s]], dhi[nbv[s]]} : iv(0.0);
+      for (int sd = 0; sd < 2; ++sd) {
+        Iv X = iv(0.0);
+        if (nbv[sd] >= 0) mat(nbv[sd], X.lo, X.hi);
         double xm = midpt(X.lo, X.hi);
         LevyVals v = ObjLevy::vals(X), vm = ObjLevy::vals(Iv{xm, xm});
-        put(nb_ + 8 * s + 0, v.u);
-        put(nb_ + 8 * s + 2, v.v);
-        put(nb_ + 8 * s + 4, vm.u);
-        put(nb_ + 8 * s + 6, vm.v);
+        put(nb_ + 8 * sd + 0, v.u);
+        put(nb_ + 8 * sd + 2, v.v);
+        put(nb_ + 8 * sd + 4, vm.u);
+        put(nb_ + 8 * sd + 6, vm.v);
       }
       int nt = 0;
       double* td = T + H_LEVY_T;
@@ -256,25 +342,13 @@ __global__ void __launch_bounds__(BS) k_prep(Problem P, const Ctl* __restrict__ 
       T[H_LEVY_LR] = (double)q.L;
       T[H_LEVY_LR + 1] = (double)q.R;
     }
-  } else {
-    block_reduce_acc<F, BS>(acc);
-    block_reduce_acc<F, BS>(accm);
-  }
-  wmax = block_max<BS>(wmax);
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < 2; ++k) {
-      put(T + H_REST + 2 * k, acc[k]);
-      put(T + H_RESTM + 2 * k, accm[k]);
-    }
-    T[H_WREST] = wmax;
-    T[H_CHUNK] = (double)c;
-    dst_sc[dst] = c;
   }
   // tables of the m pieces of the d split variables
   for (int t = threadIdx.x; t < d * m; t += BS) {
     int j = t / m, p = t % m;
     int i = (c + j) % n;
-    double a = dlo[i], bb = dhi[i];
+    double a, bb;
+    mat(i, a, bb);
     double pa = part_point(a, bb, m, p), pb = part_point(a, bb, m, p + 1);
     double xm = midpt(pa, pb);
     double* e = T + HDR + (size_t)t * ENT;
@@ -310,6 +384,19 @@ __global__ void __launch_bounds__(BS) k_prep(Problem P, const Ctl* __restrict__ 
       e[E_T + 4 * F::K + 2 * F::KG] = flag;
     }
   }
+}
+
+template <class F, int BS>
+__global__ void __launch_bounds__(BS) k_prep(Problem P, const Ctl* __restrict__ ctl, const int32_t* __restrict__ sel_slot,
+                                             const uint32_t* __restrict__ sel_code, int32_t* __restrict__ new_slot,
+                                             const int32_t* __restrict__ free_list, const double* __restrict__ src_lo,
+                                             const double* __restrict__ src_hi, const int32_t* __restrict__ src_sc,
+                                             double* dst_lo, double* dst_hi, int32_t* dst_sc, double* tab,
+                                             int tab_stride, double* __restrict__ ppart,
+                                             unsigned int* __restrict__ pticket) {
+  const int b = blockIdx.x / P.pslices;
+  prep_item<F, BS>(P, ctl, sel_slot, sel_code, new_slot, free_list, src_lo, src_hi, src_sc, dst_lo, dst_hi, dst_sc,
+                   tab, tab_stride, ppart, pticket, b, blockIdx.x - b * P.pslices);
 }
 
 // ================================================================ children
@@ -475,10 +562,10 @@ __device__ __noinline__ bool child_mono_ok(const Problem& P, const double* __res
 // GT = 8: bisection (m = 2, h = 3) with the group loop fully unrolled so the
 // outer functions of the 8 children interleave (ILP); GT = 0: runtime G
 template <class F, int GT>
-__global__ void __launch_bounds__(TPB, GT ? 3 : 4) k_child_eval(Problem P, Ctl* __restrict__ ctl,
-                                                       const double* __restrict__ tab, int tab_stride,
-                                                       double* __restrict__ clb, uint64_t* zero_a, uint64_t* zero_b,
-                                                       long nzero, uint32_t* zero_ctr, unsigned int* zero_hist) {
+__device__ __forceinline__ void child_eval_dev(const Problem& P, Ctl* __restrict__ ctl,
+                                               const double* __restrict__ tab, int tab_stride,
+                                               double* __restrict__ clb, uint64_t* zero_a, uint64_t* zero_b,
+                                               long nzero, uint32_t* zero_ctr, unsigned int* zero_hist) {
   if (ctl->done) return;
   if (zero_a) {  // descriptors and tickets of the following k_cand / k_emit,
                  // histograms and accumulators of the next k_list
@@ -563,6 +650,15 @@ __global__ void __launch_bounds__(TPB, GT ? 3 : 4) k_child_eval(Problem P, Ctl* 
   }
 }
 
+template <class F, int GT>
+__global__ void __launch_bounds__(TPB, GT ? 3 : 4) k_child_eval(Problem P, Ctl* __restrict__ ctl,
+                                                               const double* __restrict__ tab, int tab_stride,
+                                                               double* __restrict__ clb, uint64_t* zero_a,
+                                                               uint64_t* zero_b, long nzero, uint32_t* zero_ctr,
+                                                               unsigned int* zero_hist) {
+  child_eval_dev<F, GT>(P, ctl, tab, tab_stride, clb, zero_a, zero_b, nzero, zero_ctr, zero_hist);
+}
+
 // Pass 2a: stable compaction of the candidates (children with lb <= GUB,
 // line 140) into cand[] (decoupled look-back).
 __device__ void cand_dev(const Problem& P, Ctl* __restrict__ ctl, const double* __restrict__ clb,
@@ -609,6 +705,17 @@ __device__ void mono_dev(const Problem& P, const Ctl* __restrict__ ctl, const do
 // Pass 2c: insert the surviving candidates into L after its current end, in
 // (parent, code) order (line 146), stable decoupled-look-back compaction.
 __device__ void iter_end_dev(Ctl* ctl, long kids);
+// the next k_fused list phase may take the single-block path: every live
+// record is in the hot index (tau = ~0) and, with this iteration's survivors,
+// it has at most min(bmax, TPB) entries (decided here, before the barrier,
+// so that every block reads the same flag)
+__device__ __forceinline__ void set_list_fast(Ctl* ctl, unsigned long long nsurv_hot) {
+  const unsigned long long nh = ctl->nhot + nsurv_hot;
+  ctl->list_fast = ctl->hot_valid && ctl->tau_key == ~0ull && nh <= ctl->bmax && nh <= (unsigned long long)TPB;
+}
+// MONO: the first-order test of each candidate is evaluated here (fused
+// kernel) instead of being read from ok[] (k_mono)
+template <class F, bool MONO>
 __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* __restrict__ tab, int tab_stride,
                          const double* __restrict__ clb, const uint32_t* __restrict__ cand,
                          const uint8_t* __restrict__ ok, const int32_t* __restrict__ new_slot, Pool out,
@@ -628,7 +735,10 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
     if (tile == 0 && threadIdx.x == 0) {
       ctl->nsurv = 0;
       ctl->nsurv_hot = 0;
-      if (finish) ctl->pending_end = 1;
+      if (finish) {
+        ctl->pending_end = 1;
+        set_list_fast(ctl, 0ull);
+      }
     }
     break;
   }
@@ -636,11 +746,21 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
   const long k0 = (long)tile * TILE + (long)threadIdx.x * IPT;
   uint32_t f = 0, fh = 0;
 #pragma unroll
-  for (int q = 0; q < IPT; ++q)
-    if (k0 + q < nc && ok[k0 + q]) {
+  for (int q = 0; q < IPT; ++q) {
+    bool okq = false;
+    if (k0 + q < nc) {
+      if constexpr (MONO) {
+        ChildIdx ci = child_of(cand[k0 + q], P);
+        okq = !P.mono || child_mono_ok<F>(P, tab + (size_t)ci.b * tab_stride, ci.code);
+      } else {
+        okq = ok[k0 + q] != 0;
+      }
+    }
+    if (okq) {
       f |= 1u << q;
       if (hot && okey(clb[cand[k0 + q]]) < tau) fh |= 1u << q;
     }
+  }
   uint32_t c2[2] = {(uint32_t)__popc(f), (uint32_t)__popc(fh)}, ex[2], tot[2];
   block_exclusive_scan<2, TPB>(c2, ex, tot);
   uint64_t pfx[2];
@@ -671,7 +791,10 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
     }
     // the iteration end is applied by the next k_list (other tiles may still
     // be reading pcount as their base here)
-    if (finish) ctl->pending_end = 1;
+    if (finish) {
+      ctl->pending_end = 1;
+      set_list_fast(ctl, pfx[1] + tot[1]);
+    }
   }
   }
 }
@@ -694,7 +817,8 @@ __global__ void __launch_bounds__(TPB) k_emit(const Problem P, Ctl* __restrict__
                                               const int32_t* __restrict__ new_slot, Pool out, uint64_t* desc,
                                               uint32_t* tile_ctr, int finish, uint32_t* hot0, uint32_t* hot1) {
   if (ctl->done) return;
-  emit_dev(P, ctl, tab, tab_stride, clb, cand, ok, new_slot, out, desc, tile_ctr, finish != 0, hot0, hot1);
+  emit_dev<ObjExample, false>(P, ctl, tab, tab_stride, clb, cand, ok, new_slot, out, desc, tile_ctr, finish != 0, hot0,
+                              hot1);
 }
 
 // ============================================================ list L kernels
@@ -835,6 +959,19 @@ __device__ void maxw_accum_dev(const Pool& p, Ctl* ctl) {
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (r0 + u * gs < cnt && lbv[u] <= gub) mw = fmax(mw, wv[u]);
+  }
+  mw = warp_max(mw);
+  if ((threadIdx.x & 31) == 0) atomicMax(&ctl->acc_max_w, (unsigned long long)__double_as_longlong(mw));
+}
+
+// max width of the live records listed in a hot index (all live records
+// are there when tau = ~0)
+__device__ void maxw_hot_dev(const Pool& p, const uint32_t* __restrict__ hot, long nh, Ctl* ctl) {
+  const double gub = okey_inv(ctl->gub_key);
+  double mw = 0.0;
+  for (long k = (long)blockIdx.x * TPB + threadIdx.x; k < nh; k += (long)gridDim.x * TPB) {
+    const uint32_t r = hot[k];
+    if (p.lb[r] <= gub) mw = fmax(mw, p.w[r]);
   }
   mw = warp_max(mw);
   if ((threadIdx.x & 31) == 0) atomicMax(&ctl->acc_max_w, (unsigned long long)__double_as_longlong(mw));
@@ -1254,9 +1391,119 @@ __device__ void hot_select_dev(const Pool& p, const uint32_t* __restrict__ hin, 
 // decisions from the same global values after each grid barrier; thread 0
 // of block 0 records them in ctl.  hists: 16 x 256 zeroed counters (zeroed
 // again by k_child_eval); the acc_* fields likewise.
-__global__ void __launch_bounds__(TPB) k_list(Pool p, Ctl* ctl, unsigned int* hists, int32_t* sel_slot,
-                                              uint32_t* sel_code, uint64_t* desc, uint64_t* desc2, uint32_t* tile_ctr,
-                                              uint32_t* hot0, uint32_t* hot1, long kids) {
+// Single-block list phase (k_fused, when ctl->list_fast): the same decisions
+// as list_dev when every live record is in a hot index of at most
+// min(bmax, TPB) entries -- then live <= bmax, the selection takes every live
+// entry in list order and no radix pass is needed.  Block 0 only.
+__device__ void list_small_dev(const Pool& p, Ctl* ctl, uint32_t* hot0, uint32_t* hot1, int32_t* sel_slot,
+                               uint32_t* sel_code, long kids) {
+  __shared__ unsigned long long s_live, s_min;
+  __shared__ double s_w;
+  __shared__ uint32_t s_scan[TPB / 32];
+  if (ctl->done) return;
+  if (threadIdx.x == 0) {
+    if (ctl->pending_end) {
+      ctl->pending_end = 0;
+      iter_end_dev(ctl, kids);
+    }
+    s_live = 0;
+    s_min = ~0ull;
+    s_w = 0.0;
+  }
+  __syncthreads();
+  const double gub = okey_inv(ctl->gub_key);
+  const int hsel = ctl->hsel;
+  const long nh = (long)ctl->nhot;
+  const uint32_t* hin = hsel ? hot1 : hot0;
+  const int t = threadIdx.x;
+  uint32_t r = 0;
+  double lb = CUDART_INF, wv = 0.0;
+  bool live = false;
+  if (t < nh) {
+    r = hin[t];
+    lb = p.lb[r];
+    wv = p.w[r];
+    live = lb <= gub;
+  }
+  const unsigned long long key = live ? okey(lb) : ~0ull;
+  // live count (exclusive scan = selection position) and min key
+  const unsigned bal = __ballot_sync(0xffffffffu, live);
+  const int lane = t & 31, wid = t >> 5;
+  unsigned long long mk = key;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long q = __shfl_xor_sync(0xffffffffu, mk, o);
+    mk = q < mk ? q : mk;
+  }
+  if (lane == 0) {
+    s_scan[wid] = __popc(bal);
+    if (mk != ~0ull) atomicMin(&s_min, mk);
+  }
+  __syncthreads();
+  uint32_t before = 0, total = 0;
+  for (int w2 = 0; w2 < TPB / 32; ++w2) {
+    if (w2 < wid) before += s_scan[w2];
+    total += s_scan[w2];
+  }
+  const uint32_t pos = before + __popc(bal & ((1u << lane) - 1u));
+  const unsigned long long nlive = total, minkey = s_min;
+  unsigned long long bytes = 12ull * nh;
+  int done = 0;
+  if (nlive == 0) {
+    done = 3;
+  } else if (__dsub_ru(gub, okey_inv(minkey)) <= ctl->eps_f) {
+    double mw = live ? wv : 0.0;
+    mw = warp_max(mw);
+    if (lane == 0) atomicMax((unsigned long long*)&s_w, (unsigned long long)__double_as_longlong(mw));
+    __syncthreads();
+    bytes += 20ull * nh;
+    if (t == 0) {
+      ctl->nwidth += 1;
+      const unsigned long long wb = (unsigned long long)__double_as_longlong(s_w);
+      if (wb > ctl->acc_max_w) ctl->acc_max_w = wb;
+    }
+    if (s_w <= ctl->eps_x) done = 1;
+  }
+  if (!done && ctl->iter >= ctl->max_iter) done = 2;
+  const unsigned long long B = nlive;  // nlive <= nh <= bmax
+  if (!done && ctl->free_top < B) done = 4;
+  if (done) {
+    __syncthreads();
+    if (t == 0) {
+      ctl->live = nlive;
+      ctl->min_lb_key = minkey;
+      ctl->max_w_bits = ctl->acc_max_w;
+      if (done == 4) ctl->err = -2;
+      ctl->list_bytes += bytes;
+      ctl->done = done;
+    }
+    return;
+  }
+  // selection (line 130): every live entry, in list order; L loses them
+  if (live) {
+    sel_slot[pos] = p.slot[r];
+    sel_code[pos] = p.code[r];
+    p.lb[r] = CUDART_INF;
+  }
+  bytes += 16ull * nh;
+  __syncthreads();
+  if (t == 0) {
+    ctl->nhot_keep = 0;
+    ctl->hsel = hsel ^ 1;
+    ctl->nhot = 0;
+    ctl->B = B;
+    ctl->live = nlive;
+    ctl->min_lb_key = minkey;
+    ctl->known = 0;
+    ctl->prefix = 0;
+    ctl->need = B;
+    ctl->list_bytes += bytes;
+  }
+}
+
+__device__ void list_dev(const Pool& p, Ctl* ctl, unsigned int* hists, int32_t* sel_slot, uint32_t* sel_code,
+                         uint64_t* desc, uint64_t* desc2, uint32_t* tile_ctr, uint32_t* hot0, uint32_t* hot1,
+                         long kids) {
   cg::grid_group grid = cg::this_grid();
   if (ctl->done) return;  // uniform: read before any block writes it
   const long gtid = (long)blockIdx.x * TPB + threadIdx.x, gsize = (long)gridDim.x * TPB;
@@ -1349,8 +1596,13 @@ __global__ void __launch_bounds__(TPB) k_list(Pool p, Ctl* ctl, unsigned int* hi
   if (live == 0) {
     done = 3;  // the refill found no live record: L is empty
   } else if (__dsub_ru(gub, okey_inv(minkey)) <= ctl->eps_f) {
-    maxw_accum_dev(p, ctl);  // the width test decides: max width of all of L
-    bytes += 16ull * pc;
+    if (tau == ~0ull) {  // every live record is in the hot index
+      maxw_hot_dev(p, hsel ? hot1 : hot0, nh, ctl);
+      bytes += 20ull * nh;
+    } else {
+      maxw_accum_dev(p, ctl);  // the width test decides: max width of all of L
+      bytes += 16ull * pc;
+    }
     if (lead) ctl->nwidth += 1;
     grid.sync();
     if (__longlong_as_double((long long)__ldcg(&ctl->acc_max_w)) <= ctl->eps_x) done = 1;
@@ -1409,6 +1661,12 @@ __global__ void __launch_bounds__(TPB) k_list(Pool p, Ctl* ctl, unsigned int* hi
   }
 }
 
+__global__ void __launch_bounds__(TPB) k_list(Pool p, Ctl* ctl, unsigned int* hists, int32_t* sel_slot,
+                                              uint32_t* sel_code, uint64_t* desc, uint64_t* desc2, uint32_t* tile_ctr,
+                                              uint32_t* hot0, uint32_t* hot1, long kids) {
+  list_dev(p, ctl, hists, sel_slot, sel_code, desc, desc2, tile_ctr, hot0, hot1, kids);
+}
+
 template <class F>
 __global__ void __launch_bounds__(TPB, 2) k_prune(Problem P, Ctl* ctl, const double* __restrict__ tab, int tab_stride,
                                                   const double* __restrict__ clb, uint32_t* __restrict__ cand,
@@ -1431,7 +1689,7 @@ __global__ void __launch_bounds__(TPB, 2) k_prune(Problem P, Ctl* ctl, const dou
   grid.sync();
   mono_dev<F>(P, ctl, tab, tab_stride, cand, ok);
   grid.sync();
-  emit_dev(P, ctl, tab, tab_stride, clb, cand, ok, new_slot, out, desc2, tile_ctr + 1, false, nullptr, nullptr);
+  emit_dev<F, false>(P, ctl, tab, tab_stride, clb, cand, ok, new_slot, out, desc2, tile_ctr + 1, false, nullptr, nullptr);
   grid.sync();
   if (gtid == 0) iter_end_dev(ctl, P.kids);
 }
@@ -1707,6 +1965,64 @@ __global__ void __launch_bounds__(TPB) k_eval_grad(int n, long nreq, const doubl
   }
 }
 
+// ===================================================== fused persistent kernel
+// Small batches (large n, few live regions): one cooperative launch runs up
+// to `iters` whole iterations, the phases of each separated by grid
+// barriers instead of kernel boundaries.  The phases are the same device
+// functions as the multi-kernel path, in the same order, so both paths take
+// identical decisions and produce identical results.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <class F, int GT>
+__global__ void __launch_bounds__(TPB, 1) k_fused(Problem P, IterBufs w, int iters, long nz) {
+  cg::grid_group grid = cg::this_grid();
+  const long kids = P.kids;
+  // optional phase timer (IBNB_TRACE): block 0 accumulates ns per phase
+  unsigned long long* ts = (w.tstamp && blockIdx.x == 0 && threadIdx.x == 0) ? w.tstamp : nullptr;
+  unsigned long long t0 = ts ? gtimer() : 0ull;
+  auto mark = [&](int ph) {
+    if (ts) {
+      unsigned long long t1 = gtimer();
+      ts[ph] += t1 - t0;
+      t0 = t1;
+    }
+  };
+  for (int it = 0; it < iters; ++it) {
+    if (w.ctl->list_fast) {  // uniform: set before the last barrier
+      if (blockIdx.x == 0) list_small_dev(w.pool, w.ctl, w.hot0, w.hot1, w.sel_slot, w.sel_code, kids);
+    } else {
+      list_dev(w.pool, w.ctl, w.hist, w.sel_slot, w.sel_code, w.desc, w.desc2, w.tile_ctr, w.hot0, w.hot1, kids);
+    }
+    grid.sync();
+    mark(0);
+    if (w.ctl->done) break;  // uniform: written before the barrier
+    const int nitems = (int)w.ctl->B * P.pslices;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+      const int b = item / P.pslices;
+      prep_item<F, TPB>(P, w.ctl, w.sel_slot, w.sel_code, w.new_slot, w.free_list, w.src_lo, w.src_hi, w.src_sc,
+                        w.dst_lo, w.dst_hi, w.dst_sc, w.tab, w.tab_stride, w.ppart, w.pticket, b,
+                        item - b * P.pslices);
+    }
+    grid.sync();
+    mark(1);
+    child_eval_dev<F, GT>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.desc, w.desc2, nz, w.tile_ctr, w.hist);
+    grid.sync();
+    mark(2);
+    cand_dev(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
+    grid.sync();
+    mark(3);
+    emit_dev<F, true>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok, w.new_slot, w.pool, w.desc2, w.tile_ctr + 1,
+                      true, w.hot0, w.hot1);
+    grid.sync();
+    mark(5);
+    if (ts) ts[6] += 1;
+  }
+}
+
 // ================================================================ launchers
 static inline unsigned grid_for(long items, int per_block, unsigned cap = 148u * 32u) {
   long g = (items + per_block - 1) / per_block;
@@ -1723,13 +2039,14 @@ static inline unsigned scan_grid(long items) { return (unsigned)std::min(tiles_f
 // pool_bound / batch_bound: host upper bounds of |L| and B * m^d for grids.
 template <class F>
 static void launch_prep_t(const Problem& P, const IterBufs& w, long nb, const int32_t* free_list, cudaStream_t st) {
+  const unsigned g = (unsigned)(nb * P.pslices);
   if (P.n <= 64)
-    k_prep<F, 32><<<(unsigned)nb, 32, 0, st>>>(P, w.ctl, w.sel_slot, w.sel_code, w.new_slot, free_list, w.src_lo,
-                                                w.src_hi, w.src_sc, w.dst_lo, w.dst_hi, w.dst_sc, w.tab, w.tab_stride);
+    k_prep<F, 32><<<g, 32, 0, st>>>(P, w.ctl, w.sel_slot, w.sel_code, w.new_slot, free_list, w.src_lo, w.src_hi,
+                                     w.src_sc, w.dst_lo, w.dst_hi, w.dst_sc, w.tab, w.tab_stride, w.ppart, w.pticket);
   else
-    k_prep<F, TPB><<<(unsigned)nb, TPB, 0, st>>>(P, w.ctl, w.sel_slot, w.sel_code, w.new_slot, free_list, w.src_lo,
-                                                  w.src_hi, w.src_sc, w.dst_lo, w.dst_hi, w.dst_sc, w.tab,
-                                                  w.tab_stride);
+    k_prep<F, TPB><<<g, TPB, 0, st>>>(P, w.ctl, w.sel_slot, w.sel_code, w.new_slot, free_list, w.src_lo, w.src_hi,
+                                       w.src_sc, w.dst_lo, w.dst_hi, w.dst_sc, w.tab, w.tab_stride, w.ppart,
+                                       w.pticket);
 }
 
 template <class F>
@@ -1742,6 +2059,13 @@ static void launch_eval_t(const Problem& P, const IterBufs& w, long nkids, cudaS
     k_child_eval<F, 8><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr, w.hist);
   else
     k_child_eval<F, 0><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr, w.hist);
+}
+
+// k_list blocks for ~hint records: a power of two in [8, g_max]
+static unsigned list_grid(long hint, unsigned g_max) {
+  unsigned g = 8;
+  while (g < g_max && (long)g * 2048 < hint) g <<= 1;
+  return std::min(g, g_max);
 }
 
 // co-resident grid of a cooperative kernel (all blocks active at once)
@@ -1763,10 +2087,13 @@ static cudaError_t coop_launch(K* fn, unsigned grid, cudaStream_t st, A... args)
 // k_cand, k_mono, k_emit), every kernel reading its sizes and decisions from ctl.
 // pool_bound / bmax: host upper bounds of |L| and B, used for grid sizes.
 int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long bmax, cudaStream_t st,
-                     IterHook* hook) {
+                     IterHook* hook, long list_hint) {
   const long kids = P.kids;
-  static unsigned g_list = 0;
-  if (!g_list) g_list = coop_grid((const void*)k_list, 8);
+  static unsigned g_max = 0;
+  if (!g_max) g_max = coop_grid((const void*)k_list, 8);
+  // k_list grid: every loop is grid-strided, so any size is correct; size it
+  // to the records it will scan (grid barriers get cheaper with fewer blocks)
+  unsigned g_list = list_grid(list_hint, g_max);
   cudaError_t e;
   // statistics + stop test + batch size + radix select + selection (a1, a7)
   if (hook) hook->begin(3, pool_bound, st);
@@ -1797,6 +2124,24 @@ int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long 
                                                   w.pool, w.desc2, w.tile_ctr + 1, 1, w.hot0, w.hot1);
   if (hook) hook->end(5, st);
   LAUNCH_OK;
+}
+
+// `iters` iterations in one cooperative launch of k_fused (small batches)
+int launch_fused(const Problem& P, const IterBufs& w, int iters, long bmax, cudaStream_t st) {
+  const long nz = tiles_for(bmax * P.kids) + 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  unsigned grid = (unsigned)sms;  // one block per SM (launch bounds: co-resident)
+  if (const char* e = std::getenv("IBNB_FUSE_GRID")) grid = (unsigned)std::max(1, std::min(atoi(e), sms));
+  cudaError_t e = cudaSuccess;
+  IB_DISPATCH_FID(P.fid, {
+    if (P.m == 2 && P.G == 8 && !F::CHAIN)
+      e = coop_launch(k_fused<F, 8>, grid, st, P, w, iters, nz);
+    else
+      e = coop_launch(k_fused<F, 0>, grid, st, P, w, iters, nz);
+  });
+  return (int)e;
 }
 
 // steps a2-a6 only, for an explicit batch already in w (ib_branch): the

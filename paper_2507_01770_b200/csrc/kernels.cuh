@@ -93,7 +93,7 @@ struct Ctl {
   int hsel;       // current hot buffer (0 / 1)
   int hot_valid;  // 0: the hot index must be rebuilt (start, after compaction)
   int compact_hint;  // a refill found L more than half dead
-  int pad4;
+  int list_fast;  // k_fused: the next list phase may run on one block (set by emit)
 };
 
 struct Problem {
@@ -103,6 +103,7 @@ struct Problem {
   int kbits;               // log2(m^d) when m is a power of two, else 0
   int ld;                  // archive row stride (doubles)
   int mono;                // apply the first-order test
+  int pslices;             // k_prep blocks per parent (variable slices)
   const double* l;         // device copies of the bounds
   const double* u;
 };
@@ -126,6 +127,9 @@ struct IterBufs {
   uint64_t *desc, *desc2;
   uint32_t* tile_ctr;
   uint32_t *hot0, *hot1;  // hot index double buffer
+  double* ppart;           // k_prep slice partials: [bmax][pslices][10]
+  unsigned int* pticket;   // k_prep per-parent arrival tickets [bmax] (zero between launches)
+  unsigned long long* tstamp;  // k_fused phase timer (trace only; nullptr otherwise)
 };
 
 // host callbacks around the kernel classes of an iteration: profiling

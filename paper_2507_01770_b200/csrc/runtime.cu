@@ -25,8 +25,9 @@
 #include "kernels.cuh"
 
 namespace ib {
-int launch_iteration(const Problem&, const IterBufs&, long, long, cudaStream_t, IterHook*);
+int launch_iteration(const Problem&, const IterBufs&, long, long, cudaStream_t, IterHook*, long);
 int launch_branch(const Problem&, const IterBufs&, long, cudaStream_t);
+int launch_fused(const Problem&, const IterBufs&, int, long, cudaStream_t);
 int launch_select_only(Pool, Ctl*, unsigned int*, long, cudaStream_t);
 int launch_xchg_put(const Ctl*, double*, cudaStream_t);
 int launch_apply_pending(Ctl*, long, cudaStream_t);
@@ -82,6 +83,7 @@ __global__ void k_root(const double* root_out, double w0, Pool p, Ctl* ctl) {
 __global__ void k_set_pcount(Ctl* ctl, const uint64_t* c) {
   ctl->pcount = *c;
   ctl->hot_valid = 0;
+  ctl->list_fast = 0;
   ctl->nhot = 0;
   ctl->compact_hint = 0;
 }
@@ -162,7 +164,7 @@ static int resolve_opts(int fid, int n, const ib_options* o, int64_t pool_cap_ar
   ib_options z;
   std::memset(&z, 0, sizeof z);
   if (!o) o = &z;
-  r.d = o->d > 0 ? o->d : std::min(n, 10);
+  r.d = o->d > 0 ? o->d : std::min(n, 16);
   if (r.d > n) r.d = n;
   r.m = o->m > 0 ? o->m : 2;
   r.mono = o->mono < 0 ? 0 : 1;
@@ -192,15 +194,23 @@ static int resolve_opts(int fid, int n, const ib_options* o, int64_t pool_cap_ar
 }
 
 // children per child-eval thread: G = m^h <= 8 (h <= d)
+// k_prep blocks per parent: one unless n is large and the batch too small
+// to fill the SMs, then slices of >= 256 variables
+static int prep_slices(int n, long bmax) {
+  if (n < 512 || bmax >= 296) return 1;
+  long s = std::min((long)(n + 255) / 256, std::max(1L, 296 / bmax));
+  return (int)std::max(1L, s);
+}
+
 static Problem make_problem(int fid, int n, int d, int m, long kids, int ld, int mono, const double* l,
-                            const double* u) {
+                            const double* u, long bmax) {
   int h = 0, G = 1;
   while (h < d && G * m <= 8) {
     G *= m;
     ++h;
   }
   int mbits = (m & (m - 1)) == 0 ? __builtin_ctz((unsigned)m) : 0;
-  return Problem{fid, n, d, m, (int)kids, h, G, mbits, mbits * d, ld, mono, l, u};
+  return Problem{fid, n, d, m, (int)kids, h, G, mbits, mbits * d, ld, mono, prep_slices(n, bmax), l, u};
 }
 
 static long tiles_of(long n) { return std::max(1L, (n + TILE - 1) / TILE); }
@@ -218,6 +228,8 @@ struct SolveWs {
   uint32_t* tile_ctr;
   Ctl* ctl;
   unsigned int* hist;
+  double* ppart;
+  unsigned int* pticket;
 };
 
 static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
@@ -254,6 +266,8 @@ static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
   w.l = A.take<double>(n);
   w.u = A.take<double>(n);
   w.root_out = A.take<double>(2);
+  w.ppart = A.take<double>((size_t)o.bmax * prep_slices(n, o.bmax) * 10);
+  w.pticket = A.take<unsigned int>(o.bmax);
   w.f_search = A.take<double>(1);
   w.search_rounds = A.take<int32_t>(1);
   w.search_bytes = search_ws_bytes(n, search_grid_max());
@@ -335,6 +349,7 @@ struct GraphKey {
   const double* pool;
   void* ws;
   long bound;
+  long list_hint;  // k_list grid size class
   long bmax, pool_cap, arch_cap;  // workspace layout
 };
 static bool same_problem(const Problem& a, const Problem& b) { return std::memcmp(&a, &b, sizeof(Problem)) == 0; }
@@ -353,6 +368,7 @@ struct ThreadCache {
   cudaGraphExec_t find(const GraphKey& k, long need_bound) {
     for (auto& e : graphs)
       if (same_problem(e.k.P, k.P) && e.k.pool == k.pool && e.k.ws == k.ws && e.k.bmax == k.bmax &&
+          e.k.list_hint == k.list_hint &&
           e.k.pool_cap == k.pool_cap && e.k.arch_cap == k.arch_cap && e.k.bound >= need_bound)
         return e.ge;
     return nullptr;
@@ -385,7 +401,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   SolveWs w;
   size_t need = layout(o, n, A, w);
   if (!ws || ws_bytes < need) return fail(IB_ENOSPACE, "workspace %zu < %zu bytes", ws_bytes, need);
-  Problem P = make_problem(fid, n, o.d, o.m, o.kids, o.ld, o.mono, w.l, w.u);
+  Problem P = make_problem(fid, n, o.d, o.m, o.kids, o.ld, o.mono, w.l, w.u, o.bmax);
   Prof prof;
   prof.on = opt && opt->profile == 1;
   const bool use_graph = !prof.on && !xfn;
@@ -446,6 +462,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   hc.hot_target = (unsigned long long)(8 * o.bmax + 16384);
   CK(cudaMemcpyAsync(w.ctl, &hc, sizeof hc, cudaMemcpyHostToDevice, st));
   CK(cudaMemsetAsync(w.hist, 0, 16 * 256 * sizeof(unsigned int), st));
+  CK(cudaMemsetAsync(w.pticket, 0, sizeof(unsigned int) * o.bmax, st));
   CK(cudaMemcpyAsync(w.alo, w.l, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(w.ahi, w.u, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemsetAsync(w.sc, 0, sizeof(int32_t), st));
@@ -489,6 +506,18 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   ib.tile_ctr = w.tile_ctr;
   ib.hot0 = w.hot0;
   ib.hot1 = w.hot1;
+  ib.ppart = w.ppart;
+  ib.pticket = w.pticket;
+  unsigned long long* tstamp = nullptr;
+  if (trace) {
+    CK(cudaMalloc(&tstamp, 8 * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(tstamp, 0, 8 * sizeof(unsigned long long), st));
+    ib.tstamp = tstamp;
+  }
+  struct FreeOnExit {
+    unsigned long long* p;
+    ~FreeOnExit() { if (p) cudaFree(p); }
+  } free_tstamp{tstamp};
   Hook hook;
   hook.prof = &prof;
   hook.xfn = xfn;
@@ -497,6 +526,10 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   hook.ctl = w.ctl;
   const int kIterKernels = 6;  // kernels per iteration (launch_iteration)
 
+  // fused-kernel thresholds (IBNB_FUSE_KIDS / IBNB_FUSE_POOL override; 0 = off)
+  long fuse_kids = 1L << 20, fuse_pool = 1L << 16;
+  if (const char* e = std::getenv("IBNB_FUSE_KIDS")) fuse_kids = std::atol(e);
+  if (const char* e = std::getenv("IBNB_FUSE_POOL")) fuse_pool = std::atol(e);
   unsigned long long pcount = 1, free_top = hc.free_top, peak = 1;
   long chunk = 1;
   for (;;) {
@@ -528,15 +561,23 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
     }
     ib.pool = w.pa;
     const long pool_bound = (long)pcount + chunk * per_it;
-    if (use_graph) {
+    // k_list grid class from the records L holds now: two classes, so that
+    // the cached iteration graphs do not multiply
+    const long list_hint = (long)pcount <= 65536 ? 65536 : (1L << 40);
+    // small batches: whole iterations in one persistent cooperative kernel
+    const bool fused = use_graph && o.bmax * o.kids <= fuse_kids && (long)pcount <= fuse_pool;
+    if (fused) {
+      CKL(launch_fused(P, ib, (int)chunk, o.bmax, st));
+      nk += 1 - chunk * kIterKernels;  // one launch for the chunk
+    } else if (use_graph) {
       // one captured iteration per (problem, buffers, grid bound), cached per
       // thread and replayed; re-captured when its grid bound is exceeded
-      GraphKey key{P, ib.pool.lb, ws, graph_bound_for(pool_bound, pcount, per_it, o.pool_cap), o.bmax, o.pool_cap,
-                   o.arch_cap};
+      GraphKey key{P, ib.pool.lb, ws, graph_bound_for(pool_bound, pcount, per_it, o.pool_cap), list_hint, o.bmax,
+                   o.pool_cap, o.arch_cap};
       cudaGraphExec_t ge = tc.find(key, pool_bound);
       if (!ge) {
         CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        int lr = launch_iteration(P, ib, key.bound, o.bmax, st, nullptr);
+        int lr = launch_iteration(P, ib, key.bound, o.bmax, st, nullptr, list_hint);
         cudaGraph_t g = nullptr;
         cudaError_t ce = cudaStreamEndCapture(st, &g);
         if (lr) return fail(lr, "capture of the iteration failed");
@@ -548,7 +589,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
       }
       for (long c = 0; c < chunk; ++c) CK(cudaGraphLaunch(ge, st));
     } else {
-      for (long c = 0; c < chunk; ++c) CKL(launch_iteration(P, ib, pool_bound, o.bmax, st, &hook));
+      for (long c = 0; c < chunk; ++c) CKL(launch_iteration(P, ib, pool_bound, o.bmax, st, &hook, list_hint));
     }
     nk += chunk * kIterKernels;
     // count the survivors of the chunk's last iteration (normally done by the
@@ -580,6 +621,16 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
       pcount = hc.pcount;
       if (trace) fprintf(stderr, "[ibnb] compacted L -> %llu records\n", pcount);
     }
+  }
+  if (trace && tstamp) {
+    unsigned long long tsh[8];
+    CK(cudaMemcpyAsync(tsh, tstamp, sizeof tsh, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const char* ph[6] = {"list", "prep", "child_eval", "cand", "mono", "emit"};
+    double it = (double)std::max(1ull, tsh[6]);
+    fprintf(stderr, "[ibnb] fused phases over %llu iterations (us/iter):", tsh[6]);
+    for (int k = 0; k < 6; ++k) fprintf(stderr, " %s=%.2f", ph[k], tsh[k] / it / 1e3);
+    fprintf(stderr, "\n");
   }
   // exact max width of the remaining regions for the result
   CKL(launch_final_width(w.pa, w.ctl, (long)pcount, st));
@@ -717,6 +768,8 @@ struct BranchWs {
   uint64_t *desc, *desc2;
   uint32_t* tile_ctr;
   Ctl* ctl;
+  double* ppart;
+  unsigned int* pticket;
 };
 static size_t branch_layout(int n, int d, int m, long nb, Arena& A, BranchWs& w) {
   long kids = (long)std::pow((double)m, (double)d);
@@ -735,6 +788,8 @@ static size_t branch_layout(int n, int d, int m, long nb, Arena& A, BranchWs& w)
   w.desc2 = A.take<uint64_t>((size_t)2 * tiles_of(nb * kids) + 4);
   w.tile_ctr = A.take<uint32_t>(4);
   w.ctl = A.take<Ctl>(1);
+  w.ppart = A.take<double>((size_t)nb * prep_slices(n, nb) * 10);
+  w.pticket = A.take<unsigned int>(nb);
   return A.off + 256;
 }
 
@@ -762,10 +817,11 @@ int ib_branch(int fid, int n, int d, int m, int mono, int64_t nb, const double* 
   size_t need = branch_layout(n, d, m, (long)nb, A, w);
   if (!ws || ws_bytes < need) return fail(IB_ENOSPACE, "ib_branch workspace %zu < %zu", ws_bytes, need);
   int ldi = (n + 1) & ~1;
-  Problem P = make_problem(fid, n, d, m, kids, ldi, mono ? 1 : 0, l, u);
+  Problem P = make_problem(fid, n, d, m, kids, ldi, mono ? 1 : 0, l, u, (long)nb);
   k_iota32<<<blocks_for(nb), 256, 0, st>>>(w.iota, nb, 0);
   k_fill_u32<<<blocks_for(nb), 256, 0, st>>>(w.whole, nb, CODE_WHOLE);
   k_branch_ctl<<<1, 1, 0, st>>>(w.ctl, gub, nb, nb * kids);
+  CK(cudaMemsetAsync(w.pticket, 0, sizeof(unsigned int) * nb, st));
   if ((int)ld != ldi) {
     // bring the parents to our even row stride first
     CK(cudaMemcpy2DAsync(w.dlo, sizeof(double) * ldi, plo, sizeof(double) * ld, sizeof(double) * n, nb,
@@ -795,6 +851,8 @@ int ib_branch(int fid, int n, int d, int m, int mono, int64_t nb, const double* 
   ib.desc = w.desc;
   ib.desc2 = w.desc2;
   ib.tile_ctr = w.tile_ctr;
+  ib.ppart = w.ppart;
+  ib.pticket = w.pticket;
   CKL(launch_branch(P, ib, (long)nb, st));
   k_branch_out<<<1, 1, 0, st>>>(w.ctl, gub, out_count);
   CK(cudaGetLastError());

@@ -13,12 +13,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=1)
 ap.add_argument("--solves", type=int, default=2)
 ap.add_argument("--bmax", type=int, default=0)
+ap.add_argument("--d", type=int, default=0)
 a = ap.parse_args()
 cfg = workloads.CONFIGS[a.config]
 l, u = workloads.config_bounds(cfg)
 ld = torch.tensor(l, device="cuda")
 ud = torch.tensor(u, device="cuda")
-o = pb.options(d=min(cfg["n"], 10), m=2, bmax=a.bmax or None)
+o = pb.options(d=a.d or min(cfg["n"], 16), m=2, bmax=a.bmax or None)
 ws = pb.Workspace(pb.solve_workspace_bytes(cfg["fid"], cfg["n"], o))
 for _ in range(a.solves):
     r = pb.ib_solve_dev(cfg["fid"], ld, ud, cfg["eps"], cfg["eps"], o, workspace=ws)

@@ -307,3 +307,29 @@ def test_search_reaches_minimum_n10000(pb, fid):
     _, f, _ = pb.ib_search(fid, cuda(l), cuda(u), 64)
     fs = {3: -0.1 * n, 9: -4.0 * n}.get(fid, STAR[fid])
     assert fs - 1e-9 * (1 + abs(fs)) <= f <= fs + 1e-6 * (1 + abs(fs)), (fid, f, fs)
+
+
+@pytest.mark.parametrize("fid", [7, 6, 5, 10, 1])
+def test_fused_graph_and_eager_paths_identical(pb, fid, monkeypatch):
+    """The persistent fused kernel (small batches), the captured multi-kernel
+    graph and the eager launches run the same device phases in the same
+    order: bit-identical solves."""
+    n = 700
+    l, u = workloads.bounds(fid, n)
+    res = {}
+    for name, env, prof in (("fused", None, 0), ("graph", "0", 0), ("eager", None, 1)):
+        if env is None:
+            monkeypatch.delenv("IBNB_FUSE_KIDS", raising=False)
+        else:
+            monkeypatch.setenv("IBNB_FUSE_KIDS", env)
+        res[name] = pb.ib_solve(fid, l, u, 1e-6, 1e-6, pb.options(d=16, profile=prof), surv_cap=64)
+    r0 = res["fused"]
+    assert r0.status == 0
+    for k in ("graph", "eager"):
+        r = res[k]
+        assert (r.iters, r.evals, r.n_surv, r.status) == (r0.iters, r0.evals, r0.n_surv, r0.status), k
+        assert r.f_lo == r0.f_lo and r.f_hi == r0.f_hi, k
+        np.testing.assert_array_equal(r.lo, r0.lo)
+        np.testing.assert_array_equal(r.hi, r0.hi)
+    fs = {1: 0.0, 5: 0.0, 6: 0.0, 7: 0.0, 10: -3.5}[fid]
+    assert r0.f_lo <= fs <= r0.f_hi and r0.f_hi - r0.f_lo <= 1e-6
