@@ -246,6 +246,7 @@ def main():
     ap.add_argument("--m", type=int, default=2)
     ap.add_argument("--d", type=int, default=0, help="variables split per iteration [min(n, 16)]")
     ap.add_argument("--no-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the configs[1] throughput-regime measurement")
     args = ap.parse_args()
     cfg = workloads.CONFIGS[args.config]
     if args.impl == "reference":
@@ -375,6 +376,44 @@ def main():
             d2h = min(rr.n_surv, cap) * (2 * n + 1) * 8 + 48
         e2e = {"value": ev2 / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 2 * n * 8, "d2h_bytes_per_step": d2h}
 
+    # ---- the throughput regime (BASELINE configs[1], Ackley n = 10: millions
+    # of live regions per iteration, multi-kernel path): value + per-kernel
+    # rooflines, so the batch kernels' fractions are reported next to the
+    # latency-bound headline
+    secondary = None
+    if rank == 0 and world == 1 and args.config != 1 and not args.no_secondary:
+        c1 = workloads.CONFIGS[1]
+        l1, u1 = workloads.config_bounds(c1)
+        ld1, ud1 = torch.tensor(l1, device=dev), torch.tensor(u1, device=dev)
+        o1 = pb.options(d=min(c1["n"], 16), m=args.m)
+        p1 = pb.options(d=min(c1["n"], 16), m=args.m, profile=1)
+        ws1 = pb.Workspace(pb.solve_workspace_bytes(c1["fid"], c1["n"], o1), device=dev)
+        for _ in range(3):
+            pb.ib_solve_dev(c1["fid"], ld1, ud1, c1["eps"], c1["eps"], o1, workspace=ws1)
+        ms1, ev1, pr1 = 0.0, 0, {}
+        for k in range(5 + 3):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r1 = pb.ib_solve_dev(c1["fid"], ld1, ud1, c1["eps"], c1["eps"], o1 if k < 5 else p1, workspace=ws1)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if k < 5:
+                ms1 += e0.elapsed_time(e1)
+                ev1 += r1.evals
+            else:
+                for c, v in r1.prof.items():
+                    q = pr1.setdefault(c, {})
+                    for kk, x in v.items():
+                        q[kk] = q.get(kk, 0) + x
+        pr1 = {c: v for c, v in pr1.items() if v.get("launches")}
+        pms = sum(v["ms"] for v in pr1.values())
+        secondary = {"workload": c1["name"], "value": ev1 / (ms1 / 1e3), "unit": UNIT, "ms_per_step": ms1 / 5,
+                     "kernel_roofline": {c: roofline({c: v}, pms, c1["fid"]) for c, v in pr1.items()}}
+        del ws1
+
     base = None
     if rank == 0 and world == 1 and not args.no_baseline:
         try:
@@ -401,6 +440,7 @@ def main():
             "kernel_roofline": {c: roofline({c: p}, prof_ms, fid) for c, p in prof.items()},
             "profiled_ms_per_step": prof_ms / len(pres),
             "cpu_baseline": base,
+            "throughput_regime": secondary,
             "e2e": e2e,
             "clocks": clocks,
             "gpu_launches": int(sum(r.n_kernels for r in res)),

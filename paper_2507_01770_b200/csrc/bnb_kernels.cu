@@ -661,14 +661,29 @@ __global__ void __launch_bounds__(TPB, GT ? 3 : 4) k_child_eval(Problem P, Ctl* 
 
 // Pass 2a: stable compaction of the candidates (children with lb <= GUB,
 // line 140) into cand[] (decoupled look-back).
+// next tile of a decoupled-look-back scan: a ticket (any launch) or, in a
+// co-resident grid (STATIC), tile = block + k * grid -- every block walks its
+// tiles in increasing order and a tile only waits on lower tiles, so no
+// ticket atomics are needed
+template <bool STATIC>
+__device__ __forceinline__ uint32_t next_tile(uint32_t* tile_ctr, uint32_t k) {
+  if constexpr (STATIC) {
+    return blockIdx.x + k * gridDim.x;
+  } else {
+    __shared__ uint32_t s_tile;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    __syncthreads();
+    return tile;
+  }
+}
+
+template <bool STATIC = false>
 __device__ void cand_dev(const Problem& P, Ctl* __restrict__ ctl, const double* __restrict__ clb,
                          uint32_t* __restrict__ cand, uint64_t* desc, uint32_t* tile_ctr) {
-  __shared__ uint32_t s_tile;
-  for (;;) {
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  __syncthreads();
+  for (uint32_t kt = 0;; ++kt) {
+  const uint32_t tile = next_tile<STATIC>(tile_ctr, kt);
   const long total = (long)ctl->B * P.kids;
   const long ntiles = (total + TILE - 1) / TILE;
   if ((long)tile >= ntiles) break;  // tiles past the end: nobody waits on them
@@ -721,14 +736,10 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
                          const uint8_t* __restrict__ ok, const int32_t* __restrict__ new_slot, Pool out,
                          uint64_t* desc, uint32_t* tile_ctr, bool finish, uint32_t* hot0, uint32_t* hot1) {
   // counters: 0 every survivor (-> L), 1 survivors with key < tau (-> hot index)
-  __shared__ uint32_t s_tile;
   uint32_t* hot = hot0 ? (ctl->hsel ? hot1 : hot0) : nullptr;
   const unsigned long long tau = ctl->tau_key;
-  for (;;) {
-  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  __syncthreads();
+  for (uint32_t kt = 0;; ++kt) {
+  const uint32_t tile = next_tile<MONO>(tile_ctr, kt);  // the fused kernel (MONO) is co-resident
   const long nc = (long)ctl->ncand;
   const long ntiles = (nc + TILE - 1) / TILE;
   if (nc == 0) {
@@ -1983,11 +1994,27 @@ __global__ void __launch_bounds__(TPB, 1) k_fused(Problem P, IterBufs w, int ite
   const long kids = P.kids;
   // optional phase timer (IBNB_TRACE): block 0 accumulates ns per phase
   unsigned long long* ts = (w.tstamp && blockIdx.x == 0 && threadIdx.x == 0) ? w.tstamp : nullptr;
-  unsigned long long t0 = ts ? gtimer() : 0ull;
+  unsigned long long* tw = (w.tstamp && threadIdx.x == 0) ? w.tstamp : nullptr;
+  unsigned long long t0 = tw ? gtimer() : 0ull, tb = t0;
+  // work(ph): this block's own work time in the phase (max over blocks is
+  // accumulated per iteration); mark(ph): phase time seen by block 0
+  const bool tracing = w.tstamp != nullptr;  // uniform over the block
+  auto work = [&](int ph) {
+    if (tracing) {
+      __syncthreads();
+      if (tw) atomicMax(&tw[16 + ph], gtimer() - tb);
+    }
+  };
   auto mark = [&](int ph) {
-    if (ts) {
+    if (tw) {
       unsigned long long t1 = gtimer();
-      ts[ph] += t1 - t0;
+      if (ts) {
+        ts[ph] += t1 - t0;
+        for (int k = 0; k < 6; ++k) {  // fold the per-iteration maxima
+          ts[8 + k] += tw[16 + k];
+          tw[16 + k] = 0;
+        }
+      }
       t0 = t1;
     }
   };
@@ -1997,7 +2024,9 @@ __global__ void __launch_bounds__(TPB, 1) k_fused(Problem P, IterBufs w, int ite
     } else {
       list_dev(w.pool, w.ctl, w.hist, w.sel_slot, w.sel_code, w.desc, w.desc2, w.tile_ctr, w.hot0, w.hot1, kids);
     }
+    work(0);
     grid.sync();
+    if (tw) tb = gtimer();
     mark(0);
     if (w.ctl->done) break;  // uniform: written before the barrier
     const int nitems = (int)w.ctl->B * P.pslices;
@@ -2007,17 +2036,25 @@ __global__ void __launch_bounds__(TPB, 1) k_fused(Problem P, IterBufs w, int ite
                         w.dst_lo, w.dst_hi, w.dst_sc, w.tab, w.tab_stride, w.ppart, w.pticket, b,
                         item - b * P.pslices);
     }
+    work(1);
     grid.sync();
+    if (tw) tb = gtimer();
     mark(1);
     child_eval_dev<F, GT>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.desc, w.desc2, nz, w.tile_ctr, w.hist);
+    work(2);
     grid.sync();
+    if (tw) tb = gtimer();
     mark(2);
-    cand_dev(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
+    cand_dev<true>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
+    work(3);
     grid.sync();
+    if (tw) tb = gtimer();
     mark(3);
     emit_dev<F, true>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok, w.new_slot, w.pool, w.desc2, w.tile_ctr + 1,
                       true, w.hot0, w.hot1);
+    work(5);
     grid.sync();
+    if (tw) tb = gtimer();
     mark(5);
     if (ts) ts[6] += 1;
   }

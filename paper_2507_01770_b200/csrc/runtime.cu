@@ -510,8 +510,8 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   ib.pticket = w.pticket;
   unsigned long long* tstamp = nullptr;
   if (trace) {
-    CK(cudaMalloc(&tstamp, 8 * sizeof(unsigned long long)));
-    CK(cudaMemsetAsync(tstamp, 0, 8 * sizeof(unsigned long long), st));
+    CK(cudaMalloc(&tstamp, 32 * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(tstamp, 0, 32 * sizeof(unsigned long long), st));
     ib.tstamp = tstamp;
   }
   struct FreeOnExit {
@@ -531,6 +531,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   if (const char* e = std::getenv("IBNB_FUSE_KIDS")) fuse_kids = std::atol(e);
   if (const char* e = std::getenv("IBNB_FUSE_POOL")) fuse_pool = std::atol(e);
   unsigned long long pcount = 1, free_top = hc.free_top, peak = 1;
+  long fused_iters = 0, iter_prev = 0;
   long chunk = 1;
   for (;;) {
     const long per_it = o.bmax * o.kids;
@@ -565,9 +566,11 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
     // the cached iteration graphs do not multiply
     const long list_hint = (long)pcount <= 65536 ? 65536 : (1L << 40);
     // small batches: whole iterations in one persistent cooperative kernel
-    const bool fused = use_graph && o.bmax * o.kids <= fuse_kids && (long)pcount <= fuse_pool;
+    const bool fused = !xfn && o.bmax * o.kids <= fuse_kids && (long)pcount <= fuse_pool;
     if (fused) {
+      prof.begin(6, st);
       CKL(launch_fused(P, ib, (int)chunk, o.bmax, st));
+      prof.end(6, st);
       nk += 1 - chunk * kIterKernels;  // one launch for the chunk
     } else if (use_graph) {
       // one captured iteration per (problem, buffers, grid bound), cached per
@@ -601,6 +604,8 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
     pcount = hc.pcount;
     free_top = hc.free_top;
     peak = std::max(peak, pcount);
+    if (fused) fused_iters += (long)hc.iter - iter_prev;
+    iter_prev = (long)hc.iter;
     if (hc.err) return fail(hc.err, "capacity exceeded on the device (L %ld, archive %ld)", o.pool_cap, o.arch_cap);
     if (trace)
       fprintf(stderr, "[ibnb] t=%.3f ms chunk=%ld iter=%llu |L|=%llu live_hot=%llu nhot=%llu B=%llu refills=%llu "
@@ -623,13 +628,15 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
     }
   }
   if (trace && tstamp) {
-    unsigned long long tsh[8];
+    unsigned long long tsh[32];
     CK(cudaMemcpyAsync(tsh, tstamp, sizeof tsh, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const char* ph[6] = {"list", "prep", "child_eval", "cand", "mono", "emit"};
     double it = (double)std::max(1ull, tsh[6]);
     fprintf(stderr, "[ibnb] fused phases over %llu iterations (us/iter):", tsh[6]);
     for (int k = 0; k < 6; ++k) fprintf(stderr, " %s=%.2f", ph[k], tsh[k] / it / 1e3);
+    fprintf(stderr, "\n[ibnb] slowest block's own work per phase (us/iter):");
+    for (int k = 0; k < 6; ++k) fprintf(stderr, " %s=%.2f", ph[k], tsh[8 + k] / it / 1e3);
     fprintf(stderr, "\n");
   }
   // exact max width of the remaining regions for the result
@@ -684,6 +691,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   res->units[3] = (int64_t)c.list_bytes;  // list: algorithmic bytes (hot scans, refills, width passes)
   res->units[4] = (int64_t)c.sum_cand;   // mono: candidates tested
   res->units[5] = (int64_t)c.sum_cand;   // emit: candidates scanned
+  res->units[6] = (int64_t)fused_iters;  // fused: iterations run inside k_fused
   res->radix_records = (int64_t)c.sum_radix;
   res->f_lo = live ? okey_inv_h(c.min_lb_key) : INFINITY;
   res->f_hi = okey_inv_h(c.gub_key);
