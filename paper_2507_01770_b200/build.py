@@ -36,7 +36,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    cflags = [f for f in FLAGS if f != "-shared"]
+    cflags = [f for f in FLAGS if f != "-shared"] + os.environ.get("IBNB_EXTRA_FLAGS", "").split()
     objs, procs = [], []
     for s in SOURCES:
         o = os.path.join(objdir, s.replace(".cu", ".o"))

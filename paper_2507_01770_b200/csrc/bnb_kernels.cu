@@ -32,6 +32,27 @@ namespace cg = cooperative_groups;
 
 namespace ib {
 
+// ------------------------------------------------------------ probes
+// -DIBNB_PROBE builds (diagnosis only): block 0 / thread 0 accumulates the
+// clock64 cycles between probe points of a device function into g_probe
+#ifdef IBNB_PROBE
+__device__ unsigned long long g_probe[64];
+#define PROBE_BEGIN unsigned long long _pt = clock64(), _pd[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define PROBE(k)                                   \
+  {                                                \
+    unsigned long long _t = clock64();             \
+    _pd[k] += _t - _pt;                            \
+    _pt = _t;                                      \
+  }
+#define PROBE_END(base)                                                    \
+  if (blockIdx.x == 0 && threadIdx.x == 0)                                 \
+    for (int _k = 0; _k < 8; ++_k) g_probe[(base) + _k] += _pd[_k];
+#else
+#define PROBE_BEGIN
+#define PROBE(k)
+#define PROBE_END(base)
+#endif
+
 // ------------------------------------------------------------ partition
 // Eq. (10)-(11) with m pieces, round-to-nearest, no FMA (bit-identical to
 // the oracle's part_point, reading R2).
@@ -247,9 +268,66 @@ __device__ __forceinline__ void prep_item(const Problem& P, const Ctl* __restric
     block_reduce_acc<F, BS>(accm);
   }
   wmax = block_max<BS>(wmax);
+  // tables of the m pieces of the d split variables, by the block that owns
+  // the variable (slices run in parallel); three threads per entry: bounds +
+  // box terms, midpoint terms, derivative ingredients + separable flag
+  for (int t = threadIdx.x; t < 3 * d * m; t += BS) {
+    const int ent = t % (d * m), part = t / (d * m);
+    int j = ent / m, p = ent % m;
+    int i = (c + j) % n;
+    if (i < i0 || i >= i1) continue;
+    double a, bb;
+    mat(i, a, bb);
+    double pa = part_point(a, bb, m, p), pb = part_point(a, bb, m, p + 1);
+    double xm = midpt(pa, pb);
+    double* e = T + HDR + (size_t)ent * ENT;
+    if constexpr (F::CHAIN) {
+      if (part == 0) {
+        LevyVals v = ObjLevy::vals(Iv{pa, pb});
+        e[E_LO] = pa;
+        e[E_HI] = pb;
+        put(e + 2, v.u);
+        put(e + 4, v.v);
+        put(e + 6, v.s0);
+        put(e + 8, v.du);
+        put(e + 10, v.sg);
+      } else if (part == 1) {
+        LevyVals vm = ObjLevy::vals(Iv{xm, xm});
+        put(e + 12, vm.u);
+        put(e + 14, vm.v);
+        put(e + 16, vm.s0);
+      }
+    } else {
+      if (part == 0) {
+        Iv tt[2];
+        F::terms(Iv{pa, pb}, i, n, tt);
+        e[E_LO] = pa;
+        e[E_HI] = pb;
+        for (int k = 0; k < F::K; ++k) put(e + E_T + 2 * k, tt[k]);
+      } else if (part == 1) {
+        Iv tm[2];
+        F::terms(Iv{xm, xm}, i, n, tm);
+        for (int k = 0; k < F::K; ++k) put(e + E_T + 2 * F::K + 2 * k, tm[k]);
+      } else {
+        Iv g[2];
+        if constexpr (F::KG > 0) {
+          F::ding(Iv{pa, pb}, i, n, g);
+          for (int k = 0; k < F::KG; ++k) put(e + E_T + 4 * F::K + 2 * k, g[k]);
+        }
+        double flag = 0.0;
+        if constexpr (F::SEP) {
+          Iv D = F::dsep(Iv{pa, pb}, i, n);
+          if ((D.lo > 0.0 && pa != P.l[i]) || (D.hi < 0.0 && pb != P.u[i])) flag = 1.0;
+        }
+        e[E_T + 4 * F::K + 2 * F::KG] = flag;
+      }
+    }
+  }
   if (S > 1) {
     // publish this slice's partial; the last slice block of parent b goes on
     __shared__ int s_last;
+    __threadfence();  // this block's rows and table entries before the ticket
+    __syncthreads();
     if (threadIdx.x == 0) {
       double* pp = ppart + ((size_t)b * S + s) * 10;
       for (int k = 0; k < 2; ++k) {
@@ -341,47 +419,6 @@ __device__ __forceinline__ void prep_item(const Problem& P, const Ctl* __restric
       T[H_LEVY_NT] = (double)nt;
       T[H_LEVY_LR] = (double)q.L;
       T[H_LEVY_LR + 1] = (double)q.R;
-    }
-  }
-  // tables of the m pieces of the d split variables
-  for (int t = threadIdx.x; t < d * m; t += BS) {
-    int j = t / m, p = t % m;
-    int i = (c + j) % n;
-    double a, bb;
-    mat(i, a, bb);
-    double pa = part_point(a, bb, m, p), pb = part_point(a, bb, m, p + 1);
-    double xm = midpt(pa, pb);
-    double* e = T + HDR + (size_t)t * ENT;
-    e[E_LO] = pa;
-    e[E_HI] = pb;
-    if constexpr (F::CHAIN) {
-      LevyVals v = ObjLevy::vals(Iv{pa, pb}), vm = ObjLevy::vals(Iv{xm, xm});
-      put(e + 2, v.u);
-      put(e + 4, v.v);
-      put(e + 6, v.s0);
-      put(e + 8, v.du);
-      put(e + 10, v.sg);
-      put(e + 12, vm.u);
-      put(e + 14, vm.v);
-      put(e + 16, vm.s0);
-    } else {
-      Iv tt[2], tm[2], g[2];
-      F::terms(Iv{pa, pb}, i, n, tt);
-      F::terms(Iv{xm, xm}, i, n, tm);
-      for (int k = 0; k < F::K; ++k) {
-        put(e + E_T + 2 * k, tt[k]);
-        put(e + E_T + 2 * F::K + 2 * k, tm[k]);
-      }
-      if constexpr (F::KG > 0) {
-        F::ding(Iv{pa, pb}, i, n, g);
-        for (int k = 0; k < F::KG; ++k) put(e + E_T + 4 * F::K + 2 * k, g[k]);
-      }
-      double flag = 0.0;
-      if constexpr (F::SEP) {
-        Iv D = F::dsep(Iv{pa, pb}, i, n);
-        if ((D.lo > 0.0 && pa != P.l[i]) || (D.hi < 0.0 && pb != P.u[i])) flag = 1.0;
-      }
-      e[E_T + 4 * F::K + 2 * F::KG] = flag;
     }
   }
 }
@@ -569,7 +606,7 @@ __device__ __forceinline__ void child_eval_dev(const Problem& P, Ctl* __restrict
   if (ctl->done) return;
   if (zero_a) {  // descriptors and tickets of the following k_cand / k_emit,
                  // histograms and accumulators of the next k_list
-    for (long i = (long)blockIdx.x * TPB + threadIdx.x; i < 2 * nzero; i += (long)gridDim.x * TPB) {
+    for (long i = (long)blockIdx.x * TPB + threadIdx.x; i < 3 * nzero; i += (long)gridDim.x * TPB) {
       if (i < nzero) zero_a[i] = 0;
       zero_b[i] = 0;
     }
@@ -607,7 +644,29 @@ __device__ __forceinline__ void child_eval_dev(const Problem& P, Ctl* __restrict
         Am[k] = get(T + H_RESTM + 2 * k);
       }
       const uint32_t code0 = hcode * (uint32_t)G;
-      for (int j = h; j < d; ++j) {
+      int j = h;
+      // batches of 4 pieces: the loads of a batch are issued together (one
+      // L2 round trip instead of four), the combination order is unchanged
+      for (; j + 4 <= d; j += 4) {
+        Iv t[4][2], tm[4][2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double* e = T + HDR + (size_t)((j + u) * m + piece(code0, j + u, P)) * ENT + E_T;
+#pragma unroll
+          for (int k = 0; k < F::K; ++k) {
+            t[u][k] = get(e + 2 * k);
+            tm[u][k] = get(e + 2 * F::K + 2 * k);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int k = 0; k < F::K; ++k) {
+            A[k] = acc_comb<F>(k, A[k], t[u][k]);
+            Am[k] = acc_comb<F>(k, Am[k], tm[u][k]);
+          }
+      }
+      for (; j < d; ++j) {
         const double* e = T + HDR + (size_t)(j * m + piece(code0, j, P)) * ENT + E_T;
 #pragma unroll
         for (int k = 0; k < F::K; ++k) {
@@ -736,6 +795,7 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
                          const uint8_t* __restrict__ ok, const int32_t* __restrict__ new_slot, Pool out,
                          uint64_t* desc, uint32_t* tile_ctr, bool finish, uint32_t* hot0, uint32_t* hot1) {
   // counters: 0 every survivor (-> L), 1 survivors with key < tau (-> hot index)
+  PROBE_BEGIN
   uint32_t* hot = hot0 ? (ctl->hsel ? hot1 : hot0) : nullptr;
   const unsigned long long tau = ctl->tau_key;
   for (uint32_t kt = 0;; ++kt) {
@@ -755,14 +815,47 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
   }
   if ((long)tile >= ntiles) break;
   const long k0 = (long)tile * TILE + (long)threadIdx.x * IPT;
+  const long kbeg = (long)tile * TILE;
+  // MONO: width and (separable f) first-order flags of the tile's candidates,
+  // one warp per candidate with a lane per split variable
+  __shared__ uint8_t s_ok[MONO ? TILE : 1];
+  __shared__ double s_w[MONO ? TILE : 1];
+  if constexpr (MONO) {
+    const int cnt = (int)min((long)TILE, nc - kbeg);
+    const int lane = threadIdx.x & 31;
+    for (int q = threadIdx.x >> 5; q < cnt; q += TPB / 32) {
+      ChildIdx ci = child_of(cand[kbeg + q], P);
+      const double* T = tab + (size_t)ci.b * tab_stride;
+      double wl = 0.0;
+      bool bad = false;
+      if (lane < P.d) {
+        const double* e = T + HDR + (size_t)(lane * P.m + piece(ci.code, lane, P)) * ENT;
+        wl = __dsub_rn(e[E_HI], e[E_LO]);
+        if constexpr (F::SEP) bad = e[E_T + 4 * F::K + 2 * F::KG] != 0.0;
+      }
+      wl = warp_max(wl);
+      const unsigned anybad = __ballot_sync(0xffffffffu, bad);
+      if (lane == 0) {
+        s_w[q] = fmax(T[H_WREST], wl);
+        s_ok[q] = anybad == 0u;
+      }
+    }
+    PROBE(1)
+    __syncthreads();
+    PROBE(2)
+  }
   uint32_t f = 0, fh = 0;
 #pragma unroll
   for (int q = 0; q < IPT; ++q) {
     bool okq = false;
     if (k0 + q < nc) {
       if constexpr (MONO) {
-        ChildIdx ci = child_of(cand[k0 + q], P);
-        okq = !P.mono || child_mono_ok<F>(P, tab + (size_t)ci.b * tab_stride, ci.code);
+        if constexpr (F::SEP) {
+          okq = !P.mono || s_ok[k0 + q - kbeg] != 0;
+        } else {
+          ChildIdx ci = child_of(cand[k0 + q], P);
+          okq = !P.mono || child_mono_ok<F>(P, tab + (size_t)ci.b * tab_stride, ci.code);
+        }
       } else {
         okq = ok[k0 + q] != 0;
       }
@@ -772,10 +865,13 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
       if (hot && okey(clb[cand[k0 + q]]) < tau) fh |= 1u << q;
     }
   }
+  PROBE(3)
   uint32_t c2[2] = {(uint32_t)__popc(f), (uint32_t)__popc(fh)}, ex[2], tot[2];
   block_exclusive_scan<2, TPB>(c2, ex, tot);
+  PROBE(4)
   uint64_t pfx[2];
   dl_lookback<2>(desc, tile, tot, pfx);
+  PROBE(5)
   const uint64_t base = ctl->pcount, cap = ctl->pool_cap, hbase = ctl->nhot;
   uint64_t pos = base + pfx[0] + ex[0], hpos = hbase + pfx[1] + ex[1];
 #pragma unroll
@@ -785,7 +881,10 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
         uint32_t g = cand[k0 + q];
         ChildIdx ci = child_of(g, P);
         out.lb[pos] = clb[g];
-        out.w[pos] = child_width(P, tab + (size_t)ci.b * tab_stride, ci.code);
+        if constexpr (MONO)
+          out.w[pos] = s_w[k0 + q - kbeg];
+        else
+          out.w[pos] = child_width(P, tab + (size_t)ci.b * tab_stride, ci.code);
         out.slot[pos] = new_slot[ci.b];
         out.code[pos] = ci.code;
         if (fh & (1u << q)) hot[hpos++] = (uint32_t)pos;
@@ -807,6 +906,122 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
       set_list_fast(ctl, pfx[1] + tot[1]);
     }
   }
+  PROBE(6)
+  }
+  PROBE(7)
+  PROBE_END(0)
+}
+
+// k_fused: candidates (lb <= GUB, line 140), first-order test (lines
+// 142-144) and insertion into L (line 146) in one pass over the children of
+// the batch, static tiles; the same survivors in the same order as
+// k_cand -> k_mono -> k_emit.  Scan counters: 0 candidates, 1 survivors (-> L),
+// 2 survivors with key < tau (-> hot index).  The descriptors (desc, 3 per
+// tile) were zeroed by child_eval_dev.
+template <class F>
+__device__ void cand_emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* __restrict__ tab, int tab_stride,
+                              const double* __restrict__ clb, const int32_t* __restrict__ new_slot, Pool out,
+                              uint64_t* desc, uint32_t* hot0, uint32_t* hot1) {
+  __shared__ uint32_t s_cidx[TILE];
+  __shared__ uint8_t s_ok[TILE];
+  __shared__ double s_w[TILE];
+  uint32_t* hot = ctl->hsel ? hot1 : hot0;
+  const unsigned long long tau = ctl->tau_key;
+  const double gub = okey_inv(ctl->gub_key);
+  const long total = (long)ctl->B * P.kids;
+  const long ntiles = (total + TILE - 1) / TILE;
+  const int lane = threadIdx.x & 31;
+  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long g0 = tile * TILE + (long)threadIdx.x * IPT;
+    uint32_t fc = 0;
+    double lbv[IPT];
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      lbv[q] = g0 + q < total ? clb[g0 + q] : CUDART_INF;
+      if (g0 + q < total && lbv[q] <= gub) fc |= 1u << q;
+    }
+    uint32_t c1[1] = {(uint32_t)__popc(fc)}, ex1[1], tot1[1];
+    block_exclusive_scan<1, TPB>(c1, ex1, tot1);
+    {
+      uint32_t pl = ex1[0];
+#pragma unroll
+      for (int q = 0; q < IPT; ++q)
+        if (fc & (1u << q)) s_cidx[pl++] = (uint32_t)(g0 + q);
+    }
+    const int ncl = (int)tot1[0];
+    __syncthreads();
+    // widths (+ separable first-order flags): a warp per candidate, a lane
+    // per split variable
+    for (int k = threadIdx.x >> 5; k < ncl; k += TPB / 32) {
+      ChildIdx ci = child_of(s_cidx[k], P);
+      const double* T = tab + (size_t)ci.b * tab_stride;
+      double wl = 0.0;
+      bool bad = false;
+      if (lane < P.d) {
+        const double* e = T + HDR + (size_t)(lane * P.m + piece(ci.code, lane, P)) * ENT;
+        wl = __dsub_rn(e[E_HI], e[E_LO]);
+        if constexpr (F::SEP) bad = e[E_T + 4 * F::K + 2 * F::KG] != 0.0;
+      }
+      wl = warp_max(wl);
+      const unsigned anybad = __ballot_sync(0xffffffffu, bad);
+      if (lane == 0) {
+        s_w[k] = fmax(T[H_WREST], wl);
+        s_ok[k] = anybad == 0u;
+      }
+    }
+    __syncthreads();
+    uint32_t f = 0, fh = 0;
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      const int k = threadIdx.x * IPT + q;
+      if (k < ncl) {
+        bool okq;
+        if constexpr (F::SEP) {
+          okq = !P.mono || s_ok[k] != 0;
+        } else {
+          ChildIdx ci = child_of(s_cidx[k], P);
+          okq = !P.mono || child_mono_ok<F>(P, tab + (size_t)ci.b * tab_stride, ci.code);
+        }
+        if (okq) {
+          f |= 1u << q;
+          if (okey(clb[s_cidx[k]]) < tau) fh |= 1u << q;
+        }
+      }
+    }
+    uint32_t c3[3] = {threadIdx.x == 0 ? (uint32_t)ncl : 0u, (uint32_t)__popc(f), (uint32_t)__popc(fh)}, ex[3], tot[3];
+    block_exclusive_scan<3, TPB>(c3, ex, tot);
+    uint64_t pfx[3];
+    dl_lookback<3>(desc, (uint32_t)tile, tot, pfx);
+    const uint64_t base = ctl->pcount, cap = ctl->pool_cap, hbase = ctl->nhot;
+    uint64_t pos = base + pfx[1] + ex[1], hpos = hbase + pfx[2] + ex[2];
+#pragma unroll
+    for (int q = 0; q < IPT; ++q) {
+      if (f & (1u << q)) {
+        if (pos < cap) {
+          const int k = threadIdx.x * IPT + q;
+          const uint32_t g = s_cidx[k];
+          ChildIdx ci = child_of(g, P);
+          out.lb[pos] = clb[g];
+          out.w[pos] = s_w[k];
+          out.slot[pos] = new_slot[ci.b];
+          out.code[pos] = ci.code;
+          if (fh & (1u << q)) hot[hpos++] = (uint32_t)pos;
+        }
+        ++pos;
+      }
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+      ctl->ncand = pfx[0] + tot[0];
+      ctl->nsurv = pfx[1] + tot[1];
+      ctl->nsurv_hot = pfx[2] + tot[2];
+      if (base + pfx[1] + tot[1] > cap) {
+        ctl->err = -2;  // IB_ENOSPACE
+        ctl->done = 4;
+      }
+      ctl->pending_end = 1;
+      set_list_fast(ctl, pfx[2] + tot[2]);
+    }
+    __syncthreads();  // shared arrays are reused by the next tile
   }
 }
 
@@ -954,7 +1169,7 @@ __device__ void stats_accum_dev(const Pool& p, Ctl* ctl, unsigned int* hist) {
 }
 
 // max width of the live records (only needed once the enclosure test passes)
-__device__ void maxw_accum_dev(const Pool& p, Ctl* ctl) {
+__device__ __noinline__ void maxw_accum_dev(const Pool& p, Ctl* ctl) {
   const double gub = okey_inv(ctl->gub_key);
   const long cnt = (long)ctl->pcount;
   double mw = 0.0;
@@ -977,7 +1192,7 @@ __device__ void maxw_accum_dev(const Pool& p, Ctl* ctl) {
 
 // max width of the live records listed in a hot index (all live records
 // are there when tau = ~0)
-__device__ void maxw_hot_dev(const Pool& p, const uint32_t* __restrict__ hot, long nh, Ctl* ctl) {
+__device__ __noinline__ void maxw_hot_dev(const Pool& p, const uint32_t* __restrict__ hot, long nh, Ctl* ctl) {
   const double gub = okey_inv(ctl->gub_key);
   double mw = 0.0;
   for (long k = (long)blockIdx.x * TPB + threadIdx.x; k < nh; k += (long)gridDim.x * TPB) {
@@ -1210,7 +1425,7 @@ struct Pick {
   int dig;
   unsigned long long before, cnt, total;
 };
-__device__ Pick block_pick(const unsigned int* hist, unsigned long long need) {
+__device__ __noinline__ Pick block_pick(const unsigned int* hist, unsigned long long need) {
   __shared__ unsigned long long s_inc[256];
   __shared__ Pick s_p;
   const int t = threadIdx.x;
@@ -1243,7 +1458,7 @@ __device__ Pick block_pick(const unsigned int* hist, unsigned long long need) {
 // accumulate (live count, min key) of a set of records of L and the
 // histogram of digit (64 - known - 8 .. 64 - known) of the live keys whose
 // top `known` bits equal prefix.  idx == nullptr: records [0, n) of L.
-__device__ void scan_keys_dev(const Pool& p, const uint32_t* __restrict__ idx, long n, double gub, int known,
+__device__ __noinline__ void scan_keys_dev(const Pool& p, const uint32_t* __restrict__ idx, long n, double gub, int known,
                               unsigned long long prefix, unsigned int* hist, unsigned long long* acc_live,
                               unsigned long long* acc_min) {
   __shared__ unsigned int s_h[256];
@@ -1288,7 +1503,7 @@ __device__ void scan_keys_dev(const Pool& p, const uint32_t* __restrict__ idx, l
 }
 
 // refill: positions of the live records of L with key < tau, in order
-__device__ void hot_collect_dev(const Pool& p, long n, double gub, unsigned long long tau, uint32_t* out,
+__device__ __noinline__ void hot_collect_dev(const Pool& p, long n, double gub, unsigned long long tau, uint32_t* out,
                                 unsigned long long* out_count, uint64_t* desc, uint32_t* tile_ctr) {
   __shared__ uint32_t s_tile;
   for (;;) {
@@ -1323,7 +1538,7 @@ __device__ void hot_collect_dev(const Pool& p, long n, double gub, unsigned long
 // (key, position) go to the batch and are removed from L (lb = +inf); the
 // other live hot entries are kept, in order, in `hout`.  counters: 0 lt
 // (selected), 1 eq (tie class), 2 gt (kept).  known == 0 selects all.
-__device__ void hot_select_dev(const Pool& p, const uint32_t* __restrict__ hin, long n, uint32_t* hout, double gub,
+__device__ __noinline__ void hot_select_dev(const Pool& p, const uint32_t* __restrict__ hin, long n, uint32_t* hout, double gub,
                                int known, unsigned long long prefix, unsigned long long r_need, int32_t* sel_slot,
                                uint32_t* sel_code, unsigned long long* keep_count, uint64_t* desc,
                                uint32_t* tile_ctr) {
@@ -1512,7 +1727,7 @@ __device__ void list_small_dev(const Pool& p, Ctl* ctl, uint32_t* hot0, uint32_t
   }
 }
 
-__device__ void list_dev(const Pool& p, Ctl* ctl, unsigned int* hists, int32_t* sel_slot, uint32_t* sel_code,
+__device__ __noinline__ void list_dev(const Pool& p, Ctl* ctl, unsigned int* hists, int32_t* sel_slot, uint32_t* sel_code,
                          uint64_t* desc, uint64_t* desc2, uint32_t* tile_ctr, uint32_t* hot0, uint32_t* hot1,
                          long kids) {
   cg::grid_group grid = cg::this_grid();
@@ -2018,16 +2233,19 @@ __global__ void __launch_bounds__(TPB, 1) k_fused(Problem P, IterBufs w, int ite
       t0 = t1;
     }
   };
+  bool need_list = true;  // the first iteration of a launch starts with its list phase
   for (int it = 0; it < iters; ++it) {
-    if (w.ctl->list_fast) {  // uniform: set before the last barrier
-      if (blockIdx.x == 0) list_small_dev(w.pool, w.ctl, w.hot0, w.hot1, w.sel_slot, w.sel_code, kids);
-    } else {
-      list_dev(w.pool, w.ctl, w.hist, w.sel_slot, w.sel_code, w.desc, w.desc2, w.tile_ctr, w.hot0, w.hot1, kids);
+    if (need_list) {
+      if (w.ctl->list_fast) {  // uniform: set before the last barrier
+        if (blockIdx.x == 0) list_small_dev(w.pool, w.ctl, w.hot0, w.hot1, w.sel_slot, w.sel_code, kids);
+      } else {
+        list_dev(w.pool, w.ctl, w.hist, w.sel_slot, w.sel_code, w.desc, w.desc2, w.tile_ctr, w.hot0, w.hot1, kids);
+      }
+      work(0);
+      grid.sync();
+      if (tw) tb = gtimer();
+      mark(0);
     }
-    work(0);
-    grid.sync();
-    if (tw) tb = gtimer();
-    mark(0);
     if (w.ctl->done) break;  // uniform: written before the barrier
     const int nitems = (int)w.ctl->B * P.pslices;
     for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
@@ -2045,16 +2263,33 @@ __global__ void __launch_bounds__(TPB, 1) k_fused(Problem P, IterBufs w, int ite
     grid.sync();
     if (tw) tb = gtimer();
     mark(2);
-    cand_dev<true>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
+    cand_emit_dev<F>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.new_slot, w.pool, w.desc2, w.hot0, w.hot1);
     work(3);
-    grid.sync();
-    if (tw) tb = gtimer();
-    mark(3);
-    emit_dev<F, true>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok, w.new_slot, w.pool, w.desc2, w.tile_ctr + 1,
-                      true, w.hot0, w.hot1);
-    work(5);
-    grid.sync();
-    if (tw) tb = gtimer();
+    // the last block to finish the insertion runs the next iteration's list
+    // phase when it fits one block (no barrier between insertion and list)
+    need_list = true;
+    if (it + 1 < iters) {
+      __shared__ int s_lastblk;
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) s_lastblk = atomicAdd(&w.ctl->fused_ticket, 1u) == gridDim.x - 1;
+      __syncthreads();
+      if (s_lastblk) {
+        __threadfence();
+        const bool fast = w.ctl->list_fast != 0 && !w.ctl->done;
+        if (fast) list_small_dev(w.pool, w.ctl, w.hot0, w.hot1, w.sel_slot, w.sel_code, kids);
+        if (threadIdx.x == 0) {
+          w.ctl->fused_ticket = 0u;
+          w.ctl->list_pre = fast ? 1 : 0;
+        }
+      }
+      work(5);
+      grid.sync();
+      if (tw) tb = gtimer();
+      need_list = w.ctl->list_pre == 0;
+    } else {
+      grid.sync();
+    }
     mark(5);
     if (ts) ts[6] += 1;
   }
@@ -2279,6 +2514,9 @@ int launch_eval_grad(int fid, int n, long nreq, const double* lo, const double* 
   LAUNCH_OK;
 }
 
+#ifdef IBNB_PROBE
+int probe_read(unsigned long long* out) { return (int)cudaMemcpyFromSymbol(out, g_probe, sizeof(g_probe)); }
+#endif
 }  // namespace ib
 
 namespace ib {

@@ -100,12 +100,15 @@ __device__ __forceinline__ Iv isqrt(Iv a) {
   return Iv{__dsqrt_rd(fmax(a.lo, 0.0)), __dsqrt_ru(fmax(a.hi, 0.0))};
 }
 
-__device__ __forceinline__ Iv iexp(Iv a) {
+// the transcendental enclosures are out-of-line: one copy of their code per
+// kernel keeps the instruction footprint of the large kernels (k_fused,
+// k_search) small enough to stay in the instruction caches
+static __device__ __noinline__ Iv iexp(Iv a) {
   return Iv{fmax(widen_dn<ULPS_EXP>(exp(a.lo)), 0.0), widen_up<ULPS_EXP>(exp(a.hi))};
 }
 
 // cos(pi u) over U: maxima at even integers, minima at odd integers.
-__device__ __forceinline__ Iv icospi(Iv u) {
+static __device__ __noinline__ Iv icospi(Iv u) {
   if (!(u.lo <= u.hi) || !(__dsub_ru(u.hi, u.lo) < 2.0) || fabs(u.lo) > 0x1p50 || fabs(u.hi) > 0x1p50)
     return Iv{-1.0, 1.0};
   double c0 = cospi(u.lo), c1 = cospi(u.hi);
@@ -121,7 +124,7 @@ __device__ __forceinline__ Iv icospi(Iv u) {
 }
 
 // sin(pi u) over U: maxima at u = k + 1/2 with k even, minima with k odd.
-__device__ __forceinline__ Iv isinpi(Iv u) {
+static __device__ __noinline__ Iv isinpi(Iv u) {
   if (!(u.lo <= u.hi) || !(__dsub_ru(u.hi, u.lo) < 2.0) || fabs(u.lo) > 0x1p50 || fabs(u.hi) > 0x1p50)
     return Iv{-1.0, 1.0};
   double s0 = sinpi(u.lo), s1 = sinpi(u.hi);

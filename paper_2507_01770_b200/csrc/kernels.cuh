@@ -75,6 +75,8 @@ struct Ctl {
   unsigned long long acc_live3, acc_min_key3;           // rebuilt hot index
   unsigned long long list_bytes;                        // algorithmic bytes of k_list
   unsigned int blocks_done;      // last-block election counter
+  unsigned int fused_ticket;     // k_fused: last block of the insertion pass
+  int list_pre;                  // k_fused: the next list phase already ran (last block)
   unsigned int pending_end;      // the survivors of the last iteration are not yet counted in pcount
   unsigned long long sum_pool;   // records scanned by the statistics pass
   unsigned long long sum_radix;  // records scanned by radix passes 2..8

@@ -198,7 +198,7 @@ static int resolve_opts(int fid, int n, const ib_options* o, int64_t pool_cap_ar
 // to fill the SMs, then slices of >= 256 variables
 static int prep_slices(int n, long bmax) {
   if (n < 512 || bmax >= 296) return 1;
-  long s = std::min((long)(n + 255) / 256, std::max(1L, 296 / bmax));
+  long s = std::min((long)(n + 255) / 256, std::max(1L, 1184 / bmax));
   return (int)std::max(1L, s);
 }
 
@@ -233,6 +233,35 @@ struct SolveWs {
 };
 
 static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
+  // Order matters for the latency-bound small-batch regime: the control
+  // block and every small per-iteration array come first and share a few
+  // 2 MB pages (TLB reach), then the per-iteration child arrays, then the
+  // hot index, the list L and the archive (the large, sparsely touched
+  // regions) and the search workspace.
+  const long kids_tot = o.bmax * o.kids;
+  w.ctl = A.take<Ctl>(1);
+  w.cnt = A.take<uint64_t>(4);
+  w.tile_ctr = A.take<uint32_t>(4);
+  w.hist = A.take<unsigned int>(16 * 256);
+  w.sel_slot = A.take<int32_t>(o.bmax);
+  w.sel_code = A.take<uint32_t>(o.bmax);
+  w.new_slot = A.take<int32_t>(o.bmax);
+  w.ppart = A.take<double>((size_t)o.bmax * prep_slices(n, o.bmax) * 10);
+  w.pticket = A.take<unsigned int>(o.bmax);
+  w.root_out = A.take<double>(2);
+  w.f_search = A.take<double>(1);
+  w.search_rounds = A.take<int32_t>(1);
+  w.l = A.take<double>(n);
+  w.u = A.take<double>(n);
+  w.tab = A.take<double>((size_t)o.bmax * o.tab_stride);
+  long tiles = tiles_of(std::max({o.pool_cap, kids_tot, o.arch_cap})) + 2;
+  w.desc = A.take<uint64_t>((size_t)tiles * 3);
+  w.desc2 = A.take<uint64_t>((size_t)tiles * 3);
+  w.clb = A.take<double>((size_t)kids_tot);
+  w.cand = A.take<uint32_t>((size_t)kids_tot);
+  w.ok = A.take<uint8_t>((size_t)kids_tot);
+  w.hot0 = A.take<uint32_t>(o.pool_cap);
+  w.hot1 = A.take<uint32_t>(o.pool_cap);
   auto pool = [&](Pool& p) {
     p.lb = A.take<double>(o.pool_cap);
     p.w = A.take<double>(o.pool_cap);
@@ -241,35 +270,11 @@ static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
   };
   pool(w.pa);
   pool(w.pb);
-  const long kids_tot = o.bmax * o.kids;
-  w.sel_slot = A.take<int32_t>(o.bmax);
-  w.sel_code = A.take<uint32_t>(o.bmax);
-  w.new_slot = A.take<int32_t>(o.bmax);
-  w.alo = A.take<double>((size_t)o.arch_cap * o.ld);
-  w.ahi = A.take<double>((size_t)o.arch_cap * o.ld);
   w.sc = A.take<int32_t>(o.arch_cap);
   w.free_list = A.take<int32_t>(o.arch_cap);
   w.mark = A.take<uint8_t>(o.arch_cap);
-  w.tab = A.take<double>((size_t)o.bmax * o.tab_stride);
-  w.clb = A.take<double>((size_t)kids_tot);
-  w.cand = A.take<uint32_t>((size_t)kids_tot);
-  w.ok = A.take<uint8_t>((size_t)kids_tot);
-  long tiles = tiles_of(std::max({o.pool_cap, kids_tot, o.arch_cap})) + 2;
-  w.desc = A.take<uint64_t>((size_t)tiles * 3);
-  w.desc2 = A.take<uint64_t>((size_t)tiles * 3);
-  w.hot0 = A.take<uint32_t>(o.pool_cap);
-  w.hot1 = A.take<uint32_t>(o.pool_cap);
-  w.cnt = A.take<uint64_t>(4);
-  w.tile_ctr = A.take<uint32_t>(4);
-  w.ctl = A.take<Ctl>(1);
-  w.hist = A.take<unsigned int>(16 * 256);
-  w.l = A.take<double>(n);
-  w.u = A.take<double>(n);
-  w.root_out = A.take<double>(2);
-  w.ppart = A.take<double>((size_t)o.bmax * prep_slices(n, o.bmax) * 10);
-  w.pticket = A.take<unsigned int>(o.bmax);
-  w.f_search = A.take<double>(1);
-  w.search_rounds = A.take<int32_t>(1);
+  w.alo = A.take<double>((size_t)o.arch_cap * o.ld);
+  w.ahi = A.take<double>((size_t)o.arch_cap * o.ld);
   w.search_bytes = search_ws_bytes(n, search_grid_max());
   w.search_ws = A.take<char>(w.search_bytes);
   return A.off + 256;
@@ -635,6 +640,17 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
     double it = (double)std::max(1ull, tsh[6]);
     fprintf(stderr, "[ibnb] fused phases over %llu iterations (us/iter):", tsh[6]);
     for (int k = 0; k < 6; ++k) fprintf(stderr, " %s=%.2f", ph[k], tsh[k] / it / 1e3);
+#ifdef IBNB_PROBE
+    {
+      extern int probe_read(unsigned long long*);
+      unsigned long long pr[64];
+      if (probe_read(pr) == 0) {
+        fprintf(stderr, "\n[ibnb] probes (cycles/iter):");
+        for (int k = 0; k < 64; ++k)
+          if (pr[k]) fprintf(stderr, " p%d=%.0f", k, pr[k] / it);
+      }
+    }
+#endif
     fprintf(stderr, "\n[ibnb] slowest block's own work per phase (us/iter):");
     for (int k = 0; k < 6; ++k) fprintf(stderr, " %s=%.2f", ph[k], tsh[8 + k] / it / 1e3);
     fprintf(stderr, "\n");
