@@ -14,10 +14,12 @@ case).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): the domain is partitioned into N slabs along x_1, one per
-rank, and the incumbent GUB is all-reduced (MIN, NCCL) every iteration; the
-time is the max over ranks of the device time.  Prints ONE JSON line on
-rank 0.
+N > 1 (torchrun), --mode replicas (default): every GPU runs its own solve of
+the workload (the n = 10,000 deep dive keeps one region live per iteration
+and does not shard -- DESIGN.md "Multi-GPU"); --mode partition: the domain is
+cut into N slabs along x_1, one per rank, and the incumbent GUB is
+all-reduced (MIN, NCCL) after every chunk of iterations.  Time is the max over
+ranks of the device time.  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -247,6 +249,9 @@ def main():
     ap.add_argument("--d", type=int, default=0, help="variables split per iteration [min(n, 16)]")
     ap.add_argument("--no-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the configs[1] throughput-regime measurement")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "partition"],
+                    help="N > 1: independent solves per GPU (replicas) or one domain partitioned into slabs along x_1 "
+                         "with the incumbent all-reduced (MIN) every chunk of iterations")
     args = ap.parse_args()
     cfg = workloads.CONFIGS[args.config]
     if args.impl == "reference":
@@ -266,7 +271,8 @@ def main():
     dev = torch.device("cuda", lrank)
     fid, n = cfg["fid"], cfg["n"]
     L, U = workloads.config_bounds(cfg)
-    l, u = slab(L, U, rank, world)
+    partition = world > 1 and args.mode == "partition"
+    l, u = slab(L, U, rank, world) if partition else (L, U)
     ld = torch.tensor(l, device=dev)
     ud = torch.tensor(u, device=dev)
     dsplit = args.d or min(n, 16)
@@ -274,7 +280,7 @@ def main():
     popts = pb.options(d=dsplit, m=args.m, bmax=args.bmax or None, profile=1)
     ws = pb.Workspace(pb.solve_workspace_bytes(fid, n, opts), device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
-    ex = exchange_fn(dist) if dist else None
+    ex = exchange_fn(dist) if partition else None
 
     def solve(o):
         if ex:
@@ -326,7 +332,7 @@ def main():
     value = evals / (total_ms / 1e3)
     r0 = res[-1]
     f_lo, f_hi = r0.f_lo, r0.f_hi
-    if dist:
+    if partition:
         enc = torch.tensor([f_lo, f_hi], dtype=torch.float64, device=dev)
         dist.all_reduce(enc, op=dist.ReduceOp.MIN)
         f_lo, f_hi = enc.tolist()
@@ -425,13 +431,16 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if partition else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": cfg["name"], "fid": fid, "n": n, "domain": [cfg["lo"], cfg["hi"]],
                        "eps": cfg["eps"], "d": dsplit, "m": args.m, "bmax": int(opts.bmax) or "auto",
                        "step": "one full solve (root region -> eps-enclosure)",
                        "l2": "flushed between steps (256 MiB write)",
-                       "parallelism": f"domain slabs x{world}, NCCL all-reduce(MIN) of GUB per iteration"},
+                       "parallelism": (f"domain slabs x{world} along x_1, NCCL all-reduce(MIN) of GUB per chunk"
+                                       if partition else
+                                       f"replicas x{world}: one independent solve per GPU (the n = 10k deep dive "
+                                       "has one live region per iteration and does not shard; DESIGN.md)")},
             "time_to_enclose_s": total_ms / args.steps / 1e3,
             "enclosure": [f_lo, f_hi],
             "iters": r0.iters, "evals_per_step": r0.evals, "peak_pool": r0.peak_pool,

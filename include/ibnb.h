@@ -105,13 +105,16 @@ typedef struct {
 } ib_result;
 
 /* Multi-GPU incumbent exchange (GUB is the best sample
- * found anywhere).  When fn != NULL, every iteration after the midpoint
- * samples are min-reduced the runtime writes xchg[0] = local GUB and
- * xchg[1] = (local search finished ? 0 : -1) to the DEVICE buffer xchg and
- * calls fn(user) on the host thread; fn must replace xchg by its element-wise
- * minimum over all ranks (e.g. an NCCL all-reduce(MIN) on the same stream).
- * The run ends when every rank has finished; a rank whose list L empties
- * (all its regions ruled out by the shared GUB) is finished, not failed. */
+ * found anywhere).  When fn != NULL, after every chunk of iterations (the
+ * runtime's unit of host synchronisation, at most 32 iterations) the runtime
+ * writes xchg[0] = local GUB and xchg[1] = (local search finished ? 0 : -1)
+ * to the DEVICE buffer xchg and calls fn(user) on the host thread; fn must
+ * replace xchg by its element-wise minimum over all ranks, enqueued on the
+ * caller's `stream` (e.g. an NCCL all-reduce(MIN)); the runtime orders it
+ * between its own kernels with events.  The run ends when every rank has
+ * finished; a rank whose list L empties (all its regions ruled out by the
+ * shared GUB) is finished, not failed.  A stale GUB between exchanges only
+ * delays pruning (any upper bound of the minimum is valid). */
 typedef void (*ib_exchange_fn)(void* user);
 
 /* Bytes of caller-owned device workspace needed by ib_solve*() for a problem

@@ -332,12 +332,9 @@ struct Hook : IterHook {
   Ctl* ctl = nullptr;
   void begin(int cls, long, cudaStream_t st) override { prof->begin(cls, st); }
   void end(int cls, cudaStream_t st) override { prof->end(cls, st); }
-  void exchange(cudaStream_t st) override {
-    if (!xfn) return;
-    launch_xchg_put(ctl, xchg, st);
-    xfn(xuser);
-    launch_xchg_take(ctl, xchg, st);
-  }
+  // the incumbent exchange runs once per chunk of iterations (see below), not
+  // inside an iteration
+  void exchange(cudaStream_t) override {}
 };
 
 // grid bound baked into a captured iteration: generous, so that one graph
@@ -409,7 +406,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   Problem P = make_problem(fid, n, o.d, o.m, o.kids, o.ld, o.mono, w.l, w.u, o.bmax);
   Prof prof;
   prof.on = opt && opt->profile == 1;
-  const bool use_graph = !prof.on && !xfn;
+  const bool use_graph = !prof.on;
   // graph capture needs a non-legacy stream: work on a private stream (cached
   // per thread) ordered after the caller's stream (the call is synchronous)
   cudaStream_t st = user_st;
@@ -571,7 +568,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
     // the cached iteration graphs do not multiply
     const long list_hint = (long)pcount <= 65536 ? 65536 : (1L << 40);
     // small batches: whole iterations in one persistent cooperative kernel
-    const bool fused = !xfn && o.bmax * o.kids <= fuse_kids && (long)pcount <= fuse_pool;
+    const bool fused = o.bmax * o.kids <= fuse_kids && (long)pcount <= fuse_pool;
     if (fused) {
       prof.begin(6, st);
       CKL(launch_fused(P, ib, (int)chunk, o.bmax, st));
@@ -604,6 +601,23 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
     // next iteration's k_list) before the host looks at L
     CKL(launch_apply_pending(w.ctl, o.kids, st));
     nk += 1;
+    if (xfn) {
+      // multi-GPU incumbent exchange, once per chunk (<= 32 iterations): the
+      // caller's all-reduce(MIN) runs on the caller's stream, ordered between
+      // the put and the take on the solve stream by events
+      CKL(launch_xchg_put(w.ctl, xchg, st));
+      if (st != user_st) {
+        CK(cudaEventRecord(tc.ev, st));
+        CK(cudaStreamWaitEvent(user_st, tc.ev, 0));
+      }
+      xfn(xuser);
+      if (st != user_st) {
+        CK(cudaEventRecord(tc.ev, user_st));
+        CK(cudaStreamWaitEvent(st, tc.ev, 0));
+      }
+      CKL(launch_xchg_take(w.ctl, xchg, st));
+      nk += 2;
+    }
     CK(cudaMemcpyAsync(&hc, w.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     pcount = hc.pcount;

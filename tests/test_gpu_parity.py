@@ -365,3 +365,37 @@ def test_full_size_n10000_paper_domains(pb, fid):
         o = oracle.eval_box(fid, a, b)
         assert abs(o[0] - g) <= tol(fid, a, b)
         assert o[0] <= r.f_hi + tol(fid, a, b)
+
+
+# ------------------------------------------------------------ incumbent exchange hook (multi-GPU)
+@pytest.mark.parametrize("fid,n,d", [(7, 2000, 16), (1, 10, 10)])
+def test_exchange_hook_identity_matches_plain_solve(pb, fid, n, d):
+    """ib_solve_dev_ex with an exchange that changes nothing (a world of one
+    rank) gives the plain solve, bit for bit (fused path / graph path)."""
+    l, u = workloads.bounds(fid, n)
+    ld, ud = cuda(l), cuda(u)
+    calls = []
+    a = pb.ib_solve_dev(fid, ld, ud, 1e-6, 1e-6, pb.options(d=d), surv_cap=64)
+    b = pb.ib_solve_dev_ex(fid, ld, ud, lambda x: calls.append(1), 1e-6, 1e-6, pb.options(d=d), surv_cap=64)
+    assert calls, "the exchange hook was never called"
+    assert (a.iters, a.evals, a.n_surv, a.status) == (b.iters, b.evals, b.n_surv, b.status)
+    assert a.f_lo == b.f_lo and a.f_hi == b.f_hi
+    np.testing.assert_array_equal(a.lo.cpu().numpy(), b.lo.cpu().numpy())
+
+
+def test_exchange_hook_foreign_incumbent_empties_slab(pb):
+    """A slab without the minimiser, told by the 'other rank' that f* = 0 was
+    found and that rank is finished: every region is ruled out (status
+    EMPTY), never a wrong enclosure."""
+    import torch
+
+    n = 2000
+    l, u = workloads.bounds(7, n)
+    l[0] = 1.0  # x_1 in [1, 6]: the minimiser x* = 0 is elsewhere
+
+    def other_rank(x):
+        x.copy_(torch.minimum(x, torch.tensor([0.0, 0.0], dtype=torch.float64, device=x.device)))
+
+    r = pb.ib_solve_dev_ex(7, cuda(l), cuda(u), other_rank, 1e-6, 1e-6, pb.options(d=16))
+    assert r.status == 2  # IB_STATUS_EMPTY
+    assert r.f_hi == 0.0
