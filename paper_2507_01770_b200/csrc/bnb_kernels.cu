@@ -598,11 +598,27 @@ __device__ __noinline__ bool child_mono_ok(const Problem& P, const double* __res
 // bounds are stored per child for pass 2.
 // GT = 8: bisection (m = 2, h = 3) with the group loop fully unrolled so the
 // outer functions of the 8 children interleave (ILP); GT = 0: runtime G
+// warp-aggregated append of child g to the potential-candidate list (k_fused)
+__device__ __forceinline__ void pot_append(Ctl* ctl, uint32_t* pot, bool cond, uint32_t g) {
+  const unsigned am = __activemask();
+  const unsigned m = __ballot_sync(am, cond);
+  if (!m) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(&ctl->npot, (unsigned long long)__popc(m));
+  base = __shfl_sync(am, base, leader);
+  if (cond) {
+    const unsigned long long idx = base + __popc(m & ((1u << lane) - 1u));
+    if (idx < (unsigned long long)PCAP) pot[idx] = g;
+  }
+}
+
 template <class F, int GT>
 __device__ __forceinline__ void child_eval_dev(const Problem& P, Ctl* __restrict__ ctl,
                                                const double* __restrict__ tab, int tab_stride,
                                                double* __restrict__ clb, uint64_t* zero_a, uint64_t* zero_b,
-                                               long nzero, uint32_t* zero_ctr, unsigned int* zero_hist) {
+                                               long nzero, uint32_t* zero_ctr, unsigned int* zero_hist,
+                                               uint32_t* pot = nullptr) {
   if (ctl->done) return;
   if (zero_a) {  // descriptors and tickets of the following k_cand / k_emit,
                  // histograms and accumulators of the next k_list
@@ -635,6 +651,7 @@ __device__ __forceinline__ void child_eval_dev(const Problem& P, Ctl* __restrict
         const double lbq = canon_lb(ObjLevy::outer(V.acc(false), n).lo);
         clb[gi * G + q] = lbq;
         if (lbq <= gub0) best = fmin(best, ObjLevy::outer(V.acc(true), n).hi);
+        if (pot) pot_append(ctl, pot, lbq <= gub0, (uint32_t)(gi * G + q));
       }
     } else {
       Iv A[2], Am[2];
@@ -696,6 +713,7 @@ __device__ __forceinline__ void child_eval_dev(const Problem& P, Ctl* __restrict
         const double lbq = canon_lb(outer_lo<F>(B, n));
         clb[gi * G + q] = lbq;
         if (lbq <= gub0) best = fmin(best, outer_hi<F>(Bm, n));
+        if (pot) pot_append(ctl, pot, lbq <= gub0, (uint32_t)(gi * G + q));
       }
     }
   }
@@ -910,6 +928,93 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
   }
   PROBE(7)
   PROBE_END(0)
+}
+
+// k_fused, one block: the insertion pass when at most PCAP children had
+// lb <= GUB at the iteration start (the candidates, lb <= final GUB, are
+// among them).  Sorting the potential list by child index gives the same
+// survivors in the same order as k_cand -> k_mono -> k_emit, without a scan
+// over all children.
+template <class F>
+__device__ void emit_small_dev(const Problem& P, Ctl* __restrict__ ctl, const double* __restrict__ tab,
+                               int tab_stride, const double* __restrict__ clb, const int32_t* __restrict__ new_slot,
+                               Pool out, const uint32_t* __restrict__ pot, int np, uint32_t* hot0, uint32_t* hot1) {
+  __shared__ uint32_t s_in[PCAP], s_g[PCAP];
+  __shared__ uint8_t s_c[PCAP], s_ok[PCAP];
+  __shared__ double s_w[PCAP];
+  const int t = threadIdx.x, lane = t & 31;
+  const double gub = okey_inv(ctl->gub_key);
+  uint32_t* hot = ctl->hsel ? hot1 : hot0;
+  const unsigned long long tau = ctl->tau_key;
+  const uint32_t gin = t < np ? pot[t] : 0xffffffffu;
+  if (t < PCAP) s_in[t] = gin;
+  __syncthreads();
+  if (t < np) {  // rank sort (child indices are distinct)
+    int r = 0;
+    for (int j = 0; j < np; ++j) r += s_in[j] < gin;
+    s_g[r] = gin;
+  }
+  __syncthreads();
+  const uint32_t g = t < np ? s_g[t] : 0u;
+  const double lb = t < np ? clb[g] : CUDART_INF;
+  const bool cand = t < np && lb <= gub;
+  if (t < PCAP) s_c[t] = cand;
+  __syncthreads();
+  for (int k = t >> 5; k < np; k += TPB / 32) {
+    if (!s_c[k]) continue;  // warp-uniform
+    ChildIdx ci = child_of(s_g[k], P);
+    const double* T = tab + (size_t)ci.b * tab_stride;
+    double wl = 0.0;
+    bool bad = false;
+    if (lane < P.d) {
+      const double* e = T + HDR + (size_t)(lane * P.m + piece(ci.code, lane, P)) * ENT;
+      wl = __dsub_rn(e[E_HI], e[E_LO]);
+      if constexpr (F::SEP) bad = e[E_T + 4 * F::K + 2 * F::KG] != 0.0;
+    }
+    wl = warp_max(wl);
+    const unsigned anybad = __ballot_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      s_w[k] = fmax(T[H_WREST], wl);
+      s_ok[k] = anybad == 0u;
+    }
+  }
+  __syncthreads();
+  bool surv = false;
+  if (cand) {
+    if constexpr (F::SEP) {
+      surv = !P.mono || s_ok[t] != 0;
+    } else {
+      ChildIdx ci = child_of(g, P);
+      surv = !P.mono || child_mono_ok<F>(P, tab + (size_t)ci.b * tab_stride, ci.code);
+    }
+  }
+  const bool hotf = surv && hot0 && okey(lb) < tau;
+  uint32_t c3[3] = {cand ? 1u : 0u, surv ? 1u : 0u, hotf ? 1u : 0u}, ex[3], tot[3];
+  block_exclusive_scan<3, TPB>(c3, ex, tot);
+  const uint64_t base = ctl->pcount, cap = ctl->pool_cap, hbase = ctl->nhot;
+  if (surv) {
+    const uint64_t pos = base + ex[1];
+    if (pos < cap) {
+      ChildIdx ci = child_of(g, P);
+      out.lb[pos] = lb;
+      out.w[pos] = s_w[t];
+      out.slot[pos] = new_slot[ci.b];
+      out.code[pos] = ci.code;
+      if (hotf) hot[hbase + ex[2]] = (uint32_t)pos;
+    }
+  }
+  if (t == 0) {
+    ctl->ncand = tot[0];
+    ctl->nsurv = tot[1];
+    ctl->nsurv_hot = tot[2];
+    if (base + tot[1] > cap) {
+      ctl->err = -2;  // IB_ENOSPACE
+      ctl->done = 4;
+    }
+    ctl->pending_end = 1;
+    set_list_fast(ctl, tot[2]);
+  }
+  __syncthreads();
 }
 
 // k_fused: candidates (lb <= GUB, line 140), first-order test (lines
@@ -2247,6 +2352,8 @@ __global__ void __launch_bounds__(TPB, 1) k_fused(Problem P, IterBufs w, int ite
       mark(0);
     }
     if (w.ctl->done) break;  // uniform: written before the barrier
+    // every block read the last count before the previous barrier
+    if (blockIdx.x == 0 && threadIdx.x == 0) w.ctl->npot = 0ull;
     const int nitems = (int)w.ctl->B * P.pslices;
     for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
       const int b = item / P.pslices;
@@ -2258,11 +2365,32 @@ __global__ void __launch_bounds__(TPB, 1) k_fused(Problem P, IterBufs w, int ite
     grid.sync();
     if (tw) tb = gtimer();
     mark(1);
-    child_eval_dev<F, GT>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.desc, w.desc2, nz, w.tile_ctr, w.hist);
+    child_eval_dev<F, GT>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.desc, w.desc2, nz, w.tile_ctr, w.hist, w.pot);
     work(2);
     grid.sync();
     if (tw) tb = gtimer();
     mark(2);
+    const unsigned long long npot = w.ctl->npot;  // uniform: complete before the barrier
+    if (npot <= (unsigned long long)PCAP) {
+      // few potential candidates: insertion and the next list phase on block 0
+      need_list = true;
+      if (blockIdx.x == 0) {
+        emit_small_dev<F>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.new_slot, w.pool, w.pot, (int)npot, w.hot0,
+                          w.hot1);
+        if (it + 1 < iters) {
+          const bool fast = w.ctl->list_fast != 0 && !w.ctl->done;
+          if (fast) list_small_dev(w.pool, w.ctl, w.hot0, w.hot1, w.sel_slot, w.sel_code, kids);
+          if (threadIdx.x == 0) w.ctl->list_pre = fast ? 1 : 0;
+        }
+      }
+      work(3);
+      grid.sync();
+      if (tw) tb = gtimer();
+      if (it + 1 < iters) need_list = w.ctl->list_pre == 0;
+      mark(5);
+      if (ts) ts[6] += 1;
+      continue;
+    }
     cand_emit_dev<F>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.new_slot, w.pool, w.desc2, w.hot0, w.hot1);
     work(3);
     // the last block to finish the insertion runs the next iteration's list

@@ -15,6 +15,7 @@ constexpr int ENT = 24;                         // doubles per (variable, piece)
 constexpr int TPB = 256;                        // threads per block (all kernels)
 constexpr int IPT = 4;                          // items per thread in scans
 constexpr int TILE = TPB * IPT;
+constexpr int PCAP = 256;                       // k_fused: potential candidates handled by one block
 
 // header offsets (doubles)
 constexpr int H_REST = 0;    // K intervals (K <= 2): rest accumulators
@@ -77,6 +78,7 @@ struct Ctl {
   unsigned int blocks_done;      // last-block election counter
   unsigned int fused_ticket;     // k_fused: last block of the insertion pass
   int list_pre;                  // k_fused: the next list phase already ran (last block)
+  unsigned long long npot;       // k_fused: children with lb <= GUB at the iteration start (potential candidates)
   unsigned int pending_end;      // the survivors of the last iteration are not yet counted in pcount
   unsigned long long sum_pool;   // records scanned by the statistics pass
   unsigned long long sum_radix;  // records scanned by radix passes 2..8
@@ -132,6 +134,7 @@ struct IterBufs {
   double* ppart;           // k_prep slice partials: [bmax][pslices][10]
   unsigned int* pticket;   // k_prep per-parent arrival tickets [bmax] (zero between launches)
   unsigned long long* tstamp;  // k_fused phase timer (trace only; nullptr otherwise)
+  uint32_t* pot;               // k_fused: potential candidates (child indices), PCAP entries
 };
 
 // host callbacks around the kernel classes of an iteration: profiling

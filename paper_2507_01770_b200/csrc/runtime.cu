@@ -230,6 +230,7 @@ struct SolveWs {
   unsigned int* hist;
   double* ppart;
   unsigned int* pticket;
+  uint32_t* pot;
 };
 
 static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
@@ -248,6 +249,7 @@ static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
   w.new_slot = A.take<int32_t>(o.bmax);
   w.ppart = A.take<double>((size_t)o.bmax * prep_slices(n, o.bmax) * 10);
   w.pticket = A.take<unsigned int>(o.bmax);
+  w.pot = A.take<uint32_t>(PCAP);
   w.root_out = A.take<double>(2);
   w.f_search = A.take<double>(1);
   w.search_rounds = A.take<int32_t>(1);
@@ -510,6 +512,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   ib.hot1 = w.hot1;
   ib.ppart = w.ppart;
   ib.pticket = w.pticket;
+  ib.pot = w.pot;
   unsigned long long* tstamp = nullptr;
   if (trace) {
     CK(cudaMalloc(&tstamp, 32 * sizeof(unsigned long long)));
