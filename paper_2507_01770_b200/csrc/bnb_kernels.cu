@@ -154,7 +154,53 @@ __device__ __forceinline__ LevyChunk levy_chunk(int c, int d, int n) {
   return q;
 }
 
-// ====================================================================== prep
+// prep: one block reduction of the rest accumulators of the box (acc) and of
+// its midpoint (accm) and of the max unsplit width, in a single pass
+// (results valid in thread 0); Levy reduces one chain sum each
+template <class F, int BS>
+__device__ __forceinline__ void block_reduce_prep(Iv* acc, Iv* accm, double& wmax) {
+  constexpr int K = F::CHAIN ? 1 : F::K;
+  auto comb = [](int k, Iv a, Iv b) -> Iv {
+    if constexpr (F::CHAIN) return a + b;
+    else return acc_comb<F>(k, a, b);
+  };
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      Iv t{__shfl_xor_sync(0xffffffffu, acc[k].lo, o), __shfl_xor_sync(0xffffffffu, acc[k].hi, o)};
+      Iv tm{__shfl_xor_sync(0xffffffffu, accm[k].lo, o), __shfl_xor_sync(0xffffffffu, accm[k].hi, o)};
+      acc[k] = comb(k, acc[k], t);
+      accm[k] = comb(k, accm[k], tm);
+    }
+    wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+  }
+  if constexpr (BS > 32) {
+    __shared__ Iv s_a[BS / 32][2], s_m[BS / 32][2];
+    __shared__ double s_w[BS / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+      for (int k = 0; k < K; ++k) {
+        s_a[wid][k] = acc[k];
+        s_m[wid][k] = accm[k];
+      }
+      s_w[wid] = wmax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < BS / 32; ++w) {
+        for (int k = 0; k < K; ++k) {
+          acc[k] = comb(k, acc[k], s_a[w][k]);
+          accm[k] = comb(k, accm[k], s_m[w][k]);
+        }
+        wmax = fmax(wmax, s_w[w]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ====================================================================== prep// ====================================================================== prep
 // Parent b of the batch is handled by P.pslices blocks (one block when the
 // batch is large; for large n and small batches the n variables are cut into
 // slices so that the O(n) reduction spreads over the SMs).  Block (b, s):
@@ -257,17 +303,7 @@ __device__ __forceinline__ void prep_item(const Problem& P, const Ctl* __restric
       }
     }
   }
-  if constexpr (F::CHAIN) {
-    Iv a2[2] = {acc[0], iv(0.0)}, am2[2] = {accm[0], iv(0.0)};
-    block_reduce_acc<ObjRastrigin, BS>(a2);  // any K=1 SUM reducer
-    block_reduce_acc<ObjRastrigin, BS>(am2);
-    acc[0] = a2[0];
-    accm[0] = am2[0];
-  } else {
-    block_reduce_acc<F, BS>(acc);
-    block_reduce_acc<F, BS>(accm);
-  }
-  wmax = block_max<BS>(wmax);
+  block_reduce_prep<F, BS>(acc, accm, wmax);
   // tables of the m pieces of the d split variables, by the block that owns
   // the variable (slices run in parallel); three threads per entry: bounds +
   // box terms, midpoint terms, derivative ingredients + separable flag
@@ -325,9 +361,9 @@ __device__ __forceinline__ void prep_item(const Problem& P, const Ctl* __restric
   }
   if (S > 1) {
     // publish this slice's partial; the last slice block of parent b goes on
+    // (the rows and tables of this block are read only after the next grid
+    // barrier or kernel boundary; only the partial must precede the ticket)
     __shared__ int s_last;
-    __threadfence();  // this block's rows and table entries before the ticket
-    __syncthreads();
     if (threadIdx.x == 0) {
       double* pp = ppart + ((size_t)b * S + s) * 10;
       for (int k = 0; k < 2; ++k) {
@@ -366,14 +402,7 @@ __device__ __forceinline__ void prep_item(const Problem& P, const Ctl* __restric
         }
         rw = fmax(rw, pt[8]);
       }
-      if constexpr (F::CHAIN) {
-        block_reduce_acc<ObjRastrigin, BS>(ra);
-        block_reduce_acc<ObjRastrigin, BS>(rm);
-      } else {
-        block_reduce_acc<F, BS>(ra);
-        block_reduce_acc<F, BS>(rm);
-      }
-      rw = block_max<BS>(rw);
+      block_reduce_prep<F, BS>(ra, rm, rw);
       for (int k = 0; k < 2; ++k) {
         acc[k] = ra[k];
         accm[k] = rm[k];
