@@ -540,7 +540,10 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   long chunk = 1;
   for (;;) {
     const long per_it = o.bmax * o.kids;
-    // capacity planning for the chunk: compact L / collect archive slots
+    // capacity planning for the chunk: shorten it to what L can take in the
+    // worst case (every child survives), compact L only when even one
+    // iteration might not fit, collect archive slots when short
+    chunk = std::max(1L, std::min(chunk, (o.pool_cap - (long)pcount) / std::max(1L, per_it)));
     if ((long)pcount + chunk * per_it > o.pool_cap) {
       // compact L: keep the live records (lb <= GUB), list order preserved
       CKL(launch_partition(w.pa, (long)pcount, &w.ctl->gub_key, 64, 0ull, 0ull, nullptr, nullptr, nullptr, w.pb,
@@ -634,7 +637,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
               "width_passes=%llu done=%d\n", now() - t_start, chunk, hc.iter, hc.pcount, hc.live, hc.nhot, hc.B,
               hc.nrefill, hc.nwidth, hc.done);
     if (xfn ? hc.gdone : hc.done) break;
-    chunk = std::min(chunk * 2, 32L);
+    chunk = std::min(chunk * 2, 64L);
     // lazy deletion leaves selected / ruled-out records in L: compact when a
     // refill of the hot index found it more than half dead
     if (hc.compact_hint && (long)pcount > (1L << 18)) {
