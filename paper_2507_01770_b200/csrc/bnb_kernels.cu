@@ -668,10 +668,32 @@ __device__ __forceinline__ void child_eval_dev(const Problem& P, Ctl* __restrict
   const long ngroups = (long)ctl->B * gpp;
   const double gub0 = okey_inv(ctl->gub_key);  // incumbent before this iteration
   double best = CUDART_INF;
-  for (long gi = (long)blockIdx.x * TPB + threadIdx.x; gi < ngroups; gi += (long)gridDim.x * TPB) {
+  // bisection path: the tables of the (at most two) parents of a block's 256
+  // groups are staged in shared memory (one coalesced load instead of a
+  // dependent L2 round trip per piece)
+  constexpr int TS = GT ? HDR + 2 * D_MAX * ENT : 1;
+  __shared__ double s_tab[2][TS];
+  for (long base = (long)blockIdx.x * TPB; base < ngroups; base += (long)gridDim.x * TPB) {
+    const long gi = base + threadIdx.x;
+    const double* __restrict__ Tsh = nullptr;
+    int b0 = 0;
+    if constexpr (GT != 0 && !F::CHAIN) {
+      const long glast = min(base + TPB, ngroups) - 1;
+      b0 = P.mbits ? (int)(base >> (P.kbits - h * P.mbits)) : (int)(base / gpp);
+      const int b1 = P.mbits ? (int)(glast >> (P.kbits - h * P.mbits)) : (int)(glast / gpp);
+      if (b1 - b0 <= 1 && tab_stride <= TS) {
+        __syncthreads();  // the previous iteration's readers are done
+        const int nb = b1 - b0 + 1;
+        for (int t = threadIdx.x; t < nb * tab_stride; t += TPB)
+          s_tab[t / tab_stride][t % tab_stride] = tab[(size_t)b0 * tab_stride + t];
+        __syncthreads();
+        Tsh = &s_tab[0][0];
+      }
+    }
+    if (gi >= ngroups) continue;
     const int b = P.mbits ? (int)(gi >> (P.kbits - h * P.mbits)) : (int)(gi / gpp);
     const uint32_t hcode = P.mbits ? (uint32_t)gi & (uint32_t)(gpp - 1) : (uint32_t)(gi % gpp);
-    const double* __restrict__ T = tab + (size_t)b * tab_stride;
+    const double* __restrict__ T = Tsh ? Tsh + (size_t)(b - b0) * TS : tab + (size_t)b * tab_stride;
     if constexpr (F::CHAIN) {
       for (int q = 0; q < G; ++q) {
         int e[D_MAX];
@@ -1536,12 +1558,11 @@ __global__ void k_apply_pending(Ctl* ctl, long kids) {
   }
 }
 
-// ===================================================== fused cooperative kernels
-// One iteration = 4 launches: k_list (statistics, stop test, batch size,
-// radix select, selection), k_prep, k_child_eval, k_prune (candidates,
-// first-order test, insertion into L, iteration end).  The phases of k_list
-// and k_prune are separated by grid-wide barriers (cooperative launch, every
-// block resident); after a barrier the control block is re-read from L2.
+// ===================================================== list L (cooperative)
+// k_list runs the list phase of an iteration as one cooperative kernel; its
+// steps are separated by grid-wide barriers (every block resident) and after
+// a barrier the control block is re-read from L2.  k_fused calls the same
+// device functions.
 __device__ __forceinline__ int vload(const int* p) { return *(const volatile int*)p; }
 
 // ------------------------------------------------------------ hot index of L
@@ -1757,7 +1778,7 @@ __device__ __noinline__ void hot_select_dev(const Pool& p, const uint32_t* __res
 // entry in list order and no radix pass is needed.  Block 0 only.
 __device__ void list_small_dev(const Pool& p, Ctl* ctl, uint32_t* hot0, uint32_t* hot1, int32_t* sel_slot,
                                uint32_t* sel_code, long kids) {
-  __shared__ unsigned long long s_live, s_min;
+  __shared__ unsigned long long s_min;
   __shared__ double s_w;
   __shared__ uint32_t s_scan[TPB / 32];
   if (ctl->done) return;
@@ -1766,7 +1787,6 @@ __device__ void list_small_dev(const Pool& p, Ctl* ctl, uint32_t* hot0, uint32_t
       ctl->pending_end = 0;
       iter_end_dev(ctl, kids);
     }
-    s_live = 0;
     s_min = ~0ull;
     s_w = 0.0;
   }
@@ -2025,33 +2045,6 @@ __global__ void __launch_bounds__(TPB) k_list(Pool p, Ctl* ctl, unsigned int* hi
                                               uint32_t* sel_code, uint64_t* desc, uint64_t* desc2, uint32_t* tile_ctr,
                                               uint32_t* hot0, uint32_t* hot1, long kids) {
   list_dev(p, ctl, hists, sel_slot, sel_code, desc, desc2, tile_ctr, hot0, hot1, kids);
-}
-
-template <class F>
-__global__ void __launch_bounds__(TPB, 2) k_prune(Problem P, Ctl* ctl, const double* __restrict__ tab, int tab_stride,
-                                                  const double* __restrict__ clb, uint32_t* __restrict__ cand,
-                                                  uint8_t* __restrict__ ok, const int32_t* __restrict__ new_slot,
-                                                  Pool out, uint64_t* desc, uint64_t* desc2, uint32_t* tile_ctr) {
-  cg::grid_group grid = cg::this_grid();
-  if (ctl->done) return;
-  const long gtid = (long)blockIdx.x * TPB + threadIdx.x, gsize = (long)gridDim.x * TPB;
-  const long ntiles = ((long)ctl->B * P.kids + TILE - 1) / TILE + 1;
-  for (long i = gtid; i < ntiles + 1; i += gsize) {
-    desc[i] = 0;
-    desc2[i] = 0;
-  }
-  if (gtid == 0) {
-    tile_ctr[0] = 0;
-    tile_ctr[1] = 0;
-  }
-  grid.sync();
-  cand_dev(P, ctl, clb, cand, desc, tile_ctr);
-  grid.sync();
-  mono_dev<F>(P, ctl, tab, tab_stride, cand, ok);
-  grid.sync();
-  emit_dev<F, false>(P, ctl, tab, tab_stride, clb, cand, ok, new_slot, out, desc2, tile_ctr + 1, false, nullptr, nullptr);
-  grid.sync();
-  if (gtid == 0) iter_end_dev(ctl, P.kids);
 }
 
 // multi-GPU exchange of the incumbent (2 doubles: GUB, finished flag)

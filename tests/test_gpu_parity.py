@@ -317,15 +317,19 @@ def test_fused_graph_and_eager_paths_identical(pb, fid, monkeypatch):
     n = 700
     l, u = workloads.bounds(fid, n)
     res = {}
-    for name, env, prof in (("fused", None, 0), ("graph", "0", 0), ("eager", None, 1)):
-        if env is None:
-            monkeypatch.delenv("IBNB_FUSE_KIDS", raising=False)
-        else:
-            monkeypatch.setenv("IBNB_FUSE_KIDS", env)
+    # fused forced for every chunk (large batches early: the static-tile
+    # insertion pass; few candidates later: the one-block path), graph only,
+    # eager launches (profiling, thresholds off)
+    for name, env, prof in (("fused", str(1 << 40), 0), ("fused_timed", str(1 << 40), 1), ("graph", "0", 0),
+                            ("eager", "0", 1)):
+        monkeypatch.setenv("IBNB_FUSE_KIDS", env)
+        monkeypatch.setenv("IBNB_FUSE_POOL", str(1 << 40))
         res[name] = pb.ib_solve(fid, l, u, 1e-6, 1e-6, pb.options(d=16, profile=prof), surv_cap=64)
+    assert res["fused_timed"].prof["fused"]["launches"] > 0  # the persistent kernel really ran
+    assert res["eager"].prof["fused"]["launches"] == 0
     r0 = res["fused"]
     assert r0.status == 0
-    for k in ("graph", "eager"):
+    for k in ("fused_timed", "graph", "eager"):
         r = res[k]
         assert (r.iters, r.evals, r.n_surv, r.status) == (r0.iters, r0.evals, r0.n_surv, r0.status), k
         assert r.f_lo == r0.f_lo and r.f_hi == r0.f_hi, k
