@@ -403,3 +403,28 @@ def test_exchange_hook_foreign_incumbent_empties_slab(pb):
     r = pb.ib_solve_dev_ex(7, cuda(l), cuda(u), other_rank, 1e-6, 1e-6, pb.options(d=16))
     assert r.status == 2  # IB_STATUS_EMPTY
     assert r.f_hi == 0.0
+
+
+def test_full_size_first_iterations_match_oracle(pb, monkeypatch):
+    """Rastrigin at n = 10,000 (BASELINE configs[4] domain) through the fused
+    persistent kernel -- the launch configuration bench.py times: the first
+    two iterations (d = 8 split variables, 256 children per parent, batches of
+    up to 2 parents) leave exactly the oracle's list L (same regions, bit for
+    bit; lower bounds within the tolerance).  The R9 search is off on both
+    sides (the oracle's is O(n^2) per round at this size)."""
+    monkeypatch.delenv("IBNB_FUSE_KIDS", raising=False)
+    monkeypatch.delenv("IBNB_FUSE_POOL", raising=False)
+    cfg = workloads.CONFIGS[4]
+    l, u = workloads.config_bounds(cfg)
+    n = cfg["n"]
+    o = oracle.solve(cfg["fid"], l, u, eps_f=1e-6, eps_x=1e-6, d=8, m=2, bmax=2, max_iter=2, cap=4096, search=0)
+    g = pb.ib_solve(cfg["fid"], l, u, 1e-6, 1e-6, pb.options(d=8, m=2, bmax=2, max_iter=2, search=-1, profile=1),
+                    surv_cap=4096)
+    assert g.prof["fused"]["launches"] > 0  # the persistent kernel ran the iterations
+    assert (g.iters, g.evals, g.n_surv, g.status) == (o["iters"], o["evals"], o["n_surv"], o["status"])
+    t = tol(cfg["fid"], l, u)
+    assert abs(g.f_lo - o["glb"]) <= t and abs(g.f_hi - o["gub"]) <= t
+    np.testing.assert_array_equal(g.lo, o["lo"])
+    np.testing.assert_array_equal(g.hi, o["hi"])
+    np.testing.assert_allclose(g.lb, o["lb"], rtol=0, atol=t)
+    assert g.lo.shape[1] == n
