@@ -779,7 +779,7 @@ __device__ __forceinline__ void child_eval_dev(const Problem& P, Ctl* __restrict
 }
 
 template <class F, int GT>
-__global__ void __launch_bounds__(TPB, GT ? 3 : 4) k_child_eval(Problem P, Ctl* __restrict__ ctl,
+__global__ void __launch_bounds__(TPB, 4) k_child_eval(Problem P, Ctl* __restrict__ ctl,
                                                                const double* __restrict__ tab, int tab_stride,
                                                                double* __restrict__ clb, uint64_t* zero_a,
                                                                uint64_t* zero_b, long nzero, uint32_t* zero_ctr,
