@@ -987,9 +987,18 @@ __device__ void emit_dev(const Problem& P, Ctl* __restrict__ ctl, const double* 
 // survivors in the same order as k_cand -> k_mono -> k_emit, without a scan
 // over all children.
 template <class F>
-__device__ void emit_small_dev(const Problem& P, Ctl* __restrict__ ctl, const double* __restrict__ tab,
+// Returns true when it also ran the next iteration's list phase (select):
+// the common deep-dive case -- every live record is hot (tau = ~0), the hot
+// index held nothing before this iteration's survivors and they fit one
+// selection (<= min(bmax, TPB)) -- takes the iteration end and the list
+// phase's decisions (stop test, batch size, selection of every live entry in
+// list order) directly from the survivors in registers, with the same
+// results as list_small_dev.
+__device__ bool emit_small_dev(const Problem& P, Ctl* __restrict__ ctl, const double* __restrict__ tab,
                                int tab_stride, const double* __restrict__ clb, const int32_t* __restrict__ new_slot,
-                               Pool out, const uint32_t* __restrict__ pot, int np, uint32_t* hot0, uint32_t* hot1) {
+                               Pool out, const uint32_t* __restrict__ pot, int np, uint32_t* hot0, uint32_t* hot1,
+                               bool try_select = false, long kids = 0, int32_t* sel_slot = nullptr,
+                               uint32_t* sel_code = nullptr) {
   __shared__ uint32_t s_in[PCAP], s_g[PCAP];
   __shared__ uint8_t s_c[PCAP], s_ok[PCAP];
   __shared__ double s_w[PCAP];
@@ -1043,16 +1052,106 @@ __device__ void emit_small_dev(const Problem& P, Ctl* __restrict__ ctl, const do
   uint32_t c3[3] = {cand ? 1u : 0u, surv ? 1u : 0u, hotf ? 1u : 0u}, ex[3], tot[3];
   block_exclusive_scan<3, TPB>(c3, ex, tot);
   const uint64_t base = ctl->pcount, cap = ctl->pool_cap, hbase = ctl->nhot;
+  const bool combined = try_select && hbase == 0 && ctl->hot_valid && tau == ~0ull && tot[2] == tot[1] &&
+                        tot[1] <= ctl->bmax && tot[1] <= (uint32_t)TPB && base + tot[1] <= cap && !ctl->done;
+  int32_t my_slot = 0;
+  uint32_t my_code = 0;
   if (surv) {
     const uint64_t pos = base + ex[1];
     if (pos < cap) {
       ChildIdx ci = child_of(g, P);
+      my_slot = new_slot[ci.b];
+      my_code = ci.code;
       out.lb[pos] = lb;
       out.w[pos] = s_w[t];
-      out.slot[pos] = new_slot[ci.b];
-      out.code[pos] = ci.code;
+      out.slot[pos] = my_slot;
+      out.code[pos] = my_code;
       if (hotf) hot[hbase + ex[2]] = (uint32_t)pos;
     }
+  }
+  if (combined) {
+    // iteration end (iter_end_dev) and the list phase (list_small_dev) on the
+    // survivors: all of them are live (lb <= GUB) and form the hot index
+    __shared__ unsigned long long s_mk;
+    __shared__ double s_mw;
+    if (t == 0) {
+      s_mk = ~0ull;
+      s_mw = 0.0;
+    }
+    __syncthreads();
+    const unsigned long long key = surv ? okey(lb) : ~0ull;
+    unsigned long long mk = key;
+    double mw = surv ? s_w[t] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long q = __shfl_xor_sync(0xffffffffu, mk, o);
+      mk = q < mk ? q : mk;
+      mw = fmax(mw, __shfl_xor_sync(0xffffffffu, mw, o));
+    }
+    if (lane == 0) {
+      if (mk != ~0ull) atomicMin(&s_mk, mk);
+      atomicMax((unsigned long long*)&s_mw, (unsigned long long)__double_as_longlong(mw));
+    }
+    __syncthreads();
+    const unsigned long long nlive = tot[1], minkey = s_mk;
+    const unsigned long long Bold = ctl->B, iter1 = ctl->iter + 1, free1 = ctl->free_top - Bold;
+    unsigned long long bytes = 12ull * nlive;
+    int done = 0;
+    bool wpass = false;
+    if (nlive == 0) {
+      done = 3;
+    } else if (__dsub_ru(gub, okey_inv(minkey)) <= ctl->eps_f) {
+      wpass = true;
+      bytes += 20ull * nlive;
+      if (s_mw <= ctl->eps_x) done = 1;
+    }
+    if (!done && iter1 >= ctl->max_iter) done = 2;
+    if (!done && free1 < nlive) done = 4;
+    if (!done && surv) {  // selection: every live entry in list order
+      sel_slot[ex[1]] = my_slot;
+      sel_code[ex[1]] = my_code;
+      out.lb[base + ex[1]] = CUDART_INF;  // removed from L
+    }
+    if (t == 0) {
+      // iteration end
+      ctl->ncand = tot[0];
+      ctl->nsurv = tot[1];
+      ctl->nsurv_hot = tot[2];
+      ctl->sum_cand += tot[0];
+      ctl->sum_pool += base;
+      ctl->sum_B += Bold;
+      ctl->free_top = free1;
+      ctl->pcount = base + tot[1];
+      ctl->iter = iter1;
+      ctl->evals += Bold * (unsigned long long)kids;
+      ctl->pending_end = 0;
+      if (wpass) {
+        ctl->nwidth += 1;
+        const unsigned long long wb = (unsigned long long)__double_as_longlong(s_mw);
+        if (wb > ctl->acc_max_w) ctl->acc_max_w = wb;
+      }
+      ctl->live = nlive;
+      ctl->min_lb_key = minkey;
+      if (done) {
+        ctl->nhot = tot[2];  // the survivors stay in the hot index
+        ctl->max_w_bits = ctl->acc_max_w;
+        if (done == 4) ctl->err = -2;
+        ctl->list_bytes += bytes;
+        ctl->done = done;
+      } else {
+        bytes += 16ull * nlive;
+        ctl->nhot_keep = 0;
+        ctl->hsel ^= 1;
+        ctl->nhot = 0;
+        ctl->B = nlive;
+        ctl->known = 0;
+        ctl->prefix = 0;
+        ctl->need = nlive;
+        ctl->list_bytes += bytes;
+      }
+    }
+    __syncthreads();
+    return true;
   }
   if (t == 0) {
     ctl->ncand = tot[0];
@@ -1066,6 +1165,7 @@ __device__ void emit_small_dev(const Problem& P, Ctl* __restrict__ ctl, const do
     set_list_fast(ctl, tot[2]);
   }
   __syncthreads();
+  return false;
 }
 
 // k_fused: candidates (lb <= GUB, line 140), first-order test (lines
@@ -2397,11 +2497,11 @@ __global__ void __launch_bounds__(TPB, 1) k_fused(Problem P, IterBufs w, int ite
       // few potential candidates: insertion and the next list phase on block 0
       need_list = true;
       if (blockIdx.x == 0) {
-        emit_small_dev<F>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.new_slot, w.pool, w.pot, (int)npot, w.hot0,
-                          w.hot1);
+        const bool sel = emit_small_dev<F>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.new_slot, w.pool, w.pot, (int)npot,
+                                           w.hot0, w.hot1, it + 1 < iters, kids, w.sel_slot, w.sel_code);
         if (it + 1 < iters) {
-          const bool fast = w.ctl->list_fast != 0 && !w.ctl->done;
-          if (fast) list_small_dev(w.pool, w.ctl, w.hot0, w.hot1, w.sel_slot, w.sel_code, kids);
+          const bool fast = sel || (w.ctl->list_fast != 0 && !w.ctl->done);
+          if (fast && !sel) list_small_dev(w.pool, w.ctl, w.hot0, w.hot1, w.sel_slot, w.sel_code, kids);
           if (threadIdx.x == 0) w.ctl->list_pre = fast ? 1 : 0;
         }
       }
