@@ -172,6 +172,19 @@ def exchange_fn(dist):
     return ex
 
 
+def transfer_fn(dist, rank):
+    """ib_transfer_fn contract: move nbytes of rank src's buffer to rank dst
+    (point-to-point; every rank is called, only the two involved act)."""
+
+    def tr(src, dst, tbuf, nbytes):
+        if rank == src:
+            dist.send(tbuf[:nbytes], dst)
+        elif rank == dst:
+            dist.recv(tbuf[:nbytes], src)
+
+    return tr
+
+
 def cpu_baseline(cfg, seconds=12.0):
     """The CPU oracle, as it stands, on a bounded sample of the same workload:
     or_branch on parents of the workload's first iterations (the root and its
@@ -282,9 +295,11 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     ex = exchange_fn(dist) if partition else None
 
+    tr = transfer_fn(dist, rank) if partition else None
+
     def solve(o):
-        if ex:
-            return pb.ib_solve_dev_ex(fid, ld, ud, ex, cfg["eps"], cfg["eps"], o, workspace=ws)
+        if ex:  # partitioned domain: incumbent exchange + box rebalancing
+            return pb.ib_solve_dev_mg(fid, ld, ud, ex, tr, rank, cfg["eps"], cfg["eps"], o, workspace=ws)
         return pb.ib_solve_dev(fid, ld, ud, cfg["eps"], cfg["eps"], o, workspace=ws)
 
     def barrier():
@@ -437,7 +452,8 @@ def main():
                        "eps": cfg["eps"], "d": dsplit, "m": args.m, "bmax": int(opts.bmax) or "auto",
                        "step": "one full solve (root region -> eps-enclosure)",
                        "l2": "flushed between steps (256 MiB write)",
-                       "parallelism": (f"domain slabs x{world} along x_1, NCCL all-reduce(MIN) of GUB per chunk"
+                       "parallelism": (f"domain slabs x{world} along x_1, NCCL all-reduce(MIN) of GUB per chunk, "
+                                       "box rebalancing (NCCL send/recv) when the lists skew"
                                        if partition else
                                        f"replicas x{world}: one independent solve per GPU (the n = 10k deep dive "
                                        "has one live region per iteration and does not shard; DESIGN.md)")},

@@ -102,6 +102,8 @@ typedef struct {
     int64_t radix_records; /* records scanned by radix passes 2..8 */
     double f_search;       /* GUB supplied by the initial search (+inf: none) */
     int64_t search_rounds; /* accepted moves of that search */
+    int64_t rebalanced;    /* ib_solve_dev_mg: regions received (> 0) or sent (< 0) */
+    int64_t transfers;     /* ib_solve_dev_mg: rebalancing transfers this rank took part in */
 } ib_result;
 
 /* Multi-GPU incumbent exchange (GUB is the best sample
@@ -148,6 +150,29 @@ int ib_solve_dev_ex(int fid, int n, const double* l_dev, const double* u_dev, do
                     const ib_options* opt, void* ws, size_t ws_bytes, ib_result* res, double* surv_lo,
                     double* surv_hi, double* surv_lb, int64_t surv_cap, void* stream, ib_exchange_fn fn,
                     void* user, double* xchg);
+
+/* Multi-GPU box rebalancing (north_star: "periodic NVLink box rebalancing
+ * when survivor counts skew").  tfn(user, src, dst, buf, bytes) is called on
+ * EVERY rank with the same arguments; the caller must copy `bytes` bytes from
+ * rank src's buf to rank dst's buf (e.g. NCCL send / recv on the caller's
+ * stream, ordered with the solve by events); other ranks do nothing. */
+typedef void (*ib_transfer_fn)(void* user, int src, int dst, void* buf, size_t bytes);
+
+/* ib_solve_dev_ex with box rebalancing.  xchg: device, 4 doubles (GUB,
+ * finished flag, -(live * 1024 + rank), live * 1024 + rank -- fn reduces all
+ * four with MIN).  fn is called twice per chunk: for the incumbent, then for
+ * the list sizes under the shared incumbent.  After that, when the largest list of live
+ * regions (rank a) holds more than twice the smallest (rank b) plus two
+ * batches, rank a sends its last K = (largest - smallest) / 2 live regions
+ * (capped by the transfer buffer: 8 (2n + 3) bytes per region) to rank b
+ * through tfn; the received regions join rank b's list L.  Any region of the
+ * domain stays in exactly one list, so the union of the enclosures is the
+ * enclosure of the global minimum.  rank: 0 <= rank < 1024 (this process);
+ * tbuf: device buffer of tbuf_bytes bytes (same size on every rank). */
+int ib_solve_dev_mg(int fid, int n, const double* l_dev, const double* u_dev, double eps_f, double eps_x,
+                    const ib_options* opt, void* ws, size_t ws_bytes, ib_result* res, double* surv_lo,
+                    double* surv_hi, double* surv_lb, int64_t surv_cap, void* stream, ib_exchange_fn fn,
+                    ib_transfer_fn tfn, void* user, double* xchg, int rank, double* tbuf, size_t tbuf_bytes);
 
 /* Natural interval extension of f over nbox explicit boxes (device):
  * out[2k], out[2k+1] = lower / upper bound of f over box k.  For points pass

@@ -17,7 +17,7 @@ import numpy as np
 from . import build as _build
 
 __all__ = [
-    "ib_version", "ib_last_error", "ib_num_functions", "IbOptions", "ib_solve", "ib_solve_dev", "ib_solve_dev_ex",
+    "ib_version", "ib_last_error", "ib_num_functions", "IbOptions", "ib_solve", "ib_solve_dev", "ib_solve_dev_ex", "ib_solve_dev_mg",
     "ib_eval_boxes", "ib_eval_grad", "ib_branch", "ib_search", "ib_compact_le", "ib_select", "lib", "LIB_PATH",
 ]
 
@@ -46,6 +46,7 @@ class IbResult(ctypes.Structure):
         ("status", ctypes.c_int), ("n_kernels", ctypes.c_int),
         ("t_ms", ctypes.c_double * NPROF), ("launches", _i64 * NPROF), ("units", _i64 * NPROF),
         ("radix_records", _i64), ("f_search", ctypes.c_double), ("search_rounds", _i64),
+        ("rebalanced", _i64), ("transfers", _i64),
     ]
 
 
@@ -63,6 +64,10 @@ EXPORTS = {
     "ib_solve_dev_ex": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _vp, _vp, ctypes.c_double, ctypes.c_double,
                                       ctypes.POINTER(IbOptions), _vp, ctypes.c_size_t, ctypes.POINTER(IbResult),
                                       _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "ib_solve_dev_mg": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _vp, _vp, ctypes.c_double, ctypes.c_double,
+                                      ctypes.POINTER(IbOptions), _vp, ctypes.c_size_t, ctypes.POINTER(IbResult),
+                                      _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, ctypes.c_int, _vp,
+                                      ctypes.c_size_t]),
     "ib_eval_boxes": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _i64, _vp, _vp, _i64, _vp, _vp]),
     "ib_eval_grad": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "ib_branch_workspace_size": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _i64]),
@@ -155,6 +160,8 @@ class SolveResult:
     n_kernels: int = 0
     f_search: float = float("inf")
     search_rounds: int = 0
+    rebalanced: int = 0
+    transfers: int = 0
 
 
 def _res(r: IbResult, lo=None, hi=None, lb=None) -> SolveResult:
@@ -162,10 +169,11 @@ def _res(r: IbResult, lo=None, hi=None, lb=None) -> SolveResult:
             for i, c in enumerate(PROF_CLASSES)}
     prof["list"]["radix_records"] = r.radix_records
     return SolveResult(r.f_lo, r.f_hi, r.iters, r.evals, r.n_surv, r.peak_pool, r.max_width, r.status,
-                       lo, hi, lb, prof, r.n_kernels, r.f_search, r.search_rounds)
+                       lo, hi, lb, prof, r.n_kernels, r.f_search, r.search_rounds, r.rebalanced, r.transfers)
 
 
 EXCHANGE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p)
+TRANSFER_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t)
 
 
 class Workspace:
@@ -256,6 +264,38 @@ def ib_solve_dev_ex(fid: int, l, u, exchange, eps_f: float = 1e-6, eps_x: float 
                                ws.nbytes, ctypes.byref(r), _ptr(slo), _ptr(shi), _ptr(slb), int(surv_cap),
                                _stream(stream), ctypes.cast(cb, ctypes.c_void_p), None, _ptr(xchg))
     _check(rc, "ib_solve_dev_ex")
+    k = min(r.n_surv, surv_cap)
+    return _res(r, None if slo is None else slo[:k], None if shi is None else shi[:k],
+                None if slb is None else slb[:k])
+
+
+def ib_solve_dev_mg(fid: int, l, u, exchange, transfer, rank: int, eps_f: float = 1e-6, eps_x: float = 1e-6,
+                    opts: IbOptions | None = None, surv_cap: int = 0, workspace: Workspace | None = None,
+                    tbuf_bytes: int = 64 << 20, stream=None) -> SolveResult:
+    """ib_solve_dev with the per-chunk incumbent exchange and box rebalancing.
+    ``exchange(xchg)``: replace the cuda float64 tensor of 4 elements by its
+    element-wise MIN over all ranks.  ``transfer(src, dst, tbuf, nbytes)``:
+    called on every rank; copy the first nbytes of rank src's tbuf (cuda uint8
+    tensor) to rank dst's tbuf."""
+    torch = _torch()
+    n = l.numel()
+    o = opts or IbOptions()
+    ws = workspace or Workspace(solve_workspace_bytes(fid, n, o))
+    xchg = torch.zeros(4, dtype=torch.float64, device=l.device)
+    tbuf = torch.empty(int(tbuf_bytes), dtype=torch.uint8, device=l.device)
+    cb = EXCHANGE_FN(lambda _user: exchange(xchg))
+    tcb = TRANSFER_FN(lambda _user, src, dst, _buf, nbytes: transfer(src, dst, tbuf, int(nbytes)))
+    slo = shi = slb = None
+    if surv_cap > 0:
+        slo = torch.empty((surv_cap, n), dtype=torch.float64, device=l.device)
+        shi = torch.empty_like(slo)
+        slb = torch.empty(surv_cap, dtype=torch.float64, device=l.device)
+    r = IbResult()
+    rc = lib().ib_solve_dev_mg(fid, n, _ptr(l), _ptr(u), float(eps_f), float(eps_x), ctypes.byref(o), ws.ptr(),
+                               ws.nbytes, ctypes.byref(r), _ptr(slo), _ptr(shi), _ptr(slb), int(surv_cap),
+                               _stream(stream), ctypes.cast(cb, ctypes.c_void_p), ctypes.cast(tcb, ctypes.c_void_p),
+                               None, _ptr(xchg), int(rank), _ptr(tbuf), int(tbuf_bytes))
+    _check(rc, "ib_solve_dev_mg")
     k = min(r.n_surv, surv_cap)
     return _res(r, None if slo is None else slo[:k], None if shi is None else shi[:k],
                 None if slb is None else slb[:k])

@@ -87,6 +87,69 @@ __global__ void k_set_pcount(Ctl* ctl, const uint64_t* c) {
   ctl->nhot = 0;
   ctl->compact_hint = 0;
 }
+// ---- multi-GPU rebalancing (ib_solve_dev_mg)
+// live records of L (lb <= GUB) -> xchg[2], xchg[3] = -(live * 1024 + rank),
+// live * 1024 + rank: after an element-wise MIN over ranks they hold the
+// largest and the smallest list (ties: highest / lowest rank)
+__global__ void k_count_live(Pool p, const Ctl* ctl, unsigned long long* acc) {
+  const double gub = okey_inv_d(ctl->gub_key);
+  const long cnt = (long)ctl->pcount;
+  unsigned long long c = 0;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (long)gridDim.x * blockDim.x)
+    c += p.lb[i] <= gub;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(acc, c);
+}
+__global__ void k_live_key(const unsigned long long* acc, int rank, double* xchg) {
+  const double key = (double)(*acc) * 1024.0 + (double)rank;
+  xchg[2] = -key;
+  xchg[3] = key;
+}
+// exported regions [first, first + k) of a compacted list: width and the
+// cycling index the region will be split on next (k_prep's rule, line 184)
+__global__ void k_export_meta(Pool p, long first, long k, const int32_t* sc, int d, int n, double* out_w,
+                              double* out_cyc) {
+  for (long r = (long)blockIdx.x * blockDim.x + threadIdx.x; r < k; r += (long)gridDim.x * blockDim.x) {
+    const long q = first + r;
+    const int psc = sc[p.slot[q]];
+    out_w[r] = p.w[q];
+    out_cyc[r] = (double)(p.code[q] == CODE_WHOLE ? psc : (psc + d) % n);
+  }
+}
+// received regions: archive slots from the free list, records appended to L
+__global__ void k_import(Pool p, const Ctl* ctl, const double* in_lo, const double* in_hi, const double* in_lb,
+                         const double* in_w, const double* in_cyc, long k, int n, int ld, double* alo, double* ahi,
+                         int32_t* sc, const int32_t* free_list) {
+  const unsigned long long top = ctl->free_top, base = ctl->pcount;
+  for (long r = blockIdx.x; r < k; r += gridDim.x) {
+    const int slot = free_list[top - 1 - r];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      alo[(size_t)slot * ld + i] = in_lo[(size_t)r * n + i];
+      ahi[(size_t)slot * ld + i] = in_hi[(size_t)r * n + i];
+    }
+    if (threadIdx.x == 0) {
+      sc[slot] = (int32_t)in_cyc[r];
+      p.lb[base + r] = in_lb[r];
+      p.w[base + r] = in_w[r];
+      p.slot[base + r] = slot;
+      p.code[base + r] = CODE_WHOLE;
+    }
+  }
+}
+// list changed outside an iteration: new record count, hot index rebuilt
+__global__ void k_list_changed(Ctl* ctl, long pcount, long taken_slots) {
+  // a rank that had converged or run out of regions works again on what it
+  // received (an error or the iteration limit stays final)
+  if (taken_slots > 0 && (ctl->done == 1 || ctl->done == 3)) ctl->done = 0;
+  ctl->pcount = (unsigned long long)pcount;
+  ctl->free_top -= (unsigned long long)taken_slots;
+  ctl->hot_valid = 0;
+  ctl->list_fast = 0;
+  ctl->nhot = 0;
+  ctl->compact_hint = 0;
+}
+
 __global__ void k_branch_ctl(Ctl* ctl, const double* gub, long nb, long cap) {
   unsigned long long* z = reinterpret_cast<unsigned long long*>(ctl);
   for (size_t i = 0; i < sizeof(Ctl) / 8; ++i) z[i] = 0ull;
@@ -394,12 +457,14 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
                       const double* u_host, double eps_f, double eps_x, const ib_options* opt, void* ws,
                       size_t ws_bytes, ib_result* res, double* so_lo, double* so_hi, double* so_lb,
                       int64_t surv_cap, bool host_out, cudaStream_t user_st, ib_exchange_fn xfn, void* xuser,
-                      double* xchg) {
+                      double* xchg, ib_transfer_fn tfn = nullptr, int rank = 0, double* tbuf = nullptr,
+                      size_t tbuf_bytes = 0) {
   Opts o;
   int rc = resolve_opts(fid, n, opt, 0, o);
   if (rc) return rc;
   if (!res) return fail(IB_EINVAL, "res is NULL");
   if (xfn && !xchg) return fail(IB_EINVAL, "exchange buffer is NULL");
+  if (tfn && (!xfn || !tbuf || rank < 0 || rank > 1023)) return fail(IB_EINVAL, "rebalancing needs xfn, tbuf, 0 <= rank < 1024");
   std::memset(res, 0, sizeof(*res));
   Arena A{(char*)ws, 0, ws_bytes, false};
   SolveWs w;
@@ -608,7 +673,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
     CKL(launch_apply_pending(w.ctl, o.kids, st));
     nk += 1;
     if (xfn) {
-      // multi-GPU incumbent exchange, once per chunk (<= 32 iterations): the
+      // multi-GPU incumbent exchange, once per chunk (<= 64 iterations): the
       // caller's all-reduce(MIN) runs on the caller's stream, ordered between
       // the put and the take on the solve stream by events
       CKL(launch_xchg_put(w.ctl, xchg, st));
@@ -623,12 +688,97 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
       }
       CKL(launch_xchg_take(w.ctl, xchg, st));
       nk += 2;
+      if (tfn) {
+        // list sizes under the shared incumbent, for the rebalancing
+        // decision: a second MIN exchange (GUB and flag entries unchanged)
+        CK(cudaMemsetAsync(w.cnt + 3, 0, 8, st));
+        k_count_live<<<148 * 4, 256, 0, st>>>(w.pa, w.ctl, (unsigned long long*)(w.cnt + 3));
+        k_live_key<<<1, 1, 0, st>>>((unsigned long long*)(w.cnt + 3), rank, xchg);
+        nk += 2;
+        if (st != user_st) {
+          CK(cudaEventRecord(tc.ev, st));
+          CK(cudaStreamWaitEvent(user_st, tc.ev, 0));
+        }
+        xfn(xuser);
+        if (st != user_st) {
+          CK(cudaEventRecord(tc.ev, user_st));
+          CK(cudaStreamWaitEvent(st, tc.ev, 0));
+        }
+      }
     }
+    double xh[4] = {0, 0, 0, 0};
+    if (tfn) CK(cudaMemcpyAsync(xh, xchg, sizeof xh, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&hc, w.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     pcount = hc.pcount;
     free_top = hc.free_top;
     peak = std::max(peak, pcount);
+    if (tfn && !hc.gdone) {
+      // box rebalancing (north_star): when the largest list is more than twice
+      // the smallest (+ 2 batches), its rank sends the last K of its live
+      // regions to the rank with the smallest list.  Every rank takes the same
+      // decision from the reduced values.
+      const double kmax = -xh[2], kmin = xh[3];
+      const long lmax = (long)(kmax / 1024.0), lmin = (long)(kmin / 1024.0);
+      const int donor = (int)(kmax - 1024.0 * (double)lmax), recv = (int)(kmin - 1024.0 * (double)lmin);
+      const long per = 2L * n + 3;  // doubles per region in the transfer buffer
+      long K = std::min((lmax - lmin) / 2, (long)(tbuf_bytes / (8 * (size_t)per)));
+      K = std::min(K, std::min(o.pool_cap / 8, o.arch_cap / 8));
+      if (donor != recv && lmax > 2 * lmin + 2 * o.bmax && K > 0) {
+        double* t_lo = tbuf;
+        double* t_hi = tbuf + (size_t)K * n;
+        double* t_lb = tbuf + (size_t)2 * K * n;
+        double* t_w = t_lb + K;
+        double* t_cyc = t_w + K;
+        if (rank == donor) {
+          // compact the live records (list order kept), export the last K
+          CKL(launch_partition(w.pa, (long)pcount, &w.ctl->gub_key, 64, 0ull, 0ull, nullptr, nullptr, nullptr, w.pb,
+                               w.desc, w.tile_ctr, w.cnt, st));
+          uint64_t live_c = 0;
+          CK(cudaMemcpyAsync(&live_c, w.cnt, 8, cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+          std::swap(w.pa, w.pb);
+          const long keep = (long)live_c - K;
+          if (keep < 0) return fail(IB_EINVAL, "rebalancing: %ld live records, %ld to send", (long)live_c, K);
+          Pool sub{w.pa.lb + keep, w.pa.w + keep, w.pa.slot + keep, w.pa.code + keep};
+          CKL(launch_extract(P, sub, K, w.alo, w.ahi, w.sc, t_lo, t_hi, t_lb, st));
+          k_export_meta<<<blocks_for(K), 256, 0, st>>>(w.pa, keep, K, w.sc, o.d, n, t_w, t_cyc);
+          k_list_changed<<<1, 1, 0, st>>>(w.ctl, keep, 0);
+          nk += 4;
+          pcount = (unsigned long long)keep;
+        }
+        // the caller moves K regions from the donor's tbuf to the receiver's
+        if (st != user_st) {
+          CK(cudaEventRecord(tc.ev, st));
+          CK(cudaStreamWaitEvent(user_st, tc.ev, 0));
+        }
+        tfn(xuser, donor, recv, tbuf, (size_t)(8 * per * K));
+        if (st != user_st) {
+          CK(cudaEventRecord(tc.ev, user_st));
+          CK(cudaStreamWaitEvent(st, tc.ev, 0));
+        }
+        if (rank == recv) {
+          if ((long)free_top < K + o.bmax) {
+            CKL(launch_gc(w.pa.slot, w.ctl, (long)pcount, w.mark, o.arch_cap, w.free_list, w.desc, w.tile_ctr, st));
+            CK(cudaMemcpyAsync(&hc, w.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            free_top = hc.free_top;
+            nk += 2;
+          }
+          if ((long)free_top < K + o.bmax || (long)pcount + K > o.pool_cap)
+            return fail(IB_ENOSPACE, "rebalancing: no room for %ld received regions", K);
+          k_import<<<(unsigned)std::min(K, 148L * 8), 128, 0, st>>>(w.pa, w.ctl, t_lo, t_hi, t_lb, t_w, t_cyc, K, n,
+                                                                    o.ld, w.alo, w.ahi, w.sc, w.free_list);
+          k_list_changed<<<1, 1, 0, st>>>(w.ctl, (long)pcount + K, K);
+          nk += 2;
+          pcount += (unsigned long long)K;
+          free_top -= (unsigned long long)K;
+        }
+        CK(cudaStreamSynchronize(st));
+        res->rebalanced += (rank == donor ? -K : (rank == recv ? K : 0));
+        res->transfers += 1;
+      }
+    }
     if (fused) fused_iters += (long)hc.iter - iter_prev;
     iter_prev = (long)hc.iter;
     if (hc.err) return fail(hc.err, "capacity exceeded on the device (L %ld, archive %ld)", o.pool_cap, o.arch_cap);
@@ -787,6 +937,16 @@ int ib_solve_dev_ex(int fid, int n, const double* l_dev, const double* u_dev, do
   g_err.clear();
   return solve_impl(fid, n, l_dev, u_dev, nullptr, nullptr, eps_f, eps_x, opt, ws, ws_bytes, res, surv_lo, surv_hi,
                     surv_lb, surv_cap, false, (cudaStream_t)stream, fn, user, xchg);
+}
+
+int ib_solve_dev_mg(int fid, int n, const double* l_dev, const double* u_dev, double eps_f, double eps_x,
+                    const ib_options* opt, void* ws, size_t ws_bytes, ib_result* res, double* surv_lo,
+                    double* surv_hi, double* surv_lb, int64_t surv_cap, void* stream, ib_exchange_fn fn,
+                    ib_transfer_fn tfn, void* user, double* xchg, int rank, double* tbuf, size_t tbuf_bytes) {
+  if (!l_dev || !u_dev) return fail(IB_EINVAL, "l/u NULL");
+  g_err.clear();
+  return solve_impl(fid, n, l_dev, u_dev, nullptr, nullptr, eps_f, eps_x, opt, ws, ws_bytes, res, surv_lo, surv_hi,
+                    surv_lb, surv_cap, false, (cudaStream_t)stream, fn, user, xchg, tfn, rank, tbuf, tbuf_bytes);
 }
 
 int ib_eval_boxes(int fid, int n, int64_t nbox, const double* lo, const double* hi, int64_t ld, double* out,

@@ -428,3 +428,84 @@ def test_full_size_first_iterations_match_oracle(pb, monkeypatch):
     np.testing.assert_array_equal(g.hi, o["hi"])
     np.testing.assert_allclose(g.lb, o["lb"], rtol=0, atol=t)
     assert g.lo.shape[1] == n
+
+
+def test_two_rank_rebalancing_on_one_gpu(pb):
+    """Two ranks (threads) on one GPU solve the two slabs of a domain with
+    ib_solve_dev_mg: the all-reduce and the box transfer are emulated with
+    device copies behind host barriers.  The slab without the minimiser
+    empties and receives regions from the other (rebalancing); the union of
+    the two enclosures is still the eps-enclosure of the global minimum."""
+    import threading
+
+    import torch
+
+    import bench
+
+    # Ackley n = 10 on [-32.768, 32.768]^10 (BASELINE configs[1]) cut at
+    # x_1 = 0.5: rank 0 holds the minimiser x* = 0 and its 2^9 corner regions,
+    # rank 1's slab empties under the shared incumbent and then works on
+    # regions rank 0 sends it
+    fid, n = 1, 10
+    L, U = workloads.config_bounds(workloads.CONFIGS[1])
+    l0, u0, l1, u1 = L.copy(), U.copy(), L.copy(), U.copy()
+    u0[0] = l1[0] = 0.5
+    slabs = [(l0, u0), (l1, u1)]
+    bar = threading.Barrier(2, timeout=120)
+    xs, bufs, moves, out, errs = [None, None], [None, None], [], [None, None], []
+
+    def exchange(rank):
+        def ex(x):
+            xs[rank] = x
+            bar.wait()
+            if rank == 0:
+                torch.cuda.synchronize()
+                m = torch.minimum(xs[0], xs[1])
+                xs[0].copy_(m)
+                xs[1].copy_(m)
+                torch.cuda.synchronize()
+            bar.wait()
+
+        return ex
+
+    def transfer(rank):
+        def tr(src, dst, tbuf, nbytes):
+            bufs[rank] = tbuf
+            bar.wait()
+            if rank == 0:
+                torch.cuda.synchronize()
+                bufs[dst][:nbytes].copy_(bufs[src][:nbytes])
+                torch.cuda.synchronize()
+                moves.append((src, dst, nbytes))
+            bar.wait()
+
+        return tr
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(0)
+            l, u = slabs[rank]
+            out[rank] = pb.ib_solve_dev_mg(fid, cuda(l), cuda(u), exchange(rank), transfer(rank), rank, 1e-6, 1e-6,
+                                           pb.options(d=10, m=2, bmax=64, max_iter=20000),
+                                           surv_cap=4096,
+                                           tbuf_bytes=8 << 20)
+        except Exception as e:  # surface failures of either thread
+            errs.append(repr(e))
+            bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    a, b = out
+    assert moves, "no rebalancing transfer happened"
+    assert a.transfers == b.transfers == len(moves)
+    assert a.rebalanced + b.rebalanced == 0  # every region sent was received
+    f_lo, f_hi = min(a.f_lo, b.f_lo), min(a.f_hi, b.f_hi)
+    assert f_lo <= 0.0 <= f_hi and f_hi - f_lo <= 1e-6
+    assert a.status in (0, 2) and b.status in (0, 2)
+    boxes = [(lo, hi) for r in out if r.n_surv for lo, hi in zip(r.lo.cpu().numpy(), r.hi.cpu().numpy())]
+    assert any(np.all(lo <= 0.0) and np.all(0.0 <= hi) for lo, hi in boxes)
+    assert all(np.all(hi - lo <= 1e-6) for lo, hi in boxes)

@@ -1,7 +1,9 @@
 """N > 1 host logic on CPU with torch.distributed (gloo, world size 2):
 
 * bench.slab: the per-rank slabs of the domain are an exact cover;
-* bench.exchange_fn: the per-iteration exchange of [GUB, finished flag]
+* bench.transfer_fn: the rebalancing transfer moves bytes from the donor's
+  buffer to the receiver's only (include/ibnb.h ib_transfer_fn contract);
+* bench.exchange_fn: the per-chunk exchange of [GUB, finished flag]
   is an element-wise MIN over ranks (include/ibnb.h ib_exchange_fn contract):
   GUB = the best sample of any rank, "all finished" only when every rank is;
 * partitioned search: every rank solves its slab (CPU oracle) and the
@@ -39,6 +41,11 @@ def _worker(rank, world, port, q):
     try:
         out = {}
         ex = bench.exchange_fn(dist)
+        # rebalancing transfer: rank 1 sends the first 24 bytes of its buffer to rank 0
+        tr = bench.transfer_fn(dist, rank)
+        buf = torch.arange(8, dtype=torch.uint8) + (100 if rank == 1 else 0)
+        tr(1, 0, buf, 3)
+        out["buf"] = buf.tolist()
         # exchange: rank 0 has the better incumbent and is finished, rank 1 not
         x = torch.tensor([1.5, 0.0] if rank == 0 else [2.5, -1.0], dtype=torch.float64)
         ex(x)
@@ -82,6 +89,9 @@ def test_two_rank_exchange_and_partitioned_enclosure():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    # rebalancing transfer: rank 0 received rank 1's first 3 bytes, rank 1 unchanged
+    assert res[0]["buf"] == [100, 101, 102, 3, 4, 5, 6, 7]
+    assert res[1]["buf"] == [100, 101, 102, 103, 104, 105, 106, 107]
     for r in (0, 1):
         # min GUB over ranks; not everybody finished (-1) in round 1
         assert res[r]["x1"] == [1.5, -1.0]
