@@ -619,7 +619,78 @@ __device__ __noinline__ bool child_mono_ok(const Problem& P, const double* __res
   }
 }
 
-// Pass 1: upper bound at the midpoint and lower bound of every child.
+// The first-order test of child_mono_ok with one lane per split variable
+// (called by all 32 lanes of a warp, d <= 16 lanes work): each lane repeats
+// the serial function's shared steps (child accumulators, context, and for
+// product accumulators its own left-to-right prefix and right-to-left
+// suffix) in the same order, so every per-variable enclosure is bit-identical
+// to child_mono_ok's and so is the decision.
+template <class F>
+__device__ __noinline__ bool child_mono_ok_warp(const Problem& P, const double* __restrict__ T, uint32_t code) {
+  const int d = P.d, m = P.m, n = P.n;
+  const int lane = threadIdx.x & 31;
+  const int c = (int)T[H_CHUNK];
+  bool bad = false;
+  if (lane < d) {
+    const int j = lane;
+    const int i = (c + j) % n;
+    if constexpr (F::CHAIN) {
+      int e[D_MAX];
+      entries_of(code, P, e);
+      LevyView V{T, e, d};
+      LevyChunk q = levy_chunk(c, d, n);
+      const double* ej = T + HDR + (size_t)e[j] * ENT;
+      LevyVals me;
+      me.u = get(ej + 2);
+      me.v = get(ej + 4);
+      me.s0 = get(ej + 6);
+      me.du = get(ej + 8);
+      me.sg = get(ej + 10);
+      Iv up = i > 0 ? V.u(q.local(i - 1), false) : iv(0.0);
+      Iv vn = i < n - 1 ? V.v(q.local(i + 1), false) : iv(0.0);
+      Iv D = ObjLevy::deriv(me, up, vn, i, n);
+      bad = (D.lo > 0.0 && ej[E_LO] != P.l[i]) || (D.hi < 0.0 && ej[E_HI] != P.u[i]);
+    } else if constexpr (F::SEP) {
+      bad = T[HDR + (size_t)(j * m + piece(code, j, P)) * ENT + E_T + 4 * F::K + 2 * F::KG] != 0.0;
+    } else {
+      Iv A[2];
+      child_acc<F>(P, T, code, A);
+      typename F::Ctx cx = F::ctx(A, n);
+      const double* ej = T + HDR + (size_t)(j * m + piece(code, j, P)) * ENT;
+      Iv g[2], excl[2] = {iv(0.0), iv(0.0)};
+#pragma unroll
+      for (int k = 0; k < F::KG; ++k) g[k] = get(ej + E_T + 4 * F::K + 2 * k);
+      if constexpr (F::HASPROD) {
+        Iv pre[2], suf[2];
+#pragma unroll
+        for (int k = 0; k < F::K; ++k) {
+          pre[k] = get(T + H_REST + 2 * k);
+          suf[k] = iv(1.0);
+        }
+        for (int t = 0; t < j; ++t) {  // prefix: rest * t_0 * ... * t_{j-1}
+          const double* et = T + HDR + (size_t)(t * m + piece(code, t, P)) * ENT + E_T;
+#pragma unroll
+          for (int k = 0; k < F::K; ++k)
+            if (F::kind(k) == PROD) pre[k] = pre[k] * get(et + 2 * k);
+        }
+        for (int t = d - 1; t > j; --t) {  // suffix: t_{j+1} * (... * (t_{d-1} * 1))
+          const double* et = T + HDR + (size_t)(t * m + piece(code, t, P)) * ENT + E_T;
+#pragma unroll
+          for (int k = 0; k < F::K; ++k)
+            if (F::kind(k) == PROD) suf[k] = get(et + 2 * k) * suf[k];
+        }
+#pragma unroll
+        for (int k = 0; k < F::K; ++k) excl[k] = F::kind(k) == PROD ? pre[k] * suf[k] : iv(0.0);
+      }
+      Iv X{ej[E_LO], ej[E_HI]};
+      Iv D = F::dfin(cx, g, X, i, n, excl);
+      bad = (D.lo > 0.0 && X.lo != P.l[i]) || (D.hi < 0.0 && X.hi != P.u[i]);
+    }
+  }
+  return __ballot_sync(0xffffffffu, bad) == 0u;
+}
+
+// Pass 1: upper bound at the midpoint and lower bound of every child.// Pass 1: upper bound at the midpoint and lower bound of every child.
 // A thread owns G = m^h consecutive children (all pieces of the h lowest
 // split variables): the terms of the d - h higher variables are combined
 // once per group.  Midpoint bounds are min-reduced (warp shuffle -> block ->
@@ -1019,7 +1090,9 @@ __device__ bool emit_small_dev(const Problem& P, Ctl* __restrict__ ctl, const do
   const double lb = t < np ? clb[g] : CUDART_INF;
   const bool cand = t < np && lb <= gub;
   if (t < PCAP) s_c[t] = cand;
-  __syncthreads();
+  // few candidates: first-order test with a warp per candidate (lane per
+  // split variable); many: a thread per candidate (more of them at once)
+  const bool warp_mono = __syncthreads_count(cand) <= TPB / 32;
   for (int k = t >> 5; k < np; k += TPB / 32) {
     if (!s_c[k]) continue;  // warp-uniform
     ChildIdx ci = child_of(s_g[k], P);
@@ -1032,7 +1105,9 @@ __device__ bool emit_small_dev(const Problem& P, Ctl* __restrict__ ctl, const do
       if constexpr (F::SEP) bad = e[E_T + 4 * F::K + 2 * F::KG] != 0.0;
     }
     wl = warp_max(wl);
-    const unsigned anybad = __ballot_sync(0xffffffffu, bad);
+    unsigned anybad = __ballot_sync(0xffffffffu, bad);
+    if constexpr (!F::SEP)
+      if (warp_mono) anybad = (!P.mono || child_mono_ok_warp<F>(P, T, ci.code)) ? 0u : 1u;
     if (lane == 0) {
       s_w[k] = fmax(T[H_WREST], wl);
       s_ok[k] = anybad == 0u;
@@ -1041,7 +1116,7 @@ __device__ bool emit_small_dev(const Problem& P, Ctl* __restrict__ ctl, const do
   __syncthreads();
   bool surv = false;
   if (cand) {
-    if constexpr (F::SEP) {
+    if (F::SEP || warp_mono) {
       surv = !P.mono || s_ok[t] != 0;
     } else {
       ChildIdx ci = child_of(g, P);
@@ -1206,8 +1281,10 @@ __device__ void cand_emit_dev(const Problem& P, Ctl* __restrict__ ctl, const dou
     }
     const int ncl = (int)tot1[0];
     __syncthreads();
-    // widths (+ separable first-order flags): a warp per candidate, a lane
-    // per split variable
+    // widths (+ first-order flags): a warp per candidate, a lane per split
+    // variable; with many candidates the non-separable test runs a thread
+    // per candidate instead
+    const bool warp_mono = ncl <= TPB / 32;
     for (int k = threadIdx.x >> 5; k < ncl; k += TPB / 32) {
       ChildIdx ci = child_of(s_cidx[k], P);
       const double* T = tab + (size_t)ci.b * tab_stride;
@@ -1219,7 +1296,9 @@ __device__ void cand_emit_dev(const Problem& P, Ctl* __restrict__ ctl, const dou
         if constexpr (F::SEP) bad = e[E_T + 4 * F::K + 2 * F::KG] != 0.0;
       }
       wl = warp_max(wl);
-      const unsigned anybad = __ballot_sync(0xffffffffu, bad);
+      unsigned anybad = __ballot_sync(0xffffffffu, bad);
+      if constexpr (!F::SEP)
+        if (warp_mono) anybad = (!P.mono || child_mono_ok_warp<F>(P, T, ci.code)) ? 0u : 1u;
       if (lane == 0) {
         s_w[k] = fmax(T[H_WREST], wl);
         s_ok[k] = anybad == 0u;
@@ -1232,7 +1311,7 @@ __device__ void cand_emit_dev(const Problem& P, Ctl* __restrict__ ctl, const dou
       const int k = threadIdx.x * IPT + q;
       if (k < ncl) {
         bool okq;
-        if constexpr (F::SEP) {
+        if (F::SEP || warp_mono) {
           okq = !P.mono || s_ok[k] != 0;
         } else {
           ChildIdx ci = child_of(s_cidx[k], P);
