@@ -739,16 +739,16 @@ __device__ __forceinline__ void child_eval_dev(const Problem& P, Ctl* __restrict
   const long ngroups = (long)ctl->B * gpp;
   const double gub0 = okey_inv(ctl->gub_key);  // incumbent before this iteration
   double best = CUDART_INF;
-  // bisection path: the tables of the (at most two) parents of a block's 256
-  // groups are staged in shared memory (one coalesced load instead of a
-  // dependent L2 round trip per piece)
-  constexpr int TS = GT ? HDR + 2 * D_MAX * ENT : 1;
+  // the tables of the (at most two) parents of a block's 256 groups are
+  // staged in shared memory when they fit (bisection): one coalesced load
+  // instead of a dependent L2 round trip per piece / chain term
+  constexpr int TS = HDR + 2 * D_MAX * ENT;  // bisection tables (m = 2, d <= 16)
   __shared__ double s_tab[2][TS];
   for (long base = (long)blockIdx.x * TPB; base < ngroups; base += (long)gridDim.x * TPB) {
     const long gi = base + threadIdx.x;
     const double* __restrict__ Tsh = nullptr;
     int b0 = 0;
-    if constexpr (GT != 0 && !F::CHAIN) {
+    {
       const long glast = min(base + TPB, ngroups) - 1;
       b0 = P.mbits ? (int)(base >> (P.kbits - h * P.mbits)) : (int)(base / gpp);
       const int b1 = P.mbits ? (int)(glast >> (P.kbits - h * P.mbits)) : (int)(glast / gpp);

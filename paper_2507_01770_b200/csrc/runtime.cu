@@ -267,8 +267,12 @@ static int prep_slices(int n, long bmax) {
 
 static Problem make_problem(int fid, int n, int d, int m, long kids, int ld, int mono, const double* l,
                             const double* u, long bmax) {
+  // a child-eval thread owns G = m^h children when they share work (the
+  // combination of the d - h higher pieces of K-accumulator objectives); the
+  // Levy chain (fid 6) recomputes its chain terms per child, so a thread per
+  // child spreads them over more threads
   int h = 0, G = 1;
-  while (h < d && G * m <= 8) {
+  while (fid != 6 && h < d && G * m <= 8) {
     G *= m;
     ++h;
   }
