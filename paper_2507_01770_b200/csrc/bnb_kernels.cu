@@ -260,14 +260,14 @@ __device__ __forceinline__ void prep_item(const Problem& P, const Ctl* __restric
   }
   double wmax = 0.0;
   LevyChunk q = levy_chunk(c, d, n);
-  for (int i = i0 + threadIdx.x; i < i1; i += BS) {
-    double a, bb;
-    mat(i, a, bb);
-    dlo[i] = a;
-    dhi[i] = bb;
-    if (((i - c + n) % n) >= d) {
-      wmax = fmax(wmax, __dsub_rn(bb, a));
-      if constexpr (!F::CHAIN) {
+  if constexpr (!F::CHAIN) {
+    for (int i = i0 + threadIdx.x; i < i1; i += BS) {
+      double a, bb;
+      mat(i, a, bb);
+      dlo[i] = a;
+      dhi[i] = bb;
+      if (((i - c + n) % n) >= d) {
+        wmax = fmax(wmax, __dsub_rn(bb, a));
         Iv t[2], tm[2];
         F::terms(Iv{a, bb}, i, n, t);
         double xm = midpt(a, bb);
@@ -279,28 +279,55 @@ __device__ __forceinline__ void prep_item(const Problem& P, const Ctl* __restric
         }
       }
     }
-    if constexpr (F::CHAIN) {
-      // Levy: rest = sum of chain terms that involve no split variable
-      const bool ji = q.inJ(i);
-      Iv X{a, bb};
-      double xm = midpt(a, bb);
-      LevyVals v = ObjLevy::vals(X), vm = ObjLevy::vals(Iv{xm, xm});
-      if (i == 0 && !ji) {
-        acc[0] = acc[0] + v.s0;
-        accm[0] = accm[0] + vm.s0;
+  } else {
+    // Levy: rest = sum of chain terms that involve no split variable; the
+    // values of variable i + 1 come from the neighbouring thread (shared
+    // memory), recomputed only across block boundaries
+    __shared__ Iv s_v[BS], s_vm[BS];
+    for (int base = i0; base < i1; base += BS) {  // block-uniform trip count
+      const int i = base + threadIdx.x;
+      const bool in = i < i1;
+      LevyVals v, vm;
+      if (in) {
+        double a, bb;
+        mat(i, a, bb);
+        dlo[i] = a;
+        dhi[i] = bb;
+        if (((i - c + n) % n) >= d) wmax = fmax(wmax, __dsub_rn(bb, a));
+        const double xm = midpt(a, bb);
+        v = ObjLevy::vals(Iv{a, bb});
+        vm = ObjLevy::vals(Iv{xm, xm});
+        s_v[threadIdx.x] = v.v;
+        s_vm[threadIdx.x] = vm.v;
       }
-      if (i <= n - 2 && !ji && !q.inJ(i + 1)) {
-        double a1, b1;
-        mat(i + 1, a1, b1);
-        double xm1 = midpt(a1, b1);
-        LevyVals w = ObjLevy::vals(Iv{a1, b1}), wm = ObjLevy::vals(Iv{xm1, xm1});
-        acc[0] = acc[0] + mulpos(v.u, w.v);
-        accm[0] = accm[0] + mulpos(vm.u, wm.v);
+      __syncthreads();
+      if (in) {
+        const bool ji = q.inJ(i);
+        if (i == 0 && !ji) {
+          acc[0] = acc[0] + v.s0;
+          accm[0] = accm[0] + vm.s0;
+        }
+        if (i <= n - 2 && !ji && !q.inJ(i + 1)) {
+          Iv wv, wmv;
+          if (threadIdx.x + 1 < BS && i + 1 < i1) {
+            wv = s_v[threadIdx.x + 1];
+            wmv = s_vm[threadIdx.x + 1];
+          } else {
+            double a1, b1;
+            mat(i + 1, a1, b1);
+            const double xm1 = midpt(a1, b1);
+            wv = ObjLevy::vals(Iv{a1, b1}).v;
+            wmv = ObjLevy::vals(Iv{xm1, xm1}).v;
+          }
+          acc[0] = acc[0] + mulpos(v.u, wv);
+          accm[0] = accm[0] + mulpos(vm.u, wmv);
+        }
+        if (i == n - 1 && !ji) {
+          acc[0] = acc[0] + v.u;
+          accm[0] = accm[0] + vm.u;
+        }
       }
-      if (i == n - 1 && !ji) {
-        acc[0] = acc[0] + v.u;
-        accm[0] = accm[0] + vm.u;
-      }
+      __syncthreads();
     }
   }
   block_reduce_prep<F, BS>(acc, accm, wmax);
