@@ -260,72 +260,80 @@ __device__ __forceinline__ void prep_item(const Problem& P, const Ctl* __restric
   }
   double wmax = 0.0;
   LevyChunk q = levy_chunk(c, d, n);
+  // two threads per variable: half 0 the box (and the row, the width), half 1
+  // the midpoint, so that each thread's transcendental chain is one
+  // enclosure long; block_reduce_prep combines both halves
+  constexpr int HB = BS / 2;
+  const int hv = threadIdx.x % HB, half = threadIdx.x / HB;
   if constexpr (!F::CHAIN) {
-    for (int i = i0 + threadIdx.x; i < i1; i += BS) {
+    for (int i = i0 + hv; i < i1; i += HB) {
       double a, bb;
       mat(i, a, bb);
-      dlo[i] = a;
-      dhi[i] = bb;
+      if (half == 0) {
+        dlo[i] = a;
+        dhi[i] = bb;
+      }
       if (((i - c + n) % n) >= d) {
-        wmax = fmax(wmax, __dsub_rn(bb, a));
-        Iv t[2], tm[2];
-        F::terms(Iv{a, bb}, i, n, t);
-        double xm = midpt(a, bb);
-        F::terms(Iv{xm, xm}, i, n, tm);
+        Iv t[2];
+        if (half == 0) {
+          wmax = fmax(wmax, __dsub_rn(bb, a));
+          F::terms(Iv{a, bb}, i, n, t);
+        } else {
+          const double xm = midpt(a, bb);
+          F::terms(Iv{xm, xm}, i, n, t);
+        }
 #pragma unroll
         for (int k = 0; k < F::K; ++k) {
-          acc[k] = acc_comb<F>(k, acc[k], t[k]);
-          accm[k] = acc_comb<F>(k, accm[k], tm[k]);
+          if (half == 0) acc[k] = acc_comb<F>(k, acc[k], t[k]);
+          else accm[k] = acc_comb<F>(k, accm[k], t[k]);
         }
       }
     }
   } else {
     // Levy: rest = sum of chain terms that involve no split variable; the
-    // values of variable i + 1 come from the neighbouring thread (shared
-    // memory), recomputed only across block boundaries
-    __shared__ Iv s_v[BS], s_vm[BS];
-    for (int base = i0; base < i1; base += BS) {  // block-uniform trip count
-      const int i = base + threadIdx.x;
+    // values of variable i + 1 come from the neighbouring thread of the same
+    // half (shared memory), recomputed only across block boundaries
+    __shared__ Iv s_v[BS];
+    for (int base = i0; base < i1; base += HB) {  // block-uniform trip count
+      const int i = base + hv;
       const bool in = i < i1;
-      LevyVals v, vm;
+      LevyVals v;
+      double a = 0.0, bb = 0.0;
       if (in) {
-        double a, bb;
         mat(i, a, bb);
-        dlo[i] = a;
-        dhi[i] = bb;
-        if (((i - c + n) % n) >= d) wmax = fmax(wmax, __dsub_rn(bb, a));
-        const double xm = midpt(a, bb);
-        v = ObjLevy::vals(Iv{a, bb});
-        vm = ObjLevy::vals(Iv{xm, xm});
+        if (half == 0) {
+          dlo[i] = a;
+          dhi[i] = bb;
+          if (((i - c + n) % n) >= d) wmax = fmax(wmax, __dsub_rn(bb, a));
+          v = ObjLevy::vals(Iv{a, bb});
+        } else {
+          const double xm = midpt(a, bb);
+          v = ObjLevy::vals(Iv{xm, xm});
+        }
         s_v[threadIdx.x] = v.v;
-        s_vm[threadIdx.x] = vm.v;
       }
       __syncthreads();
       if (in) {
+        Iv& r = half == 0 ? acc[0] : accm[0];
         const bool ji = q.inJ(i);
-        if (i == 0 && !ji) {
-          acc[0] = acc[0] + v.s0;
-          accm[0] = accm[0] + vm.s0;
-        }
+        if (i == 0 && !ji) r = r + v.s0;
         if (i <= n - 2 && !ji && !q.inJ(i + 1)) {
-          Iv wv, wmv;
-          if (threadIdx.x + 1 < BS && i + 1 < i1) {
+          Iv wv;
+          if (hv + 1 < HB && i + 1 < i1) {
             wv = s_v[threadIdx.x + 1];
-            wmv = s_vm[threadIdx.x + 1];
           } else {
             double a1, b1;
             mat(i + 1, a1, b1);
-            const double xm1 = midpt(a1, b1);
-            wv = ObjLevy::vals(Iv{a1, b1}).v;
-            wmv = ObjLevy::vals(Iv{xm1, xm1}).v;
+            if (half == 0) {
+              wv = ObjLevy::vals(Iv{a1, b1}).v;
+            } else {
+              const double xm1 = midpt(a1, b1);
+              wv = ObjLevy::vals(Iv{xm1, xm1}).v;
+            }
           }
-          acc[0] = acc[0] + mulpos(v.u, wv);
-          accm[0] = accm[0] + mulpos(vm.u, wmv);
+          r = r + mulpos(v.u, wv);
         }
-        if (i == n - 1 && !ji) {
-          acc[0] = acc[0] + v.u;
-          accm[0] = accm[0] + vm.u;
-        }
+        if (i == n - 1 && !ji) r = r + v.u;
       }
       __syncthreads();
     }
@@ -440,6 +448,24 @@ __device__ __forceinline__ void prep_item(const Problem& P, const Ctl* __restric
       pticket[b] = 0u;  // every slice block of b has arrived: reset for the next launch
     }
   }
+  if constexpr (F::CHAIN) {
+    // neighbour values of the chunk (box and midpoint of the left and the
+    // right neighbour variable), one thread each
+    if (threadIdx.x < 4) {
+      const int sd = threadIdx.x >> 1, mid = threadIdx.x & 1;
+      const int nbv = sd == 0 ? q.L : q.R;
+      Iv X = iv(0.0);
+      if (nbv >= 0) mat(nbv, X.lo, X.hi);
+      if (mid) {
+        const double xm = midpt(X.lo, X.hi);
+        X = Iv{xm, xm};
+      }
+      const LevyVals v = ObjLevy::vals(X);
+      double* nb_ = T + H_LEVY_NB + 8 * sd + 4 * mid;
+      put(nb_ + 0, v.u);
+      put(nb_ + 2, v.v);
+    }
+  }
   if (threadIdx.x == 0) {
     for (int k = 0; k < 2; ++k) {
       put(T + H_REST + 2 * k, acc[k]);
@@ -449,19 +475,7 @@ __device__ __forceinline__ void prep_item(const Problem& P, const Ctl* __restric
     T[H_CHUNK] = (double)c;
     dst_sc[dst] = c;
     if constexpr (F::CHAIN) {
-      // neighbour values and the list of affected chain terms
-      double* nb_ = T + H_LEVY_NB;
-      int nbv[2] = {q.L, q.R};
-      for (int sd = 0; sd < 2; ++sd) {
-        Iv X = iv(0.0);
-        if (nbv[sd] >= 0) mat(nbv[sd], X.lo, X.hi);
-        double xm = midpt(X.lo, X.hi);
-        LevyVals v = ObjLevy::vals(X), vm = ObjLevy::vals(Iv{xm, xm});
-        put(nb_ + 8 * sd + 0, v.u);
-        put(nb_ + 8 * sd + 2, v.v);
-        put(nb_ + 8 * sd + 4, vm.u);
-        put(nb_ + 8 * sd + 6, vm.v);
-      }
+      // the list of affected chain terms
       int nt = 0;
       double* td = T + H_LEVY_T;
       if (q.inJ(0)) td[nt++] = (double)(0 * 65536 + q.local(0) * 256);

@@ -261,7 +261,7 @@ static int resolve_opts(int fid, int n, const ib_options* o, int64_t pool_cap_ar
 // to fill the SMs, then slices of >= 256 variables
 static int prep_slices(int n, long bmax) {
   if (n < 512 || bmax >= 296) return 1;
-  long s = std::min((long)(n + 255) / 256, std::max(1L, 1184 / bmax));
+  long s = std::min((long)(n + 127) / 128, std::max(1L, 1184 / bmax));  // 128 variables: one per half-block thread
   return (int)std::max(1L, s);
 }
 
