@@ -509,3 +509,12 @@ def test_two_rank_rebalancing_on_one_gpu(pb):
     boxes = [(lo, hi) for r in out if r.n_surv for lo, hi in zip(r.lo.cpu().numpy(), r.hi.cpu().numpy())]
     assert any(np.all(lo <= 0.0) and np.all(0.0 <= hi) for lo, hi in boxes)
     assert all(np.all(hi - lo <= 1e-6) for lo, hi in boxes)
+
+
+@pytest.mark.parametrize("fid,m", [(7, 3), (1, 3), (5, 4), (6, 3), (10, 4)])
+def test_non_bisection_partitions_match_oracle(pb, fid, m):
+    """m = 3 and m = 4 pieces per split variable (Eq. (10)-(11) generalised,
+    runtime-G child groups, fused kernel) against the oracle, search on."""
+    l, u = workloads.bounds(fid, 3)
+    g, o = _solve_parity(pb, fid, l, u, 1e-6, 1e-5, 3, m, 64, 4000, search=32)
+    assert g.status == 0
