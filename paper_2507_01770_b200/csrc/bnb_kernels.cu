@@ -200,7 +200,43 @@ __device__ __forceinline__ void block_reduce_prep(Iv* acc, Iv* accm, double& wma
   }
 }
 
-// ====================================================================== prep// ====================================================================== prep
+// the S slice partials of parent b combined in a fixed tree order
+// (deterministic; results valid in thread 0)
+template <class F, int BS>
+__device__ __forceinline__ void combine_partials(const double* __restrict__ ppart, int b, int S, Iv* acc, Iv* accm,
+                                                 double& wmax) {
+  const double* pp = ppart + (size_t)b * S * 10;
+  Iv ra[2], rm[2];
+  double rw = 0.0;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) ra[k] = rm[k] = iv(0.0);
+  if constexpr (!F::CHAIN) {
+#pragma unroll
+    for (int k = 0; k < F::K; ++k) ra[k] = rm[k] = acc_ident<F>(k);
+  }
+  for (int t = threadIdx.x; t < S; t += BS) {
+    const double* pt = pp + (size_t)t * 10;
+    if constexpr (F::CHAIN) {
+      ra[0] = ra[0] + get(pt);
+      rm[0] = rm[0] + get(pt + 4);
+    } else {
+#pragma unroll
+      for (int k = 0; k < F::K; ++k) {
+        ra[k] = acc_comb<F>(k, ra[k], get(pt + 2 * k));
+        rm[k] = acc_comb<F>(k, rm[k], get(pt + 4 + 2 * k));
+      }
+    }
+    rw = fmax(rw, pt[8]);
+  }
+  block_reduce_prep<F, BS>(ra, rm, rw);
+  for (int k = 0; k < 2; ++k) {
+    acc[k] = ra[k];
+    accm[k] = rm[k];
+  }
+  wmax = rw;
+}
+
+// ====================================================================== prep// ====================================================================== prep// ====================================================================== prep
 // Parent b of the batch is handled by P.pslices blocks (one block when the
 // batch is large; for large n and small batches the n variables are cut into
 // slices so that the O(n) reduction spreads over the SMs).  Block (b, s):
@@ -394,7 +430,19 @@ __device__ __forceinline__ void prep_item(const Problem& P, const Ctl* __restric
       }
     }
   }
-  if (S > 1) {
+  if (S > 1 && P.prest) {
+    // publish this slice's partial; the child phase combines them (the next
+    // grid barrier / kernel boundary orders it); slice 0 writes the header
+    if (threadIdx.x == 0) {
+      double* pp = ppart + ((size_t)b * S + s) * 10;
+      for (int k = 0; k < 2; ++k) {
+        put(pp + 2 * k, acc[k]);
+        put(pp + 4 + 2 * k, accm[k]);
+      }
+      pp[8] = wmax;
+    }
+    if (s != 0) return;
+  } else if (S > 1) {
     // publish this slice's partial; the last slice block of parent b goes on
     // (the rows and tables of this block are read only after the next grid
     // barrier or kernel boundary; only the partial must precede the ticket)
@@ -412,38 +460,7 @@ __device__ __forceinline__ void prep_item(const Problem& P, const Ctl* __restric
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    {
-      // combine the S partials in a fixed tree order (deterministic)
-      const double* pp = ppart + (size_t)b * S * 10;
-      Iv ra[2], rm[2];
-      double rw = 0.0;
-#pragma unroll
-      for (int k = 0; k < 2; ++k) ra[k] = rm[k] = iv(0.0);
-      if constexpr (!F::CHAIN) {
-#pragma unroll
-        for (int k = 0; k < F::K; ++k) ra[k] = rm[k] = acc_ident<F>(k);
-      }
-      for (int t = threadIdx.x; t < S; t += BS) {
-        const double* pt = pp + (size_t)t * 10;
-        if constexpr (F::CHAIN) {
-          ra[0] = ra[0] + get(pt);
-          rm[0] = rm[0] + get(pt + 4);
-        } else {
-#pragma unroll
-          for (int k = 0; k < F::K; ++k) {
-            ra[k] = acc_comb<F>(k, ra[k], get(pt + 2 * k));
-            rm[k] = acc_comb<F>(k, rm[k], get(pt + 4 + 2 * k));
-          }
-        }
-        rw = fmax(rw, pt[8]);
-      }
-      block_reduce_prep<F, BS>(ra, rm, rw);
-      for (int k = 0; k < 2; ++k) {
-        acc[k] = ra[k];
-        accm[k] = rm[k];
-      }
-      wmax = rw;
-    }
+    combine_partials<F, BS>(ppart, b, S, acc, accm, wmax);
     if (threadIdx.x == 0) {
       pticket[b] = 0u;  // every slice block of b has arrived: reset for the next launch
     }
@@ -467,11 +484,13 @@ __device__ __forceinline__ void prep_item(const Problem& P, const Ctl* __restric
     }
   }
   if (threadIdx.x == 0) {
-    for (int k = 0; k < 2; ++k) {
-      put(T + H_REST + 2 * k, acc[k]);
-      put(T + H_RESTM + 2 * k, accm[k]);
+    if (!(S > 1 && P.prest)) {
+      for (int k = 0; k < 2; ++k) {
+        put(T + H_REST + 2 * k, acc[k]);
+        put(T + H_RESTM + 2 * k, accm[k]);
+      }
+      T[H_WREST] = wmax;
     }
-    T[H_WREST] = wmax;
     T[H_CHUNK] = (double)c;
     dst_sc[dst] = c;
     if constexpr (F::CHAIN) {
@@ -759,7 +778,7 @@ __device__ __forceinline__ void child_eval_dev(const Problem& P, Ctl* __restrict
                                                const double* __restrict__ tab, int tab_stride,
                                                double* __restrict__ clb, uint64_t* zero_a, uint64_t* zero_b,
                                                long nzero, uint32_t* zero_ctr, unsigned int* zero_hist,
-                                               uint32_t* pot = nullptr) {
+                                               uint32_t* pot = nullptr, const double* __restrict__ ppart = nullptr) {
   if (ctl->done) return;
   if (zero_a) {  // descriptors and tickets of the following k_cand / k_emit,
                  // histograms and accumulators of the next k_list
@@ -798,6 +817,27 @@ __device__ __forceinline__ void child_eval_dev(const Problem& P, Ctl* __restrict
         const int nb = b1 - b0 + 1;
         for (int t = threadIdx.x; t < nb * tab_stride; t += TPB)
           s_tab[t / tab_stride][t % tab_stride] = tab[(size_t)b0 * tab_stride + t];
+        if (P.prest) {
+          // rest accumulators of the parents from k_prep's slice partials;
+          // also written to the global tables for the insertion pass (every
+          // block writes the same bits)
+          for (int j = 0; j < nb; ++j) {
+            Iv ra[2], rm[2];
+            double rw;
+            combine_partials<F, TPB>(ppart, b0 + j, P.pslices, ra, rm, rw);
+            if (threadIdx.x == 0) {
+              double* Tg = const_cast<double*>(tab) + (size_t)(b0 + j) * tab_stride;
+              for (int k = 0; k < 2; ++k) {
+                put(&s_tab[j][H_REST + 2 * k], ra[k]);
+                put(&s_tab[j][H_RESTM + 2 * k], rm[k]);
+                put(Tg + H_REST + 2 * k, ra[k]);
+                put(Tg + H_RESTM + 2 * k, rm[k]);
+              }
+              s_tab[j][H_WREST] = rw;
+              Tg[H_WREST] = rw;
+            }
+          }
+        }
         __syncthreads();
         Tsh = &s_tab[0][0];
       }
@@ -895,8 +935,8 @@ __global__ void __launch_bounds__(TPB, 4) k_child_eval(Problem P, Ctl* __restric
                                                                const double* __restrict__ tab, int tab_stride,
                                                                double* __restrict__ clb, uint64_t* zero_a,
                                                                uint64_t* zero_b, long nzero, uint32_t* zero_ctr,
-                                                               unsigned int* zero_hist) {
-  child_eval_dev<F, GT>(P, ctl, tab, tab_stride, clb, zero_a, zero_b, nzero, zero_ctr, zero_hist);
+                                                               unsigned int* zero_hist, const double* ppart) {
+  child_eval_dev<F, GT>(P, ctl, tab, tab_stride, clb, zero_a, zero_b, nzero, zero_ctr, zero_hist, nullptr, ppart);
 }
 
 // Pass 2a: stable compaction of the candidates (children with lb <= GUB,
@@ -2607,7 +2647,8 @@ __global__ void __launch_bounds__(TPB, 1) k_fused(Problem P, IterBufs w, int ite
     grid.sync();
     if (tw) tb = gtimer();
     mark(1);
-    child_eval_dev<F, GT>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.desc, w.desc2, nz, w.tile_ctr, w.hist, w.pot);
+    child_eval_dev<F, GT>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.desc, w.desc2, nz, w.tile_ctr, w.hist, w.pot,
+                          w.ppart);
     work(2);
     grid.sync();
     if (tw) tb = gtimer();
@@ -2698,9 +2739,11 @@ static void launch_eval_t(const Problem& P, const IterBufs& w, long nkids, cudaS
   uint64_t* zb = zero ? w.desc2 : nullptr;
   long nz = tiles_for(nkids) + 1;
   if (P.m == 2 && P.G == 8 && !F::CHAIN)
-    k_child_eval<F, 8><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr, w.hist);
+    k_child_eval<F, 8><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr, w.hist,
+                                           w.ppart);
   else
-    k_child_eval<F, 0><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr, w.hist);
+    k_child_eval<F, 0><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr, w.hist,
+                                           w.ppart);
 }
 
 // k_list blocks for ~hint records: a power of two in [8, g_max]

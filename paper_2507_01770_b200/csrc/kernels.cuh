@@ -108,6 +108,8 @@ struct Problem {
   int ld;                  // archive row stride (doubles)
   int mono;                // apply the first-order test
   int pslices;             // k_prep blocks per parent (variable slices)
+  int prest;               // 1: the rest accumulators are combined from the slice partials by the child phase
+  int pad0;
   const double* l;         // device copies of the bounds
   const double* u;
 };

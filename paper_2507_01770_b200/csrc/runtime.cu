@@ -277,7 +277,11 @@ static Problem make_problem(int fid, int n, int d, int m, long kids, int ld, int
     ++h;
   }
   int mbits = (m & (m - 1)) == 0 ? __builtin_ctz((unsigned)m) : 0;
-  return Problem{fid, n, d, m, (int)kids, h, G, mbits, mbits * d, ld, mono, prep_slices(n, bmax), l, u};
+  const int ps = prep_slices(n, bmax);
+  // the child phase combines the slice partials when every block of it sees
+  // at most two parents and their tables fit its shared memory (bisection)
+  const int prest = ps > 1 && m == 2 && d <= D_MAX && kids / G >= TPB;
+  return Problem{fid, n, d, m, (int)kids, h, G, mbits, mbits * d, ld, mono, ps, prest, 0, l, u};
 }
 
 static long tiles_of(long n) { return std::max(1L, (n + TILE - 1) / TILE); }
