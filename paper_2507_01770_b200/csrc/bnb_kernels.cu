@@ -1174,7 +1174,7 @@ __device__ bool emit_small_dev(const Problem& P, Ctl* __restrict__ ctl, const do
   // few candidates: first-order test with a warp per candidate (lane per
   // split variable); many: a thread per candidate (more of them at once)
   const bool warp_mono = __syncthreads_count(cand) <= TPB / 32;
-  for (int k = t >> 5; k < np; k += TPB / 32) {
+  for (int k = t >> 5; warp_mono && k < np; k += TPB / 32) {
     if (!s_c[k]) continue;  // warp-uniform
     ChildIdx ci = child_of(s_g[k], P);
     const double* T = tab + (size_t)ci.b * tab_stride;
@@ -1197,11 +1197,13 @@ __device__ bool emit_small_dev(const Problem& P, Ctl* __restrict__ ctl, const do
   __syncthreads();
   bool surv = false;
   if (cand) {
-    if (F::SEP || warp_mono) {
+    if (warp_mono) {
       surv = !P.mono || s_ok[t] != 0;
-    } else {
+    } else {  // many candidates: a thread per candidate
       ChildIdx ci = child_of(g, P);
-      surv = !P.mono || child_mono_ok<F>(P, tab + (size_t)ci.b * tab_stride, ci.code);
+      const double* T = tab + (size_t)ci.b * tab_stride;
+      s_w[t] = child_width(P, T, ci.code);
+      surv = !P.mono || child_mono_ok<F>(P, T, ci.code);
     }
   }
   const bool hotf = surv && hot0 && okey(lb) < tau;
@@ -1366,7 +1368,7 @@ __device__ void cand_emit_dev(const Problem& P, Ctl* __restrict__ ctl, const dou
     // variable; with many candidates the non-separable test runs a thread
     // per candidate instead
     const bool warp_mono = ncl <= TPB / 32;
-    for (int k = threadIdx.x >> 5; k < ncl; k += TPB / 32) {
+    for (int k = threadIdx.x >> 5; warp_mono && k < ncl; k += TPB / 32) {
       ChildIdx ci = child_of(s_cidx[k], P);
       const double* T = tab + (size_t)ci.b * tab_stride;
       double wl = 0.0;
@@ -1392,11 +1394,13 @@ __device__ void cand_emit_dev(const Problem& P, Ctl* __restrict__ ctl, const dou
       const int k = threadIdx.x * IPT + q;
       if (k < ncl) {
         bool okq;
-        if (F::SEP || warp_mono) {
+        if (warp_mono) {
           okq = !P.mono || s_ok[k] != 0;
-        } else {
+        } else {  // many candidates: a thread per candidate
           ChildIdx ci = child_of(s_cidx[k], P);
-          okq = !P.mono || child_mono_ok<F>(P, tab + (size_t)ci.b * tab_stride, ci.code);
+          const double* T = tab + (size_t)ci.b * tab_stride;
+          s_w[k] = child_width(P, T, ci.code);
+          okq = !P.mono || child_mono_ok<F>(P, T, ci.code);
         }
         if (okq) {
           f |= 1u << q;
