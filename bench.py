@@ -193,7 +193,7 @@ def cpu_baseline(cfg, seconds=12.0):
 
     fid, n = cfg["fid"], cfg["n"]
     l, u = workloads.config_bounds(cfg)
-    d = min(n, 10)
+    d = min(n, 10 if n <= 1000 else 8)  # a bounded CPU sample: m^d children of O(n) each
     kids = 2 ** d
     parents = [(l, u)]
     for c in range(0, kids, max(1, kids // 64)):
@@ -221,7 +221,7 @@ def reference_arm(args, cfg):
 
     fid, n = cfg["fid"], cfg["n"]
     l, u = workloads.config_bounds(cfg)
-    d = min(n, 10)
+    d = min(n, 10 if n <= 1000 else 8)  # a bounded CPU sample: m^d children of O(n) each
     kids = 2 ** d
     parent = (l, u)
 
