@@ -262,6 +262,8 @@ def main():
     ap.add_argument("--d", type=int, default=0, help="variables split per iteration [min(n, 16)]")
     ap.add_argument("--no-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the configs[1] throughput-regime measurement")
+    ap.add_argument("--no-all-functions", action="store_true",
+                    help="skip the time to enclose of all ten paper functions at n = 10,000")
     ap.add_argument("--mode", default="replicas", choices=["replicas", "partition"],
                     help="N > 1: independent solves per GPU (replicas) or one domain partitioned into slabs along x_1 "
                          "with the incumbent all-reduced (MIN) every chunk of iterations")
@@ -435,6 +437,29 @@ def main():
                      "kernel_roofline": {c: roofline({c: v}, pms, c1["fid"]) for c, v in pr1.items()}}
         del ws1
 
+    # ---- north_star target: every paper function at n = 10,000 on its own
+    # domain (BASELINE configs[4]), time to enclose per function (one warm-up
+    # solve, one timed solve each, CUDA events)
+    all_ten = None
+    if rank == 0 and world == 1 and args.config == 4 and not args.no_all_functions:
+        all_ten = {}
+        for f10 in range(1, 11):
+            l10, u10 = workloads.bounds(f10, 10_000)
+            ld10, ud10 = torch.tensor(l10, device=dev), torch.tensor(u10, device=dev)
+            o10 = pb.options(d=16, m=args.m)
+            ws10 = pb.Workspace(pb.solve_workspace_bytes(f10, 10_000, o10), device=dev)
+            pb.ib_solve_dev(f10, ld10, ud10, 1e-6, 1e-6, o10, workspace=ws10)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r10 = pb.ib_solve_dev(f10, ld10, ud10, 1e-6, 1e-6, o10, workspace=ws10)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            all_ten[workloads.NAMES[f10]] = {"s": e0.elapsed_time(e1) / 1e3, "enclosure": [r10.f_lo, r10.f_hi],
+                                              "iters": r10.iters, "status": r10.status}
+            del ws10
+
     base = None
     if rank == 0 and world == 1 and not args.no_baseline:
         try:
@@ -466,6 +491,7 @@ def main():
             "profiled_ms_per_step": prof_ms / len(pres),
             "cpu_baseline": base,
             "throughput_regime": secondary,
+            "time_to_enclose_all_ten_n10000": all_ten,
             "e2e": e2e,
             "clocks": clocks,
             "gpu_launches": int(sum(r.n_kernels for r in res)),
