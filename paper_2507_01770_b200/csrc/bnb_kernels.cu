@@ -2742,12 +2742,15 @@ static void launch_eval_t(const Problem& P, const IterBufs& w, long nkids, cudaS
   uint64_t* za = zero ? w.desc : nullptr;
   uint64_t* zb = zero ? w.desc2 : nullptr;
   long nz = tiles_for(nkids) + 1;
-  if (P.m == 2 && P.G == 8 && !F::CHAIN)
-    k_child_eval<F, 8><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr, w.hist,
-                                           w.ppart);
-  else
-    k_child_eval<F, 0><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr, w.hist,
-                                           w.ppart);
+  if constexpr (!F::CHAIN) {  // the Levy chain never takes the G = 8 path
+    if (P.m == 2 && P.G == 8) {
+      k_child_eval<F, 8><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr, w.hist,
+                                             w.ppart);
+      return;
+    }
+  }
+  k_child_eval<F, 0><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr, w.hist,
+                                         w.ppart);
 }
 
 // k_list blocks for ~hint records: a power of two in [8, g_max]
@@ -2825,10 +2828,14 @@ int launch_fused(const Problem& P, const IterBufs& w, int iters, long bmax, cuda
   if (const char* e = std::getenv("IBNB_FUSE_GRID")) grid = (unsigned)std::max(1, std::min(atoi(e), sms));
   cudaError_t e = cudaSuccess;
   IB_DISPATCH_FID(P.fid, {
-    if (P.m == 2 && P.G == 8 && !F::CHAIN)
-      e = coop_launch(k_fused<F, 8>, grid, st, P, w, iters, nz);
-    else
-      e = coop_launch(k_fused<F, 0>, grid, st, P, w, iters, nz);
+    bool done = false;
+    if constexpr (!F::CHAIN) {  // the Levy chain never takes the G = 8 path
+      if (P.m == 2 && P.G == 8) {
+        e = coop_launch(k_fused<F, 8>, grid, st, P, w, iters, nz);
+        done = true;
+      }
+    }
+    if (!done) e = coop_launch(k_fused<F, 0>, grid, st, P, w, iters, nz);
   });
   return (int)e;
 }
