@@ -2406,10 +2406,13 @@ __global__ void __launch_bounds__(TPB) k_partition(Pool in, long cnt, const unsi
 }
 
 // ---- archive slot garbage collection (mark from L, collect the unmarked)
-__global__ void k_gc_mark(const int32_t* slot, const Ctl* ctl, uint8_t* mark) {
+// slots still needed: those of the live records (lb <= GUB); selected and
+// ruled-out records (lazy deletion) are never read again
+__global__ void k_gc_mark(Pool p, const Ctl* ctl, uint8_t* mark) {
   const long cnt = (long)ctl->pcount;
+  const double gub = okey_inv(ctl->gub_key);
   for (long r = (long)blockIdx.x * blockDim.x + threadIdx.x; r < cnt; r += (long)gridDim.x * blockDim.x)
-    mark[slot[r]] = 1;
+    if (p.lb[r] <= gub) mark[p.slot[r]] = 1;
 }
 __global__ void __launch_bounds__(TPB) k_gc_collect(const uint8_t* mark, long cap, int32_t* free_list,
                                                     uint64_t* desc, uint32_t* tile_ctr, Ctl* ctl, long ntiles) {
@@ -2891,10 +2894,10 @@ int launch_partition(Pool in, long cnt, const unsigned long long* gub_key, int k
   LAUNCH_OK;
 }
 
-int launch_gc(const int32_t* pool_slot, Ctl* ctl, long pool_bound, uint8_t* mark, long cap, int32_t* free_list,
-              uint64_t* desc, uint32_t* tile_ctr, cudaStream_t st) {
+int launch_gc(Pool pool, Ctl* ctl, long pool_bound, uint8_t* mark, long cap, int32_t* free_list, uint64_t* desc,
+              uint32_t* tile_ctr, cudaStream_t st) {
   cudaMemsetAsync(mark, 0, (size_t)cap, st);
-  k_gc_mark<<<grid_for(pool_bound, TPB, 148u * 8u), TPB, 0, st>>>(pool_slot, ctl, mark);
+  k_gc_mark<<<grid_for(pool_bound, TPB, 148u * 8u), TPB, 0, st>>>(pool, ctl, mark);
   long ntiles = tiles_for(cap);
   cudaMemsetAsync(desc, 0, sizeof(uint64_t) * (size_t)ntiles, st);
   cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t), st);

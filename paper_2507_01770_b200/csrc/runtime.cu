@@ -35,7 +35,7 @@ int launch_final_width(Pool, Ctl*, long, cudaStream_t);
 int launch_xchg_take(Ctl*, const double*, cudaStream_t);
 int launch_partition(Pool, long, const unsigned long long*, int, unsigned long long, unsigned long long, int32_t*,
                      uint32_t*, double*, Pool, uint64_t*, uint32_t*, uint64_t*, cudaStream_t);
-int launch_gc(const int32_t*, Ctl*, long, uint8_t*, long, int32_t*, uint64_t*, uint32_t*, cudaStream_t);
+int launch_gc(Pool, Ctl*, long, uint8_t*, long, int32_t*, uint64_t*, uint32_t*, cudaStream_t);
 int launch_compact_le(const double*, long, double, int64_t*, uint64_t*, uint32_t*, uint64_t*, cudaStream_t);
 int launch_extract(const Problem&, Pool, long, const double*, const double*, const int32_t*, double*, double*,
                    double*, cudaStream_t);
@@ -633,7 +633,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
       chunk = std::max(1L, std::min(chunk, (o.pool_cap - (long)pcount) / per_it));
     }
     if ((long)free_top < chunk * o.bmax) {
-      CKL(launch_gc(w.pa.slot, w.ctl, (long)pcount, w.mark, o.arch_cap, w.free_list, w.desc, w.tile_ctr, st));
+      CKL(launch_gc(w.pa, w.ctl, (long)pcount, w.mark, o.arch_cap, w.free_list, w.desc, w.tile_ctr, st));
       nk += 2;
       CK(cudaMemcpyAsync(&hc, w.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
@@ -767,7 +767,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
         }
         if (rank == recv) {
           if ((long)free_top < K + o.bmax) {
-            CKL(launch_gc(w.pa.slot, w.ctl, (long)pcount, w.mark, o.arch_cap, w.free_list, w.desc, w.tile_ctr, st));
+            CKL(launch_gc(w.pa, w.ctl, (long)pcount, w.mark, o.arch_cap, w.free_list, w.desc, w.tile_ctr, st));
             CK(cudaMemcpyAsync(&hc, w.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             free_top = hc.free_top;

@@ -518,3 +518,18 @@ def test_non_bisection_partitions_match_oracle(pb, fid, m):
     l, u = workloads.bounds(fid, 3)
     g, o = _solve_parity(pb, fid, l, u, 1e-6, 1e-5, 3, m, 64, 4000, search=32)
     assert g.status == 0
+
+
+def test_archive_slots_are_reused(pb):
+    """A deep dive longer than the archive (64 slots, 1,500 iterations): the
+    garbage collection frees the slots of selected and ruled-out records, and
+    the solve equals the one with the default archive bit for bit."""
+    n = 1000
+    l, u = workloads.bounds(7, n)
+    a = pb.ib_solve(7, l, u, 1e-6, 1e-6, pb.options(d=16, bmax=4), surv_cap=16)
+    b = pb.ib_solve(7, l, u, 1e-6, 1e-6, pb.options(d=16, bmax=4, arch_cap=64), surv_cap=16)
+    assert a.status == b.status == 0 and a.iters > 64
+    assert (a.iters, a.evals, a.n_surv) == (b.iters, b.evals, b.n_surv)
+    assert a.f_lo == b.f_lo and a.f_hi == b.f_hi
+    np.testing.assert_array_equal(a.lo, b.lo)
+    np.testing.assert_array_equal(a.hi, b.hi)
