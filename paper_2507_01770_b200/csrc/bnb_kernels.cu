@@ -1,21 +1,27 @@
 // bnb_kernels.cu -- the CUDA kernels of one branch-and-bound iteration
 // (§3.1 flowchart, §3.2 partition / variable cycling) and of the
 // explicit-batch evaluators.  Host launchers at the bottom are called by
-// runtime.cu; nothing here knows about torch.
-//
-//   k_prep      : materialise the selected boxes (SPSD, Eq. 8-11), reduce
-//                 the per-variable terms of the unsplit variables (block-
-//                 cooperative interval sums/products, coalesced FP64 loads)
-//                 and tabulate the terms of the m pieces of the d split
-//                 variables
-//   k_child_ub  : midpoint sample of every child -> warp-shuffle min ->
-//                 ordered-int atomicMin on the incumbent GUB (line 134)
-//   k_child_lb  : lower bound + first-order test of every child, pruning
-//                 (lines 140-144) and stable decoupled-look-back compaction
-//                 of the survivors into the list L (line 146)
-//   k_pool_*    : statistics, radix-select histogram and 3-way partition of
-//                 L (select the B smallest lower bounds, line 130; drop
-//                 lb > GUB, line 136)
+// runtime.cu; nothing here knows about torch.  Every phase is a device
+// function so that the multi-kernel path and the persistent k_fused run the
+// same code:
+//   k_list / list_dev   : iteration end, statistics of the hot index of L,
+//                         stop test (lines 148-150), batch size, radix select
+//                         and selection of the B smallest lower bounds
+//                         (line 130; lazy deletion, lines 136); list_small_dev
+//                         is the one-block variant
+//   k_prep / prep_item  : materialise the selected regions (Eq. 8-11), reduce
+//                         the terms of the unsplit variables over slices of
+//                         the variables (two threads per variable), tabulate
+//                         the pieces of the d split variables
+//   k_child_eval        : lower bound and midpoint upper bound of every child
+//                         (line 134: warp min -> ordered-int atomicMin on GUB)
+//   k_cand, k_mono,     : candidates (lb <= GUB, line 140), first-order test
+//   k_emit                (lines 142-144), stable decoupled-look-back
+//                         insertion of the survivors into L (line 146)
+//   k_fused             : whole iterations in one cooperative launch (small
+//                         batches), with the one-block insertion + selection
+//   k_partition, k_gc_* : compaction of L, archive slot collection
+//   k_eval_boxes/_grad  : explicit-batch evaluators (parity tests)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
