@@ -857,9 +857,23 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   const long ncopy = std::min((long)surv_cap, live);
   if (so_lo && so_hi && ncopy > 0) {
     if (host_out) {
-      // stage through the (unused) child-bound buffer, in chunks
-      long per = std::max(1L, (long)(((size_t)o.bmax * o.kids) / (size_t)(2 * n + 1)));
+      // stage through the (unused) child-bound buffer, in chunks; when it
+      // cannot hold one region (very large n, small batches) a staging buffer
+      // is allocated for the copy
+      const size_t need1 = 2 * (size_t)n + 1, cap_d = (size_t)o.bmax * o.kids;
       double* tlo = w.clb;
+      size_t stage_d = cap_d;
+      struct Owned {
+        double* p = nullptr;
+        cudaStream_t s;
+        ~Owned() { if (p) cudaFreeAsync(p, s); }
+      } owned{nullptr, st};
+      if (cap_d < need1) {
+        stage_d = need1 * (size_t)std::min(ncopy, 16L);
+        CK(cudaMallocAsync((void**)&owned.p, sizeof(double) * stage_d, st));
+        tlo = owned.p;
+      }
+      const long per = std::max(1L, (long)(stage_d / need1));
       for (long s = 0; s < ncopy; s += per) {
         long k = std::min(per, ncopy - s);
         double* thi = tlo + (size_t)k * n;

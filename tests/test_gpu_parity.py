@@ -533,3 +533,18 @@ def test_archive_slots_are_reused(pb):
     assert a.f_lo == b.f_lo and a.f_hi == b.f_hi
     np.testing.assert_array_equal(a.lo, b.lo)
     np.testing.assert_array_equal(a.hi, b.hi)
+
+
+def test_host_output_of_large_regions(pb):
+    """ib_solve (host buffers) returns regions larger than its staging buffer
+    (n = 40,000 with 4 children per iteration): the same regions as the
+    device-output path."""
+    n = 40_000
+    l, u = workloads.bounds(7, n)
+    o = pb.options(d=2, m=2, bmax=1, max_iter=3, search=-1)
+    h = pb.ib_solve(7, l, u, 1e-6, 1e-6, o, surv_cap=8)
+    g = pb.ib_solve_dev(7, cuda(l), cuda(u), 1e-6, 1e-6, o, surv_cap=8)
+    assert h.n_surv == g.n_surv and h.n_surv > 0
+    np.testing.assert_array_equal(h.lo, g.lo.cpu().numpy())
+    np.testing.assert_array_equal(h.hi, g.hi.cpu().numpy())
+    np.testing.assert_array_equal(h.lb, g.lb.cpu().numpy())
