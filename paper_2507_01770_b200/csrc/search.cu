@@ -557,9 +557,10 @@ int search_grid(int n) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // one warp per variable in phase B, at most one resident block per SM
-  int want = (n + S_TPB / 32 - 1) / (S_TPB / 32);
-  return std::max(1, std::min(std::min(want, sms), search_grid_max()));
+  // one block per SM: the diagonal stage has 2^14 + 1 candidates whatever n
+  // is (warp per candidate); phase B wants a warp per variable
+  (void)n;
+  return std::max(1, std::min(sms, search_grid_max()));
 }
 
 // run the search (rounds = round limit, 0 = evaluate the midpoint only)
