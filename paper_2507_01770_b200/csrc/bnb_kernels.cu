@@ -2314,6 +2314,10 @@ __device__ __noinline__ void list_dev(const Pool& p, Ctl* ctl, unsigned int* his
 __global__ void __launch_bounds__(TPB) k_list(Pool p, Ctl* ctl, unsigned int* hists, int32_t* sel_slot,
                                               uint32_t* sel_code, uint64_t* desc, uint64_t* desc2, uint32_t* tile_ctr,
                                               uint32_t* hot0, uint32_t* hot1, long kids) {
+  if (ctl->list_fast) {  // uniform: set by the previous insertion (emit)
+    if (blockIdx.x == 0) list_small_dev(p, ctl, hot0, hot1, sel_slot, sel_code, kids);
+    return;
+  }
   list_dev(p, ctl, hists, sel_slot, sel_code, desc, desc2, tile_ctr, hot0, hot1, kids);
 }
 
