@@ -73,7 +73,7 @@ typedef struct {
                          see ib_search) [32]; -1 = no search */
     int reserved;     /* must be 0 */
     int64_t bmax;     /* regions selected per iteration (smallest lower bounds,
-                         line 130, batched) [max(1, 2^22 / m^d)] */
+                         line 130, batched) [max(1, min(2^22 / m^d, 2^17 / n))] */
     int64_t max_iter; /* iteration limit [1,000,000] */
     int64_t pool_cap; /* capacity of the list L in records [derived from workspace] */
     int64_t arch_cap; /* capacity of the archive of selected regions [derived] */
@@ -83,7 +83,10 @@ typedef struct {
     double f_lo;      /* GLB: rigorous lower bound of the global minimum */
     double f_hi;      /* GUB: rigorous upper bound of the global minimum */
     int64_t iters;    /* iterations executed */
-    int64_t evals;    /* child boxes evaluated (lower bound + midpoint sample) */
+    int64_t evals;    /* child boxes whose lower bound was evaluated (B * m^d per
+                         iteration); the midpoint upper bound is only evaluated
+                         for children with lower bound <= the incumbent at the
+                         iteration start (any other cannot lower GUB) */
     int64_t n_surv;   /* regions left in L (all of them enclose no better point) */
     int64_t peak_pool;/* largest size of L seen */
     double max_width; /* widest remaining region (max over variables) */
@@ -108,7 +111,8 @@ typedef struct {
 
 /* Multi-GPU incumbent exchange (GUB is the best sample
  * found anywhere).  When fn != NULL, after every chunk of iterations (the
- * runtime's unit of host synchronisation, at most 32 iterations) the runtime
+ * runtime's unit of host synchronisation: 1, 2, 4, ... doubling up to 64
+ * iterations) the runtime
  * writes xchg[0] = local GUB and xchg[1] = (local search finished ? 0 : -1)
  * to the DEVICE buffer xchg and calls fn(user) on the host thread; fn must
  * replace xchg by its element-wise minimum over all ranks, enqueued on the

@@ -98,6 +98,9 @@ def lib():
             L.or_search_diag.argtypes = [ctypes.c_int, ctypes.c_int, _dp, _dp, _dp, _dp]
             L.or_search.argtypes = [ctypes.c_int, ctypes.c_int, _dp, _dp, ctypes.c_int, _dp, _dp,
                                     _ip]
+            L.or_set_trace.argtypes = [_dp, ctypes.c_long]
+            L.or_set_trace.restype = None
+            L.or_trace_len.restype = ctypes.c_long
             for fn in ("ia_add_dn", "ia_add_up", "ia_sub_dn", "ia_sub_up", "ia_mul_dn",
                        "ia_mul_up", "ia_div_dn", "ia_div_up"):
                 getattr(L, fn).argtypes = [ctypes.c_double, ctypes.c_double]
@@ -233,6 +236,30 @@ def solve(fid, l, u, eps_f=1e-6, eps_x=1e-6, d=10, m=2, bmax=4096, mono=True,
         "hi": shi[:k],
         "lb": slb[:k],
     }
+
+
+def solve_trace(fid, l, u, cap=1 << 20, **kw):
+    """or_solve with the per-iteration trace of bnb.c (test pins only).
+
+    Returns (solve result, [ {lbs, sel, gub_before, gub_after}, ... ])."""
+    buf = np.zeros(cap)
+    lib().or_set_trace(_d(buf), cap)
+    try:
+        r = solve(fid, l, u, **kw)
+        used = lib().or_trace_len()
+    finally:
+        lib().or_set_trace(None, 0)
+    if used > cap:
+        raise ValueError("trace buffer too small")
+    recs, k = [], 0
+    while k < used:
+        pn = int(buf[k]); k += 1
+        lbs = buf[k:k + pn].copy(); k += pn
+        nb = int(buf[k]); k += 1
+        sel = [int(v) for v in buf[k:k + nb]]; k += nb
+        g0, g1 = float(buf[k]), float(buf[k + 1]); k += 2
+        recs.append({"lbs": lbs, "sel": sel, "gub_before": g0, "gub_after": g1})
+    return r, recs
 
 
 # ---------------------------------------------------------------- search (R9)

@@ -164,6 +164,27 @@ typedef struct {
     double* box; /* lo[0..n-1], hi[0..n-1] */
 } rec_t;
 
+/* Optional trace of or_solve for the selection / incumbent pins
+ * (tests/test_oracle_bnb.py).  Per iteration, appended as doubles:
+ *   pn, lb[0..pn-1] (the list L in list order after step 6),
+ *   nb, idx[0..nb-1] (positions in that list of the selected regions, in the
+ *   order they are processed), gub before and after steps 2-5.
+ * Recording stops (silently) when the buffer is full. */
+static double* g_trace = NULL;
+static long g_trace_cap = 0, g_trace_len = 0;
+
+void or_set_trace(double* buf, long cap) {
+    g_trace = buf;
+    g_trace_cap = cap;
+    g_trace_len = 0;
+}
+long or_trace_len(void) { return g_trace_len; }
+
+static void trace_put(double v) {
+    if (g_trace && g_trace_len < g_trace_cap) g_trace[g_trace_len] = v;
+    if (g_trace) ++g_trace_len;
+}
+
 static int rec_cmp(const void* a, const void* b) {
     const rec_t* x = *(const rec_t* const*)a;
     const rec_t* y = *(const rec_t* const*)b;
@@ -247,6 +268,13 @@ int or_solve(int fid, int n, const double* l, const double* u, double eps_f, dou
         char* taken = (char*)calloc((size_t)pn, 1);
         for (long b = 0; b < nb; ++b) taken[order[b] - pool] = 1;
         /* the selected regions are processed in list order (R1) */
+        if (g_trace) {
+            trace_put((double)pn);
+            for (long k = 0; k < pn; ++k) trace_put(pool[k].lb);
+            trace_put((double)nb);
+            for (long k = 0; k < pn; ++k)
+                if (taken[k]) trace_put((double)k);
+        }
         long bb = 0;
         for (long k = 0; k < pn; ++k) {
             if (!taken[k]) continue;
@@ -272,8 +300,10 @@ int or_solve(int fid, int n, const double* l, const double* u, double eps_f, dou
         double* olb = (double*)malloc(sizeof(double) * (size_t)ocap);
         double* ow = (double*)malloc(sizeof(double) * (size_t)ocap);
         long ocnt = 0;
+        if (g_trace) trace_put(gub);
         or_branch(fid, n, (int)nb, plo, phi, pcyc, d, m, l, u, mono, gub, &gub, ocap, opar, ocode,
                   olb, ow, &ocnt);
+        if (g_trace) trace_put(gub);
         evals += nb * kids;
         if (pn + ocnt > pcap) {
             while (pn + ocnt > pcap) pcap *= 2;

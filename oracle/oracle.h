@@ -41,6 +41,9 @@ int or_search_diag(int fid, int n, const double* l, const double* u, double* t_o
 int or_search(int fid, int n, const double* l, const double* u, int rmax, double* x_out,
               double* f_out, int* rounds_out);
 
+void or_set_trace(double* buf, long cap);
+long or_trace_len(void);
+
 int or_solve(int fid, int n, const double* l, const double* u, double eps_f, double eps_x, int d,
              int m, long bmax, int mono, long max_iter, long cap, int search, double* surv_lo,
              double* surv_hi, double* surv_lb, or_result_t* res);

@@ -242,7 +242,7 @@ __device__ __forceinline__ void combine_partials(const double* __restrict__ ppar
   wmax = rw;
 }
 
-// ====================================================================== prep// ====================================================================== prep// ====================================================================== prep
+// ====================================================================== prep
 // Parent b of the batch is handled by P.pslices blocks (one block when the
 // batch is large; for large n and small batches the n variables are cut into
 // slices so that the O(n) reduction spreads over the SMs).  Block (b, s):
@@ -756,7 +756,7 @@ __device__ __noinline__ bool child_mono_ok_warp(const Problem& P, const double* 
   return __ballot_sync(0xffffffffu, bad) == 0u;
 }
 
-// Pass 1: upper bound at the midpoint and lower bound of every child.// Pass 1: upper bound at the midpoint and lower bound of every child.
+// Pass 1: upper bound at the midpoint and lower bound of every child.
 // A thread owns G = m^h consecutive children (all pieces of the h lowest
 // split variables): the terms of the d - h higher variables are combined
 // once per group.  Midpoint bounds are min-reduced (warp shuffle -> block ->

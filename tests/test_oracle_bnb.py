@@ -14,6 +14,7 @@ import pytest
 
 import oracle
 import workloads
+from tests import hp
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -73,8 +74,7 @@ def test_branch_ruled_out_boxes_hold_no_better_point(fid):
     cyc = np.array([0, 1, 2, 0, 1, 2], np.int32)
     gub, par, code, lb, w = oracle.branch(fid, plo, phi, cyc, d, m, l, u, mono=True)
     surv = set(zip(par.tolist(), code.tolist()))
-    # GUB is attained: it is the upper bound at some child midpoint
-    assert math.isfinite(gub)
+    assert math.isfinite(gub)  # its value is pinned by test_branch_gub_is_upper_end_*
     rng = np.random.default_rng(fid)
     for b in range(plo.shape[0]):
         for c in range(m ** d):
@@ -146,3 +146,102 @@ def test_incumbent_monotone_and_minimizer_kept_every_iteration():
         prev = r["gub"]
         assert r["glb"] <= 0.0 <= r["gub"]
         assert any(np.all(lo <= xs) and np.all(xs <= hi) for lo, hi in zip(r["lo"], r["hi"]))
+
+
+# ------------------------------------------------ selection rule (line 130)
+@pytest.mark.parametrize("fid,bmax", [(7, 1), (6, 1), (1, 1), (7, 3), (5, 3), (8, 2), (2, 2)])
+def test_selection_takes_smallest_lower_bounds(fid, bmax):
+    """PAPER.md §3.1: the region with the smallest lower bound is
+    selected (batched, R1: the bmax smallest by (lb, position)).
+    The trace gives the list L in list order at every selection; the test
+    recomputes the argmin itself, so a reversed or otherwise wrong order in
+    the oracle's rec_cmp fails here."""
+    n = 2
+    l, u = workloads.bounds(fid, n)
+    r, recs = oracle.solve_trace(fid, l, u, eps_f=1e-6, eps_x=1e-6, d=2, m=2, bmax=bmax,
+                                 max_iter=40)
+    multi = 0
+    for rec in recs:
+        lbs = rec["lbs"]
+        nb = min(len(lbs), bmax)
+        want = sorted(range(len(lbs)), key=lambda k: (lbs[k], k))[:nb]
+        assert sorted(rec["sel"]) == sorted(want)
+        assert rec["sel"] == sorted(rec["sel"])  # processed in list order
+        if len(lbs) > nb and len(set(lbs.tolist())) > 1:
+            multi += 1
+    assert multi >= 3, "trace never offered a real choice"
+
+
+# ------------------------------------------- incumbent rigour (line 134)
+def _hp_rastrigin(x):
+    """f(x) of (A14) at a point in 50-digit arithmetic (tests/hp.py)."""
+    from decimal import Decimal
+    s = Decimal(10 * len(x))
+    for v in x:
+        d = Decimal(float(v))
+        s += d * d - 10 * hp.dcos(2 * hp.PI * d)
+    return s
+
+
+@pytest.mark.parametrize("fid", list(range(1, 11)))
+def test_branch_gub_is_upper_end_at_best_child_midpoint(fid):
+    """GUB is the smallest UPPER bound of the interval
+    evaluation of f at the sample points (here every child midpoint, reading
+    R2), so f* <= GUB.  Children come from child_box (pinned by Fig. 3), the
+    midpoint a + (b - a) / 2 is recomputed here in round-to-nearest, and the
+    value is the upper end of eval_point (pinned by the closed forms); the
+    lower end would differ (checked: the pin can tell .lo from .hi)."""
+    n, d, m = 3, 3, 2
+    l, u = workloads.bounds(fid, n)
+    plo, phi = workloads.random_boxes(900 + fid, n, 4, l, u, mix=(0, 0, 0.2, 0.4, 0.4, 0))
+    cyc = np.array([0, 1, 2, 1], np.int32)
+    gub, *_ = oracle.branch(fid, plo, phi, cyc, d, m, l, u, mono=True)
+    best_hi, best_lo = math.inf, math.inf
+    for b in range(plo.shape[0]):
+        for c in range(m ** d):
+            clo, chi = oracle.child_box(plo[b], phi[b], int(cyc[b]), d, m, c)
+            mid = np.array([min(max(a + (z - a) * 0.5, a), z) for a, z in zip(clo, chi)])
+            e = oracle.eval_point(fid, mid)
+            best_hi = min(best_hi, e[1])
+            best_lo = min(best_lo, e[0])
+    assert gub == best_hi
+    assert best_lo < best_hi  # a GUB taken from the lower end would fail above
+
+
+def test_branch_gub_bounds_true_value_rastrigin():
+    """The incumbent is a rigorous upper bound of f at a feasible point:
+    GUB >= f(x) in 50 digits at the midpoint that attains it (Rastrigin A14)."""
+    fid, n, d, m = 7, 3, 3, 2
+    l, u = workloads.bounds(fid, n)
+    plo, phi = workloads.random_boxes(77, n, 3, l, u, mix=(0, 0, 0.2, 0.4, 0.4, 0))
+    cyc = np.zeros(3, np.int32)
+    gub, *_ = oracle.branch(fid, plo, phi, cyc, d, m, l, u, mono=True)
+    from fractions import Fraction
+    hit = 0
+    for b in range(plo.shape[0]):
+        for c in range(m ** d):
+            clo, chi = oracle.child_box(plo[b], phi[b], 0, d, m, c)
+            mid = [min(max(a + (z - a) * 0.5, a), z) for a, z in zip(clo, chi)]
+            true = _hp_rastrigin(mid)
+            e = oracle.eval_point(fid, np.array(mid))
+            assert hp.contains(e, true)
+            if e[1] == gub:
+                hit += 1
+                assert Fraction(gub) >= Fraction(true)
+                assert Fraction(e[0]) < Fraction(true)  # the lower end is not a bound
+    assert hit >= 1
+
+
+def test_solve_trace_gub_monotone_and_attained():
+    """Over a whole solve the incumbent never increases (line 134: best sample
+    in all previous iterations and the current one)."""
+    fid, n = 6, 2
+    l, u = workloads.bounds(fid, n)
+    r, recs = oracle.solve_trace(fid, l, u, eps_f=1e-6, eps_x=1e-6, d=2, m=2, bmax=2,
+                                 max_iter=60)
+    prev = math.inf
+    for rec in recs:
+        assert rec["gub_before"] <= prev
+        assert rec["gub_after"] <= rec["gub_before"]
+        prev = rec["gub_after"]
+    assert r["gub"] == prev
