@@ -46,7 +46,7 @@ extern "C" {
 #define IB_STATUS_CONVERGED 0 /* both tolerances met */
 #define IB_STATUS_MAX_ITER 1  /* iteration limit reached first */
 #define IB_STATUS_EMPTY 2     /* (multi-GPU) this rank's list L was emptied by the shared GUB */
-#define IB_NPROF 7
+#define IB_NPROF 8
 
 /* Version string of the library. */
 const char* ib_version(void);
@@ -98,7 +98,8 @@ typedef struct {
      * hot index, refills (units: algorithmic bytes read), 4 k_mono
      * (candidates), 5 k_emit
      * (candidates), 6 k_fused: whole iterations in one persistent kernel
-     * (units: iterations) */
+     * (units: iterations), 7 k_chain: the deep-dive chain, one region per
+     * iteration, one grid barrier per iteration (units: iterations) */
     double t_ms[IB_NPROF];
     int64_t launches[IB_NPROF];
     int64_t units[IB_NPROF];

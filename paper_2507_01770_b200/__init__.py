@@ -25,8 +25,8 @@ LIB_PATH = _build.LIB
 CODE_WHOLE = 0xFFFFFFFF
 _lib = None
 
-NPROF = 7
-PROF_CLASSES = ("prep", "child_eval", "cand", "list", "mono", "emit", "fused")
+NPROF = 8
+PROF_CLASSES = ("prep", "child_eval", "cand", "list", "mono", "emit", "fused", "chain")
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
 _dp = ctypes.POINTER(ctypes.c_double)

@@ -242,6 +242,39 @@ __device__ __forceinline__ void combine_partials(const double* __restrict__ ppar
   wmax = rw;
 }
 
+// one part of the table entry of a piece [pa, pb] (midpoint xm) of split
+// variable i (non-chain objectives): part 0 bounds + box terms, 1 midpoint
+// terms, 2 derivative ingredients + the separable first-order flag (PAPER.md
+// lines 142-144: derivative of constant sign off the domain edge)
+template <class F>
+__device__ __forceinline__ void piece_entry(const Problem& P, double pa, double pb, double xm, int i, int part,
+                                            double* e) {
+  const int n = P.n;
+  if (part == 0) {
+    Iv tt[2];
+    F::terms(Iv{pa, pb}, i, n, tt);
+    e[E_LO] = pa;
+    e[E_HI] = pb;
+    for (int k = 0; k < F::K; ++k) put(e + E_T + 2 * k, tt[k]);
+  } else if (part == 1) {
+    Iv tm[2];
+    F::terms(Iv{xm, xm}, i, n, tm);
+    for (int k = 0; k < F::K; ++k) put(e + E_T + 2 * F::K + 2 * k, tm[k]);
+  } else {
+    Iv g[2];
+    if constexpr (F::KG > 0) {
+      F::ding(Iv{pa, pb}, i, n, g);
+      for (int k = 0; k < F::KG; ++k) put(e + E_T + 4 * F::K + 2 * k, g[k]);
+    }
+    double flag = 0.0;
+    if constexpr (F::SEP) {
+      Iv D = F::dsep(Iv{pa, pb}, i, n);
+      if ((D.lo > 0.0 && pa != P.l[i]) || (D.hi < 0.0 && pb != P.u[i])) flag = 1.0;
+    }
+    e[E_T + 4 * F::K + 2 * F::KG] = flag;
+  }
+}
+
 // ====================================================================== prep
 // Parent b of the batch is handled by P.pslices blocks (one block when the
 // batch is large; for large n and small batches the n variables are cut into
@@ -411,29 +444,7 @@ __device__ __forceinline__ void prep_item(const Problem& P, const Ctl* __restric
         put(e + 16, vm.s0);
       }
     } else {
-      if (part == 0) {
-        Iv tt[2];
-        F::terms(Iv{pa, pb}, i, n, tt);
-        e[E_LO] = pa;
-        e[E_HI] = pb;
-        for (int k = 0; k < F::K; ++k) put(e + E_T + 2 * k, tt[k]);
-      } else if (part == 1) {
-        Iv tm[2];
-        F::terms(Iv{xm, xm}, i, n, tm);
-        for (int k = 0; k < F::K; ++k) put(e + E_T + 2 * F::K + 2 * k, tm[k]);
-      } else {
-        Iv g[2];
-        if constexpr (F::KG > 0) {
-          F::ding(Iv{pa, pb}, i, n, g);
-          for (int k = 0; k < F::KG; ++k) put(e + E_T + 4 * F::K + 2 * k, g[k]);
-        }
-        double flag = 0.0;
-        if constexpr (F::SEP) {
-          Iv D = F::dsep(Iv{pa, pb}, i, n);
-          if ((D.lo > 0.0 && pa != P.l[i]) || (D.hi < 0.0 && pb != P.u[i])) flag = 1.0;
-        }
-        e[E_T + 4 * F::K + 2 * F::KG] = flag;
-      }
+      piece_entry<F>(P, pa, pb, xm, i, part, e);
     }
   }
   if (S > 1 && P.prest) {
@@ -2723,6 +2734,10 @@ __global__ void __launch_bounds__(TPB, 1) k_fused(Problem P, IterBufs w, int ite
   }
 }
 
+}  // namespace ib
+#include "chain.cuh"
+namespace ib {
+
 // ================================================================ launchers
 static inline unsigned grid_for(long items, int per_block, unsigned cap = 148u * 32u) {
   long g = (items + per_block - 1) / per_block;
@@ -2849,6 +2864,31 @@ int launch_fused(const Problem& P, const IterBufs& w, int iters, long bmax, cuda
       }
     }
     if (!done) e = coop_launch(k_fused<F, 0>, grid, st, P, w, iters, nz);
+  });
+  return (int)e;
+}
+
+// deep-dive chain (chain.cuh): up to `iters` iterations in one cooperative
+// launch, one block per SM, the block slices of the region in dynamic shared
+// memory (2 * per doubles)
+int launch_chain(const Problem& P, const IterBufs& w, const ChainBufs& cb, int iters, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t smem = sizeof(double) * 2 * (size_t)cb.per;
+  cudaError_t e = cudaSuccess;
+  IB_DISPATCH_FID(P.fid, {
+    if constexpr (!F::CHAIN) {
+      static bool attr = false;  // per objective (one static per instantiation)
+      if (!attr) {
+        cudaFuncSetAttribute((const void*)k_chain<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        attr = true;
+      }
+      void* argv[] = {(void*)&P, (void*)&w, (void*)&cb, (void*)&iters};
+      e = cudaLaunchCooperativeKernel((const void*)k_chain<F>, dim3(sms), dim3(TPB), argv, smem, st);
+    } else {
+      e = cudaErrorInvalidValue;
+    }
   });
   return (int)e;
 }

@@ -1,0 +1,476 @@
+// chain.cuh -- k_chain: the deep-dive iteration kernel (included by
+// bnb_kernels.cu after the phases it reuses).
+//
+// Regime: every iteration selects ONE region R (§3.1) and
+// exactly one of its m^d subregions survives (lines 140-146), which becomes
+// the next selected region.  This is the whole run of every paper function
+// at n = 1,000 .. 10,000 once the R9 incumbent is known.  The
+// iteration is then a chain of dependent steps, and what costs time is the
+// number of grid-wide barriers and dependent memory round trips per step,
+// not arithmetic.  k_chain keeps the state of the chain on chip and needs ONE
+// grid barrier per iteration:
+//
+//  * every block holds its slice of the variables of R in shared memory and
+//    the full table of R (rest accumulators + piece terms of the split
+//    chunk c) in shared memory;
+//  * phase 1 (between barriers), each block: (a) lower bound of its share of
+//    the children (table combination, Eq. (3)-(6) natural
+//    extension), midpoint upper bound for those with lb <= GUB (line 134),
+//    potential candidates appended to a per-iteration list; (b) the partial
+//    sum S_excl over its slice of the variables outside BOTH the current
+//    chunk c and the next chunk c' = c + d (line 184): every child R' of R
+//    has the same values there, so rest(R') = S_excl + the piece terms of
+//    chunk c chosen by R' -- the O(n) reduction runs concurrently with the
+//    child evaluation instead of before it; (c) the blocks owning chunk c'
+//    tabulate its pieces (R' = R on c');
+//  * barrier;
+//  * phase 2, every block redundantly and deterministically (same inputs,
+//    same order): incumbent GUB = min(previous, this iteration's midpoint
+//    minimum), candidates lb <= GUB, first-order test (lines 142-144) and
+//    widths, the survivor; the stop test (lines 148-150); the next table
+//    (S_excl partials combined in a fixed order + chunk-c terms of the
+//    survivor, chunk-c' entries from the owners) and the slice update.  No
+//    block waits for another in phase 2, so the next phase 1 starts at once.
+//
+// Per-iteration buffers are triple (candidate lists, midpoint minima) or
+// double (slice partials, next-chunk entries) buffered by iteration index so
+// that a slow block still in phase 2 of iteration k never sees data of
+// iteration k + 1.  Whenever the iteration does not continue the chain (no or
+// several survivors, stop test, iteration budget), block 0 writes the
+// control block, the table and the region to the archive exactly as the
+// fused path would have them, and the insertion runs through the same
+// emit_small_dev / cand_emit_dev as k_fused; the next launch (k_chain or
+// k_fused) starts with its list phase.
+//
+// Requirements (checked by the host): m = 2, n >= 2 d, a non-chain objective,
+// the list phase selects one region (every live record is in a hot index of
+// one entry).  The accumulators are combined in a different order than the
+// fused path (slice partials over 148 blocks, then the chunk terms), so the
+// bounds agree with it and with the oracle to the parity tolerance, not bit
+// for bit.
+#pragma once
+
+namespace ib {
+
+__device__ __forceinline__ bool in_chunk(int i, int c, int d, int n) { return ((i - c + n) % n) < d; }
+
+// warp-aggregated append of (code, lb) to the iteration's candidate list
+__device__ __forceinline__ void chain_append(unsigned long long* cnt, uint32_t* pc, double* pl, bool cond,
+                                             uint32_t code, double lb) {
+  const unsigned am = __activemask();
+  const unsigned mk = __ballot_sync(am, cond);
+  if (!mk) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(mk) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(cnt, (unsigned long long)__popc(mk));
+  base = __shfl_sync(am, base, leader);
+  if (cond) {
+    const unsigned long long idx = base + __popc(mk & ((1u << lane) - 1u));
+    if (idx < (unsigned long long)PCAP) {
+      pc[idx] = code;
+      pl[idx] = lb;
+    }
+  }
+}
+
+// partial accumulators of a block's slice of region R (slice in s_lo / s_hi):
+// box and midpoint terms of the variables NOT in chunk c1 (and, when c2 >= 0,
+// not in chunk c2), max width of those variables -> part (thread 0)
+template <class F>
+__device__ __forceinline__ void chain_slice_partial(const Problem& P, const double* s_lo, const double* s_hi, int i0,
+                                                    int i1, int c1, int c2, double* part) {
+  const int n = P.n, d = P.d;
+  Iv acc[2], accm[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) acc[k] = accm[k] = iv(0.0);
+#pragma unroll
+  for (int k = 0; k < F::K; ++k) acc[k] = accm[k] = acc_ident<F>(k);
+  double wmax = 0.0;
+  constexpr int HB = TPB / 2;
+  const int hv = threadIdx.x % HB, half = threadIdx.x / HB;
+  for (int i = i0 + hv; i < i1; i += HB) {
+    if (in_chunk(i, c1, d, n) || (c2 >= 0 && in_chunk(i, c2, d, n))) continue;
+    const double a = s_lo[i - i0], bb = s_hi[i - i0];
+    Iv t[2];
+    if (half == 0) {
+      wmax = fmax(wmax, __dsub_rn(bb, a));
+      F::terms(Iv{a, bb}, i, n, t);
+    } else {
+      const double xm = midpt(a, bb);
+      F::terms(Iv{xm, xm}, i, n, t);
+    }
+#pragma unroll
+    for (int k = 0; k < F::K; ++k) {
+      if (half == 0) acc[k] = acc_comb<F>(k, acc[k], t[k]);
+      else accm[k] = acc_comb<F>(k, accm[k], t[k]);
+    }
+  }
+  block_reduce_prep<F, TPB>(acc, accm, wmax);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 2; ++k) {
+      put(part + 2 * k, acc[k]);
+      put(part + 4 + 2 * k, accm[k]);
+    }
+    part[8] = wmax;
+  }
+}
+
+// entries of chunk c (pieces of its d variables) for the variables in this
+// block's slice -> ent (global, d * m entries of ENT doubles)
+template <class F>
+__device__ __forceinline__ void chain_chunk_entries(const Problem& P, const double* s_lo, const double* s_hi, int i0,
+                                                    int i1, int c, double* ent) {
+  const int n = P.n, d = P.d, m = P.m;
+  for (int t = threadIdx.x; t < 3 * d * m; t += TPB) {
+    const int e = t % (d * m), part = t / (d * m);
+    const int j = e / m, p = e % m;
+    const int i = (c + j) % n;
+    if (i < i0 || i >= i1) continue;
+    const double a = s_lo[i - i0], bb = s_hi[i - i0];
+    const double pa = part_point(a, bb, m, p), pb = part_point(a, bb, m, p + 1);
+    piece_entry<F>(P, pa, pb, midpt(pa, pb), i, part, ent + (size_t)e * ENT);
+  }
+}
+
+// the G slice partials combined in a fixed order (deterministic: every block
+// gets the same bits; results valid in thread 0).  L2 loads: the partials
+// are rewritten by other blocks every second iteration.
+template <class F>
+__device__ __forceinline__ void chain_combine(const double* part, int G, Iv* acc, Iv* accm, double& wmax) {
+  Iv ra[2], rm[2];
+  double rw = 0.0;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) ra[k] = rm[k] = iv(0.0);
+#pragma unroll
+  for (int k = 0; k < F::K; ++k) ra[k] = rm[k] = acc_ident<F>(k);
+  for (int q = threadIdx.x; q < G; q += TPB) {
+    const double* pt = part + (size_t)q * CH_PART;
+#pragma unroll
+    for (int k = 0; k < F::K; ++k) {
+      ra[k] = acc_comb<F>(k, ra[k], Iv{__ldcg(pt + 2 * k), __ldcg(pt + 2 * k + 1)});
+      rm[k] = acc_comb<F>(k, rm[k], Iv{__ldcg(pt + 4 + 2 * k), __ldcg(pt + 5 + 2 * k)});
+    }
+    rw = fmax(rw, __ldcg(pt + 8));
+  }
+  block_reduce_prep<F, TPB>(ra, rm, rw);
+  for (int k = 0; k < 2; ++k) {
+    acc[k] = ra[k];
+    accm[k] = rm[k];
+  }
+  wmax = rw;
+}
+
+template <class F>
+__global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBufs cb, int iters) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double s_dyn[];
+  constexpr int TS = HDR + 2 * D_MAX * ENT;  // bisection tables (m = 2, d <= 16)
+  __shared__ double s_T[2][TS];
+  __shared__ uint32_t s_pc[PCAP];
+  __shared__ double s_pl[PCAP], s_w[PCAP];
+  __shared__ uint8_t s_ok[PCAP];
+  __shared__ uint32_t s_code;
+  __shared__ double s_lb, s_wsurv;
+  __shared__ unsigned int s_nc, s_ns;
+  Ctl* ctl = w.ctl;
+  const int n = P.n, d = P.d, t = threadIdx.x, blk = blockIdx.x, G = gridDim.x;
+  const int lane = t & 31;
+  const int tabw = d * P.m * ENT;  // doubles of the entries
+  double* s_lo = s_dyn;
+  double* s_hi = s_dyn + cb.per;
+  const int i0 = blk * cb.per, i1 = min(n, i0 + cb.per);
+
+  // ---- entry: list phase (block 0) -- the host launches k_chain only when
+  // every live record is in a hot index of one entry
+  if (blk == 0) list_small_dev(w.pool, ctl, w.hot0, w.hot1, w.sel_slot, w.sel_code, P.kids);
+  grid.sync();
+  if (__ldcg(&ctl->done) || __ldcg(&ctl->B) != 1ull) return;  // uniform
+  const unsigned long long iter0 = __ldcg(&ctl->iter), max_iter = ctl->max_iter;
+  const unsigned long long pcount0 = __ldcg(&ctl->pcount);
+  const double eps_f = ctl->eps_f, eps_x = ctl->eps_x;
+  unsigned long long gub_key = __ldcg(&ctl->gub_key);
+  // the selected region R0: materialise this block's slice (Eq. 8-11)
+  int c;
+  {
+    const int src = __ldcg(&w.sel_slot[0]);
+    const uint32_t code = __ldcg(&w.sel_code[0]);
+    const int psc = __ldcg(&w.src_sc[src]);
+    c = (code == CODE_WHOLE) ? psc : (psc + d) % n;
+    const double* slo = w.src_lo + (size_t)src * P.ld;
+    const double* shi = w.src_hi + (size_t)src * P.ld;
+    for (int i = i0 + t; i < i1; i += TPB) {
+      double a = __ldcg(&slo[i]), bb = __ldcg(&shi[i]);
+      if (code != CODE_WHOLE) {
+        const int jj = (i - psc + n) % n;
+        if (jj < d) {
+          const int p = digit(code, jj, P.m);
+          const double a2 = part_point(a, bb, P.m, p), b2 = part_point(a, bb, P.m, p + 1);
+          a = a2;
+          bb = b2;
+        }
+      }
+      s_lo[i - i0] = a;
+      s_hi[i - i0] = bb;
+    }
+  }
+  __syncthreads();
+  // rest accumulators of R0 (variables outside chunk c) and its chunk entries
+  chain_slice_partial<F>(P, s_lo, s_hi, i0, i1, c, -1, cb.part + ((size_t)1 * G + blk) * CH_PART);
+  chain_chunk_entries<F>(P, s_lo, s_hi, i0, i1, c, cb.tabn);
+  if (blk == 0 && t == 0) {
+    for (int q = 0; q < 3; ++q) {
+      cb.cnt[q] = 0ull;
+      cb.gacc[q] = ~0ull;
+    }
+  }
+  grid.sync();
+  {
+    double* T = s_T[0];
+    Iv ra[2], rm[2];
+    double rw;
+    chain_combine<F>(cb.part + (size_t)1 * G * CH_PART, G, ra, rm, rw);
+    if (t == 0) {
+      for (int k = 0; k < 2; ++k) {
+        put(T + H_REST + 2 * k, ra[k]);
+        put(T + H_RESTM + 2 * k, rm[k]);
+      }
+      T[H_WREST] = rw;
+      T[H_CHUNK] = (double)c;
+    }
+    for (int q = t; q < tabw; q += TPB) T[HDR + q] = __ldcg(&cb.tabn[q]);
+  }
+  __syncthreads();
+
+  unsigned long long sum_cand = 0, nwidth = 0;
+  int k = 0;
+  for (;; ++k) {
+    const int sl = k % 3;
+    double* T = s_T[k & 1];
+    double* Tn = s_T[(k + 1) & 1];
+    const int cn = (c + d) % n;
+    const double gub0 = okey_inv(gub_key);
+    // ================= phase 1
+    if (blk == 0 && t == 0) {  // slot of the next iteration (last read before the previous barrier)
+      cb.cnt[(k + 1) % 3] = 0ull;
+      cb.gacc[(k + 1) % 3] = ~0ull;
+    }
+    // (a) children: a thread owns the pair of children of a code with bit 0 clear
+    double best = CUDART_INF;
+    {
+      const int ng = 1 << (d - 1);
+      const int gpb = (ng + G - 1) / G;
+      const int gb = blk * gpb, ge = min(ng, gb + gpb);
+      unsigned long long* cnt = cb.cnt + sl;
+      uint32_t* pc = cb.pcode + (size_t)sl * PCAP;
+      double* pl = cb.plb + (size_t)sl * PCAP;
+      for (int gi = gb + t; gi < ge; gi += TPB) {
+        const uint32_t code0 = (uint32_t)gi << 1;
+        Iv A[2];
+#pragma unroll
+        for (int q = 0; q < F::K; ++q) A[q] = get(T + H_REST + 2 * q);
+        int j = 1;
+        for (; j + 4 <= d; j += 4) {
+          Iv tt[4][2];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double* e = T + HDR + (size_t)(2 * (j + u) + ((code0 >> (j + u)) & 1u)) * ENT + E_T;
+#pragma unroll
+            for (int q = 0; q < F::K; ++q) tt[u][q] = get(e + 2 * q);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int q = 0; q < F::K; ++q) A[q] = acc_comb<F>(q, A[q], tt[u][q]);
+        }
+        for (; j < d; ++j) {
+          const double* e = T + HDR + (size_t)(2 * j + ((code0 >> j) & 1u)) * ENT + E_T;
+#pragma unroll
+          for (int q = 0; q < F::K; ++q) A[q] = acc_comb<F>(q, A[q], get(e + 2 * q));
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          Iv B[2];
+          const double* e0 = T + HDR + (size_t)h * ENT + E_T;
+#pragma unroll
+          for (int q = 0; q < F::K; ++q) B[q] = acc_comb<F>(q, A[q], get(e0 + 2 * q));
+          const uint32_t code = code0 | (uint32_t)h;
+          const double lb = canon_lb(outer_lo<F>(B, n));
+          w.clb[code] = lb;
+          const bool pot = lb <= gub0;
+          if (pot) {  // midpoint sample (line 134): rare, recombined from the midpoint terms
+            Iv Bm[2];
+#pragma unroll
+            for (int q = 0; q < F::K; ++q) Bm[q] = get(T + H_RESTM + 2 * q);
+            for (int jj = 0; jj < d; ++jj) {
+              const double* e = T + HDR + (size_t)(2 * jj + ((code >> jj) & 1u)) * ENT + E_T + 2 * F::K;
+#pragma unroll
+              for (int q = 0; q < F::K; ++q) Bm[q] = acc_comb<F>(q, Bm[q], get(e + 2 * q));
+            }
+            best = fmin(best, outer_hi<F>(Bm, n));
+          }
+          chain_append(cnt, pc, pl, pot, code, lb);
+        }
+      }
+    }
+    // (b) S_excl of R over this block's slice, outside chunks c and c'
+    chain_slice_partial<F>(P, s_lo, s_hi, i0, i1, c, cn, cb.part + ((size_t)(k & 1) * G + blk) * CH_PART);
+    // (c) entries of chunk c' (unchanged in every child of R)
+    chain_chunk_entries<F>(P, s_lo, s_hi, i0, i1, cn, cb.tabn + (size_t)((k + 1) & 1) * DM_MAX * ENT);
+    // (d) this block's midpoint minimum
+    {
+      __shared__ double s_m[TPB / 32];
+      best = warp_min(best);
+      if (lane == 0) s_m[t >> 5] = best;
+      __syncthreads();
+      if (t == 0) {
+        for (int q = 1; q < TPB / 32; ++q) best = fmin(best, s_m[q]);
+        if (best < CUDART_INF) atomicMin(&cb.gacc[sl], (unsigned long long)okey(best));
+      }
+    }
+    grid.sync();
+    // ================= phase 2 (every block, same decisions)
+    const unsigned long long np = __ldcg(&cb.cnt[sl]);
+    {
+      const unsigned long long gk = __ldcg(&cb.gacc[sl]);
+      if (gk < gub_key) gub_key = gk;
+    }
+    const double gub = okey_inv(gub_key);
+    bool cont = np <= (unsigned long long)PCAP;
+    if (cont) {
+      const int npi = (int)np;
+      if (t < npi) {
+        s_pc[t] = __ldcg(&cb.pcode[(size_t)sl * PCAP + t]);
+        s_pl[t] = __ldcg(&cb.plb[(size_t)sl * PCAP + t]);
+      }
+      if (t == 0) {
+        s_nc = 0;
+        s_ns = 0;
+      }
+      __syncthreads();
+      // candidates (lb <= GUB): width and first-order test, a warp each
+      for (int q = t >> 5; q < npi; q += TPB / 32) {
+        if (!(s_pl[q] <= gub)) continue;  // warp-uniform
+        const uint32_t code = s_pc[q];
+        double wl = 0.0;
+        bool bad = false;
+        if (lane < d) {
+          const double* e = T + HDR + (size_t)(2 * lane + ((code >> lane) & 1u)) * ENT;
+          wl = __dsub_rn(e[E_HI], e[E_LO]);
+          if constexpr (F::SEP) bad = e[E_T + 4 * F::K + 2 * F::KG] != 0.0;
+        }
+        wl = warp_max(wl);
+        unsigned anybad = __ballot_sync(0xffffffffu, bad);
+        if constexpr (!F::SEP) anybad = (!P.mono || child_mono_ok_warp<F>(P, T, code)) ? 0u : 1u;
+        if (lane == 0) {
+          const bool ok = !P.mono || anybad == 0u;
+          s_ok[q] = ok;
+          s_w[q] = fmax(T[H_WREST], wl);
+          atomicAdd(&s_nc, 1u);
+          if (ok) {
+            atomicAdd(&s_ns, 1u);
+            s_code = code;  // the survivor when it is the only one
+            s_lb = s_pl[q];
+            s_wsurv = s_w[q];
+          }
+        }
+      }
+      __syncthreads();
+      const unsigned ns = s_ns;
+      cont = ns == 1;
+      if (cont) {
+        // the next list phase on the single live record (list_small_dev's
+        // decisions): stop test (lines 148-150), iteration limit, budget
+        if (__dsub_ru(gub, s_lb) <= eps_f) {
+          nwidth += 1;
+          if (s_wsurv <= eps_x) cont = false;
+        }
+        if (iter0 + (unsigned long long)k + 1 >= max_iter) cont = false;
+        if (k + 1 >= iters) cont = false;
+      }
+      if (cont) sum_cand += s_nc;
+    }
+    if (!cont) break;  // uniform: every block took the same decisions
+    // ---- continue: the survivor R' becomes the selected region
+    const uint32_t scode = s_code;
+    {
+      Iv ra[2], rm[2];
+      double rw;
+      chain_combine<F>(cb.part + (size_t)(k & 1) * G * CH_PART, G, ra, rm, rw);
+      if (t == 0) {
+        // rest(R') = S_excl + terms of R' in chunk c (not in c', n >= 2d)
+        for (int j = 0; j < d; ++j) {
+          const double* e = T + HDR + (size_t)(2 * j + ((scode >> j) & 1u)) * ENT;
+#pragma unroll
+          for (int q = 0; q < F::K; ++q) {
+            ra[q] = acc_comb<F>(q, ra[q], get(e + E_T + 2 * q));
+            rm[q] = acc_comb<F>(q, rm[q], get(e + E_T + 2 * F::K + 2 * q));
+          }
+          rw = fmax(rw, __dsub_rn(e[E_HI], e[E_LO]));
+        }
+        for (int q = 0; q < 2; ++q) {
+          put(Tn + H_REST + 2 * q, ra[q]);
+          put(Tn + H_RESTM + 2 * q, rm[q]);
+        }
+        Tn[H_WREST] = rw;
+        Tn[H_CHUNK] = (double)cn;
+      }
+      const double* en = cb.tabn + (size_t)((k + 1) & 1) * DM_MAX * ENT;
+      for (int q = t; q < tabw; q += TPB) Tn[HDR + q] = __ldcg(&en[q]);
+      // slice update: chunk c variables take the survivor's pieces
+      for (int j = t; j < d; j += TPB) {
+        const int i = (c + j) % n;
+        if (i >= i0 && i < i1) {
+          const double* e = T + HDR + (size_t)(2 * j + ((scode >> j) & 1u)) * ENT;
+          s_lo[i - i0] = e[E_LO];
+          s_hi[i - i0] = e[E_HI];
+        }
+      }
+    }
+    __syncthreads();
+    c = cn;
+  }
+  // ================= leave the chain at iteration k (all blocks)
+  // iterations 0 .. k-1 ended inside the chain; iteration k is ended by the
+  // insertion below and the next launch's list phase (pending end)
+  double* T = s_T[k & 1];
+  const int slot = (int)w.free_list[__ldcg(&ctl->free_top) - 1];  // archive slot of R (prep's choice)
+  for (int i = i0 + t; i < i1; i += TPB) {
+    w.dst_lo[(size_t)slot * P.ld + i] = s_lo[i - i0];
+    w.dst_hi[(size_t)slot * P.ld + i] = s_hi[i - i0];
+  }
+  if (blk == 0) {
+    for (int q = t; q < w.tab_stride; q += TPB) w.tab[q] = T[q];
+    if (t == 0) {
+      w.new_slot[0] = slot;
+      w.dst_sc[slot] = c;
+      const unsigned long long K = (unsigned long long)k;
+      ctl->gub_key = gub_key;
+      ctl->iter = iter0 + K;
+      ctl->evals += K * (unsigned long long)P.kids;
+      ctl->sum_B += K;
+      ctl->sum_cand += sum_cand;
+      ctl->sum_pool += K * pcount0;
+      ctl->nwidth += nwidth;
+    }
+    __syncthreads();
+  }
+  const unsigned long long np = __ldcg(&cb.cnt[k % 3]);
+  if (np <= (unsigned long long)PCAP) {
+    if (blk == 0) {
+      __threadfence_block();
+      emit_small_dev<F>(P, ctl, w.tab, w.tab_stride, w.clb, w.new_slot, w.pool, cb.pcode + (size_t)(k % 3) * PCAP,
+                        (int)np, w.hot0, w.hot1, false);
+    }
+    return;
+  }
+  // many potential candidates: the static-tile insertion pass over every child
+  // (descriptors zeroed first)
+  {
+    const long nz = 3 * (((long)P.kids + TILE - 1) / TILE + 1);
+    for (long q = (long)blk * TPB + t; q < nz; q += (long)G * TPB) w.desc2[q] = 0;
+  }
+  grid.sync();
+  cand_emit_dev<F>(P, ctl, w.tab, w.tab_stride, w.clb, w.new_slot, w.pool, w.desc2, w.hot0, w.hot1);
+}
+
+}  // namespace ib

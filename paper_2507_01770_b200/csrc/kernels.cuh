@@ -139,6 +139,19 @@ struct IterBufs {
   uint32_t* pot;               // k_fused: potential candidates (child indices), PCAP entries
 };
 
+// buffers of the deep-dive chain kernel (chain.cuh)
+constexpr int CH_PART = 10;  // doubles per slice partial (as k_prep's)
+struct ChainBufs {
+  unsigned long long* cnt;   // [3] potential candidates appended per iteration slot
+  unsigned long long* gacc;  // [3] midpoint minima (ordered keys) per slot
+  uint32_t* pcode;           // [3][PCAP] potential candidates (child codes)
+  double* plb;               // [3][PCAP] their lower bounds
+  double* part;              // [2][grid][CH_PART] slice partials
+  double* tabn;              // [2][DM_MAX * ENT] entries of the next chunk
+  int per;                   // variables per block slice
+  int pad;
+};
+
 // host callbacks around the kernel classes of an iteration: profiling
 // events (class 0 prep, 1 child_eval, 2 prune, 3 statistics, 4 radix,
 // 5 select) and the multi-GPU incumbent exchange

@@ -28,6 +28,7 @@ namespace ib {
 int launch_iteration(const Problem&, const IterBufs&, long, long, cudaStream_t, IterHook*, long);
 int launch_branch(const Problem&, const IterBufs&, long, cudaStream_t);
 int launch_fused(const Problem&, const IterBufs&, int, long, cudaStream_t);
+int launch_chain(const Problem&, const IterBufs&, const ChainBufs&, int, cudaStream_t);
 int launch_select_only(Pool, Ctl*, unsigned int*, long, cudaStream_t);
 int launch_xchg_put(const Ctl*, double*, cudaStream_t);
 int launch_apply_pending(Ctl*, long, cudaStream_t);
@@ -302,7 +303,24 @@ struct SolveWs {
   double* ppart;
   unsigned int* pticket;
   uint32_t* pot;
+  ChainBufs chain;
 };
+
+// blocks of the chain kernel (one per SM) and its slice of the variables
+static int chain_grid() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+static int chain_per(int n) { return (n + chain_grid() - 1) / chain_grid(); }
+// the chain kernel applies (chain.cuh): bisection, the next chunk disjoint
+// from the current one, a non-chain objective, the slices in shared memory
+static bool chain_applies(const Problem& P) {
+  if (const char* e = std::getenv("IBNB_CHAIN"))
+    if (std::atoi(e) == 0) return false;
+  return P.m == 2 && P.fid != 6 && P.n >= 2 * P.d && P.d >= 2 && 16L * chain_per(P.n) <= 150L * 1024;
+}
 
 static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
   // Order matters for the latency-bound small-batch regime: the control
@@ -321,6 +339,13 @@ static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
   w.ppart = A.take<double>((size_t)o.bmax * prep_slices(n, o.bmax) * 10);
   w.pticket = A.take<unsigned int>(o.bmax);
   w.pot = A.take<uint32_t>(PCAP);
+  w.chain.cnt = A.take<unsigned long long>(3);
+  w.chain.gacc = A.take<unsigned long long>(3);
+  w.chain.pcode = A.take<uint32_t>(3 * PCAP);
+  w.chain.plb = A.take<double>(3 * PCAP);
+  w.chain.part = A.take<double>((size_t)2 * chain_grid() * CH_PART);
+  w.chain.tabn = A.take<double>((size_t)2 * DM_MAX * ENT);
+  w.chain.per = chain_per(n);
   w.root_out = A.take<double>(2);
   w.f_search = A.take<double>(1);
   w.search_rounds = A.take<int32_t>(1);
@@ -609,7 +634,12 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   if (const char* e = std::getenv("IBNB_FUSE_KIDS")) fuse_kids = std::atol(e);
   if (const char* e = std::getenv("IBNB_FUSE_POOL")) fuse_pool = std::atol(e);
   unsigned long long pcount = 1, free_top = hc.free_top, peak = 1;
-  long fused_iters = 0, iter_prev = 0;
+  long fused_iters = 0, chain_iters = 0, iter_prev = 0, chain_launches = 0;
+  const bool use_chain = chain_applies(P);
+  // iterations per chain launch: the host reads the control block between
+  // launches (multi-GPU: the incumbent exchange runs there)
+  long chain_budget = xfn ? 64 : 4096;
+  if (const char* e = std::getenv("IBNB_CHAIN_ITERS")) chain_budget = std::max(1L, std::atol(e));
   long chunk = 1;
   for (;;) {
     const long per_it = o.bmax * o.kids;
@@ -646,9 +676,18 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
     // k_list grid class from the records L holds now: two classes, so that
     // the cached iteration graphs do not multiply
     const long list_hint = (long)pcount <= 65536 ? 65536 : (1L << 40);
-    // small batches: whole iterations in one persistent cooperative kernel
+    // small batches: whole iterations in one persistent cooperative kernel;
+    // the deep dive (one live region, one survivor per iteration) as a chain
     const bool fused = o.bmax * o.kids <= fuse_kids && (long)pcount <= fuse_pool;
-    if (fused) {
+    const bool chain = use_chain && hc.list_fast && hc.nhot == 1 && !hc.pending_end &&
+                       (long)free_top >= 2 && (long)pcount + o.kids <= o.pool_cap;
+    if (chain) {
+      prof.begin(7, st);
+      CKL(launch_chain(P, ib, w.chain, (int)chain_budget, st));
+      prof.end(7, st);
+      nk += 1 - chunk * kIterKernels;
+      ++chain_launches;
+    } else if (fused) {
       prof.begin(6, st);
       CKL(launch_fused(P, ib, (int)chunk, o.bmax, st));
       prof.end(6, st);
@@ -787,13 +826,14 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
         res->transfers += 1;
       }
     }
-    if (fused) fused_iters += (long)hc.iter - iter_prev;
+    if (chain) chain_iters += (long)hc.iter - iter_prev;
+    else if (fused) fused_iters += (long)hc.iter - iter_prev;
     iter_prev = (long)hc.iter;
     if (hc.err) return fail(hc.err, "capacity exceeded on the device (L %ld, archive %ld)", o.pool_cap, o.arch_cap);
     if (trace)
-      fprintf(stderr, "[ibnb] t=%.3f ms chunk=%ld iter=%llu |L|=%llu live_hot=%llu nhot=%llu B=%llu refills=%llu "
-              "width_passes=%llu done=%d\n", now() - t_start, chunk, hc.iter, hc.pcount, hc.live, hc.nhot, hc.B,
-              hc.nrefill, hc.nwidth, hc.done);
+      fprintf(stderr, "[ibnb] t=%.3f ms %s chunk=%ld iter=%llu |L|=%llu live_hot=%llu nhot=%llu B=%llu refills=%llu "
+              "width_passes=%llu done=%d\n", now() - t_start, chain ? "chain" : (fused ? "fused" : "graph"), chunk,
+              hc.iter, hc.pcount, hc.live, hc.nhot, hc.B, hc.nrefill, hc.nwidth, hc.done);
     if (xfn ? hc.gdone : hc.done) break;
     chunk = std::min(chunk * 2, 64L);
     // lazy deletion leaves selected / ruled-out records in L: compact when a
@@ -900,6 +940,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   res->units[4] = (int64_t)c.sum_cand;   // mono: candidates tested
   res->units[5] = (int64_t)c.sum_cand;   // emit: candidates scanned
   res->units[6] = (int64_t)fused_iters;  // fused: iterations run inside k_fused
+  res->units[7] = (int64_t)chain_iters;  // chain: iterations run inside k_chain
   res->radix_records = (int64_t)c.sum_radix;
   res->f_lo = live ? okey_inv_h(c.min_lb_key) : INFINITY;
   res->f_hi = okey_inv_h(c.gub_key);

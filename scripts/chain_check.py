@@ -1,0 +1,35 @@
+"""Chain kernel check on the GPU: every paper function solved with the chain
+kernel on and off (IBNB_CHAIN), results and wall time side by side."""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2507_01770_b200 as pb  # noqa: E402
+import workloads  # noqa: E402
+
+ns = [int(a) for a in sys.argv[1].split(",")] if len(sys.argv) > 1 else [1000, 10000]
+fids = [int(a) for a in sys.argv[2].split(",")] if len(sys.argv) > 2 else list(range(1, 11))
+for n in ns:
+    for fid in fids:
+        l, u = workloads.bounds(fid, n)
+        row = {"fid": fid, "n": n}
+        for mode in ("0", "1"):
+            os.environ["IBNB_CHAIN"] = mode
+            pb.ib_solve(fid, l, u, 1e-6, 1e-6, pb.options(), surv_cap=4)  # warm-up
+            t = time.perf_counter()
+            r = pb.ib_solve(fid, l, u, 1e-6, 1e-6, pb.options(profile=0), surv_cap=4)
+            dt = time.perf_counter() - t
+            rp = pb.ib_solve(fid, l, u, 1e-6, 1e-6, pb.options(profile=1), surv_cap=4)
+            row["chain" if mode == "1" else "fused"] = {
+                "s": round(dt, 4), "status": r.status, "iters": r.iters, "evals": r.evals,
+                "f": [r.f_lo, r.f_hi], "n_surv": r.n_surv, "w": r.max_width,
+                "chain_launches": rp.prof["chain"]["launches"], "chain_iters": rp.prof["chain"]["units"],
+                "fused_iters": rp.prof["fused"]["units"], "n_kernels": r.n_kernels,
+                "lo0": float(r.lo[0][0]) if r.n_surv else None}
+        a, b = row["fused"], row["chain"]
+        row["same"] = (a["iters"], a["n_surv"], a["status"]) == (b["iters"], b["n_surv"], b["status"])
+        print(json.dumps(row), flush=True)

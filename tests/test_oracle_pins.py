@@ -326,3 +326,24 @@ def test_tiny_box_enclosure_is_tight():
         w = 1e-10
         e = oracle.eval_box(fid, x - w, x + w)
         assert e[1] - e[0] < 1e-5, (fid, e)
+
+
+# ------------------------------------ true values at arbitrary points (50 digits)
+@pytest.mark.parametrize("fid", list(range(11)))
+def test_point_and_box_enclosures_contain_50_digit_values(fid):
+    """or_F at points and over boxes contains f(x) evaluated from the Appendix A
+    formula in 50-digit arithmetic (tests/hpfun.py) at random points of the
+    paper's domain: catches a dropped term, a wrong sign or index anywhere in
+    or_F, not only at the special points above."""
+    from tests import hpfun
+
+    rng = np.random.default_rng(4000 + fid)
+    for n in (1, 3, 7):
+        l, u = workloads.bounds(fid, n)
+        lo, hi = workloads.random_boxes(4100 + fid + n, n, 6, l, u)
+        for b in range(lo.shape[0]):
+            for p in lo[b] + rng.uniform(0, 1, (4, n)) * (hi[b] - lo[b]):
+                p = np.minimum(np.maximum(p, lo[b]), hi[b])
+                true = hpfun.f(fid, p)
+                assert hp.contains(oracle.eval_point(fid, p), true), (fid, n, p)
+                assert hp.contains(oracle.eval_box(fid, lo[b], hi[b]), true), (fid, n, b)
