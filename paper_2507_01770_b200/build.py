@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libibnb.so")
 SOURCES = ["bnb_kernels.cu", "search.cu", "runtime.cu"]
-HEADERS = ["ival.cuh", "objectives.cuh", "scan.cuh", "kernels.cuh"]
+HEADERS = ["ival.cuh", "objectives.cuh", "scan.cuh", "kernels.cuh", "chain.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
 

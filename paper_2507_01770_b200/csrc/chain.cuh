@@ -184,7 +184,10 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
   // every live record is in a hot index of one entry
   if (blk == 0) list_small_dev(w.pool, ctl, w.hot0, w.hot1, w.sel_slot, w.sel_code, P.kids);
   grid.sync();
-  if (__ldcg(&ctl->done) || __ldcg(&ctl->B) != 1ull) return;  // uniform
+  if (__ldcg(&ctl->done) || __ldcg(&ctl->B) != 1ull) {  // uniform
+    if (blk == 0 && t == 0) atomicAdd(&cb.exits[6], 1ull);
+    return;
+  }
   const unsigned long long iter0 = __ldcg(&ctl->iter), max_iter = ctl->max_iter;
   const unsigned long long pcount0 = __ldcg(&ctl->pcount);
   const double eps_f = ctl->eps_f, eps_x = ctl->eps_x;
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
   __syncthreads();
 
   unsigned long long sum_cand = 0, nwidth = 0;
-  int k = 0;
+  int k = 0, why = 0;
   for (;; ++k) {
     const int sl = k % 3;
     double* T = s_T[k & 1];
@@ -336,6 +339,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     }
     const double gub = okey_inv(gub_key);
     bool cont = np <= (unsigned long long)PCAP;
+    why = 2;
     if (cont) {
       const int npi = (int)np;
       if (t < npi) {
@@ -377,15 +381,16 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
       __syncthreads();
       const unsigned ns = s_ns;
       cont = ns == 1;
+      why = ns == 0 ? 0 : 1;
       if (cont) {
         // the next list phase on the single live record (list_small_dev's
         // decisions): stop test (lines 148-150), iteration limit, budget
         if (__dsub_ru(gub, s_lb) <= eps_f) {
           nwidth += 1;
-          if (s_wsurv <= eps_x) cont = false;
+          if (s_wsurv <= eps_x) cont = false, why = 3;
         }
-        if (iter0 + (unsigned long long)k + 1 >= max_iter) cont = false;
-        if (k + 1 >= iters) cont = false;
+        if (cont && iter0 + (unsigned long long)k + 1 >= max_iter) cont = false, why = 4;
+        if (cont && k + 1 >= iters) cont = false, why = 5;
       }
       if (cont) sum_cand += s_nc;
     }
@@ -433,6 +438,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
   // iterations 0 .. k-1 ended inside the chain; iteration k is ended by the
   // insertion below and the next launch's list phase (pending end)
   double* T = s_T[k & 1];
+  if (blk == 0 && t == 0) atomicAdd(&cb.exits[why], 1ull);
   const int slot = (int)w.free_list[__ldcg(&ctl->free_top) - 1];  // archive slot of R (prep's choice)
   for (int i = i0 + t; i < i1; i += TPB) {
     w.dst_lo[(size_t)slot * P.ld + i] = s_lo[i - i0];

@@ -148,6 +148,9 @@ struct ChainBufs {
   double* plb;               // [3][PCAP] their lower bounds
   double* part;              // [2][grid][CH_PART] slice partials
   double* tabn;              // [2][DM_MAX * ENT] entries of the next chunk
+  unsigned long long* exits;  // [8] why launches left the chain (trace statistics): 0 no survivor,
+                              // 1 several survivors, 2 > PCAP potential candidates, 3 stop test,
+                              // 4 iteration limit, 5 launch budget, 6 nothing to chain at entry
   int per;                   // variables per block slice
   int pad;
 };

@@ -345,6 +345,7 @@ static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
   w.chain.plb = A.take<double>(3 * PCAP);
   w.chain.part = A.take<double>((size_t)2 * chain_grid() * CH_PART);
   w.chain.tabn = A.take<double>((size_t)2 * DM_MAX * ENT);
+  w.chain.exits = A.take<unsigned long long>(8);
   w.chain.per = chain_per(n);
   w.root_out = A.take<double>(2);
   w.f_search = A.take<double>(1);
@@ -615,6 +616,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   if (trace) {
     CK(cudaMalloc(&tstamp, 32 * sizeof(unsigned long long)));
     CK(cudaMemsetAsync(tstamp, 0, 32 * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(w.chain.exits, 0, 8 * sizeof(unsigned long long), st));
     ib.tstamp = tstamp;
   }
   struct FreeOnExit {
@@ -871,6 +873,12 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
 #endif
     fprintf(stderr, "\n[ibnb] slowest block's own work per phase (us/iter):");
     for (int k = 0; k < 6; ++k) fprintf(stderr, " %s=%.2f", ph[k], tsh[8 + k] / it / 1e3);
+    unsigned long long ex[8];
+    CK(cudaMemcpyAsync(ex, w.chain.exits, sizeof ex, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const char* why[7] = {"no_survivor", "several_survivors", "over_pcap", "stop", "max_iter", "budget", "entry"};
+    fprintf(stderr, "\n[ibnb] chain launches %ld, exits:", chain_launches);
+    for (int k = 0; k < 7; ++k) fprintf(stderr, " %s=%llu", why[k], ex[k]);
     fprintf(stderr, "\n");
   }
   // exact max width of the remaining regions for the result
