@@ -184,6 +184,12 @@ def child_box(plo, phi, cyc: int, d: int, m: int, code: int):
     return clo, chi
 
 
+def _mono(mono) -> int:
+    """first-order test mode: False/0 off, True/1 the split variables
+    (R4), 2 every variable (PAPER.md lines 142-144 as printed)"""
+    return 2 if mono == 2 else int(bool(mono))
+
+
 def branch(fid, plo, phi, pcyc, d, m, l, u, mono=True, gub_in=float("inf")):
     """One branch-and-bound iteration on an explicit batch of parent boxes.
 
@@ -201,7 +207,7 @@ def branch(fid, plo, phi, pcyc, d, m, l, u, mono=True, gub_in=float("inf")):
     cnt = ctypes.c_long(0)
     gub = ctypes.c_double(0.0)
     rc = lib().or_branch(fid, n, nb, _d(plo), _d(phi), pcyc.ctypes.data_as(_ip), int(d), int(m),
-                         _d(l), _d(u), int(bool(mono)), float(gub_in), ctypes.byref(gub), cap,
+                         _d(l), _d(u), _mono(mono), float(gub_in), ctypes.byref(gub), cap,
                          par.ctypes.data_as(_ip), code.ctypes.data_as(_lp), _d(lb), _d(w),
                          ctypes.byref(cnt))
     if rc < 0:
@@ -219,7 +225,7 @@ def solve(fid, l, u, eps_f=1e-6, eps_x=1e-6, d=10, m=2, bmax=4096, mono=True,
     slb = np.zeros(cap)
     res = SolveResult()
     rc = lib().or_solve(fid, n, _d(l), _d(u), float(eps_f), float(eps_x), int(d), int(m),
-                        int(bmax), int(bool(mono)), int(max_iter), int(cap), int(search),
+                        int(bmax), _mono(mono), int(max_iter), int(cap), int(search),
                         _d(slo), _d(shi),
                         _d(slb), ctypes.byref(res))
     if rc < 0:

@@ -93,10 +93,14 @@ static double box_width(int n, const double* lo, const double* hi) {
     return w;
 }
 
-/* first-order test, applied to the split variables */
-static int monotone_pruned(int fid, int n, const ia_t* X, int cyc, int d, const double* l,
-                           const double* u) {
-    for (int j = 0; j < d; ++j) {
+/* first-order test: "for any i in {1, 2, ..., n}, if
+ * DLB_i > 0 and X_i.lo != l_i ... if DUB_i < 0 and X_i.hi != u_i".
+ * mono == 2: every variable, as printed; mono == 1: the d split variables
+ * only (reading R4; identical for separable objectives). */
+static int monotone_pruned(int fid, int n, const ia_t* X, int cyc, int d, int mono,
+                           const double* l, const double* u) {
+    int nv = mono == 2 ? n : d;
+    for (int j = 0; j < nv; ++j) {
         int i = (cyc + j) % n;
         ia_t D = or_dF(fid, n, X, i);
         if (D.lo > 0.0 && X[i].lo != l[i]) return 1;
@@ -137,7 +141,7 @@ int or_branch(int fid, int n, int nb, const double* plo, const double* phi, cons
             for (int i = 0; i < n; ++i) X[i] = ia_make(clo[i], chi[i]);
             double lb = canon_lb(or_F(fid, n, X).lo);
             if (!(lb <= gub)) continue;
-            if (mono && monotone_pruned(fid, n, X, pcyc[b], d, l, u)) continue;
+            if (mono && monotone_pruned(fid, n, X, pcyc[b], d, mono, l, u)) continue;
             if (cnt < cap) {
                 out_parent[cnt] = b;
                 out_code[cnt] = c;

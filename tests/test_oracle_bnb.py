@@ -245,3 +245,63 @@ def test_solve_trace_gub_monotone_and_attained():
         assert rec["gub_after"] <= rec["gub_before"]
         prev = rec["gub_after"]
     assert r["gub"] == prev
+
+
+# ------------------------------ first-order test over every variable (R4)
+def test_first_order_all_variables_prunes_on_an_unsplit_variable():
+    """PAPER.md lines 142-144 test "any i in {1, ..., n}".  Rastrigin (A14),
+    n = 2, d = 1: the parent is split along x_1 only; x_2 in [0.1, 0.2] is
+    unsplit, interior and f is increasing in it there (2 x + 20 pi sin(2 pi x)
+    > 0 on (0, 0.25)), so mono = 2 rules out every child and mono = 1 (split
+    variable only, R4) keeps those the bound keeps.  A loop that
+    stopped at the split variables would fail the first assertion."""
+    fid, n, d, m = 7, 2, 1, 2
+    l, u = workloads.bounds(fid, n)
+    plo, phi = np.array([[-0.5, 0.1]]), np.array([[0.5, 0.2]])
+    cyc = np.zeros(1, np.int32)
+    assert oracle.grad_box(fid, plo[0], phi[0], 1)[0] > 0.0
+    g2, par2, *_ = oracle.branch(fid, plo, phi, cyc, d, m, l, u, mono=2)
+    g1, par1, *_ = oracle.branch(fid, plo, phi, cyc, d, m, l, u, mono=1)
+    assert len(par2) == 0
+    assert len(par1) > 0
+
+
+@pytest.mark.parametrize("fid", list(range(1, 11)))
+def test_first_order_all_variables_superset_and_justified(fid):
+    """mono = 2 rules out a superset of mono = 1, and every child only it
+    rules out has a variable outside the split chunk with a sign-definite
+    derivative (or_grad_box) off the domain edge."""
+    n, d, m = 4, 2, 2
+    l, u = workloads.bounds(fid, n)
+    plo, phi = workloads.random_boxes(500 + fid, n, 8, l, u, mix=(0, 0, 0.3, 0.4, 0.3, 0))
+    cyc = np.array([0, 1, 2, 3, 0, 1, 2, 3], np.int32)
+    _, p1, c1, *_ = oracle.branch(fid, plo, phi, cyc, d, m, l, u, mono=1)
+    _, p2, c2, *_ = oracle.branch(fid, plo, phi, cyc, d, m, l, u, mono=2)
+    s1 = set(zip(p1.tolist(), c1.tolist()))
+    s2 = set(zip(p2.tolist(), c2.tolist()))
+    assert s2 <= s1
+    for b, c in s1 - s2:
+        clo, chi = oracle.child_box(plo[b], phi[b], int(cyc[b]), d, m, c)
+        split = {(int(cyc[b]) + j) % n for j in range(d)}
+        ok = False
+        for i in set(range(n)) - split:
+            g = oracle.grad_box(fid, clo, chi, i)
+            if (g[0] > 0 and clo[i] != l[i]) or (g[1] < 0 and chi[i] != u[i]):
+                ok = True
+        assert ok
+
+
+@pytest.mark.parametrize("fid,search", [(0, 0), (3, 0), (4, 32), (7, 0), (7, 32)])
+def test_first_order_split_only_equals_all_variables_for_separable(fid, search):
+    """For a separable objective d f / d x_i depends on x_i alone, and every
+    variable of a region of L was tested (as a split variable) when it took
+    its current range, or still spans [l_i, u_i] (on the edge): the split-only
+    test of R4 and the test over all n variables give the same solve."""
+    n, d = 6, 2
+    l, u = workloads.bounds(fid, n)
+    r1 = oracle.solve(fid, l, u, 1e-6, 1e-6, d=d, m=2, bmax=16, mono=1, search=search, max_iter=3000)
+    r2 = oracle.solve(fid, l, u, 1e-6, 1e-6, d=d, m=2, bmax=16, mono=2, search=search, max_iter=3000)
+    assert r1["status"] == r2["status"]
+    assert (r1["iters"], r1["evals"], r1["n_surv"]) == (r2["iters"], r2["evals"], r2["n_surv"])
+    np.testing.assert_array_equal(r1["lo"], r2["lo"])
+    np.testing.assert_array_equal(r1["hi"], r2["hi"])
