@@ -160,6 +160,20 @@ __device__ __forceinline__ void chain_combine(const double* part, int G, Iv* acc
   wmax = rw;
 }
 
+// first-order test of child `code` of the bisection table T (one thread):
+// separable objectives read the per-entry flags, the others take
+// child_mono_ok (bit-identical to the warp version of the other paths)
+template <class F>
+__device__ __forceinline__ bool chain_fo_ok(const Problem& P, const double* T, uint32_t code) {
+  if constexpr (F::SEP) {
+    for (int j = 0; j < P.d; ++j)
+      if (T[HDR + (size_t)(2 * j + ((code >> j) & 1u)) * ENT + E_T + 4 * F::K + 2 * F::KG] != 0.0) return false;
+    return true;
+  } else {
+    return child_mono_ok<F>(P, T, code);
+  }
+}
+
 template <class F>
 __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBufs cb, int iters) {
   cg::grid_group grid = cg::this_grid();
@@ -246,6 +260,15 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
 
   unsigned long long sum_cand = 0, nwidth = 0;
   int k = 0, why = 0;
+  // phase timer (IBNB_TRACE): block 0, thread 0, ns per part into tstamp[26..31]
+  unsigned long long* ts = (w.tstamp && blk == 0 && t == 0) ? w.tstamp : nullptr;
+  unsigned long long tb = ts ? gtimer() : 0ull;
+#define CH_TICK(slot)                      \
+  if (ts) {                                \
+    const unsigned long long tn = gtimer(); \
+    ts[slot] += tn - tb;                   \
+    tb = tn;                               \
+  }
   for (;; ++k) {
     const int sl = k % 3;
     double* T = s_T[k & 1];
@@ -300,6 +323,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
           const double lb = canon_lb(outer_lo<F>(B, n));
           w.clb[code] = lb;
           const bool pot = lb <= gub0;
+          bool keep = pot;
           if (pot) {  // midpoint sample (line 134): rare, recombined from the midpoint terms
             Iv Bm[2];
 #pragma unroll
@@ -310,11 +334,15 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
               for (int q = 0; q < F::K; ++q) Bm[q] = acc_comb<F>(q, Bm[q], get(e + 2 * q));
             }
             best = fmin(best, outer_hi<F>(Bm, n));
+            // the first-order test (lines 142-144) does not depend on GUB:
+            // taken here, so the list holds only children it keeps
+            if (P.mono) keep = chain_fo_ok<F>(P, T, code);
           }
-          chain_append(cnt, pc, pl, pot, code, lb);
+          chain_append(cnt, pc, pl, keep, code, lb);
         }
       }
     }
+    CH_TICK(26)
     // (b) S_excl of R over this block's slice, outside chunks c and c'
     chain_slice_partial<F>(P, s_lo, s_hi, i0, i1, c, cn, cb.part + ((size_t)(k & 1) * G + blk) * CH_PART);
     // (c) entries of chunk c' (unchanged in every child of R)
@@ -330,7 +358,9 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
         if (best < CUDART_INF) atomicMin(&cb.gacc[sl], (unsigned long long)okey(best));
       }
     }
+    CH_TICK(27)
     grid.sync();
+    CH_TICK(28)
     // ================= phase 2 (every block, same decisions)
     const unsigned long long np = __ldcg(&cb.cnt[sl]);
     {
@@ -351,22 +381,19 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
         s_ns = 0;
       }
       __syncthreads();
-      // candidates (lb <= GUB): width and first-order test, a warp each
+      // candidates (lb <= GUB; the first-order test was taken in phase 1):
+      // width, a warp each
       for (int q = t >> 5; q < npi; q += TPB / 32) {
         if (!(s_pl[q] <= gub)) continue;  // warp-uniform
         const uint32_t code = s_pc[q];
         double wl = 0.0;
-        bool bad = false;
         if (lane < d) {
           const double* e = T + HDR + (size_t)(2 * lane + ((code >> lane) & 1u)) * ENT;
           wl = __dsub_rn(e[E_HI], e[E_LO]);
-          if constexpr (F::SEP) bad = e[E_T + 4 * F::K + 2 * F::KG] != 0.0;
         }
         wl = warp_max(wl);
-        unsigned anybad = __ballot_sync(0xffffffffu, bad);
-        if constexpr (!F::SEP) anybad = (!P.mono || child_mono_ok_warp<F>(P, T, code)) ? 0u : 1u;
         if (lane == 0) {
-          const bool ok = !P.mono || anybad == 0u;
+          const bool ok = true;
           s_ok[q] = ok;
           s_w[q] = fmax(T[H_WREST], wl);
           atomicAdd(&s_nc, 1u);
@@ -394,6 +421,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
       }
       if (cont) sum_cand += s_nc;
     }
+    CH_TICK(29)
     if (!cont) break;  // uniform: every block took the same decisions
     // ---- continue: the survivor R' becomes the selected region
     const uint32_t scode = s_code;
@@ -433,7 +461,10 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     }
     __syncthreads();
     c = cn;
+    CH_TICK(30)
+    if (ts) ts[31] += 1;
   }
+#undef CH_TICK
   // ================= leave the chain at iteration k (all blocks)
   // iterations 0 .. k-1 ended inside the chain; iteration k is ended by the
   // insertion below and the next launch's list phase (pending end)

@@ -877,6 +877,10 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
     CK(cudaMemcpyAsync(ex, w.chain.exits, sizeof ex, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const char* why[7] = {"no_survivor", "several_survivors", "over_pcap", "stop", "max_iter", "budget", "entry"};
+    if (tsh[31])
+      fprintf(stderr, "\n[ibnb] chain phases over %llu iterations (us/iter, block 0): children=%.2f slice=%.2f "
+              "barrier=%.2f candidates=%.2f next_table=%.2f", tsh[31], tsh[26] / 1e3 / tsh[31], tsh[27] / 1e3 / tsh[31],
+              tsh[28] / 1e3 / tsh[31], tsh[29] / 1e3 / tsh[31], tsh[30] / 1e3 / tsh[31]);
     fprintf(stderr, "\n[ibnb] chain launches %ld, exits:", chain_launches);
     for (int k = 0; k < 7; ++k) fprintf(stderr, " %s=%llu", why[k], ex[k]);
     fprintf(stderr, "\n");
