@@ -11,7 +11,7 @@ LIB = os.path.join(HERE, "libibnb.so")
 SOURCES = ["bnb_kernels.cu", "search.cu", "runtime.cu"]
 HEADERS = ["ival.cuh", "objectives.cuh", "scan.cuh", "kernels.cuh", "chain.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-diag-suppress", "20281", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
 
 
 def nvcc() -> str:

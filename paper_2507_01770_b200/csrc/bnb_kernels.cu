@@ -160,11 +160,10 @@ __device__ __forceinline__ LevyChunk levy_chunk(int c, int d, int n) {
   return q;
 }
 
-// prep: one block reduction of the rest accumulators of the box (acc) and of
-// its midpoint (accm) and of the max unsplit width, in a single pass
-// (results valid in thread 0); Levy reduces one chain sum each
-template <class F, int BS>
-__device__ __forceinline__ void block_reduce_prep(Iv* acc, Iv* accm, double& wmax) {
+// warp level of block_reduce_prep (xor butterfly: every lane ends with the
+// same bits, the combinations are commutative)
+template <class F>
+__device__ __forceinline__ void warp_reduce_prep(Iv* acc, Iv* accm, double& wmax) {
   constexpr int K = F::CHAIN ? 1 : F::K;
   auto comb = [](int k, Iv a, Iv b) -> Iv {
     if constexpr (F::CHAIN) return a + b;
@@ -181,6 +180,19 @@ __device__ __forceinline__ void block_reduce_prep(Iv* acc, Iv* accm, double& wma
     }
     wmax = fmax(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
   }
+}
+
+// prep: one block reduction of the rest accumulators of the box (acc) and of
+// its midpoint (accm) and of the max unsplit width, in a single pass
+// (results valid in thread 0); Levy reduces one chain sum each
+template <class F, int BS>
+__device__ __forceinline__ void block_reduce_prep(Iv* acc, Iv* accm, double& wmax) {
+  constexpr int K = F::CHAIN ? 1 : F::K;
+  auto comb = [](int k, Iv a, Iv b) -> Iv {
+    if constexpr (F::CHAIN) return a + b;
+    else return acc_comb<F>(k, a, b);
+  };
+  warp_reduce_prep<F>(acc, accm, wmax);
   if constexpr (BS > 32) {
     __shared__ Iv s_a[BS / 32][2], s_m[BS / 32][2];
     __shared__ double s_w[BS / 32];

@@ -78,7 +78,7 @@ __device__ __forceinline__ void chain_append(unsigned long long* cnt, uint32_t* 
 // not in chunk c2), max width of those variables -> part (thread 0)
 template <class F>
 __device__ __forceinline__ void chain_slice_partial(const Problem& P, const double* s_lo, const double* s_hi, int i0,
-                                                    int i1, int c1, int c2, double* part) {
+                                                    int i1, int c1, int c2, double* part, double* keep) {
   const int n = P.n, d = P.d;
   Iv acc[2], accm[2];
 #pragma unroll
@@ -110,9 +110,143 @@ __device__ __forceinline__ void chain_slice_partial(const Problem& P, const doub
     for (int k = 0; k < 2; ++k) {
       put(part + 2 * k, acc[k]);
       put(part + 4 + 2 * k, accm[k]);
+      put(keep + 2 * k, acc[k]);
+      put(keep + 4 + 2 * k, accm[k]);
     }
-    part[8] = wmax;
+    part[8] = keep[8] = wmax;
+    part[9] = keep[9] = 0.0;
   }
+}
+
+// first-order test of child `code` of the bisection table T (one thread):
+// separable objectives read the per-entry flags, the others take
+// child_mono_ok (bit-identical to the warp version of the other paths)
+template <class F>
+__device__ __forceinline__ bool chain_fo_ok(const Problem& P, const double* T, uint32_t code) {
+  if constexpr (F::SEP) {
+    for (int j = 0; j < P.d; ++j)
+      if (T[HDR + (size_t)(2 * j + ((code >> j) & 1u)) * ENT + E_T + 4 * F::K + 2 * F::KG] != 0.0) return false;
+    return true;
+  } else {
+    return child_mono_ok<F>(P, T, code);
+  }
+}
+
+// does chunk {c, ..., c + d - 1} (mod n) meet the slice [i0, i1)?
+__device__ __forceinline__ bool meets(int i0, int i1, int c, int d, int n) {
+  if (i0 >= i1) return false;
+  const int e = c + d;  // exclusive end, may pass n (wrap)
+  if (e <= n) return c < i1 && i0 < e;
+  return (c < i1) || (i0 < e - n);
+}
+
+// children phase output: potential-candidate list of the iteration and the
+// child lower bounds (clb[code], written for the listed children, or for
+// every child when `all` -- the exit path's static-tile insertion)
+struct ChainOut {
+  unsigned long long* cnt;
+  uint32_t* pc;
+  double* pl;
+  double* clb;
+  bool all;
+};
+
+// group size 2^H of the children phase: enough groups (2^(d - H)) for every
+// thread of the grid (148 x 256 < 2^16), at most 8 children per thread
+__device__ __forceinline__ int chain_h(int d) { return max(1, min(3, d - 15)); }
+
+// one child (code) of table T with accumulators B (lower bound), the
+// midpoint sample and the first-order test for a potential candidate
+template <class F>
+__device__ __forceinline__ void chain_leaf(const Problem& P, const double* T, double gub0, const ChainOut& o,
+                                           uint32_t code, const Iv* B, double& best) {
+  const double lb = canon_lb(outer_lo<F>(B, P.n));
+  if (o.all) {
+    o.clb[code] = lb;
+    return;
+  }
+  const bool pot = lb <= gub0;
+  bool keep = pot;
+  if (pot) {  // midpoint sample (line 134): rare, recombined from the midpoint terms
+    o.clb[code] = lb;
+    Iv Bm[2];
+#pragma unroll
+    for (int q = 0; q < F::K; ++q) Bm[q] = get(T + H_RESTM + 2 * q);
+    for (int jj = 0; jj < P.d; ++jj) {
+      const double* e = T + HDR + (size_t)(2 * jj + ((code >> jj) & 1u)) * ENT + E_T + 2 * F::K;
+#pragma unroll
+      for (int q = 0; q < F::K; ++q) Bm[q] = acc_comb<F>(q, Bm[q], get(e + 2 * q));
+    }
+    best = fmin(best, outer_hi<F>(Bm, P.n));
+    // the first-order test (lines 142-144) does not depend on GUB: taken
+    // here, so the list holds only children it keeps
+    if (P.mono) keep = chain_fo_ok<F>(P, T, code);
+  }
+  chain_append(o.cnt, o.pc, o.pl, keep, code, lb);
+}
+
+// the 2^J children below accumulators A: bit J-1 first, then the lower bits
+// (summation order rest, d-1 .. H, H-1 .. 0 for every child)
+template <class F, int J>
+struct ChainTree {
+  __device__ __forceinline__ static void run(const Problem& P, const double* T, double gub0, const ChainOut& o,
+                                             uint32_t code, const Iv* A, double& best) {
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const double* e = T + HDR + (size_t)(2 * (J - 1) + b) * ENT + E_T;
+      Iv B[2];
+#pragma unroll
+      for (int q = 0; q < F::K; ++q) B[q] = acc_comb<F>(q, A[q], get(e + 2 * q));
+      ChainTree<F, J - 1>::run(P, T, gub0, o, code | ((uint32_t)b << (J - 1)), B, best);
+    }
+  }
+};
+template <class F>
+struct ChainTree<F, 0> {
+  __device__ __forceinline__ static void run(const Problem& P, const double* T, double gub0, const ChainOut& o,
+                                             uint32_t code, const Iv* A, double& best) {
+    chain_leaf<F>(P, T, gub0, o, code, A, best);
+  }
+};
+
+// lower bounds of the m^d children of table T (bisection), a thread per
+// group of 2^H; returns this thread's midpoint minimum
+template <class F, int H>
+__device__ __forceinline__ double chain_children(const Problem& P, const double* T, double gub0, const ChainOut& o) {
+  const int d = P.d;
+  const int ng = 1 << (d - H);
+  const int G = gridDim.x;
+  const int gpb = (ng + G - 1) / G;
+  const int gb = blockIdx.x * gpb, ge = min(ng, gb + gpb);
+  double best = CUDART_INF;
+  for (int gi = gb + threadIdx.x; gi < ge; gi += TPB) {
+    const uint32_t code0 = (uint32_t)gi << H;
+    Iv A[2];
+#pragma unroll
+    for (int q = 0; q < F::K; ++q) A[q] = get(T + H_REST + 2 * q);
+    int j = d - 1;
+    // batches of 4 pieces (loads issued together), highest variable first
+    for (; j - 3 >= H; j -= 4) {
+      Iv tt[4][2];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double* e = T + HDR + (size_t)(2 * (j - u) + ((code0 >> (j - u)) & 1u)) * ENT + E_T;
+#pragma unroll
+        for (int q = 0; q < F::K; ++q) tt[u][q] = get(e + 2 * q);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < F::K; ++q) A[q] = acc_comb<F>(q, A[q], tt[u][q]);
+    }
+    for (; j >= H; --j) {
+      const double* e = T + HDR + (size_t)(2 * j + ((code0 >> j) & 1u)) * ENT + E_T;
+#pragma unroll
+      for (int q = 0; q < F::K; ++q) A[q] = acc_comb<F>(q, A[q], get(e + 2 * q));
+    }
+    ChainTree<F, H>::run(P, T, gub0, o, code0, A, best);
+  }
+  return best;
 }
 
 // entries of chunk c (pieces of its d variables) for the variables in this
@@ -160,20 +294,6 @@ __device__ __forceinline__ void chain_combine(const double* part, int G, Iv* acc
   wmax = rw;
 }
 
-// first-order test of child `code` of the bisection table T (one thread):
-// separable objectives read the per-entry flags, the others take
-// child_mono_ok (bit-identical to the warp version of the other paths)
-template <class F>
-__device__ __forceinline__ bool chain_fo_ok(const Problem& P, const double* T, uint32_t code) {
-  if constexpr (F::SEP) {
-    for (int j = 0; j < P.d; ++j)
-      if (T[HDR + (size_t)(2 * j + ((code >> j) & 1u)) * ENT + E_T + 4 * F::K + 2 * F::KG] != 0.0) return false;
-    return true;
-  } else {
-    return child_mono_ok<F>(P, T, code);
-  }
-}
-
 template <class F>
 __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBufs cb, int iters) {
   cg::grid_group grid = cg::this_grid();
@@ -181,8 +301,10 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
   constexpr int TS = HDR + 2 * D_MAX * ENT;  // bisection tables (m = 2, d <= 16)
   __shared__ double s_T[2][TS];
   __shared__ uint32_t s_pc[PCAP];
-  __shared__ double s_pl[PCAP], s_w[PCAP];
-  __shared__ uint8_t s_ok[PCAP];
+  __shared__ double s_pl[PCAP];
+  __shared__ Iv s_ra[TPB / 32][2], s_rm[TPB / 32][2];
+  __shared__ double s_rw[TPB / 32];
+  __shared__ double s_my[CH_PART];  // this block's last published slice partial
   __shared__ uint32_t s_code;
   __shared__ double s_lb, s_wsurv;
   __shared__ unsigned int s_nc, s_ns;
@@ -232,7 +354,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
   }
   __syncthreads();
   // rest accumulators of R0 (variables outside chunk c) and its chunk entries
-  chain_slice_partial<F>(P, s_lo, s_hi, i0, i1, c, -1, cb.part + ((size_t)1 * G + blk) * CH_PART);
+  chain_slice_partial<F>(P, s_lo, s_hi, i0, i1, c, -1, cb.part + ((size_t)1 * G + blk) * CH_PART, s_my);
   chain_chunk_entries<F>(P, s_lo, s_hi, i0, i1, c, cb.tabn);
   if (blk == 0 && t == 0) {
     for (int q = 0; q < 3; ++q) {
@@ -259,7 +381,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
   __syncthreads();
 
   unsigned long long sum_cand = 0, nwidth = 0;
-  int k = 0, why = 0;
+  int k = 0, why = 0, cprev = c;
   // phase timer (IBNB_TRACE): block 0, thread 0, ns per part into tstamp[26..31]
   unsigned long long* ts = (w.tstamp && blk == 0 && t == 0) ? w.tstamp : nullptr;
   unsigned long long tb = ts ? gtimer() : 0ull;
@@ -280,71 +402,28 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
       cb.cnt[(k + 1) % 3] = 0ull;
       cb.gacc[(k + 1) % 3] = ~0ull;
     }
-    // (a) children: a thread owns the pair of children of a code with bit 0 clear
+    // (a) children: a thread owns the 2^H children of a code whose H low bits
+    // are clear (enough groups for every thread of the grid, H <= 3)
     double best = CUDART_INF;
     {
-      const int ng = 1 << (d - 1);
-      const int gpb = (ng + G - 1) / G;
-      const int gb = blk * gpb, ge = min(ng, gb + gpb);
-      unsigned long long* cnt = cb.cnt + sl;
-      uint32_t* pc = cb.pcode + (size_t)sl * PCAP;
-      double* pl = cb.plb + (size_t)sl * PCAP;
-      for (int gi = gb + t; gi < ge; gi += TPB) {
-        const uint32_t code0 = (uint32_t)gi << 1;
-        Iv A[2];
-#pragma unroll
-        for (int q = 0; q < F::K; ++q) A[q] = get(T + H_REST + 2 * q);
-        int j = 1;
-        for (; j + 4 <= d; j += 4) {
-          Iv tt[4][2];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const double* e = T + HDR + (size_t)(2 * (j + u) + ((code0 >> (j + u)) & 1u)) * ENT + E_T;
-#pragma unroll
-            for (int q = 0; q < F::K; ++q) tt[u][q] = get(e + 2 * q);
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int q = 0; q < F::K; ++q) A[q] = acc_comb<F>(q, A[q], tt[u][q]);
-        }
-        for (; j < d; ++j) {
-          const double* e = T + HDR + (size_t)(2 * j + ((code0 >> j) & 1u)) * ENT + E_T;
-#pragma unroll
-          for (int q = 0; q < F::K; ++q) A[q] = acc_comb<F>(q, A[q], get(e + 2 * q));
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          Iv B[2];
-          const double* e0 = T + HDR + (size_t)h * ENT + E_T;
-#pragma unroll
-          for (int q = 0; q < F::K; ++q) B[q] = acc_comb<F>(q, A[q], get(e0 + 2 * q));
-          const uint32_t code = code0 | (uint32_t)h;
-          const double lb = canon_lb(outer_lo<F>(B, n));
-          w.clb[code] = lb;
-          const bool pot = lb <= gub0;
-          bool keep = pot;
-          if (pot) {  // midpoint sample (line 134): rare, recombined from the midpoint terms
-            Iv Bm[2];
-#pragma unroll
-            for (int q = 0; q < F::K; ++q) Bm[q] = get(T + H_RESTM + 2 * q);
-            for (int jj = 0; jj < d; ++jj) {
-              const double* e = T + HDR + (size_t)(2 * jj + ((code >> jj) & 1u)) * ENT + E_T + 2 * F::K;
-#pragma unroll
-              for (int q = 0; q < F::K; ++q) Bm[q] = acc_comb<F>(q, Bm[q], get(e + 2 * q));
-            }
-            best = fmin(best, outer_hi<F>(Bm, n));
-            // the first-order test (lines 142-144) does not depend on GUB:
-            // taken here, so the list holds only children it keeps
-            if (P.mono) keep = chain_fo_ok<F>(P, T, code);
-          }
-          chain_append(cnt, pc, pl, keep, code, lb);
-        }
+      ChainOut o{cb.cnt + sl, cb.pcode + (size_t)sl * PCAP, cb.plb + (size_t)sl * PCAP, w.clb, false};
+      switch (chain_h(d)) {
+        case 1: best = chain_children<F, 1>(P, T, gub0, o); break;
+        case 2: best = chain_children<F, 2>(P, T, gub0, o); break;
+        default: best = chain_children<F, 3>(P, T, gub0, o); break;
       }
     }
     CH_TICK(26)
-    // (b) S_excl of R over this block's slice, outside chunks c and c'
-    chain_slice_partial<F>(P, s_lo, s_hi, i0, i1, c, cn, cb.part + ((size_t)(k & 1) * G + blk) * CH_PART);
+    // (b) S_excl of R over this block's slice, outside chunks c and c'; a
+    // slice that meets none of them (nor the chunk the last iteration changed)
+    // republishes the bits of its previous partial (the full slice sum)
+    {
+      double* dst = cb.part + ((size_t)(k & 1) * G + blk) * CH_PART;
+      if (meets(i0, i1, c, d, n) || meets(i0, i1, cn, d, n) || (k > 0 && meets(i0, i1, cprev, d, n)))
+        chain_slice_partial<F>(P, s_lo, s_hi, i0, i1, c, cn, dst, s_my);
+      else if (t < CH_PART)
+        dst[t] = s_my[t];
+    }
     // (c) entries of chunk c' (unchanged in every child of R)
     chain_chunk_entries<F>(P, s_lo, s_hi, i0, i1, cn, cb.tabn + (size_t)((k + 1) & 1) * DM_MAX * ENT);
     // (d) this block's midpoint minimum
@@ -362,50 +441,85 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     grid.sync();
     CH_TICK(28)
     // ================= phase 2 (every block, same decisions)
+    // every L2 load of the phase is issued first (one round trip): counts,
+    // midpoint minimum, potential candidates, slice partials, the entries of
+    // chunk c' (into Tn: the table of iteration k - 1 is no longer read)
     const unsigned long long np = __ldcg(&cb.cnt[sl]);
-    {
-      const unsigned long long gk = __ldcg(&cb.gacc[sl]);
-      if (gk < gub_key) gub_key = gk;
+    const unsigned long long gk = __ldcg(&cb.gacc[sl]);
+    uint32_t my_pc = 0;
+    double my_pl = CUDART_INF;
+    if (t < PCAP) {
+      my_pc = __ldcg(&cb.pcode[(size_t)sl * PCAP + t]);
+      my_pl = __ldcg(&cb.plb[(size_t)sl * PCAP + t]);
     }
+    Iv ra[2], rm[2];
+    double rw = 0.0;
+    {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) ra[q] = rm[q] = iv(0.0);
+#pragma unroll
+      for (int q = 0; q < F::K; ++q) ra[q] = rm[q] = acc_ident<F>(q);
+      const double* part = cb.part + (size_t)(k & 1) * G * CH_PART;
+      for (int q = t; q < G; q += TPB) {  // G <= TPB: one partial per thread
+        const double* pt = part + (size_t)q * CH_PART;
+#pragma unroll
+        for (int kk = 0; kk < F::K; ++kk) {
+          ra[kk] = acc_comb<F>(kk, ra[kk], Iv{__ldcg(pt + 2 * kk), __ldcg(pt + 2 * kk + 1)});
+          rm[kk] = acc_comb<F>(kk, rm[kk], Iv{__ldcg(pt + 4 + 2 * kk), __ldcg(pt + 5 + 2 * kk)});
+        }
+        rw = fmax(rw, __ldcg(pt + 8));
+      }
+      const double* en = cb.tabn + (size_t)((k + 1) & 1) * DM_MAX * ENT;
+      for (int q = t; q < tabw; q += TPB) Tn[HDR + q] = __ldcg(&en[q]);
+    }
+    if (gk < gub_key) gub_key = gk;
     const double gub = okey_inv(gub_key);
-    bool cont = np <= (unsigned long long)PCAP;
-    why = 2;
-    if (cont) {
-      const int npi = (int)np;
+    const bool fits = np <= (unsigned long long)PCAP;
+    const int npi = fits ? (int)np : 0;
+    // warp level of the (fixed-order) reduction of the slice partials
+    warp_reduce_prep<F>(ra, rm, rw);
+    {
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < F::K; ++q) {
+          s_ra[t >> 5][q] = ra[q];
+          s_rm[t >> 5][q] = rm[q];
+        }
+        s_rw[t >> 5] = rw;
+      }
       if (t < npi) {
-        s_pc[t] = __ldcg(&cb.pcode[(size_t)sl * PCAP + t]);
-        s_pl[t] = __ldcg(&cb.plb[(size_t)sl * PCAP + t]);
+        s_pc[t] = my_pc;
+        s_pl[t] = my_pl;
       }
       if (t == 0) {
         s_nc = 0;
         s_ns = 0;
       }
-      __syncthreads();
-      // candidates (lb <= GUB; the first-order test was taken in phase 1):
-      // width, a warp each
-      for (int q = t >> 5; q < npi; q += TPB / 32) {
-        if (!(s_pl[q] <= gub)) continue;  // warp-uniform
-        const uint32_t code = s_pc[q];
-        double wl = 0.0;
-        if (lane < d) {
-          const double* e = T + HDR + (size_t)(2 * lane + ((code >> lane) & 1u)) * ENT;
-          wl = __dsub_rn(e[E_HI], e[E_LO]);
-        }
-        wl = warp_max(wl);
-        if (lane == 0) {
-          const bool ok = true;
-          s_ok[q] = ok;
-          s_w[q] = fmax(T[H_WREST], wl);
-          atomicAdd(&s_nc, 1u);
-          if (ok) {
-            atomicAdd(&s_ns, 1u);
-            s_code = code;  // the survivor when it is the only one
-            s_lb = s_pl[q];
-            s_wsurv = s_w[q];
-          }
-        }
+    }
+    __syncthreads();
+    // candidates (lb <= GUB; the first-order test was taken in phase 1): the
+    // survivors and their widths, a warp each
+    for (int q = t >> 5; q < npi; q += TPB / 32) {
+      if (!(s_pl[q] <= gub)) continue;  // warp-uniform
+      const uint32_t code = s_pc[q];
+      double wl = 0.0;
+      if (lane < d) {
+        const double* e = T + HDR + (size_t)(2 * lane + ((code >> lane) & 1u)) * ENT;
+        wl = __dsub_rn(e[E_HI], e[E_LO]);
       }
-      __syncthreads();
+      wl = warp_max(wl);
+      if (lane == 0) {
+        atomicAdd(&s_nc, 1u);
+        atomicAdd(&s_ns, 1u);
+        s_code = code;  // the survivor when it is the only one
+        s_lb = s_pl[q];
+        s_wsurv = fmax(T[H_WREST], wl);
+      }
+    }
+    __syncthreads();
+    bool cont = fits;
+    why = 2;
+    if (cont) {
       const unsigned ns = s_ns;
       cont = ns == 1;
       why = ns == 0 ? 0 : 1;
@@ -425,41 +539,44 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     if (!cont) break;  // uniform: every block took the same decisions
     // ---- continue: the survivor R' becomes the selected region
     const uint32_t scode = s_code;
-    {
-      Iv ra[2], rm[2];
-      double rw;
-      chain_combine<F>(cb.part + (size_t)(k & 1) * G * CH_PART, G, ra, rm, rw);
-      if (t == 0) {
-        // rest(R') = S_excl + terms of R' in chunk c (not in c', n >= 2d)
-        for (int j = 0; j < d; ++j) {
-          const double* e = T + HDR + (size_t)(2 * j + ((scode >> j) & 1u)) * ENT;
+    if (t == 0) {
+      // block level of the partials' reduction (block_reduce_prep's order),
+      // then rest(R') = S_excl + terms of R' in chunk c (not in c', n >= 2d)
+      for (int wq = 1; wq < TPB / 32; ++wq) {
 #pragma unroll
-          for (int q = 0; q < F::K; ++q) {
-            ra[q] = acc_comb<F>(q, ra[q], get(e + E_T + 2 * q));
-            rm[q] = acc_comb<F>(q, rm[q], get(e + E_T + 2 * F::K + 2 * q));
-          }
-          rw = fmax(rw, __dsub_rn(e[E_HI], e[E_LO]));
+        for (int q = 0; q < F::K; ++q) {
+          ra[q] = acc_comb<F>(q, ra[q], s_ra[wq][q]);
+          rm[q] = acc_comb<F>(q, rm[q], s_rm[wq][q]);
         }
-        for (int q = 0; q < 2; ++q) {
-          put(Tn + H_REST + 2 * q, ra[q]);
-          put(Tn + H_RESTM + 2 * q, rm[q]);
-        }
-        Tn[H_WREST] = rw;
-        Tn[H_CHUNK] = (double)cn;
+        rw = fmax(rw, s_rw[wq]);
       }
-      const double* en = cb.tabn + (size_t)((k + 1) & 1) * DM_MAX * ENT;
-      for (int q = t; q < tabw; q += TPB) Tn[HDR + q] = __ldcg(&en[q]);
-      // slice update: chunk c variables take the survivor's pieces
-      for (int j = t; j < d; j += TPB) {
-        const int i = (c + j) % n;
-        if (i >= i0 && i < i1) {
-          const double* e = T + HDR + (size_t)(2 * j + ((scode >> j) & 1u)) * ENT;
-          s_lo[i - i0] = e[E_LO];
-          s_hi[i - i0] = e[E_HI];
+      for (int j = 0; j < d; ++j) {
+        const double* e = T + HDR + (size_t)(2 * j + ((scode >> j) & 1u)) * ENT;
+#pragma unroll
+        for (int q = 0; q < F::K; ++q) {
+          ra[q] = acc_comb<F>(q, ra[q], get(e + E_T + 2 * q));
+          rm[q] = acc_comb<F>(q, rm[q], get(e + E_T + 2 * F::K + 2 * q));
         }
+        rw = fmax(rw, __dsub_rn(e[E_HI], e[E_LO]));
+      }
+      for (int q = 0; q < 2; ++q) {
+        put(Tn + H_REST + 2 * q, ra[q]);
+        put(Tn + H_RESTM + 2 * q, rm[q]);
+      }
+      Tn[H_WREST] = rw;
+      Tn[H_CHUNK] = (double)cn;
+    }
+    // slice update: chunk c variables take the survivor's pieces
+    for (int j = t; j < d; j += TPB) {
+      const int i = (c + j) % n;
+      if (i >= i0 && i < i1) {
+        const double* e = T + HDR + (size_t)(2 * j + ((scode >> j) & 1u)) * ENT;
+        s_lo[i - i0] = e[E_LO];
+        s_hi[i - i0] = e[E_HI];
       }
     }
     __syncthreads();
+    cprev = c;
     c = cn;
     CH_TICK(30)
     if (ts) ts[31] += 1;
@@ -501,10 +618,17 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     return;
   }
   // many potential candidates: the static-tile insertion pass over every child
-  // (descriptors zeroed first)
+  // (descriptors zeroed first; the phase wrote clb for listed children only,
+  // so every child's lower bound is recomputed -- same bits)
   {
     const long nz = 3 * (((long)P.kids + TILE - 1) / TILE + 1);
     for (long q = (long)blk * TPB + t; q < nz; q += (long)G * TPB) w.desc2[q] = 0;
+    ChainOut o{nullptr, nullptr, nullptr, w.clb, true};
+    switch (chain_h(d)) {
+      case 1: chain_children<F, 1>(P, T, 0.0, o); break;
+      case 2: chain_children<F, 2>(P, T, 0.0, o); break;
+      default: chain_children<F, 3>(P, T, 0.0, o); break;
+    }
   }
   grid.sync();
   cand_emit_dev<F>(P, ctl, w.tab, w.tab_stride, w.clb, w.new_slot, w.pool, w.desc2, w.hot0, w.hot1);
