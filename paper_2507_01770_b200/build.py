@@ -9,9 +9,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libibnb.so")
 SOURCES = ["bnb_kernels.cu", "search.cu", "runtime.cu"]
-HEADERS = ["ival.cuh", "objectives.cuh", "scan.cuh", "kernels.cuh", "chain.cuh"]
+HEADERS = ["ival.cuh", "objectives.cuh", "scan.cuh", "kernels.cuh", "chain.cuh", "chainc.cuh"]
+# bnb_kernels.cu is compiled once as the common unit and once per objective
+# (-DIBNB_OBJ_TU -DIBNB_FID=f: the kernels templated on that objective only)
+NUM_FIDS = 11
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-diag-suppress", "20281", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-diag-suppress", "20281,177", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
 
 
 def nvcc() -> str:
@@ -37,17 +40,35 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     cflags = [f for f in FLAGS if f != "-shared"] + os.environ.get("IBNB_EXTRA_FLAGS", "").split()
-    objs, procs = [], []
-    for s in SOURCES:
-        o = os.path.join(objdir, s.replace(".cu", ".o"))
-        cmd = [nvcc(), *ARCH, *cflags, "-c", os.path.join(CSRC, s), "-o", o]
+    units = [(s, s.replace(".cu", ".o"), []) for s in SOURCES]
+    units += [("bnb_kernels.cu", f"bnb_obj{f}.o", ["-DIBNB_OBJ_TU", f"-DIBNB_FID={f}"]) for f in range(NUM_FIDS)]
+    # the slow units first; at most os.cpu_count() compilers at a time
+    units.sort(key=lambda u: 0 if u[2] else 1)
+    objs, running = [], []
+    jobs = max(1, os.cpu_count() or 1)
+
+    def reap(block):
+        for item in list(running):
+            name, p = item
+            if block or p.poll() is not None:
+                if p.wait() != 0:
+                    raise subprocess.CalledProcessError(p.returncode, f"nvcc {name}")
+                running.remove(item)
+                if not block:
+                    return
+
+    for src, obj, defs in units:
+        while len(running) >= jobs:
+            reap(False)
+            if len(running) >= jobs:
+                running[0][1].wait()
+        o = os.path.join(objdir, obj)
+        cmd = [nvcc(), *ARCH, *cflags, *defs, "-c", os.path.join(CSRC, src), "-o", o]
         if verbose:
             print(" ".join(cmd))
-        procs.append((s, subprocess.Popen(cmd)))
+        running.append((obj, subprocess.Popen(cmd)))
         objs.append(o)
-    for s, p in procs:
-        if p.wait() != 0:
-            raise subprocess.CalledProcessError(p.returncode, f"nvcc {s}")
+    reap(True)
     cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", LIB + ".tmp"]
     if verbose:
         print(" ".join(cmd))

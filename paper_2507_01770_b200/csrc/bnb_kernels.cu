@@ -36,12 +36,28 @@
 
 namespace cg = cooperative_groups;
 
-namespace ib {
+// every definition of this file (and of chain.cuh / chainc.cuh) lives in a
+// namespace of its own per objective translation unit, so that the units'
+// copies of the non-template device functions do not collide at link time
+#ifdef IBNB_OBJ_TU
+#define IBNB_CAT2(a, b) a##b
+#define IBNB_CAT(a, b) IBNB_CAT2(a, b)
+#define IB_NS_BEGIN namespace ib { inline namespace IBNB_CAT(obj, IBNB_FID) {
+#define IB_NS_END } }
+#else
+#define IB_NS_BEGIN namespace ib {
+#define IB_NS_END }
+#endif
+
+IB_NS_BEGIN
 
 // ------------------------------------------------------------ probes
 // -DIBNB_PROBE builds (diagnosis only): block 0 / thread 0 accumulates the
 // clock64 cycles between probe points of a device function into g_probe
 #ifdef IBNB_PROBE
+#ifdef IBNB_OBJ_TU
+static
+#endif
 __device__ unsigned long long g_probe[64];
 #define PROBE_BEGIN unsigned long long _pt = clock64(), _pd[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #define PROBE(k)                                   \
@@ -1474,11 +1490,13 @@ __device__ void cand_emit_dev(const Problem& P, Ctl* __restrict__ ctl, const dou
   }
 }
 
+#ifndef IBNB_OBJ_TU
 __global__ void __launch_bounds__(TPB) k_cand(const Problem P, Ctl* __restrict__ ctl, const double* __restrict__ clb,
                                               uint32_t* __restrict__ cand, uint64_t* desc, uint32_t* tile_ctr) {
   if (ctl->done) return;
   cand_dev(P, ctl, clb, cand, desc, tile_ctr);
 }
+#endif  // IBNB_OBJ_TU
 template <class F>
 __global__ void __launch_bounds__(TPB, 4) k_mono(Problem P, const Ctl* __restrict__ ctl, const double* __restrict__ tab,
                                                  int tab_stride, const uint32_t* __restrict__ cand,
@@ -1486,6 +1504,7 @@ __global__ void __launch_bounds__(TPB, 4) k_mono(Problem P, const Ctl* __restric
   if (ctl->done) return;
   mono_dev<F>(P, ctl, tab, tab_stride, cand, ok);
 }
+#ifndef IBNB_OBJ_TU
 __global__ void __launch_bounds__(TPB) k_emit(const Problem P, Ctl* __restrict__ ctl, const double* __restrict__ tab,
                                               int tab_stride, const double* __restrict__ clb,
                                               const uint32_t* __restrict__ cand, const uint8_t* __restrict__ ok,
@@ -1495,6 +1514,7 @@ __global__ void __launch_bounds__(TPB) k_emit(const Problem P, Ctl* __restrict__
   emit_dev<ObjExample, false>(P, ctl, tab, tab_stride, clb, cand, ok, new_slot, out, desc, tile_ctr, finish != 0, hot0,
                               hot1);
 }
+#endif  // IBNB_OBJ_TU
 
 // ============================================================ list L kernels
 // Statistics of the live part of L (lb <= GUB, lines 136 and 148-150) and the
@@ -1711,12 +1731,14 @@ __device__ void stats_control_dev(Ctl* ctl, unsigned int* hist, int wstage = 0) 
   }
 }
 
+#ifndef IBNB_OBJ_TU
 __global__ void __launch_bounds__(TPB) k_stats(Pool p, Ctl* ctl, unsigned int* hist) {
   if (ctl->done) return;
   stats_accum_dev(p, ctl, hist);
   if (!last_block(ctl)) return;
   stats_control_dev(ctl, hist);
 }
+#endif  // IBNB_OBJ_TU
 
 // radix pass: histogram of the next digit among live records matching the
 // known prefix; the last block picks the digit
@@ -1746,6 +1768,7 @@ __device__ void radix_accum_dev(const Pool& p, const Ctl* __restrict__ ctl, unsi
     if (s_h[i]) atomicAdd(&hist[i], s_h[i]);
 }
 
+#ifndef IBNB_OBJ_TU
 __global__ void __launch_bounds__(TPB) k_radix(Pool p, Ctl* __restrict__ ctl, unsigned int* hist) {
   if (ctl->done || ctl->resolved) return;
   radix_accum_dev(p, ctl, hist);
@@ -1756,6 +1779,7 @@ __global__ void __launch_bounds__(TPB) k_radix(Pool p, Ctl* __restrict__ ctl, un
   }
   block_pick_digit(ctl, hist);
 }
+#endif  // IBNB_OBJ_TU
 
 // Selection (line 130): the B live records with the smallest (lb, position)
 // are copied, in list order, to the batch arrays and marked dead in L
@@ -1825,11 +1849,13 @@ __device__ void select_dev(const Pool& p, Ctl* __restrict__ ctl, int32_t* sel_sl
   }
   }
 }
+#ifndef IBNB_OBJ_TU
 __global__ void __launch_bounds__(TPB) k_select(Pool p, Ctl* __restrict__ ctl, int32_t* sel_slot, uint32_t* sel_code,
                                                 uint64_t* desc, uint32_t* tile_ctr) {
   if (ctl->done) return;
   select_dev(p, ctl, sel_slot, sel_code, desc, tile_ctr);
 }
+#endif  // IBNB_OBJ_TU
 
 // iteration end: the survivors become part of L
 __device__ void iter_end_dev(Ctl* ctl, long kids) {
@@ -1843,13 +1869,17 @@ __device__ void iter_end_dev(Ctl* ctl, long kids) {
   ctl->iter += 1;
   ctl->evals += ctl->B * (unsigned long long)kids;
 }
+#ifndef IBNB_OBJ_TU
 __global__ void k_iter_end(Ctl* ctl, long kids) { iter_end_dev(ctl, kids); }
+#endif  // IBNB_OBJ_TU
+#ifndef IBNB_OBJ_TU
 __global__ void k_apply_pending(Ctl* ctl, long kids) {
   if (ctl->pending_end) {
     ctl->pending_end = 0;
     iter_end_dev(ctl, kids);
   }
 }
+#endif  // IBNB_OBJ_TU
 
 // ===================================================== list L (cooperative)
 // k_list runs the list phase of an iteration as one cooperative kernel; its
@@ -2334,6 +2364,7 @@ __device__ __noinline__ void list_dev(const Pool& p, Ctl* ctl, unsigned int* his
   }
 }
 
+#ifndef IBNB_OBJ_TU
 __global__ void __launch_bounds__(TPB) k_list(Pool p, Ctl* ctl, unsigned int* hists, int32_t* sel_slot,
                                               uint32_t* sel_code, uint64_t* desc, uint64_t* desc2, uint32_t* tile_ctr,
                                               uint32_t* hot0, uint32_t* hot1, long kids) {
@@ -2343,17 +2374,22 @@ __global__ void __launch_bounds__(TPB) k_list(Pool p, Ctl* ctl, unsigned int* hi
   }
   list_dev(p, ctl, hists, sel_slot, sel_code, desc, desc2, tile_ctr, hot0, hot1, kids);
 }
+#endif  // IBNB_OBJ_TU
 
 // multi-GPU exchange of the incumbent (2 doubles: GUB, finished flag)
+#ifndef IBNB_OBJ_TU
 __global__ void k_xchg_put(const Ctl* ctl, double* xchg) {
   xchg[0] = okey_inv(ctl->gub_key);
   xchg[1] = ctl->done ? 0.0 : -1.0;
 }
+#endif  // IBNB_OBJ_TU
+#ifndef IBNB_OBJ_TU
 __global__ void k_xchg_take(Ctl* ctl, const double* xchg) {
   unsigned long long k = okey(xchg[0]);
   if (k < ctl->gub_key) ctl->gub_key = k;
   ctl->gdone = xchg[1] == 0.0 ? 1 : 0;
 }
+#endif  // IBNB_OBJ_TU
 
 // Stable 3-way partition of L with a host-given selection spec (ib_select,
 // compaction of L, final output).  Live records (lb <= GUB) whose key's top
@@ -2361,6 +2397,7 @@ __global__ void k_xchg_take(Ctl* ctl, const double* xchg) {
 // while their rank among equals is < r_need; the other live records are
 // kept.  known == 0 selects every live record; (known = 64, prefix = 0,
 // r_need = 0) keeps every live record.  counters: 0 lt, 1 eq, 2 gt.
+#ifndef IBNB_OBJ_TU
 __global__ void __launch_bounds__(TPB) k_partition(Pool in, long cnt, const unsigned long long* gub_key,
                                                    int known, unsigned long long prefix,
                                                    unsigned long long r_need, int32_t* sel_slot,
@@ -2437,16 +2474,20 @@ __global__ void __launch_bounds__(TPB) k_partition(Pool in, long cnt, const unsi
   }
   }
 }
+#endif  // IBNB_OBJ_TU
 
 // ---- archive slot garbage collection (mark from L, collect the unmarked)
 // slots still needed: those of the live records (lb <= GUB); selected and
 // ruled-out records (lazy deletion) are never read again
+#ifndef IBNB_OBJ_TU
 __global__ void k_gc_mark(Pool p, const Ctl* ctl, uint8_t* mark) {
   const long cnt = (long)ctl->pcount;
   const double gub = okey_inv(ctl->gub_key);
   for (long r = (long)blockIdx.x * blockDim.x + threadIdx.x; r < cnt; r += (long)gridDim.x * blockDim.x)
     if (p.lb[r] <= gub) mark[p.slot[r]] = 1;
 }
+#endif  // IBNB_OBJ_TU
+#ifndef IBNB_OBJ_TU
 __global__ void __launch_bounds__(TPB) k_gc_collect(const uint8_t* mark, long cap, int32_t* free_list,
                                                     uint64_t* desc, uint32_t* tile_ctr, Ctl* ctl, long ntiles) {
   __shared__ uint32_t s_tile;
@@ -2472,8 +2513,10 @@ __global__ void __launch_bounds__(TPB) k_gc_collect(const uint8_t* mark, long ca
   if (tile == (uint32_t)(ntiles - 1) && threadIdx.x == 0) ctl->free_top = pfx[0] + tot[0];
   }
 }
+#endif  // IBNB_OBJ_TU
 
 // generic stable compaction of indices with key <= threshold (ib_compact_le)
+#ifndef IBNB_OBJ_TU
 __global__ void __launch_bounds__(TPB) k_compact_le(const double* keys, long cnt, double thr, int64_t* out_idx,
                                                     uint64_t* desc, uint32_t* tile_ctr, uint64_t* out_count,
                                                     long ntiles) {
@@ -2500,8 +2543,10 @@ __global__ void __launch_bounds__(TPB) k_compact_le(const double* keys, long cnt
   if (tile == (uint32_t)(ntiles - 1) && threadIdx.x == 0) *out_count = pfx[0] + tot[0];
   }
 }
+#endif  // IBNB_OBJ_TU
 
 // materialise records (slot, code) of L into explicit boxes
+#ifndef IBNB_OBJ_TU
 __global__ void k_extract(Problem P, Pool p, long cnt, const double* A_lo, const double* A_hi,
                           const int32_t* sc, double* out_lo, double* out_hi, double* out_lb) {
   for (long r = blockIdx.x; r < cnt; r += gridDim.x) {
@@ -2525,6 +2570,7 @@ __global__ void k_extract(Problem P, Pool p, long cnt, const double* A_lo, const
     if (threadIdx.x == 0 && out_lb) out_lb[r] = p.lb[r];
   }
 }
+#endif  // IBNB_OBJ_TU
 
 // ========================================================= explicit batches
 // f over explicit boxes: one warp per box, lanes stride over variables,
@@ -2746,9 +2792,10 @@ __global__ void __launch_bounds__(TPB, 1) k_fused(Problem P, IterBufs w, int ite
   }
 }
 
-}  // namespace ib
+IB_NS_END  // namespace ib
 #include "chain.cuh"
-namespace ib {
+#include "chainc.cuh"
+IB_NS_BEGIN
 
 // ================================================================ launchers
 static inline unsigned grid_for(long items, int per_block, unsigned cap = 148u * 32u) {
@@ -2815,6 +2862,146 @@ static cudaError_t coop_launch(K* fn, unsigned grid, cudaStream_t st, A... args)
   return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(TPB), argv, 0, st);
 }
 
+// ---------------------------------------------------------------- per objective
+// The kernels templated on the objective are instantiated in one translation
+// unit per objective (build.py compiles this file once more per fid with
+// -DIBNB_OBJ_TU -DIBNB_FID=f); the common unit reaches them through a table
+// of launchers (ObjLaunch) instead of instantiating all eleven itself.
+
+
+template <class F>
+struct ObjImpl {
+  static void prep(const Problem& P, const IterBufs& w, long nb, const int32_t* fl, cudaStream_t st) {
+    launch_prep_t<F>(P, w, nb, fl, st);
+  }
+  static void eval(const Problem& P, const IterBufs& w, long nk, cudaStream_t st, bool zero) {
+    launch_eval_t<F>(P, w, nk, st, zero);
+  }
+  static void mono(const Problem& P, const IterBufs& w, long nitems, cudaStream_t st) {
+    k_mono<F><<<grid_for(nitems, TPB, 148u * 12u), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.cand, w.ok);
+  }
+  // `iters` iterations in one cooperative launch of k_fused (small batches)
+  static int fused(const Problem& P, const IterBufs& w, int iters, long nz, unsigned grid, cudaStream_t st) {
+    if constexpr (!F::CHAIN) {  // the Levy chain never takes the G = 8 path
+      if (P.m == 2 && P.G == 8) return (int)coop_launch(k_fused<F, 8>, grid, st, P, w, iters, nz);
+    }
+    return (int)coop_launch(k_fused<F, 0>, grid, st, P, w, iters, nz);
+  }
+  // deep-dive chain (chain.cuh): one cooperative launch, one block per SM,
+  // the block slices in dynamic shared memory (2 * per doubles)
+  static int chain(const Problem& P, const IterBufs& w, const ChainBufs& cb, int iters, unsigned sms,
+                   cudaStream_t st) {
+    if constexpr (!F::CHAIN) {
+      const size_t smem = sizeof(double) * 2 * (size_t)cb.per;
+      static size_t attr = 0;  // dynamic shared memory opted in so far (per instantiation)
+      if (smem > attr) {
+        cudaError_t e = cudaFuncSetAttribute((const void*)k_chain<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        attr = smem;
+      }
+      void* argv[] = {(void*)&P, (void*)&w, (void*)&cb, (void*)&iters};
+      return (int)cudaLaunchCooperativeKernel((const void*)k_chain<F>, dim3(sms), dim3(TPB), argv, smem, st);
+    } else {
+      return (int)cudaErrorInvalidValue;
+    }
+  }
+  template <int CS>
+  static int chainc_cs(const Problem& P, const IterBufs& w, const ChainBufs& cb, int iters, cudaStream_t st) {
+    if constexpr (!F::CHAIN) {
+      const size_t smem = chainc_smem(cb.per);
+      static size_t attr = 0;  // dynamic shared memory opted in so far (per instantiation)
+      if (smem > attr) {
+        cudaError_t e = cudaFuncSetAttribute((const void*)k_chainc<F, CS>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+        if (CS > 8) {
+          e = cudaFuncSetAttribute((const void*)k_chainc<F, CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+          if (e != cudaSuccess) return (int)e;
+        }
+        attr = smem;
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(CS);
+      cfg.blockDim = dim3(TPB);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CS;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      return (int)cudaLaunchKernelEx(&cfg, k_chainc<F, CS>, P, w, cb, iters);
+    } else {
+      return (int)cudaErrorInvalidValue;
+    }
+  }
+  static int chainc(const Problem& P, const IterBufs& w, const ChainBufs& cb, int cs, int iters, cudaStream_t st) {
+    return cs == 8 ? chainc_cs<8>(P, w, cb, iters, st) : chainc_cs<16>(P, w, cb, iters, st);
+  }
+  static void eval_boxes(int n, long nbox, const double* lo, const double* hi, long ld, double* out, unsigned g,
+                         cudaStream_t st) {
+    k_eval_boxes<F><<<g, TPB, 0, st>>>(n, nbox, lo, hi, ld, out);
+  }
+  static void eval_grad(int n, long nreq, const double* lo, const double* hi, long ld, const int64_t* req_box,
+                        const int32_t* req_dim, double* out, unsigned g, cudaStream_t st) {
+    k_eval_grad<F><<<g, TPB, 0, st>>>(n, nreq, lo, hi, ld, req_box, req_dim, out);
+  }
+  static const ObjLaunch* table() {
+    static const ObjLaunch t{&prep, &eval, &mono, &fused, &chain, &chainc, &eval_boxes, &eval_grad};
+    return &t;
+  }
+};
+
+#ifdef IBNB_OBJ_TU
+#if IBNB_FID == 0
+using FObj = ObjExample;
+#elif IBNB_FID == 1
+using FObj = ObjAckley;
+#elif IBNB_FID == 2
+using FObj = ObjBelegundu;
+#elif IBNB_FID == 3
+using FObj = ObjBreiman;
+#elif IBNB_FID == 4
+using FObj = ObjFu;
+#elif IBNB_FID == 5
+using FObj = ObjGriewank;
+#elif IBNB_FID == 6
+using FObj = ObjLevy;
+#elif IBNB_FID == 7
+using FObj = ObjRastrigin;
+#elif IBNB_FID == 8
+using FObj = ObjSalomon;
+#elif IBNB_FID == 9
+using FObj = ObjStyblinski;
+#elif IBNB_FID == 10
+using FObj = ObjZabinsky;
+#endif
+IB_NS_END
+namespace ib {  // the exported entry point, outside the per-objective namespace
+const ObjLaunch* IBNB_CAT(obj_launch_, IBNB_FID)() { return ObjImpl<FObj>::table(); }
+}  // namespace ib
+#else  // the common translation unit
+const ObjLaunch* obj_launch_0();
+const ObjLaunch* obj_launch_1();
+const ObjLaunch* obj_launch_2();
+const ObjLaunch* obj_launch_3();
+const ObjLaunch* obj_launch_4();
+const ObjLaunch* obj_launch_5();
+const ObjLaunch* obj_launch_6();
+const ObjLaunch* obj_launch_7();
+const ObjLaunch* obj_launch_8();
+const ObjLaunch* obj_launch_9();
+const ObjLaunch* obj_launch_10();
+static const ObjLaunch* obj_launch(int fid) {
+  static const ObjLaunch* tab[11] = {obj_launch_0(), obj_launch_1(), obj_launch_2(), obj_launch_3(),
+                                     obj_launch_4(), obj_launch_5(), obj_launch_6(), obj_launch_7(),
+                                     obj_launch_8(), obj_launch_9(), obj_launch_10()};
+  return tab[fid];
+}
+
 // One iteration of the hot path: 6 launches (k_list, k_prep, k_child_eval,
 // k_cand, k_mono, k_emit), every kernel reading its sizes and decisions from ctl.
 // pool_bound / bmax: host upper bounds of |L| and B, used for grid sizes.
@@ -2835,11 +3022,11 @@ int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long 
   if (hook) hook->end(3, st);
   // partition (SPSD) + tables (a2, a3)
   if (hook) hook->begin(0, bmax, st);
-  IB_DISPATCH_FID(P.fid, launch_prep_t<F>(P, w, bmax, w.free_list, st));
+  obj_launch(P.fid)->prep(P, w, bmax, w.free_list, st);
   if (hook) hook->end(0, st);
   // bounds of every child + incumbent (a3, a4); zeroes the scan descriptors
   if (hook) hook->begin(1, bmax * kids, st);
-  IB_DISPATCH_FID(P.fid, launch_eval_t<F>(P, w, bmax * kids, st, true));
+  obj_launch(P.fid)->eval(P, w, bmax * kids, st, true);
   if (hook) hook->end(1, st);
   if (hook) hook->exchange(st);
   // rule out (a5): candidates lb <= GUB, then the first-order test
@@ -2847,8 +3034,7 @@ int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long 
   k_cand<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
   if (hook) hook->end(2, st);
   if (hook) hook->begin(4, bmax * kids, st);
-  IB_DISPATCH_FID(P.fid, k_mono<F><<<grid_for(bmax * kids, TPB, 148u * 12u), TPB, 0, st>>>(
-                             P, w.ctl, w.tab, w.tab_stride, w.cand, w.ok));
+  obj_launch(P.fid)->mono(P, w, bmax * kids, st);
   if (hook) hook->end(4, st);
   // insert the survivors into L (a6)
   if (hook) hook->begin(5, bmax * kids, st);
@@ -2866,18 +3052,7 @@ int launch_fused(const Problem& P, const IterBufs& w, int iters, long bmax, cuda
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   unsigned grid = (unsigned)sms;  // one block per SM (launch bounds: co-resident)
   if (const char* e = std::getenv("IBNB_FUSE_GRID")) grid = (unsigned)std::max(1, std::min(atoi(e), sms));
-  cudaError_t e = cudaSuccess;
-  IB_DISPATCH_FID(P.fid, {
-    bool done = false;
-    if constexpr (!F::CHAIN) {  // the Levy chain never takes the G = 8 path
-      if (P.m == 2 && P.G == 8) {
-        e = coop_launch(k_fused<F, 8>, grid, st, P, w, iters, nz);
-        done = true;
-      }
-    }
-    if (!done) e = coop_launch(k_fused<F, 0>, grid, st, P, w, iters, nz);
-  });
-  return (int)e;
+  return obj_launch(P.fid)->fused(P, w, iters, nz, grid, st);
 }
 
 // deep-dive chain (chain.cuh): up to `iters` iterations in one cooperative
@@ -2887,43 +3062,40 @@ int launch_chain(const Problem& P, const IterBufs& w, const ChainBufs& cb, int i
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem = sizeof(double) * 2 * (size_t)cb.per;
-  cudaError_t e = cudaSuccess;
-  IB_DISPATCH_FID(P.fid, {
-    if constexpr (!F::CHAIN) {
-      static bool attr = false;  // per objective (one static per instantiation)
-      if (!attr) {
-        cudaFuncSetAttribute((const void*)k_chain<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        attr = true;
-      }
-      void* argv[] = {(void*)&P, (void*)&w, (void*)&cb, (void*)&iters};
-      e = cudaLaunchCooperativeKernel((const void*)k_chain<F>, dim3(sms), dim3(TPB), argv, smem, st);
-    } else {
-      e = cudaErrorInvalidValue;
-    }
-  });
-  return (int)e;
+  return obj_launch(P.fid)->chain(P, w, cb, iters, (unsigned)sms, st);
+}
+
+size_t chainc_smem(int per) {
+  return sizeof(double) * (2 * (size_t)per + 2 * (size_t)DM_MAX * ENT + 2 * (size_t)PCAP) +
+         sizeof(uint32_t) * 2 * (size_t)PCAP;
+}
+
+int launch_chainc(const Problem& P, const IterBufs& w, const ChainBufs& cb, int cs, int iters, cudaStream_t st) {
+  return obj_launch(P.fid)->chainc(P, w, cb, cs, iters, st);
 }
 
 // steps a2-a6 only, for an explicit batch already in w (ib_branch): the
 // parents are selected, ctl->B = nb, ctl->pcount = 0
 int launch_branch(const Problem& P, const IterBufs& w, long nb, cudaStream_t st) {
   const long kids = P.kids;
-  IB_DISPATCH_FID(P.fid, launch_prep_t<F>(P, w, nb, nullptr, st));
-  IB_DISPATCH_FID(P.fid, launch_eval_t<F>(P, w, nb * kids, st));
+  obj_launch(P.fid)->prep(P, w, nb, nullptr, st);
+  obj_launch(P.fid)->eval(P, w, nb * kids, st, false);
   cudaMemsetAsync(w.desc, 0, sizeof(uint64_t) * (size_t)tiles_for(nb * kids), st);
   cudaMemsetAsync(w.desc2, 0, sizeof(uint64_t) * 2 * (size_t)tiles_for(nb * kids), st);
   cudaMemsetAsync(w.tile_ctr, 0, sizeof(uint32_t) * 4, st);
   k_cand<<<scan_grid(nb * kids), TPB, 0, st>>>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
-  IB_DISPATCH_FID(P.fid, k_mono<F><<<grid_for(nb * kids, TPB, 148u * 12u), TPB, 0, st>>>(P, w.ctl, w.tab,
-                                                                                        w.tab_stride, w.cand, w.ok));
+  obj_launch(P.fid)->mono(P, w, nb * kids, st);
   k_emit<<<scan_grid(nb * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok,
                                                           w.new_slot, w.pool, w.desc2, w.tile_ctr + 1, 0, nullptr, nullptr);
   LAUNCH_OK;
 }
 
+#ifndef IBNB_OBJ_TU
 __global__ void k_zero_w(Ctl* ctl) { ctl->acc_max_w = 0; }
+#endif  // IBNB_OBJ_TU
+#ifndef IBNB_OBJ_TU
 __global__ void __launch_bounds__(TPB) k_final_w(Pool p, Ctl* ctl) { maxw_accum_dev(p, ctl); }
+#endif  // IBNB_OBJ_TU
 // max width of the live records into ctl->acc_max_w (final result)
 int launch_final_width(Pool p, Ctl* ctl, long pool_bound, cudaStream_t st) {
   k_zero_w<<<1, 1, 0, st>>>(ctl);
@@ -2991,7 +3163,7 @@ int launch_eval_boxes(int fid, int n, long nbox, const double* lo, const double*
                       cudaStream_t st) {
   if (nbox <= 0) return 0;
   unsigned g = (unsigned)((nbox * 32 + TPB - 1) / TPB);
-  IB_DISPATCH_FID(fid, k_eval_boxes<F><<<g, TPB, 0, st>>>(n, nbox, lo, hi, ld, out));
+  obj_launch(fid)->eval_boxes(n, nbox, lo, hi, ld, out, g, st);
   LAUNCH_OK;
 }
 
@@ -2999,16 +3171,16 @@ int launch_eval_grad(int fid, int n, long nreq, const double* lo, const double* 
                      const int64_t* req_box, const int32_t* req_dim, double* out, cudaStream_t st) {
   if (nreq <= 0) return 0;
   unsigned g = (unsigned)((nreq * 32 + TPB - 1) / TPB);
-  IB_DISPATCH_FID(fid, k_eval_grad<F><<<g, TPB, 0, st>>>(n, nreq, lo, hi, ld, req_box, req_dim, out));
+  obj_launch(fid)->eval_grad(n, nreq, lo, hi, ld, req_box, req_dim, out, g, st);
   LAUNCH_OK;
 }
 
 #ifdef IBNB_PROBE
 int probe_read(unsigned long long* out) { return (int)cudaMemcpyFromSymbol(out, g_probe, sizeof(g_probe)); }
 #endif
-}  // namespace ib
+IB_NS_END  // namespace ib
 
-namespace ib {
+IB_NS_BEGIN
 // statistics + control + radix passes of an iteration on an explicit list
 // (ib_select): leaves (known, prefix, need) of the B-th smallest key in ctl
 int launch_select_only(Pool p, Ctl* ctl, unsigned int* hist, long n, cudaStream_t st) {
@@ -3017,4 +3189,5 @@ int launch_select_only(Pool p, Ctl* ctl, unsigned int* hist, long n, cudaStream_
   for (int pass = 1; pass < 8; ++pass) k_radix<<<grid_for(n, TPB * 8, 148u * 4u), TPB, 0, st>>>(p, ctl, hist);
   LAUNCH_OK;
 }
-}  // namespace ib
+IB_NS_END  // namespace ib
+#endif  // IBNB_OBJ_TU

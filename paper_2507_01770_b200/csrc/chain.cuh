@@ -50,7 +50,7 @@
 // for bit.
 #pragma once
 
-namespace ib {
+IB_NS_BEGIN
 
 __device__ __forceinline__ bool in_chunk(int i, int c, int d, int n) { return ((i - c + n) % n) < d; }
 
@@ -634,4 +634,4 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
   cand_emit_dev<F>(P, ctl, w.tab, w.tab_stride, w.clb, w.new_slot, w.pool, w.desc2, w.hot0, w.hot1);
 }
 
-}  // namespace ib
+IB_NS_END  // namespace ib

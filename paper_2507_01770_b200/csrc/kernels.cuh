@@ -165,4 +165,23 @@ struct IterHook {
   virtual ~IterHook() {}
 };
 
+// dynamic shared memory of k_chainc (chainc.cuh): the slice (2 per doubles)
+// and the exchange buffers (chunk entries, potential-candidate lists, both
+// parities)
+size_t chainc_smem(int per);
+
+// launchers of the kernels templated on one objective, instantiated in that
+// objective's translation unit (bnb_kernels.cu, -DIBNB_OBJ_TU -DIBNB_FID=f)
+struct ObjLaunch {
+  void (*prep)(const Problem&, const IterBufs&, long, const int32_t*, cudaStream_t);
+  void (*eval)(const Problem&, const IterBufs&, long, cudaStream_t, bool);
+  void (*mono)(const Problem&, const IterBufs&, long, cudaStream_t);
+  int (*fused)(const Problem&, const IterBufs&, int, long, unsigned, cudaStream_t);
+  int (*chain)(const Problem&, const IterBufs&, const ChainBufs&, int, unsigned, cudaStream_t);
+  int (*chainc)(const Problem&, const IterBufs&, const ChainBufs&, int, int, cudaStream_t);
+  void (*eval_boxes)(int, long, const double*, const double*, long, double*, unsigned, cudaStream_t);
+  void (*eval_grad)(int, long, const double*, const double*, long, const int64_t*, const int32_t*, double*, unsigned,
+                    cudaStream_t);
+};
+
 }  // namespace ib

@@ -29,6 +29,7 @@ int launch_iteration(const Problem&, const IterBufs&, long, long, cudaStream_t, 
 int launch_branch(const Problem&, const IterBufs&, long, cudaStream_t);
 int launch_fused(const Problem&, const IterBufs&, int, long, cudaStream_t);
 int launch_chain(const Problem&, const IterBufs&, const ChainBufs&, int, cudaStream_t);
+int launch_chainc(const Problem&, const IterBufs&, const ChainBufs&, int, int, cudaStream_t);
 int launch_select_only(Pool, Ctl*, unsigned int*, long, cudaStream_t);
 int launch_xchg_put(const Ctl*, double*, cudaStream_t);
 int launch_apply_pending(Ctl*, long, cudaStream_t);
@@ -314,6 +315,19 @@ static int chain_grid() {
   return sms;
 }
 static int chain_per(int n) { return (n + chain_grid() - 1) / chain_grid(); }
+// the cluster form of the chain (chainc.cuh): CS CTAs with DSMEM exchange;
+// IBNB_CHAIN=1 forces the grid form, IBNB_CHAIN_CS=8 a cluster of 8
+static int chain_cs() {
+  if (const char* e = std::getenv("IBNB_CHAIN_CS")) return std::atoi(e) == 8 ? 8 : 16;
+  return 16;
+}
+static bool chainc_applies(const Problem& P) {
+  if (const char* e = std::getenv("IBNB_CHAIN"))
+    if (std::atoi(e) != 2) return false;
+  const int cs = chain_cs();
+  const int per = (P.n + cs - 1) / cs;
+  return chainc_smem(per) <= 150u * 1024u;
+}
 // the chain kernel applies (chain.cuh): bisection, the next chunk disjoint
 // from the current one, a non-chain objective, the slices in shared memory
 static bool chain_applies(const Problem& P) {
@@ -638,6 +652,9 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   unsigned long long pcount = 1, free_top = hc.free_top, peak = 1;
   long fused_iters = 0, chain_iters = 0, iter_prev = 0, chain_launches = 0;
   const bool use_chain = chain_applies(P);
+  const bool use_chainc = use_chain && chainc_applies(P);
+  ChainBufs cbc = w.chain;
+  cbc.per = (n + chain_cs() - 1) / chain_cs();
   // iterations per chain launch: the host reads the control block between
   // launches (multi-GPU: the incumbent exchange runs there)
   long chain_budget = xfn ? 64 : 4096;
@@ -685,7 +702,8 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
                        (long)free_top >= 2 && (long)pcount + o.kids <= o.pool_cap;
     if (chain) {
       prof.begin(7, st);
-      CKL(launch_chain(P, ib, w.chain, (int)chain_budget, st));
+      if (use_chainc) CKL(launch_chainc(P, ib, cbc, chain_cs(), (int)chain_budget, st));
+      else CKL(launch_chain(P, ib, w.chain, (int)chain_budget, st));
       prof.end(7, st);
       nk += 1 - chunk * kIterKernels;
       ++chain_launches;

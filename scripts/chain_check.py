@@ -1,5 +1,6 @@
-"""Chain kernel check on the GPU: every paper function solved with the chain
-kernel on and off (IBNB_CHAIN), results and wall time side by side."""
+"""Chain kernel check on the GPU: every paper function solved with the fused
+path (IBNB_CHAIN=0), the grid chain (1) and the cluster chain (2), results
+and wall time side by side."""
 import json
 import os
 import sys
@@ -17,19 +18,19 @@ for n in ns:
     for fid in fids:
         l, u = workloads.bounds(fid, n)
         row = {"fid": fid, "n": n}
-        for mode in ("0", "1"):
+        for mode in ("0", "1", "2"):
             os.environ["IBNB_CHAIN"] = mode
             pb.ib_solve(fid, l, u, 1e-6, 1e-6, pb.options(), surv_cap=4)  # warm-up
             t = time.perf_counter()
             r = pb.ib_solve(fid, l, u, 1e-6, 1e-6, pb.options(profile=0), surv_cap=4)
             dt = time.perf_counter() - t
             rp = pb.ib_solve(fid, l, u, 1e-6, 1e-6, pb.options(profile=1), surv_cap=4)
-            row["chain" if mode == "1" else "fused"] = {
+            row[{"0": "fused", "1": "chain", "2": "chainc"}[mode]] = {
                 "s": round(dt, 4), "status": r.status, "iters": r.iters, "evals": r.evals,
                 "f": [r.f_lo, r.f_hi], "n_surv": r.n_surv, "w": r.max_width,
                 "chain_launches": rp.prof["chain"]["launches"], "chain_iters": rp.prof["chain"]["units"],
                 "fused_iters": rp.prof["fused"]["units"], "n_kernels": r.n_kernels,
                 "lo0": float(r.lo[0][0]) if r.n_surv else None}
-        a, b = row["fused"], row["chain"]
-        row["same"] = (a["iters"], a["n_surv"], a["status"]) == (b["iters"], b["n_surv"], b["status"])
+        key = lambda r: (r["iters"], r["n_surv"], r["status"], r["lo0"])
+        row["same"] = key(row["fused"]) == key(row["chain"]) == key(row["chainc"])
         print(json.dumps(row), flush=True)

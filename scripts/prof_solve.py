@@ -14,8 +14,11 @@ ap.add_argument("--config", type=int, default=1)
 ap.add_argument("--solves", type=int, default=2)
 ap.add_argument("--bmax", type=int, default=0)
 ap.add_argument("--d", type=int, default=0)
+ap.add_argument("--fid", type=int, default=-1, help="a paper function on its own domain at the config's n")
 a = ap.parse_args()
-cfg = workloads.CONFIGS[a.config]
+cfg = dict(workloads.CONFIGS[a.config])
+if a.fid >= 0:
+    cfg.update(fid=a.fid, lo=workloads.PAPER_DOMAIN[a.fid][0], hi=workloads.PAPER_DOMAIN[a.fid][1])
 l, u = workloads.config_bounds(cfg)
 ld = torch.tensor(l, device="cuda")
 ud = torch.tensor(u, device="cuda")
@@ -24,4 +27,8 @@ ws = pb.Workspace(pb.solve_workspace_bytes(cfg["fid"], cfg["n"], o))
 for _ in range(a.solves):
     r = pb.ib_solve_dev(cfg["fid"], ld, ud, cfg["eps"], cfg["eps"], o, workspace=ws)
 torch.cuda.synchronize()
-print(r.iters, r.evals, r.f_lo, r.f_hi, r.n_kernels)
+import json  # noqa: E402
+
+print(json.dumps({"config": a.config, "fid": cfg["fid"], "n": cfg["n"], "iters": r.iters, "evals": r.evals,
+                  "enclosure": [r.f_lo, r.f_hi], "n_kernels": r.n_kernels,
+                  "chain_iters": r.prof["chain"]["units"], "fused_iters": r.prof["fused"]["units"]}))
