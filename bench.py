@@ -43,13 +43,8 @@ import workloads  # noqa: E402
 METRIC = "box-evals/sec"
 UNIT = "box-evals/s"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-FP64_PATH = os.path.join(ROOT, "profiles", "fp64_ops_per_child.json")
-TRAFFIC_PATH = os.path.join(ROOT, "profiles", "traffic_r01.json")
-
-# B200: 148 SMs x 64 FP64 FMA lanes per SM per clock (half the FP32 rate; the
-# 37 TFLOP/s FP64 of the B200 datasheet) -- DESIGN.md "Roofline".
-SMS = 148
-FP64_LANES = 64
+FP64_PEAK_PATH = os.path.join(ROOT, "profiles", "fp64_peak_r02.json")
+FP64_OPS_PATH = os.path.join(ROOT, "profiles", "fp64_ops_r02.json")
 
 # algorithmic HBM bytes of the memory-bound kernels:
 #   list: 12 B (index + lb) per hot entry per pass over the hot index, 8 B per
@@ -60,34 +55,47 @@ HBM_BYTES = {
     "cand": lambda p: 8 * p["units"],
     "emit": lambda p: 13 * p["units"],
 }
-FP64_KERNELS = ("child_eval", "mono", "prep")
+
+
+def fp64_peak():
+    """Measured FP64-pipe peak of this GPU model (scripts/micro/fp64_peak.cu on
+    a B200: DADD / DMUL with .RD / .RU rounding, the instructions interval
+    arithmetic executes, 64 per SM per clock), in T instructions/s."""
+    pk = load_json(FP64_PEAK_PATH) or {}
+    if "fp64_tops_dadd_directed" in pk:
+        return pk["fp64_tops_dadd_directed"], "measured: profiles/fp64_peak_r02.json (DADD/DMUL .RD/.RU)"
+    return 148 * 64 * 1.965e9 / 1e12, "derived: 148 SM x 64 FP64 lanes x 1.965 GHz"
 
 
 def roofline(prof, prof_ms, fid):
-    """Roofline entry of the kernel with the largest device time."""
+    """Roofline entry of the kernel class with the largest device time:
+    executed FP64-pipe instructions per unit of work (ncu, committed in
+    profiles/fp64_ops_r02.json for this objective) x units per launch /
+    average launch time (CUDA events on the solve stream), against the measured
+    FP64-pipe peak; HBM classes against the measured copy bandwidth."""
     dom = max(prof, key=lambda c: prof[c]["ms"])
     pd = prof[dom]
     peaks = load_json(PEAKS_PATH) or {}
     avg_s = pd["ms"] / 1e3 / max(1, pd["launches"])
-    traffic = (load_json(TRAFFIC_PATH) or {}).get(dom)
     if dom in HBM_BYTES:
         hbm = peaks.get("hbm_gbs", 6650.0)
         per_launch = HBM_BYTES[dom](pd) / max(1, pd["launches"])
         ach = per_launch / avg_s / 1e9
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                "traffic": traffic, "algorithmic_bytes_per_launch": per_launch,
+                "traffic": None, "algorithmic_bytes_per_launch": per_launch,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s"}
     else:
-        fp = load_json(FP64_PATH) or {}
-        per_unit = (fp.get(str(fid)) or {}).get(dom)
-        clock_ghz = (peaks.get("sm_max_mhz") or 1965.0) / 1e3
-        peak = SMS * FP64_LANES * 2 * clock_ghz / 1e3  # TFLOP/s
+        ops = ((load_json(FP64_OPS_PATH) or {}).get(str(fid)) or {}).get("kernels", {}).get(dom) or {}
+        per_unit = ops.get("fp64_inst_per_unit")
+        peak, src = fp64_peak()
         units = pd["units"] / max(1, pd["launches"])
         ach = per_unit * units / avg_s / 1e12 if per_unit else None
-        roof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": peak, "unit": "TFLOP/s (FP64)",
-                "frac": (ach / peak) if ach else None, "traffic": traffic, "per_unit_flops": per_unit,
-                "units_per_launch": units,
-                "peak_source": "148 SM x 64 FP64 FMA/clk x 2 flop x sm_max_mhz (DESIGN.md)"}
+        roof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": peak, "unit": "T FP64-pipe instr/s",
+                "frac": (ach / peak) if ach else None, "traffic": ops.get("dram_bytes_per_launch"),
+                "fp64_inst_per_unit": per_unit, "unit_of_work": ops.get("unit"), "units_per_launch": units,
+                "issue_active_pct_ncu": ops.get("issue_active_pct"), "fp64_pipe_pct_ncu": ops.get("fp64_pipe_pct"),
+                "peak_source": src, "counts_source": "ncu sm__sass_thread_inst_executed_op_{dadd,dmul,dfma} "
+                                                     "over one solve, profiles/fp64_ops_r02.json"}
     roof["share_of_step"] = pd["ms"] / max(1e-9, prof_ms)
     roof["avg_launch_us"] = avg_s * 1e6
     return roof
@@ -479,6 +487,32 @@ def main():
                                               "iters": r10.iters, "status": r10.status}
             del ws10
 
+    # ---- the other BASELINE.json configs (one warm-up + one timed solve each,
+    # CUDA events): Ackley n = 10, Griewank n = 100 (m = 3 on the symmetric
+    # domain), Levy n = 1000
+    other = None
+    if rank == 0 and world == 1 and args.config == 4 and not args.no_all_functions:
+        other = {}
+        for ci, m_c, d_c in ((1, 2, 10), (2, 3, 10), (3, 2, 16)):
+            cc = workloads.CONFIGS[ci]
+            lc, uc = workloads.config_bounds(cc)
+            ldc, udc = torch.tensor(lc, device=dev), torch.tensor(uc, device=dev)
+            oc = pb.options(d=d_c, m=m_c)
+            wsc = pb.Workspace(pb.solve_workspace_bytes(cc["fid"], cc["n"], oc), device=dev)
+            pb.ib_solve_dev(cc["fid"], ldc, udc, cc["eps"], cc["eps"], oc, workspace=wsc)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rc_ = pb.ib_solve_dev(cc["fid"], ldc, udc, cc["eps"], cc["eps"], oc, workspace=wsc)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            sec = e0.elapsed_time(e1) / 1e3
+            other[cc["name"]] = {"s": sec, "m": m_c, "d": d_c, "iters": rc_.iters, "evals": rc_.evals,
+                                 "box_evals_per_s": rc_.evals / sec, "enclosure": [rc_.f_lo, rc_.f_hi],
+                                 "regions": rc_.n_surv, "status": rc_.status}
+            del wsc
+
     base = None
     if rank == 0 and world == 1 and not args.no_baseline:
         try:
@@ -511,6 +545,7 @@ def main():
             "cpu_baseline": base,
             "throughput_regime": secondary,
             "time_to_enclose_all_ten_n10000": all_ten,
+            "baseline_configs": other,
             "e2e": e2e,
             "clocks": clocks,
             "gpu_launches": int(sum(r.n_kernels for r in res)),

@@ -1504,6 +1504,15 @@ __global__ void __launch_bounds__(TPB, 4) k_mono(Problem P, const Ctl* __restric
   if (ctl->done) return;
   mono_dev<F>(P, ctl, tab, tab_stride, cand, ok);
 }
+// insertion in one pass (a5 + a6): candidates lb <= GUB, the first-order
+// test, stable compaction of the survivors into L -- k_cand + k_mono + k_emit
+// of the explicit-batch path as one cooperative kernel (static tiles, every
+// block resident)
+template <class F>
+__global__ void __launch_bounds__(TPB) k_insert(Problem P, IterBufs w) {
+  if (w.ctl->done) return;
+  cand_emit_dev<F>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.new_slot, w.pool, w.desc2, w.hot0, w.hot1);
+}
 #ifndef IBNB_OBJ_TU
 __global__ void __launch_bounds__(TPB) k_emit(const Problem P, Ctl* __restrict__ ctl, const double* __restrict__ tab,
                                               int tab_stride, const double* __restrict__ clb,
@@ -2877,6 +2886,12 @@ struct ObjImpl {
   static void eval(const Problem& P, const IterBufs& w, long nk, cudaStream_t st, bool zero) {
     launch_eval_t<F>(P, w, nk, st, zero);
   }
+  static int insert(const Problem& P, const IterBufs& w, long nitems, cudaStream_t st) {
+    static unsigned g_max = 0;
+    if (!g_max) g_max = coop_grid((const void*)k_insert<F>, 4);
+    const unsigned g = (unsigned)std::min((long)g_max, tiles_for(nitems));
+    return (int)coop_launch(k_insert<F>, g, st, P, w);
+  }
   static void mono(const Problem& P, const IterBufs& w, long nitems, cudaStream_t st) {
     k_mono<F><<<grid_for(nitems, TPB, 148u * 12u), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.cand, w.ok);
   }
@@ -2950,7 +2965,7 @@ struct ObjImpl {
     k_eval_grad<F><<<g, TPB, 0, st>>>(n, nreq, lo, hi, ld, req_box, req_dim, out);
   }
   static const ObjLaunch* table() {
-    static const ObjLaunch t{&prep, &eval, &mono, &fused, &chain, &chainc, &eval_boxes, &eval_grad};
+    static const ObjLaunch t{&prep, &eval, &mono, &insert, &fused, &chain, &chainc, &eval_boxes, &eval_grad};
     return &t;
   }
 };
@@ -3002,8 +3017,8 @@ static const ObjLaunch* obj_launch(int fid) {
   return tab[fid];
 }
 
-// One iteration of the hot path: 6 launches (k_list, k_prep, k_child_eval,
-// k_cand, k_mono, k_emit), every kernel reading its sizes and decisions from ctl.
+// One iteration of the hot path: 4 launches (k_list, k_prep, k_child_eval,
+// k_insert), every kernel reading its sizes and decisions from ctl.
 // pool_bound / bmax: host upper bounds of |L| and B, used for grid sizes.
 int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long bmax, cudaStream_t st,
                      IterHook* hook, long list_hint) {
@@ -3029,17 +3044,11 @@ int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long 
   obj_launch(P.fid)->eval(P, w, bmax * kids, st, true);
   if (hook) hook->end(1, st);
   if (hook) hook->exchange(st);
-  // rule out (a5): candidates lb <= GUB, then the first-order test
-  if (hook) hook->begin(2, bmax * kids, st);
-  k_cand<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
-  if (hook) hook->end(2, st);
-  if (hook) hook->begin(4, bmax * kids, st);
-  obj_launch(P.fid)->mono(P, w, bmax * kids, st);
-  if (hook) hook->end(4, st);
-  // insert the survivors into L (a6)
+  // rule out (a5: lb > GUB, the first-order test) and insert the survivors
+  // into L (a6), one pass
   if (hook) hook->begin(5, bmax * kids, st);
-  k_emit<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok, w.new_slot,
-                                                  w.pool, w.desc2, w.tile_ctr + 1, 1, w.hot0, w.hot1);
+  const int ie = obj_launch(P.fid)->insert(P, w, bmax * kids, st);
+  if (ie) return ie;
   if (hook) hook->end(5, st);
   LAUNCH_OK;
 }
@@ -3066,7 +3075,7 @@ int launch_chain(const Problem& P, const IterBufs& w, const ChainBufs& cb, int i
 }
 
 size_t chainc_smem(int per) {
-  return sizeof(double) * (2 * (size_t)per + 2 * (size_t)DM_MAX * ENT + 2 * (size_t)PCAP) +
+  return sizeof(MitmTabs) + sizeof(double) * (2 * (size_t)per + 2 * (size_t)DM_MAX * ENT + 2 * (size_t)PCAP) +
          sizeof(uint32_t) * 2 * (size_t)PCAP;
 }
 

@@ -186,7 +186,7 @@ __device__ __forceinline__ void chain_leaf(const Problem& P, const double* T, do
 }
 
 // the 2^J children below accumulators A: bit J-1 first, then the lower bits
-// (summation order rest, d-1 .. H, H-1 .. 0 for every child)
+// (summation order: rest + tree(H .. d-1), then H-1 .. 0 for every child)
 template <class F, int J>
 struct ChainTree {
   __device__ __forceinline__ static void run(const Problem& P, const double* T, double gub0, const ChainOut& o,
@@ -221,30 +221,106 @@ __device__ __forceinline__ double chain_children(const Problem& P, const double*
   double best = CUDART_INF;
   for (int gi = gb + threadIdx.x; gi < ge; gi += TPB) {
     const uint32_t code0 = (uint32_t)gi << H;
+    // the terms of variables H .. d-1 summed as a balanced tree (depth 4 over
+    // D_MAX slots, identity padding): a short dependence chain instead of
+    // d - H sequential combinations -- another association of the natural
+    // extension's sum, rigorous (§2.1)
+    Iv tt[D_MAX][2];
+#pragma unroll
+    for (int u = 0; u < D_MAX; ++u) {
+      const int j = H + u;
+#pragma unroll
+      for (int q = 0; q < F::K; ++q) {
+        if (j < d) {
+          const double* e = T + HDR + (size_t)(2 * j + ((code0 >> j) & 1u)) * ENT + E_T;
+          tt[u][q] = get(e + 2 * q);
+        } else {
+          tt[u][q] = acc_ident<F>(q);
+        }
+      }
+    }
+#pragma unroll
+    for (int st = 1; st < D_MAX; st *= 2)
+#pragma unroll
+      for (int u = 0; u + st < D_MAX; u += 2 * st)
+#pragma unroll
+        for (int q = 0; q < F::K; ++q) tt[u][q] = acc_comb<F>(q, tt[u][q], tt[u + st][q]);
     Iv A[2];
 #pragma unroll
-    for (int q = 0; q < F::K; ++q) A[q] = get(T + H_REST + 2 * q);
-    int j = d - 1;
-    // batches of 4 pieces (loads issued together), highest variable first
-    for (; j - 3 >= H; j -= 4) {
-      Iv tt[4][2];
+    for (int q = 0; q < F::K; ++q) A[q] = acc_comb<F>(q, get(T + H_REST + 2 * q), tt[0][q]);
+    ChainTree<F, H>::run(P, T, gub0, o, code0, A, best);
+  }
+  return best;
+}
+
+// Meet in the middle: with the split variables cut into a low half (bits
+// 0 .. dl-1 of the child code) and a high half (dl .. d-1), every child's
+// accumulators are ONE combination  RH[h] (+) LO[l]  of two tables built once
+// per iteration and block:  RH[h] = rest (+) terms of the high half chosen by
+// h (increasing j),  LO[l] = terms of the low half chosen by l (increasing
+// j).  The natural interval extension of the sum (§2.1, Eq. 3-6)
+// in another association: rigorous, equal to the oracle's left-to-right
+// evaluation up to rounding (tests/tol.py).  2^dl + 2^dh <= 512 entries.
+constexpr int MITM_MAX = 256;  // entries of one half (d <= 16)
+struct MitmTabs {
+  Iv lo[MITM_MAX][2];
+  Iv rh[MITM_MAX][2];
+};
+
+template <class F>
+__device__ __forceinline__ void mitm_build(const Problem& P, const double* T, MitmTabs& M) {
+  const int d = P.d, dl = d / 2, dh = d - dl;
+  for (int q = threadIdx.x; q < (1 << dl) + (1 << dh); q += blockDim.x) {
+    Iv A[2];
+    if (q < (1 << dl)) {
+      const int l = q;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const double* e = T + HDR + (size_t)(2 * (j - u) + ((code0 >> (j - u)) & 1u)) * ENT + E_T;
+      for (int k = 0; k < 2; ++k) A[k] = iv(0.0);
 #pragma unroll
-        for (int q = 0; q < F::K; ++q) tt[u][q] = get(e + 2 * q);
+      for (int k = 0; k < F::K; ++k) A[k] = acc_ident<F>(k);
+      for (int j = 0; j < dl; ++j) {
+        const double* e = T + HDR + (size_t)(2 * j + ((l >> j) & 1)) * ENT + E_T;
+#pragma unroll
+        for (int k = 0; k < F::K; ++k) A[k] = acc_comb<F>(k, A[k], get(e + 2 * k));
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int k = 0; k < 2; ++k) M.lo[l][k] = A[k];
+    } else {
+      const int h = q - (1 << dl);
 #pragma unroll
-        for (int q = 0; q < F::K; ++q) A[q] = acc_comb<F>(q, A[q], tt[u][q]);
-    }
-    for (; j >= H; --j) {
-      const double* e = T + HDR + (size_t)(2 * j + ((code0 >> j) & 1u)) * ENT + E_T;
+      for (int k = 0; k < 2; ++k) A[k] = iv(0.0);
 #pragma unroll
-      for (int q = 0; q < F::K; ++q) A[q] = acc_comb<F>(q, A[q], get(e + 2 * q));
+      for (int k = 0; k < F::K; ++k) A[k] = get(T + H_REST + 2 * k);
+      for (int j = 0; j < dh; ++j) {
+        const double* e = T + HDR + (size_t)(2 * (dl + j) + ((h >> j) & 1)) * ENT + E_T;
+#pragma unroll
+        for (int k = 0; k < F::K; ++k) A[k] = acc_comb<F>(k, A[k], get(e + 2 * k));
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) M.rh[h][k] = A[k];
     }
-    ChainTree<F, H>::run(P, T, gub0, o, code0, A, best);
+  }
+}
+
+// lower bounds of the 2^d children of table T from the tables M (built and
+// synchronised by the caller): this block's share, a child per thread and
+// step; returns this thread's midpoint minimum
+template <class F>
+__device__ __forceinline__ double chain_children_mitm(const Problem& P, const double* T, const MitmTabs& M,
+                                                      double gub0, const ChainOut& o) {
+  const int d = P.d, dl = d / 2;
+  const uint32_t lmask = (1u << dl) - 1u;
+  const long nk = 1L << d;
+  const long per = (nk + gridDim.x - 1) / gridDim.x;
+  const long cb = (long)blockIdx.x * per, ce = min(nk, cb + per);
+  double best = CUDART_INF;
+  for (long ci = cb + threadIdx.x; ci < ce; ci += blockDim.x) {
+    const uint32_t code = (uint32_t)ci;
+    const uint32_t h = code >> dl, l = code & lmask;
+    Iv B[2];
+#pragma unroll
+    for (int k = 0; k < F::K; ++k) B[k] = acc_comb<F>(k, M.rh[h][k], M.lo[l][k]);
+    chain_leaf<F>(P, T, gub0, o, code, B, best);
   }
   return best;
 }

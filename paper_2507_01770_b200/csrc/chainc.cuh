@@ -61,9 +61,10 @@ __global__ void __launch_bounds__(TPB, 1) k_chainc(Problem P, IterBufs w, ChainB
   const int lane = t & 31, wid = t >> 5;
   const int tabw = d * P.m * ENT;
   const int per = cb.per;
-  double* s_lo = s_dyn;
-  double* s_hi = s_dyn + per;
-  double* x_ent = s_dyn + 2 * per;                      // [2][XENT]
+  MitmTabs& M = *reinterpret_cast<MitmTabs*>(s_dyn);
+  double* s_lo = s_dyn + sizeof(MitmTabs) / sizeof(double);
+  double* s_hi = s_lo + per;
+  double* x_ent = s_lo + 2 * per;                       // [2][XENT]
   double* x_pl = x_ent + 2 * XENT;                      // [2][XCAP]
   uint32_t* x_pc = reinterpret_cast<uint32_t*>(x_pl + 2 * XCAP);  // [2][XCAP]
   const int i0 = blk * per, i1 = min(n, i0 + per);
@@ -146,11 +147,9 @@ __global__ void __launch_bounds__(TPB, 1) k_chainc(Problem P, IterBufs w, ChainB
     double best = CUDART_INF;
     {
       ChainOut o{&x_cnt[par], x_pc + par * XCAP, x_pl + par * XCAP, w.clb, false};
-      switch (chain_h(d)) {
-        case 1: best = chain_children<F, 1>(P, T, gub0, o); break;
-        case 2: best = chain_children<F, 2>(P, T, gub0, o); break;
-        default: best = chain_children<F, 3>(P, T, gub0, o); break;
-      }
+      mitm_build<F>(P, T, M);
+      __syncthreads();
+      best = chain_children_mitm<F>(P, T, M, gub0, o);
     }
     CH_TICK(26)
     if (meets(i0, i1, c, d, n) || meets(i0, i1, cn, d, n) || (k > 0 && meets(i0, i1, cprev, d, n)))
@@ -361,11 +360,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chainc(Problem P, IterBufs w, ChainB
     const long nz = 3 * (((long)P.kids + TILE - 1) / TILE + 1);
     for (long q = (long)blk * TPB + t; q < nz; q += (long)CS * TPB) w.desc2[q] = 0;
     ChainOut o{nullptr, nullptr, nullptr, w.clb, true};
-    switch (chain_h(d)) {
-      case 1: chain_children<F, 1>(P, T, 0.0, o); break;
-      case 2: chain_children<F, 2>(P, T, 0.0, o); break;
-      default: chain_children<F, 3>(P, T, 0.0, o); break;
-    }
+    chain_children_mitm<F>(P, T, M, 0.0, o);  // the tables of T: built in its phase 1
   }
   cl.sync();
   cand_emit_dev<F>(P, ctl, w.tab, w.tab_stride, w.clb, w.new_slot, w.pool, w.desc2, w.hot0, w.hot1);

@@ -176,6 +176,7 @@ struct ObjLaunch {
   void (*prep)(const Problem&, const IterBufs&, long, const int32_t*, cudaStream_t);
   void (*eval)(const Problem&, const IterBufs&, long, cudaStream_t, bool);
   void (*mono)(const Problem&, const IterBufs&, long, cudaStream_t);
+  int (*insert)(const Problem&, const IterBufs&, long, cudaStream_t);
   int (*fused)(const Problem&, const IterBufs&, int, long, unsigned, cudaStream_t);
   int (*chain)(const Problem&, const IterBufs&, const ChainBufs&, int, unsigned, cudaStream_t);
   int (*chainc)(const Problem&, const IterBufs&, const ChainBufs&, int, int, cudaStream_t);

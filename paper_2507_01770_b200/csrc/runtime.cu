@@ -316,24 +316,25 @@ static int chain_grid() {
 }
 static int chain_per(int n) { return (n + chain_grid() - 1) / chain_grid(); }
 // the cluster form of the chain (chainc.cuh): CS CTAs with DSMEM exchange;
-// IBNB_CHAIN=1 forces the grid form, IBNB_CHAIN_CS=8 a cluster of 8
+// IBNB_CHAIN=2 selects it (the grid form is the default), IBNB_CHAIN_CS=8 a
+// cluster of 8
 static int chain_cs() {
   if (const char* e = std::getenv("IBNB_CHAIN_CS")) return std::atoi(e) == 8 ? 8 : 16;
   return 16;
 }
 static bool chainc_applies(const Problem& P) {
-  if (const char* e = std::getenv("IBNB_CHAIN"))
-    if (std::atoi(e) != 2) return false;
+  const char* e = std::getenv("IBNB_CHAIN");
+  if (!e || std::atoi(e) != 2) return false;  // opt-in (IBNB_CHAIN=2)
   const int cs = chain_cs();
   const int per = (P.n + cs - 1) / cs;
-  return chainc_smem(per) <= 150u * 1024u;
+  return chainc_smem(per) <= 170u * 1024u;
 }
 // the chain kernel applies (chain.cuh): bisection, the next chunk disjoint
 // from the current one, a non-chain objective, the slices in shared memory
 static bool chain_applies(const Problem& P) {
   if (const char* e = std::getenv("IBNB_CHAIN"))
     if (std::atoi(e) == 0) return false;
-  return P.m == 2 && P.fid != 6 && P.n >= 2 * P.d && P.d >= 2 && 16L * chain_per(P.n) <= 150L * 1024;
+  return P.m == 2 && P.fid != 6 && P.n >= 2 * P.d && P.d >= 2 && 16L * chain_per(P.n) <= 130L * 1024;
 }
 
 static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
@@ -643,7 +644,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   hook.xuser = xuser;
   hook.xchg = xchg;
   hook.ctl = w.ctl;
-  const int kIterKernels = 6;  // kernels per iteration (launch_iteration)
+  const int kIterKernels = 4;  // kernels per iteration (launch_iteration)
 
   // fused-kernel thresholds (IBNB_FUSE_KIDS / IBNB_FUSE_POOL override; 0 = off)
   long fuse_kids = 1L << 20, fuse_pool = 1L << 16;

@@ -32,7 +32,8 @@ for arg in sys.argv[2:]:
         c = kclass(r[ki])
         if c:
             per[c][r[ii]][r[mi]] = float(r[vi].replace(",", ""))
-    units = {"chain": info["chain_iters"], "fused": info["fused_iters"], "child_eval": info["evals"]}
+    units = dict(info.get("units", {}))
+    units.update({"chain": info["chain_iters"], "fused": info["fused_iters"], "child_eval": info["evals"]})
     res = {}
     for c, launches in per.items():
         fp = sum(m.get(k, 0.0) for m in launches.values() for k in FP)
@@ -46,7 +47,8 @@ for arg in sys.argv[2:]:
         w = [m.get("gpu__time_duration.sum", 0.0) for m in launches.values()]
         wavg = lambda xs: sum(a * b for a, b in zip(xs, w)) / max(1e-9, sum(w)) if xs else None
         res[c] = {"launches": len(launches), "fp64_inst": fp, "units": u,
-                  "unit": {"chain": "iteration", "fused": "iteration", "child_eval": "child box"}.get(c),
+                  "unit": {"chain": "iteration", "fused": "iteration", "child_eval": "child box", "prep": "parent",
+                           "mono": "candidate", "emit": "candidate", "cand": "child box"}.get(c),
                   "fp64_inst_per_unit": fp / u if u else None, "ncu_ms": ns / 1e6,
                   "issue_active_pct": wavg(issue), "fp64_pipe_pct": wavg(pipe),
                   "dram_bytes_per_launch": dram / max(1, len(launches))}

@@ -31,4 +31,5 @@ import json  # noqa: E402
 
 print(json.dumps({"config": a.config, "fid": cfg["fid"], "n": cfg["n"], "iters": r.iters, "evals": r.evals,
                   "enclosure": [r.f_lo, r.f_hi], "n_kernels": r.n_kernels,
-                  "chain_iters": r.prof["chain"]["units"], "fused_iters": r.prof["fused"]["units"]}))
+                  "chain_iters": r.prof["chain"]["units"], "fused_iters": r.prof["fused"]["units"],
+                  "units": {c: v["units"] for c, v in r.prof.items()}}))

@@ -402,6 +402,64 @@ def test_full_size_n10000_paper_domains(pb, fid):
         assert o[0] <= r.f_hi + tol(fid, a, b)
 
 
+# ------------------------------------------------------------ BASELINE configs[2] and [3] as solves
+def test_baseline_config2_griewank_n100_full_solve_parity(pb):
+    """BASELINE configs[2]: Griewank n = 100 on [-600, 600]^100 (symmetric:
+    m = 3), eps = 1e-6, R9 search on, a whole
+    solve against the oracle's: iterations, evaluations and every surviving
+    region bit for bit, the enclosure within the tolerance and around f* = 0
+    (d = 3 so that the O(n)-per-child oracle finishes in seconds)."""
+    cfg = workloads.CONFIGS[2]
+    l, u = workloads.config_bounds(cfg)
+    o = oracle.solve(cfg["fid"], l, u, 1e-6, 1e-6, d=3, m=3, bmax=1, max_iter=4000, search=32)
+    g = pb.ib_solve(cfg["fid"], l, u, 1e-6, 1e-6, pb.options(d=3, m=3, bmax=1, max_iter=4000, search=32))
+    t = tol(cfg["fid"], l, u)
+    assert g.status == o["status"] == 0
+    assert g.iters == o["iters"] and g.evals == o["evals"]
+    assert abs(g.f_lo - o["glb"]) <= t and abs(g.f_hi - o["gub"]) <= t
+    assert g.f_lo <= 0.0 <= g.f_hi + t and g.f_hi - g.f_lo <= 1e-6
+    assert g.n_surv == o["n_surv"]
+    np.testing.assert_array_equal(g.lo, o["lo"])
+    np.testing.assert_array_equal(g.hi, o["hi"])
+
+
+def test_baseline_config3_levy_n1000_first_iterations_parity(pb):
+    """BASELINE configs[3]: Levy n = 1000 on [-10, 10]^1000.  The oracle's
+    search costs minutes at n = 1000, so the first 6 iterations run with the
+    search off on both sides (incumbent from the midpoint samples alone, many
+    live regions, batches of 2): iterations, evaluations and every region of L
+    bit for bit."""
+    cfg = workloads.CONFIGS[3]
+    l, u = workloads.config_bounds(cfg)
+    o = oracle.solve(cfg["fid"], l, u, 1e-6, 1e-6, d=8, m=2, bmax=2, max_iter=6, search=0, cap=1 << 12)
+    g = pb.ib_solve(cfg["fid"], l, u, 1e-6, 1e-6, pb.options(d=8, m=2, bmax=2, max_iter=6, search=-1),
+                    surv_cap=1 << 12)
+    assert g.status == o["status"] == 1
+    assert g.iters == o["iters"] == 6 and g.evals == o["evals"]
+    assert g.n_surv == o["n_surv"] and 30 < g.n_surv <= 1 << 12
+    t = tol(cfg["fid"], l, u)
+    assert abs(g.f_hi - o["gub"]) <= t
+    key = lambda lo, hi: sorted(zip(map(tuple, lo), map(tuple, hi)))
+    assert key(g.lo, g.hi) == key(o["lo"], o["hi"])
+
+
+def test_baseline_config3_levy_n1000_full_solve(pb):
+    """BASELINE configs[3] solved to eps = 1e-6 in the bench's launch
+    configuration (d = 16, search on): the enclosure holds f* = 0 (x* = 1,
+    Appendix A) with width <= eps, the regions hold x*, and the oracle
+    recomputes every surviving region's lower bound."""
+    cfg = workloads.CONFIGS[3]
+    l, u = workloads.config_bounds(cfg)
+    r = pb.ib_solve_dev(cfg["fid"], cuda(l), cuda(u), 1e-6, 1e-6, pb.options(d=16), surv_cap=16)
+    assert r.status == 0
+    assert r.f_lo <= 1e-12 and -1e-12 <= r.f_hi and r.f_hi - r.f_lo <= 1e-6 and r.max_width <= 1e-6
+    lo, hi, lb = r.lo.cpu().numpy(), r.hi.cpu().numpy(), r.lb.cpu().numpy()
+    assert any(np.all(a <= 1.0) and np.all(1.0 <= b) for a, b in zip(lo, hi))
+    for a, b, g in zip(lo, hi, lb):
+        ob = oracle.eval_box(cfg["fid"], a, b)
+        assert abs(ob[0] - g) <= tol(cfg["fid"], a, b)
+
+
 # ------------------------------------------------------------ incumbent exchange hook (multi-GPU)
 @pytest.mark.parametrize("fid,n,d", [(7, 2000, 16), (1, 10, 10)])
 def test_exchange_hook_identity_matches_plain_solve(pb, fid, n, d):
@@ -620,6 +678,35 @@ def test_solve_parity_at_headline_chunk_sizes(pb, monkeypatch, fid, n, d, eps, s
     assert g.n_surv == o["n_surv"]
     np.testing.assert_array_equal(g.lo, o["lo"])
     np.testing.assert_array_equal(g.hi, o["hi"])
+
+
+@pytest.mark.parametrize("fid,n,d,eps,search", [(7, 24, 8, 1e-6, 32), (1, 30, 8, 1e-6, 32), (5, 27, 8, 1e-6, 32),
+                                                (10, 24, 8, 1e-6, 32), (9, 27, 8, 1e-6, 32), (8, 40, 8, 1e-6, 32),
+                                                (3, 25, 8, 1e-6, 32), (4, 24, 8, 1e-6, 32), (2, 26, 8, 1e-6, 32),
+                                                (7, 24, 8, 1e-6, 0), (1, 24, 8, 1e-4, 0)])
+@pytest.mark.parametrize("chain", ["1", "2"])
+def test_chain_solve_parity(pb, monkeypatch, fid, n, d, eps, search, chain):
+    """Whole solves through the deep-dive chain kernels (n >= 2 d: k_chain on
+    the whole grid, 1; k_chainc on one thread-block cluster, 2), with the R9
+    search on (one region live per iteration) or off (many potential
+    candidates: the static-tile exit path): iterations, evaluations and every
+    surviving region bit for bit against the oracle, the enclosure within the
+    tolerance, and the chain kernel really ran."""
+    monkeypatch.setenv("IBNB_CHAIN", chain)
+    l, u = workloads.bounds(fid, n)
+    bmax = 1 if search > 0 else 4
+    o = _oracle_solve_cached(fid, n, eps, d, bmax, 4000, search)
+    g = pb.ib_solve(fid, l, u, eps, eps, pb.options(d=d, m=2, bmax=bmax, max_iter=4000,
+                                                    search=search if search > 0 else -1))
+    t = tol(fid, l, u)
+    assert g.status == o["status"] == 0
+    assert g.iters == o["iters"] and g.evals == o["evals"] and g.iters >= 2
+    assert abs(g.f_lo - o["glb"]) <= t and abs(g.f_hi - o["gub"]) <= t
+    assert g.n_surv == o["n_surv"]
+    np.testing.assert_array_equal(g.lo, o["lo"])
+    np.testing.assert_array_equal(g.hi, o["hi"])
+    if search > 0:
+        assert g.prof["chain"]["units"] >= g.iters // 2, g.prof["chain"]
 
 
 def _child_surv_oracle(fid, plo, phi, cyc, d, m, code, l, u, gub):
