@@ -14,12 +14,15 @@ case).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun), --mode replicas (default): every GPU runs its own solve of
-the workload (the n = 10,000 deep dive keeps one region live per iteration
-and does not shard -- DESIGN.md "Multi-GPU"); --mode partition: the domain is
-cut into N slabs along x_1, one per rank, and the incumbent GUB is
-all-reduced (MIN, NCCL) after every chunk of iterations.  Time is the max over
-ranks of the device time.  Prints ONE JSON line on rank 0.
+N > 1 (torchrun), --mode partition (default; north_star): the domain is cut
+into N slabs along x_1, one per rank (an exact cover); every rank runs the
+hot path on its slab, the incumbent GUB is all-reduced (MIN, NCCL) after
+every chunk of iterations (<= 64) and regions are rebalanced (NCCL
+send/recv) when the lists skew; the job ends when every rank has its
+eps-enclosure and the reported enclosure is the union's -- strong scaling of
+one solve (time to enclose).  --mode replicas: every GPU runs its own
+independent solve (weak scaling).  Time is the max over ranks of the device
+time.  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -291,7 +294,7 @@ def main():
     ap.add_argument("--no-secondary", action="store_true", help="skip the configs[1] throughput-regime measurement")
     ap.add_argument("--no-all-functions", action="store_true",
                     help="skip the time to enclose of all ten paper functions at n = 10,000")
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "partition"],
+    ap.add_argument("--mode", default="partition", choices=["replicas", "partition"],
                     help="N > 1: independent solves per GPU (replicas) or one domain partitioned into slabs along x_1 "
                          "with the incumbent all-reduced (MIN) every chunk of iterations")
     args = ap.parse_args()
@@ -394,6 +397,34 @@ def main():
 
     # ---- e2e through the public host-buffer API (pinned host buffers)
     e2e = None
+    if world > 1:
+        # N GPUs: the Python API call a user makes per rank, with this step's
+        # inputs copied from pinned host memory and the enclosure read back
+        # inside the timed region; max over ranks
+        lh = torch.tensor(l, dtype=torch.float64).pin_memory()
+        uh = torch.tensor(u, dtype=torch.float64).pin_memory()
+        ms = 0.0
+        ev2 = 0
+        for _ in range(args.steps):
+            flush.fill_(1)
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ld.copy_(lh, non_blocking=True)
+            ud.copy_(uh, non_blocking=True)
+            r2 = solve(opts)
+            enc_h = torch.tensor([r2.f_lo, r2.f_hi], dtype=torch.float64)  # host values: already read back
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+            ev2 += r2.evals
+        tt = torch.tensor([ms, float(ev2)], dtype=torch.float64, device=dev)
+        tmx, tev = tt[:1].clone(), tt[1:].clone()
+        dist.all_reduce(tmx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tev, op=dist.ReduceOp.SUM)
+        e2e = {"value": float(tev.item()) / (float(tmx.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": 2 * n * 8, "d2h_bytes_per_step": int(enc_h.numel() * 8) + 48}
     if world == 1:
         lh = torch.tensor(l, dtype=torch.float64).pin_memory()
         uh = torch.tensor(u, dtype=torch.float64).pin_memory()
