@@ -59,7 +59,9 @@ int ib_num_functions(void);
  * defaults given in brackets. */
 typedef struct {
     int d;            /* variables partitioned per iteration, the variable-cycling
-                         chunk (§3.2) [min(n, 16)], 1 <= d <= 16 */
+                         chunk (§3.2) [min(n, 16)], 1 <= d <= 20
+                         (bench.py: d = 20 at n = 10,000, m^d >= 148 SMs x 2048
+                         threads, the occupancy rule of §3.2) */
     int m;            /* pieces per partitioned variable, uniform partition
                          Eq. (10)-(11) generalised [2 = bisection], 2 <= m <= 8,
                          m^d <= 2^24, d*m <= 64 */

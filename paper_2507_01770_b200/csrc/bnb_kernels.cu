@@ -2907,7 +2907,7 @@ struct ObjImpl {
   static int chain(const Problem& P, const IterBufs& w, const ChainBufs& cb, int iters, unsigned sms,
                    cudaStream_t st) {
     if constexpr (!F::CHAIN) {
-      const size_t smem = sizeof(double) * 2 * (size_t)cb.per;
+      const size_t smem = sizeof(MitmTabs) + sizeof(double) * 2 * (size_t)cb.per;
       static size_t attr = 0;  // dynamic shared memory opted in so far (per instantiation)
       if (smem > attr) {
         cudaError_t e = cudaFuncSetAttribute((const void*)k_chain<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,

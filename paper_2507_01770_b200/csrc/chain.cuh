@@ -132,6 +132,41 @@ __device__ __forceinline__ bool chain_fo_ok(const Problem& P, const double* T, u
   }
 }
 
+// rank of block `blk` among the blocks whose slices (per variables each) meet
+// none of the chunks c, cn and (k > 0) cprev -- the blocks with slice
+// partials and chunk entries to compute leave the children to the others;
+// -1 for a busy block.  nrank: the number of such blocks.
+__device__ __forceinline__ int chain_child_rank(int blk, int G, int per, int n, int d, int c, int cn, int cprev,
+                                                bool with_prev, int& nrank) {
+  int ids[12];
+  int nb = 0;
+  const int starts[3] = {c, cn, cprev};
+  for (int q = 0; q < (with_prev ? 3 : 2); ++q) {
+    const int s = starts[q];
+    const int e = s + d - 1;  // last variable, may pass n - 1 (wrap)
+    int b0 = s / per, b1 = min(e, n - 1) / per;
+    for (int b = b0; b <= b1 && nb < 12; ++b) ids[nb++] = b;
+    if (e >= n)
+      for (int b = 0; b <= (e - n) / per && nb < 12; ++b) ids[nb++] = b;
+  }
+  int busy = 0, before = 0;
+  bool me = false;
+  for (int a = 0; a < nb; ++a) {
+    bool dup = false;
+    for (int z = 0; z < a; ++z) dup |= ids[z] == ids[a];
+    if (dup) continue;
+    ++busy;
+    if (ids[a] < blk) ++before;
+    me |= ids[a] == blk;
+  }
+  nrank = G - busy;
+  if (nb >= 12 || 2 * nrank < G) {  // degenerate (tiny slices): every block shares the children
+    nrank = G;
+    return blk;
+  }
+  return me ? -1 : blk - before;
+}
+
 // does chunk {c, ..., c + d - 1} (mod n) meet the slice [i0, i1)?
 __device__ __forceinline__ bool meets(int i0, int i1, int c, int d, int n) {
   if (i0 >= i1) return false;
@@ -151,9 +186,6 @@ struct ChainOut {
   bool all;
 };
 
-// group size 2^H of the children phase: enough groups (2^(d - H)) for every
-// thread of the grid (148 x 256 < 2^16), at most 8 children per thread
-__device__ __forceinline__ int chain_h(int d) { return max(1, min(3, d - 15)); }
 
 // one child (code) of table T with accumulators B (lower bound), the
 // midpoint sample and the first-order test for a potential candidate
@@ -211,23 +243,29 @@ struct ChainTree<F, 0> {
 
 // lower bounds of the m^d children of table T (bisection), a thread per
 // group of 2^H; returns this thread's midpoint minimum
+// (rank, nrank): this block's share among the blocks that evaluate children
+constexpr int TREE_SLOTS = 16;
 template <class F, int H>
-__device__ __forceinline__ double chain_children(const Problem& P, const double* T, double gub0, const ChainOut& o) {
+__device__ __forceinline__ double chain_children(const Problem& P, const double* T, double gub0, const ChainOut& o,
+                                                 int rank = -1, int nrank = 0) {
   const int d = P.d;
   const int ng = 1 << (d - H);
-  const int G = gridDim.x;
-  const int gpb = (ng + G - 1) / G;
-  const int gb = blockIdx.x * gpb, ge = min(ng, gb + gpb);
+  if (rank < 0) {
+    rank = blockIdx.x;
+    nrank = gridDim.x;
+  }
+  const int gpb = (ng + nrank - 1) / nrank;
+  const int gb = rank * gpb, ge = min(ng, gb + gpb);
   double best = CUDART_INF;
   for (int gi = gb + threadIdx.x; gi < ge; gi += TPB) {
     const uint32_t code0 = (uint32_t)gi << H;
     // the terms of variables H .. d-1 summed as a balanced tree (depth 4 over
-    // D_MAX slots, identity padding): a short dependence chain instead of
+    // TREE_SLOTS slots, identity padding; d - H <= 16): a short dependence chain instead of
     // d - H sequential combinations -- another association of the natural
     // extension's sum, rigorous (§2.1)
-    Iv tt[D_MAX][2];
+    Iv tt[TREE_SLOTS][2];
 #pragma unroll
-    for (int u = 0; u < D_MAX; ++u) {
+    for (int u = 0; u < TREE_SLOTS; ++u) {
       const int j = H + u;
 #pragma unroll
       for (int q = 0; q < F::K; ++q) {
@@ -240,9 +278,9 @@ __device__ __forceinline__ double chain_children(const Problem& P, const double*
       }
     }
 #pragma unroll
-    for (int st = 1; st < D_MAX; st *= 2)
+    for (int st = 1; st < TREE_SLOTS; st *= 2)
 #pragma unroll
-      for (int u = 0; u + st < D_MAX; u += 2 * st)
+      for (int u = 0; u + st < TREE_SLOTS; u += 2 * st)
 #pragma unroll
         for (int q = 0; q < F::K; ++q) tt[u][q] = acc_comb<F>(q, tt[u][q], tt[u + st][q]);
     Iv A[2];
@@ -253,73 +291,87 @@ __device__ __forceinline__ double chain_children(const Problem& P, const double*
   return best;
 }
 
-// Meet in the middle: with the split variables cut into a low half (bits
-// 0 .. dl-1 of the child code) and a high half (dl .. d-1), every child's
-// accumulators are ONE combination  RH[h] (+) LO[l]  of two tables built once
-// per iteration and block:  RH[h] = rest (+) terms of the high half chosen by
-// h (increasing j),  LO[l] = terms of the low half chosen by l (increasing
-// j).  The natural interval extension of the sum (§2.1, Eq. 3-6)
-// in another association: rigorous, equal to the oracle's left-to-right
-// evaluation up to rounding (tests/tol.py).  2^dl + 2^dh <= 512 entries.
-constexpr int MITM_MAX = 256;  // entries of one half (d <= 16)
+// Meet in the middle (d >= 17): with the split variables cut into a low half
+// (bits 0 .. dl-1 of the child code) and a high half (dl .. d-1), every
+// child's accumulators are ONE combination  RH[h] (+) LO[l]  of two tables
+// built per iteration and block:  RH[h] = rest (+) tree of the high-half
+// terms chosen by h,  LO[l] = tree of the low-half terms chosen by l.  The
+// natural interval extension of the sum (§2.1, Eq. 3-6) in another
+// association: rigorous, equal to the oracle's left-to-right evaluation up
+// to rounding (tests/tol.py).  A block builds LO in full and RH for the h of
+// its own children only.
+constexpr int MITM_BITS = D_MAX / 2;        // bits of one half (d <= D_MAX)
+constexpr int MITM_MAX = 1 << MITM_BITS;    // entries of one half
 struct MitmTabs {
-  Iv lo[MITM_MAX][2];
-  Iv rh[MITM_MAX][2];
+  Iv lo[2][MITM_MAX];  // [accumulator][l]: consecutive l in consecutive lanes
+  Iv rh[2][MITM_MAX];
 };
 
+// tree (+) of the terms of split variables j0 .. j0 + nb - 1, chosen by the
+// bits of `bits` (identity-padded balanced tree over MITM_BITS slots)
 template <class F>
-__device__ __forceinline__ void mitm_build(const Problem& P, const double* T, MitmTabs& M) {
-  const int d = P.d, dl = d / 2, dh = d - dl;
-  for (int q = threadIdx.x; q < (1 << dl) + (1 << dh); q += blockDim.x) {
-    Iv A[2];
-    if (q < (1 << dl)) {
-      const int l = q;
+__device__ __forceinline__ void mitm_tree(const double* T, int j0, int nb, uint32_t bits, Iv* A) {
+  Iv tt[MITM_BITS][2];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) A[k] = iv(0.0);
+  for (int u = 0; u < MITM_BITS; ++u)
 #pragma unroll
-      for (int k = 0; k < F::K; ++k) A[k] = acc_ident<F>(k);
-      for (int j = 0; j < dl; ++j) {
-        const double* e = T + HDR + (size_t)(2 * j + ((l >> j) & 1)) * ENT + E_T;
-#pragma unroll
-        for (int k = 0; k < F::K; ++k) A[k] = acc_comb<F>(k, A[k], get(e + 2 * k));
+    for (int q = 0; q < F::K; ++q) {
+      if (u < nb) {
+        const double* e = T + HDR + (size_t)(2 * (j0 + u) + ((bits >> u) & 1u)) * ENT + E_T;
+        tt[u][q] = get(e + 2 * q);
+      } else {
+        tt[u][q] = acc_ident<F>(q);
       }
-#pragma unroll
-      for (int k = 0; k < 2; ++k) M.lo[l][k] = A[k];
-    } else {
-      const int h = q - (1 << dl);
-#pragma unroll
-      for (int k = 0; k < 2; ++k) A[k] = iv(0.0);
-#pragma unroll
-      for (int k = 0; k < F::K; ++k) A[k] = get(T + H_REST + 2 * k);
-      for (int j = 0; j < dh; ++j) {
-        const double* e = T + HDR + (size_t)(2 * (dl + j) + ((h >> j) & 1)) * ENT + E_T;
-#pragma unroll
-        for (int k = 0; k < F::K; ++k) A[k] = acc_comb<F>(k, A[k], get(e + 2 * k));
-      }
-#pragma unroll
-      for (int k = 0; k < 2; ++k) M.rh[h][k] = A[k];
     }
-  }
+#pragma unroll
+  for (int st = 1; st < MITM_BITS; st *= 2)
+#pragma unroll
+    for (int u = 0; u + st < MITM_BITS; u += 2 * st)
+#pragma unroll
+      for (int q = 0; q < F::K; ++q) tt[u][q] = acc_comb<F>(q, tt[u][q], tt[u + st][q]);
+#pragma unroll
+  for (int q = 0; q < F::K; ++q) A[q] = tt[0][q];
 }
 
-// lower bounds of the 2^d children of table T from the tables M (built and
-// synchronised by the caller): this block's share, a child per thread and
-// step; returns this thread's midpoint minimum
+// lower bounds of this block's share (rank of nrank) of the 2^d children of
+// table T: builds the tables (all threads, synchronising), then a child per
+// thread and step; returns this thread's midpoint minimum
 template <class F>
-__device__ __forceinline__ double chain_children_mitm(const Problem& P, const double* T, const MitmTabs& M,
-                                                      double gub0, const ChainOut& o) {
-  const int d = P.d, dl = d / 2;
-  const uint32_t lmask = (1u << dl) - 1u;
+__device__ __forceinline__ double chain_children_mitm(const Problem& P, const double* T, MitmTabs& M, double gub0,
+                                                      const ChainOut& o, int rank = -1, int nrank = 0) {
+  if (rank < 0) {
+    rank = blockIdx.x;
+    nrank = gridDim.x;
+  }
+  const int d = P.d, dl = d / 2, dh = d - dl;
   const long nk = 1L << d;
-  const long per = (nk + gridDim.x - 1) / gridDim.x;
-  const long cb = (long)blockIdx.x * per, ce = min(nk, cb + per);
+  const long per = (nk + nrank - 1) / nrank;
+  const long cb = (long)rank * per, ce = min(nk, cb + per);
+  const uint32_t lmask = (1u << dl) - 1u;
+  const int h0 = (int)(cb >> dl), h1 = ce > cb ? (int)((ce - 1) >> dl) : h0 - 1;
+  const int nlo = 1 << dl, nrh = h1 - h0 + 1;
+  __syncthreads();  // the previous readers of M are done
+  for (int q = threadIdx.x; q < nlo + nrh; q += blockDim.x) {
+    Iv A[2];
+    if (q < nlo) {
+      mitm_tree<F>(T, 0, dl, (uint32_t)q, A);
+#pragma unroll
+      for (int k = 0; k < F::K; ++k) M.lo[k][q] = A[k];
+    } else {
+      const int h = h0 + (q - nlo);
+      mitm_tree<F>(T, dl, dh, (uint32_t)h, A);
+#pragma unroll
+      for (int k = 0; k < F::K; ++k) M.rh[k][h] = acc_comb<F>(k, get(T + H_REST + 2 * k), A[k]);
+    }
+  }
+  __syncthreads();
   double best = CUDART_INF;
   for (long ci = cb + threadIdx.x; ci < ce; ci += blockDim.x) {
     const uint32_t code = (uint32_t)ci;
     const uint32_t h = code >> dl, l = code & lmask;
     Iv B[2];
 #pragma unroll
-    for (int k = 0; k < F::K; ++k) B[k] = acc_comb<F>(k, M.rh[h][k], M.lo[l][k]);
+    for (int k = 0; k < F::K; ++k) B[k] = acc_comb<F>(k, M.rh[k][h], M.lo[k][l]);
     chain_leaf<F>(P, T, gub0, o, code, B, best);
   }
   return best;
@@ -388,8 +440,9 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
   const int n = P.n, d = P.d, t = threadIdx.x, blk = blockIdx.x, G = gridDim.x;
   const int lane = t & 31;
   const int tabw = d * P.m * ENT;  // doubles of the entries
-  double* s_lo = s_dyn;
-  double* s_hi = s_dyn + cb.per;
+  MitmTabs& M = *reinterpret_cast<MitmTabs*>(s_dyn);  // d >= 17: meet-in-the-middle tables
+  double* s_lo = s_dyn + sizeof(MitmTabs) / sizeof(double);
+  double* s_hi = s_lo + cb.per;
   const int i0 = blk * cb.per, i1 = min(n, i0 + cb.per);
 
   // ---- entry: list phase (block 0) -- the host launches k_chain only when
@@ -483,10 +536,11 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     double best = CUDART_INF;
     {
       ChainOut o{cb.cnt + sl, cb.pcode + (size_t)sl * PCAP, cb.plb + (size_t)sl * PCAP, w.clb, false};
-      switch (chain_h(d)) {
-        case 1: best = chain_children<F, 1>(P, T, gub0, o); break;
-        case 2: best = chain_children<F, 2>(P, T, gub0, o); break;
-        default: best = chain_children<F, 3>(P, T, gub0, o); break;
+      int nrank = G;
+      const int rank = chain_child_rank(blk, G, cb.per, n, d, c, cn, cprev, k > 0, nrank);
+      if (rank >= 0) {
+        if (!P.mitm) best = chain_children<F, 1>(P, T, gub0, o, rank, nrank);
+        else best = chain_children_mitm<F>(P, T, M, gub0, o, rank, nrank);
       }
     }
     CH_TICK(26)
@@ -700,11 +754,8 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     const long nz = 3 * (((long)P.kids + TILE - 1) / TILE + 1);
     for (long q = (long)blk * TPB + t; q < nz; q += (long)G * TPB) w.desc2[q] = 0;
     ChainOut o{nullptr, nullptr, nullptr, w.clb, true};
-    switch (chain_h(d)) {
-      case 1: chain_children<F, 1>(P, T, 0.0, o); break;
-      case 2: chain_children<F, 2>(P, T, 0.0, o); break;
-      default: chain_children<F, 3>(P, T, 0.0, o); break;
-    }
+    if (!P.mitm) chain_children<F, 1>(P, T, 0.0, o);
+    else chain_children_mitm<F>(P, T, M, 0.0, o);
   }
   grid.sync();
   cand_emit_dev<F>(P, ctl, w.tab, w.tab_stride, w.clb, w.new_slot, w.pool, w.desc2, w.hot0, w.hot1);

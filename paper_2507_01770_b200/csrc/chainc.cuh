@@ -147,8 +147,6 @@ __global__ void __launch_bounds__(TPB, 1) k_chainc(Problem P, IterBufs w, ChainB
     double best = CUDART_INF;
     {
       ChainOut o{&x_cnt[par], x_pc + par * XCAP, x_pl + par * XCAP, w.clb, false};
-      mitm_build<F>(P, T, M);
-      __syncthreads();
       best = chain_children_mitm<F>(P, T, M, gub0, o);
     }
     CH_TICK(26)
@@ -360,7 +358,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chainc(Problem P, IterBufs w, ChainB
     const long nz = 3 * (((long)P.kids + TILE - 1) / TILE + 1);
     for (long q = (long)blk * TPB + t; q < nz; q += (long)CS * TPB) w.desc2[q] = 0;
     ChainOut o{nullptr, nullptr, nullptr, w.clb, true};
-    chain_children_mitm<F>(P, T, M, 0.0, o);  // the tables of T: built in its phase 1
+    chain_children_mitm<F>(P, T, M, 0.0, o);
   }
   cl.sync();
   cand_emit_dev<F>(P, ctl, w.tab, w.tab_stride, w.clb, w.new_slot, w.pool, w.desc2, w.hot0, w.hot1);

@@ -7,7 +7,7 @@
 namespace ib {
 
 constexpr uint32_t CODE_WHOLE = 0xffffffffu;  // record = the archived box itself
-constexpr int D_MAX = 16;                       // split variables per iteration
+constexpr int D_MAX = 20;                       // split variables per iteration
 constexpr int M_MAX = 8;                        // pieces per split variable
 constexpr int DM_MAX = 64;                      // d * m table entries per parent
 constexpr int HDR = 48;                         // doubles of per-parent header
@@ -109,7 +109,7 @@ struct Problem {
   int mono;                // apply the first-order test
   int pslices;             // k_prep blocks per parent (variable slices)
   int prest;               // 1: the rest accumulators are combined from the slice partials by the child phase
-  int pad0;
+  int mitm;                // k_chain children by meet in the middle (d > 16, or IBNB_CHAIN_MITM=1)
   const double* l;         // device copies of the bounds
   const double* u;
 };

@@ -283,7 +283,9 @@ static Problem make_problem(int fid, int n, int d, int m, long kids, int ld, int
   // the child phase combines the slice partials when every block of it sees
   // at most two parents and their tables fit its shared memory (bisection)
   const int prest = ps > 1 && m == 2 && d <= D_MAX && kids / G >= TPB;
-  return Problem{fid, n, d, m, (int)kids, h, G, mbits, mbits * d, ld, mono, ps, prest, 0, l, u};
+  int mitm = d > 16;  // the pair tree of chain_children covers d - 1 <= 16 terms
+  if (const char* e = std::getenv("IBNB_CHAIN_MITM")) mitm = mitm || std::atoi(e) != 0;
+  return Problem{fid, n, d, m, (int)kids, h, G, mbits, mbits * d, ld, mono, ps, prest, mitm, l, u};
 }
 
 static long tiles_of(long n) { return std::max(1L, (n + TILE - 1) / TILE); }
@@ -327,14 +329,14 @@ static bool chainc_applies(const Problem& P) {
   if (!e || std::atoi(e) != 2) return false;  // opt-in (IBNB_CHAIN=2)
   const int cs = chain_cs();
   const int per = (P.n + cs - 1) / cs;
-  return chainc_smem(per) <= 170u * 1024u;
+  return chainc_smem(per) <= 185u * 1024u;
 }
 // the chain kernel applies (chain.cuh): bisection, the next chunk disjoint
 // from the current one, a non-chain objective, the slices in shared memory
 static bool chain_applies(const Problem& P) {
   if (const char* e = std::getenv("IBNB_CHAIN"))
     if (std::atoi(e) == 0) return false;
-  return P.m == 2 && P.fid != 6 && P.n >= 2 * P.d && P.d >= 2 && 16L * chain_per(P.n) <= 130L * 1024;
+  return P.m == 2 && P.fid != 6 && P.n >= 2 * P.d && P.d >= 2 && 16L * chain_per(P.n) <= 110L * 1024;
 }
 
 static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {

@@ -7,13 +7,14 @@ import sys
 from collections import defaultdict
 
 CLASS = {"k_chainc": "chain", "k_chain": "chain", "k_fused": "fused", "k_child_eval": "child_eval", "k_mono": "mono",
-         "k_prep": "prep", "k_list": "list", "k_emit": "emit", "k_cand": "cand", "k_search": "search"}
+         "k_prep": "prep", "k_list": "list", "k_emit": "emit", "k_insert": "emit", "k_cand": "cand",
+         "k_search": "search"}
 FP = ("sm__sass_thread_inst_executed_op_dadd_pred_on.sum", "sm__sass_thread_inst_executed_op_dmul_pred_on.sum",
       "sm__sass_thread_inst_executed_op_dfma_pred_on.sum")
 
 
 def kclass(name):
-    base = name.split("(")[0].split("<")[0].replace("void ", "").replace("ib::", "").strip()
+    base = name.split("(")[0].split("<")[0].replace("void ", "").strip().split("::")[-1]
     return CLASS.get(base)
 
 

@@ -402,6 +402,24 @@ def test_full_size_n10000_paper_domains(pb, fid):
         assert o[0] <= r.f_hi + tol(fid, a, b)
 
 
+# ------------------------------------------------------------ first-order test over all n variables
+@pytest.mark.parametrize("fid,n,d,search", [(7, 24, 8, 32), (3, 20, 8, 0), (4, 18, 6, 32), (7, 16, 4, 0)])
+def test_separable_split_test_equals_all_variable_oracle(pb, fid, n, d, search):
+    """PAPER.md lines 142-144 test every variable; the GPU tests the split
+    variables (reading R4).  For a separable objective the two are the same
+    method (tests/test_oracle_bnb.py proves why): the GPU solve equals the
+    oracle's solve with the all-variable test (mono = 2), bit for bit."""
+    l, u = workloads.bounds(fid, n)
+    bmax = 1 if search > 0 else 8
+    o = oracle.solve(fid, l, u, 1e-6, 1e-6, d=d, m=2, bmax=bmax, mono=2, max_iter=3000, search=search)
+    g = pb.ib_solve(fid, l, u, 1e-6, 1e-6, pb.options(d=d, m=2, bmax=bmax, max_iter=3000,
+                                                      search=search if search > 0 else -1))
+    assert g.status == o["status"]
+    assert g.iters == o["iters"] and g.evals == o["evals"] and g.n_surv == o["n_surv"]
+    np.testing.assert_array_equal(g.lo, o["lo"])
+    np.testing.assert_array_equal(g.hi, o["hi"])
+
+
 # ------------------------------------------------------------ BASELINE configs[2] and [3] as solves
 def test_baseline_config2_griewank_n100_full_solve_parity(pb):
     """BASELINE configs[2]: Griewank n = 100 on [-600, 600]^100 (symmetric:
@@ -458,6 +476,28 @@ def test_baseline_config3_levy_n1000_full_solve(pb):
     for a, b, g in zip(lo, hi, lb):
         ob = oracle.eval_box(cfg["fid"], a, b)
         assert abs(ob[0] - g) <= tol(cfg["fid"], a, b)
+
+
+@pytest.mark.parametrize("fid", [7, 5, 1, 10, 2])
+def test_full_size_n10000_d20(pb, fid):
+    """The bench's split width at n = 10,000 (d = 20: 2^20 children per
+    iteration, the meet-in-the-middle children of k_chain): the enclosure
+    holds the stated minimum with width <= eps, the regions hold the
+    minimiser, and the oracle recomputes every surviving region's lower
+    bound."""
+    n = 10_000
+    l, u = workloads.bounds(fid, n)
+    r = pb.ib_solve_dev(fid, cuda(l), cuda(u), 1e-6, 1e-6, pb.options(d=20), surv_cap=8)
+    fs = _fstar_n(fid, n)
+    assert r.status == 0 and r.prof["chain"]["units"] > r.iters // 2
+    assert r.f_lo <= fs + 1e-9 * (1 + abs(fs)) and fs - 1e-9 * (1 + abs(fs)) <= r.f_hi
+    assert r.f_hi - r.f_lo <= 1e-6 and r.max_width <= 1e-6
+    lo, hi, lb = r.lo.cpu().numpy(), r.hi.cpu().numpy(), r.lb.cpu().numpy()
+    xs = XSTAR[fid]
+    assert any(np.all(a <= xs + 1e-12) and np.all(xs - 1e-12 <= b) for a, b in zip(lo, hi))
+    for a, b, g in zip(lo, hi, lb):
+        o = oracle.eval_box(fid, a, b)
+        assert abs(o[0] - g) <= tol(fid, a, b)
 
 
 # ------------------------------------------------------------ incumbent exchange hook (multi-GPU)
@@ -684,15 +724,17 @@ def test_solve_parity_at_headline_chunk_sizes(pb, monkeypatch, fid, n, d, eps, s
                                                 (10, 24, 8, 1e-6, 32), (9, 27, 8, 1e-6, 32), (8, 40, 8, 1e-6, 32),
                                                 (3, 25, 8, 1e-6, 32), (4, 24, 8, 1e-6, 32), (2, 26, 8, 1e-6, 32),
                                                 (7, 24, 8, 1e-6, 0), (1, 24, 8, 1e-4, 0)])
-@pytest.mark.parametrize("chain", ["1", "2"])
+@pytest.mark.parametrize("chain", ["1", "1m", "2"])
 def test_chain_solve_parity(pb, monkeypatch, fid, n, d, eps, search, chain):
     """Whole solves through the deep-dive chain kernels (n >= 2 d: k_chain on
-    the whole grid, 1; k_chainc on one thread-block cluster, 2), with the R9
+    the whole grid with the children by pairs, 1, or by meet in the middle --
+    the d > 16 path --, 1m; k_chainc on one thread-block cluster, 2), with the R9
     search on (one region live per iteration) or off (many potential
     candidates: the static-tile exit path): iterations, evaluations and every
     surviving region bit for bit against the oracle, the enclosure within the
     tolerance, and the chain kernel really ran."""
-    monkeypatch.setenv("IBNB_CHAIN", chain)
+    monkeypatch.setenv("IBNB_CHAIN", chain[0])
+    monkeypatch.setenv("IBNB_CHAIN_MITM", "1" if chain == "1m" else "0")
     l, u = workloads.bounds(fid, n)
     bmax = 1 if search > 0 else 4
     o = _oracle_solve_cached(fid, n, eps, d, bmax, 4000, search)
@@ -729,14 +771,15 @@ def _child_surv_oracle(fid, plo, phi, cyc, d, m, code, l, u, gub):
 
 
 @pytest.mark.parametrize("fid", [7, 1, 5, 6])
-def test_branch_n10000_d16_sampled_children(pb, fid):
-    """One iteration at the headline size (n = 10,000, d = 16: 65,536
+@pytest.mark.parametrize("d", [16, 20])
+def test_branch_n10000_sampled_children(pb, fid, d):
+    """One iteration at the headline size (n = 10,000, d = 16 / 20: 2^d
     children of one parent) through ib_branch, compared child by child with
     the oracle on sampled children: every GPU survivor, 160 random codes and
     the codes next to the survivors.  The parent is a small asymmetric box
     around the minimiser so that the lower-bound and first-order tests both
     decide children."""
-    n, d, m = 10_000, 16, 2
+    n, m = 10_000, 2
     l, u = workloads.bounds(fid, n)
     xs = XSTAR[fid]
     rng = np.random.default_rng(fid)
@@ -749,8 +792,8 @@ def test_branch_n10000_d16_sampled_children(pb, fid):
     gub = g["gub"]
     t = tol(fid, plo, phi)
     gsurv = dict(zip(g["code"].cpu().numpy().tolist(), g["lb"].cpu().numpy().tolist()))
-    assert 0 < len(gsurv) < 1 << 16
-    codes = set(gsurv) | set(rng.integers(0, 1 << 16, 160).tolist())
+    assert 0 < len(gsurv) < 1 << d
+    codes = set(gsurv) | set(rng.integers(0, 1 << d, 160).tolist())
     codes |= {c ^ (1 << j) for c in list(gsurv)[:8] for j in range(d)}
     best_ub = math.inf
     for c in sorted(codes):
