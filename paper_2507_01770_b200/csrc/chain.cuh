@@ -187,19 +187,28 @@ struct ChainOut {
 };
 
 
-// one child (code) of table T with accumulators B (lower bound), the
-// midpoint sample and the first-order test for a potential candidate
+// lower bound of a child from its accumulators B
+template <class F>
+__device__ __forceinline__ double chain_lb(const Problem& P, const Iv* B) {
+  return canon_lb(outer_lo<F>(B, P.n));
+}
+
+// the rest of a child's evaluation (called by every lane of the warp, the
+// child's lower bound lb already known; valid = false for a lane without a
+// child): the midpoint sample (line 134) and the first-order test (lines
+// 142-144) of a potential candidate (lb <= GUB at the iteration start,
+// recombined from the midpoint terms -- rare), the append to the list; with
+// o.all only the lower bound is stored
 template <class F>
 __device__ __forceinline__ void chain_leaf(const Problem& P, const double* T, double gub0, const ChainOut& o,
-                                           uint32_t code, const Iv* B, double& best) {
-  const double lb = canon_lb(outer_lo<F>(B, P.n));
+                                           uint32_t code, double lb, bool valid, double& best) {
   if (o.all) {
-    o.clb[code] = lb;
+    if (valid) o.clb[code] = lb;
     return;
   }
-  const bool pot = lb <= gub0;
+  const bool pot = valid && lb <= gub0;
   bool keep = pot;
-  if (pot) {  // midpoint sample (line 134): rare, recombined from the midpoint terms
+  if (pot) {
     o.clb[code] = lb;
     Iv Bm[2];
 #pragma unroll
@@ -210,39 +219,36 @@ __device__ __forceinline__ void chain_leaf(const Problem& P, const double* T, do
       for (int q = 0; q < F::K; ++q) Bm[q] = acc_comb<F>(q, Bm[q], get(e + 2 * q));
     }
     best = fmin(best, outer_hi<F>(Bm, P.n));
-    // the first-order test (lines 142-144) does not depend on GUB: taken
-    // here, so the list holds only children it keeps
+    // the first-order test does not depend on GUB: taken here, so the list
+    // holds only children it keeps
     if (P.mono) keep = chain_fo_ok<F>(P, T, code);
   }
   chain_append(o.cnt, o.pc, o.pl, keep, code, lb);
 }
 
-// the 2^J children below accumulators A: bit J-1 first, then the lower bits
-// (summation order: rest + tree(H .. d-1), then H-1 .. 0 for every child)
+// lower bounds of the 2^J children below accumulators A into lbs[idx ..]:
+// bit J-1 first, then the lower bits (summation order: rest + tree(H .. d-1),
+// then H-1 .. 0 for every child)
 template <class F, int J>
 struct ChainTree {
-  __device__ __forceinline__ static void run(const Problem& P, const double* T, double gub0, const ChainOut& o,
-                                             uint32_t code, const Iv* A, double& best) {
+  __device__ __forceinline__ static void run(const Problem& P, const double* T, const Iv* A, double* lbs, int idx) {
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
       const double* e = T + HDR + (size_t)(2 * (J - 1) + b) * ENT + E_T;
       Iv B[2];
 #pragma unroll
       for (int q = 0; q < F::K; ++q) B[q] = acc_comb<F>(q, A[q], get(e + 2 * q));
-      ChainTree<F, J - 1>::run(P, T, gub0, o, code | ((uint32_t)b << (J - 1)), B, best);
+      ChainTree<F, J - 1>::run(P, T, B, lbs, idx + (b << (J - 1)));
     }
   }
 };
 template <class F>
 struct ChainTree<F, 0> {
-  __device__ __forceinline__ static void run(const Problem& P, const double* T, double gub0, const ChainOut& o,
-                                             uint32_t code, const Iv* A, double& best) {
-    chain_leaf<F>(P, T, gub0, o, code, A, best);
+  __device__ __forceinline__ static void run(const Problem& P, const double*, const Iv* A, double* lbs, int idx) {
+    lbs[idx] = chain_lb<F>(P, A);
   }
 };
 
-// lower bounds of the m^d children of table T (bisection), a thread per
-// group of 2^H; returns this thread's midpoint minimum
 // (rank, nrank): this block's share among the blocks that evaluate children
 constexpr int TREE_SLOTS = 16;
 template <class F, int H>
@@ -257,8 +263,10 @@ __device__ __forceinline__ double chain_children(const Problem& P, const double*
   const int gpb = (ng + nrank - 1) / nrank;
   const int gb = rank * gpb, ge = min(ng, gb + gpb);
   double best = CUDART_INF;
-  for (int gi = gb + threadIdx.x; gi < ge; gi += TPB) {
-    const uint32_t code0 = (uint32_t)gi << H;
+  for (int g0 = gb; g0 < ge; g0 += TPB) {  // warp-uniform trip count (votes below)
+    const int gi = g0 + threadIdx.x;
+    const bool valid = gi < ge;
+    const uint32_t code0 = (uint32_t)(valid ? gi : gb) << H;
     // the terms of variables H .. d-1 summed as a balanced tree (depth 4 over
     // TREE_SLOTS slots, identity padding; d - H <= 16): a short dependence chain instead of
     // d - H sequential combinations -- another association of the natural
@@ -286,7 +294,14 @@ __device__ __forceinline__ double chain_children(const Problem& P, const double*
     Iv A[2];
 #pragma unroll
     for (int q = 0; q < F::K; ++q) A[q] = acc_comb<F>(q, get(T + H_REST + 2 * q), tt[0][q]);
-    ChainTree<F, H>::run(P, T, gub0, o, code0, A, best);
+    double lbs[1 << H];
+    ChainTree<F, H>::run(P, T, A, lbs, 0);
+    bool any = o.all;
+#pragma unroll
+    for (int q = 0; q < (1 << H); ++q) any |= valid && lbs[q] <= gub0;
+    if (__any_sync(0xffffffffu, any))  // rare: a potential candidate in the warp
+#pragma unroll
+      for (int q = 0; q < (1 << H); ++q) chain_leaf<F>(P, T, gub0, o, code0 | (uint32_t)q, lbs[q], valid, best);
   }
   return best;
 }
@@ -366,13 +381,27 @@ __device__ __forceinline__ double chain_children_mitm(const Problem& P, const do
   }
   __syncthreads();
   double best = CUDART_INF;
-  for (long ci = cb + threadIdx.x; ci < ce; ci += blockDim.x) {
-    const uint32_t code = (uint32_t)ci;
-    const uint32_t h = code >> dl, l = code & lmask;
-    Iv B[2];
+  constexpr int U = 4;  // children per thread and step (independent loads)
+  for (long c0 = cb; c0 < ce; c0 += (long)U * blockDim.x) {  // warp-uniform trip count
+    double lbs[U];
+    bool any = o.all;
 #pragma unroll
-    for (int k = 0; k < F::K; ++k) B[k] = acc_comb<F>(k, M.rh[k][h], M.lo[k][l]);
-    chain_leaf<F>(P, T, gub0, o, code, B, best);
+    for (int u = 0; u < U; ++u) {
+      const long ci = c0 + threadIdx.x + (long)u * blockDim.x;
+      const uint32_t code = (uint32_t)(ci < ce ? ci : cb);
+      const uint32_t h = code >> dl, l = code & lmask;
+      Iv B[2];
+#pragma unroll
+      for (int k = 0; k < F::K; ++k) B[k] = acc_comb<F>(k, M.rh[k][h], M.lo[k][l]);
+      lbs[u] = chain_lb<F>(P, B);
+      any |= ci < ce && lbs[u] <= gub0;
+    }
+    if (__any_sync(0xffffffffu, any))  // rare: a potential candidate in the warp
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long ci = c0 + threadIdx.x + (long)u * blockDim.x;
+        chain_leaf<F>(P, T, gub0, o, (uint32_t)(ci < ce ? ci : cb), lbs[u], ci < ce, best);
+      }
   }
   return best;
 }

@@ -10,7 +10,7 @@ constexpr uint32_t CODE_WHOLE = 0xffffffffu;  // record = the archived box itsel
 constexpr int D_MAX = 20;                       // split variables per iteration
 constexpr int M_MAX = 8;                        // pieces per split variable
 constexpr int DM_MAX = 64;                      // d * m table entries per parent
-constexpr int HDR = 48;                         // doubles of per-parent header
+constexpr int HDR = 56;                         // doubles of per-parent header
 constexpr int ENT = 24;                         // doubles per (variable, piece) entry
 constexpr int TPB = 256;                        // threads per block (all kernels)
 constexpr int IPT = 4;                          // items per thread in scans
@@ -24,8 +24,8 @@ constexpr int H_WREST = 8;   // max width over the unsplit variables
 constexpr int H_CHUNK = 9;   // first split variable c
 constexpr int H_LEVY_NB = 10;  // Levy: neighbour values [L: u v um vm][R: u v um vm]
 constexpr int H_LEVY_NT = 26;  // Levy: number of affected chain terms
-constexpr int H_LEVY_T = 27;   // Levy: term descriptors kind*65536 + li*256 + lj
-constexpr int H_LEVY_LR = 46;  // Levy: left / right neighbour variable (or -1)
+constexpr int H_LEVY_T = 27;   // Levy: term descriptors kind*65536 + li*256 + lj (<= d + 3 = 23)
+constexpr int H_LEVY_LR = 50;  // Levy: left / right neighbour variable (or -1)
 
 // entry offsets (doubles)
 constexpr int E_LO = 0, E_HI = 1, E_T = 2;  // then T[K] (2K), Tm[K] (2K), G[KG] (2KG), flag
