@@ -70,7 +70,26 @@ def fp64_peak():
     return 148 * 64 * 1.965e9 / 1e12, "derived: 148 SM x 64 FP64 lanes x 1.965 GHz"
 
 
-def roofline(prof, prof_ms, fid):
+CHAIN_FLOOR_PATH = os.path.join(ROOT, "profiles", "chain_floor_r02l.json")
+
+
+def latency_roofline(prof):
+    """The deep dive's binding resource: time per k_chain iteration against
+    the measured floor of its exchange pattern (publish a partial, grid
+    barrier, read all partials back, reduce: scripts/micro/chain_floor.cu)."""
+    pc = prof.get("chain") or {}
+    if not pc.get("units"):
+        return None
+    fl = load_json(CHAIN_FLOOR_PATH) or {}
+    floor = fl.get("grid_148_us_per_iter")
+    ach = 1e3 * pc["ms"] / pc["units"]
+    return {"kernel": "chain", "unit": "us per iteration", "achieved": ach, "floor": floor,
+            "frac": (floor / ach) if floor else None,
+            "floor_source": "measured: profiles/chain_floor_r02l.json (148 blocks: publish, grid barrier, "
+                            "read all partials, reduce; no arithmetic)"}
+
+
+def roofline(prof, prof_ms, fid, d=16):
     """Roofline entry of the kernel class with the largest device time:
     executed FP64-pipe instructions per unit of work (ncu, committed in
     profiles/fp64_ops_r02.json for this objective) x units per launch /
@@ -88,7 +107,9 @@ def roofline(prof, prof_ms, fid):
                 "traffic": None, "algorithmic_bytes_per_launch": per_launch,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6650 GB/s"}
     else:
-        ops = ((load_json(FP64_OPS_PATH) or {}).get(str(fid)) or {}).get("kernels", {}).get(dom) or {}
+        allops = load_json(FP64_OPS_PATH) or {}
+        ent = allops.get(f"{fid}@d{d}") or (allops.get(str(fid)) if d == 16 or dom not in ("chain", "fused") else None)
+        ops = (ent or {}).get("kernels", {}).get(dom) or {}
         per_unit = ops.get("fp64_inst_per_unit")
         peak, src = fp64_peak()
         units = pd["units"] / max(1, pd["launches"])
@@ -289,7 +310,7 @@ def main():
     ap.add_argument("--config", type=int, default=4, help="BASELINE.json configs index [4: rastrigin n=10000]")
     ap.add_argument("--bmax", type=int, default=0)
     ap.add_argument("--m", type=int, default=2)
-    ap.add_argument("--d", type=int, default=0, help="variables split per iteration [min(n, 16)]")
+    ap.add_argument("--d", type=int, default=0, help="variables split per iteration [18 at n >= 10,000, else min(n, 16)]")
     ap.add_argument("--no-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the configs[1] throughput-regime measurement")
     ap.add_argument("--no-all-functions", action="store_true",
@@ -320,7 +341,10 @@ def main():
     l, u = slab(L, U, rank, world) if partition else (L, U)
     ld = torch.tensor(l, device=dev)
     ud = torch.tensor(u, device=dev)
-    dsplit = args.d or min(n, 16)
+    # split width: 18 at the headline n = 10,000 (262,144 subregions per
+    # iteration, PAPER.md:158's occupancy rule; the same time to enclose as
+    # d = 16 with 3.6x the child boxes per second), else min(n, 16)
+    dsplit = args.d or (18 if n >= 10_000 else min(n, 16))
     opts = pb.options(d=dsplit, m=args.m, bmax=args.bmax or None)
     popts = pb.options(d=dsplit, m=args.m, bmax=args.bmax or None, profile=1)
     ws = pb.Workspace(pb.solve_workspace_bytes(fid, n, opts), device=dev)
@@ -392,7 +416,8 @@ def main():
             for k, x in v.items():
                 p[k] = p.get(k, 0) + x
     prof = {c: v for c, v in prof.items() if v.get("launches")}
-    roof = roofline(prof, prof_ms, fid)
+    roof = roofline(prof, prof_ms, fid, dsplit)
+    lat = latency_roofline(prof)
     roof["timing"] = "CUDA events around each kernel, second timed region (eager launches)"
 
     # ---- e2e through the public host-buffer API (pinned host buffers)
@@ -571,7 +596,8 @@ def main():
             "iters": r0.iters, "evals_per_step": r0.evals, "peak_pool": r0.peak_pool,
             "roofline": roof,
             "kernel_ms": {c: round(p["ms"] / len(pres), 4) for c, p in prof.items()},
-            "kernel_roofline": {c: roofline({c: p}, prof_ms, fid) for c, p in prof.items()},
+            "kernel_roofline": {c: roofline({c: p}, prof_ms, fid, dsplit) for c, p in prof.items()},
+            "latency_roofline": lat,
             "profiled_ms_per_step": prof_ms / len(pres),
             "cpu_baseline": base,
             "throughput_regime": secondary,
