@@ -1515,152 +1515,16 @@ __global__ void __launch_bounds__(TPB, 4) k_mono(Problem P, const Ctl* __restric
 //      survivors are counted per tile (integer atomics);
 //  (C) grid barrier; every block scans the tile survivor counts and
 //      compacts its tiles' survivors into L at their stable positions.
-constexpr int INS_MAXT = 4096;  // k_insert: tiles of one launch (4 M children)
-
-// exclusive prefix over per-tile counts cnt(t) (t < ntiles <= INS_MAXT) into
-// pre[0 .. ntiles] (pre[ntiles] = total), one block-wide scan: thread t sums
-// a run of consecutive tiles
-template <class Get>
-__device__ __forceinline__ void tile_prefix(long ntiles, uint32_t* pre, Get cnt) {
-  const int per = (int)((ntiles + TPB - 1) / TPB);
-  const long t0 = (long)threadIdx.x * per;
-  uint32_t sum = 0;
-  for (int q = 0; q < per; ++q)
-    if (t0 + q < ntiles) sum += cnt(t0 + q);
-  const uint32_t c1[1] = {sum};
-  uint32_t ex1[1], tot1[1];
-  block_exclusive_scan<1, TPB>(c1, ex1, tot1);
-  uint32_t run = ex1[0];
-  for (int q = 0; q < per; ++q)
-    if (t0 + q < ntiles) {
-      pre[t0 + q] = run;
-      run += cnt(t0 + q);
-    }
-  if (threadIdx.x == 0) pre[ntiles] = tot1[0];
-  __syncthreads();
-}
-
+// insertion in one pass (a5 + a6): candidates lb <= GUB, the first-order
+// test, stable compaction of the survivors into L -- k_cand + k_mono + k_emit
+// of the explicit-batch path as one cooperative kernel (static tiles with
+// decoupled look-back, every block resident).  Measured against two- and
+// three-phase variants (tile counts + grid barrier + scan, candidates tested
+// by every warp of the grid): this single pass was the fastest.
 template <class F>
 __global__ void __launch_bounds__(TPB) k_insert(Problem P, IterBufs w) {
-  cg::grid_group grid = cg::this_grid();
-  Ctl* ctl = w.ctl;
-  if (ctl->done) return;  // uniform
-  extern __shared__ uint32_t s_ins[];
-  uint32_t* s_pre = s_ins;                      // [INS_MAXT + 1] candidates before tile t
-  uint32_t* s_sb = s_ins + (INS_MAXT + 1);      // [INS_MAXT + 1] survivors before tile t
-  uint32_t* s_hb = s_ins + 2 * (INS_MAXT + 1);  // [INS_MAXT + 1] hot survivors before tile t
-  const double gub = okey_inv(ctl->gub_key);
-  const unsigned long long tau = ctl->tau_key;
-  const long total = (long)ctl->B * P.kids;
-  const long ntiles = (total + TILE - 1) / TILE;
-  uint32_t* tcnt = reinterpret_cast<uint32_t*>(w.desc2);  // [ntiles][4]: candidates, survivors, hot
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  // ---- (A)
-  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long g0 = tile * TILE + (long)threadIdx.x * IPT;
-    uint32_t fc = 0;
-#pragma unroll
-    for (int q = 0; q < IPT; ++q)
-      if (g0 + q < total && w.clb[g0 + q] <= gub) fc |= 1u << q;
-    const uint32_t nb = __syncthreads_count(fc != 0u);
-    if (nb == 0) {  // no candidate in the tile (the common case)
-      if (threadIdx.x == 0) tcnt[4 * tile] = tcnt[4 * tile + 1] = tcnt[4 * tile + 2] = 0u;
-      continue;
-    }
-    uint32_t c1[1] = {(uint32_t)__popc(fc)}, ex1[1], tot1[1];
-    block_exclusive_scan<1, TPB>(c1, ex1, tot1);
-    uint32_t pl = ex1[0];
-#pragma unroll
-    for (int q = 0; q < IPT; ++q)
-      if (fc & (1u << q)) w.cand[tile * TILE + pl++] = (uint32_t)(g0 + q);
-    if (threadIdx.x == 0) {
-      tcnt[4 * tile + 0] = tot1[0];
-      tcnt[4 * tile + 1] = 0u;
-      tcnt[4 * tile + 2] = 0u;
-    }
-    __syncthreads();
-  }
-  grid.sync();
-  // ---- (B) candidate numbering, then a warp per candidate over the grid
-  tile_prefix(ntiles, s_pre, [&](long t) { return __ldcg(&tcnt[4 * t]); });
-  const uint32_t ncand = s_pre[ntiles];
-  {
-    const long nwarps = (long)gridDim.x * (TPB / 32);
-    for (long j = (long)blockIdx.x * (TPB / 32) + wib; j < ncand; j += nwarps) {
-      long lo = 0, hi = ntiles - 1;  // the tile of candidate j: the last t with s_pre[t] <= j
-      while (lo < hi) {
-        const long mid = (lo + hi + 1) >> 1;
-        if (s_pre[mid] <= (uint32_t)j) lo = mid;
-        else hi = mid - 1;
-      }
-      const long tile = lo;
-      uint32_t* slot = &w.cand[tile * TILE + (j - s_pre[tile])];
-      const uint32_t g = __ldcg(slot);
-      ChildIdx ci = child_of(g, P);
-      const double* T = w.tab + (size_t)ci.b * w.tab_stride;
-      bool ok = true;
-      if (P.mono) {
-        if constexpr (F::SEP) {
-          bool bad = false;
-          if (lane < P.d)
-            bad = T[HDR + (size_t)(lane * P.m + piece(ci.code, lane, P)) * ENT + E_T + 4 * F::K + 2 * F::KG] != 0.0;
-          ok = __ballot_sync(0xffffffffu, bad) == 0u;
-        } else {
-          ok = child_mono_ok_warp<F>(P, T, ci.code);
-        }
-      }
-      if (lane == 0 && ok) {
-        const bool h = okey(w.clb[g]) < tau;
-        *slot = g | 0x80000000u | (h ? 0x40000000u : 0u);
-        atomicAdd(&tcnt[4 * tile + 1], 1u);
-        if (h) atomicAdd(&tcnt[4 * tile + 2], 1u);
-      }
-    }
-  }
-  grid.sync();
-  // ---- (C) survivors to L at their stable positions: tile prefixes, then
-  // the block's own tiles with candidates, a thread per candidate slot
-  tile_prefix(ntiles, s_sb, [&](long t) { return __ldcg(&tcnt[4 * t + 1]); });
-  tile_prefix(ntiles, s_hb, [&](long t) { return __ldcg(&tcnt[4 * t + 2]); });
-  const uint64_t base = ctl->pcount, cap = ctl->pool_cap, hbase = ctl->nhot;
-  uint32_t* hot = ctl->hsel ? w.hot1 : w.hot0;
-  for (long tq = blockIdx.x; tq < ntiles; tq += gridDim.x) {
-    const uint32_t nc = s_pre[tq + 1] - s_pre[tq];
-    if (s_sb[tq + 1] == s_sb[tq]) continue;  // no survivor (block-uniform)
-    uint32_t srun = 0, hrun = 0;
-    for (uint32_t k0 = 0; k0 < nc; k0 += TPB) {
-      const uint32_t k = k0 + threadIdx.x;
-      const uint32_t e = k < nc ? __ldcg(&w.cand[tq * TILE + k]) : 0u;
-      const uint32_t f2[2] = {(e & 0x80000000u) ? 1u : 0u, (e & 0x40000000u) ? 1u : 0u};
-      uint32_t sx[2], st[2];
-      block_exclusive_scan<2, TPB>(f2, sx, st);
-      const uint64_t pos = base + s_sb[tq] + srun + sx[0];
-      if (f2[0] && pos < cap) {
-        const uint32_t g = e & 0x3fffffffu;
-        ChildIdx ci = child_of(g, P);
-        const double* T = w.tab + (size_t)ci.b * w.tab_stride;
-        w.pool.lb[pos] = w.clb[g];
-        w.pool.w[pos] = child_width(P, T, ci.code);
-        w.pool.slot[pos] = w.new_slot[ci.b];
-        w.pool.code[pos] = ci.code;
-        if (f2[1]) hot[hbase + s_hb[tq] + hrun + sx[1]] = (uint32_t)pos;
-      }
-      srun += st[0];
-      hrun += st[1];
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    const unsigned long long ns = s_sb[ntiles], nh = s_hb[ntiles];
-    ctl->ncand = ncand;
-    ctl->nsurv = ns;
-    ctl->nsurv_hot = nh;
-    if (base + ns > cap) {
-      ctl->err = -2;  // IB_ENOSPACE
-      ctl->done = 4;
-    }
-    ctl->pending_end = 1;
-    set_list_fast(ctl, nh);
-  }
+  if (w.ctl->done) return;
+  cand_emit_dev<F>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.new_slot, w.pool, w.desc2, w.hot0, w.hot1);
 }
 #ifndef IBNB_OBJ_TU
 __global__ void __launch_bounds__(TPB) k_emit(const Problem P, Ctl* __restrict__ ctl, const double* __restrict__ tab,
@@ -3036,19 +2900,10 @@ struct ObjImpl {
     launch_eval_t<F>(P, w, nk, st, zero);
   }
   static int insert(const Problem& P, const IterBufs& w, long nitems, cudaStream_t st) {
-    const size_t smem = sizeof(uint32_t) * 3 * (INS_MAXT + 1);
     static unsigned g_max = 0;
-    if (!g_max) {
-      cudaFuncSetAttribute((const void*)k_insert<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      int nb = 0, dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)k_insert<F>, TPB, smem);
-      g_max = (unsigned)(std::max(1, std::min(nb, 2)) * sms);
-    }
+    if (!g_max) g_max = coop_grid((const void*)k_insert<F>, 4);
     const unsigned g = (unsigned)std::min((long)g_max, tiles_for(nitems));
-    void* argv[] = {(void*)&P, (void*)&w};
-    return (int)cudaLaunchCooperativeKernel((const void*)k_insert<F>, dim3(g), dim3(TPB), argv, smem, st);
+    return (int)coop_launch(k_insert<F>, g, st, P, w);
   }
   static void mono(const Problem& P, const IterBufs& w, long nitems, cudaStream_t st) {
     k_mono<F><<<grid_for(nitems, TPB, 148u * 12u), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.cand, w.ok);
@@ -3205,15 +3060,8 @@ int launch_iteration(const Problem& P, const IterBufs& w, long pool_bound, long 
   // rule out (a5: lb > GUB, the first-order test) and insert the survivors
   // into L (a6), one pass
   if (hook) hook->begin(5, bmax * kids, st);
-  if (bmax * kids <= (long)INS_MAXT * TILE) {  // k_insert's tile bound (4 M children)
-    const int ie = obj_launch(P.fid)->insert(P, w, bmax * kids, st);
-    if (ie) return ie;
-  } else {  // larger batches (an explicit bmax): three kernels
-    k_cand<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.clb, w.cand, w.desc, w.tile_ctr);
-    obj_launch(P.fid)->mono(P, w, bmax * kids, st);
-    k_emit<<<scan_grid(bmax * kids), TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.cand, w.ok, w.new_slot,
-                                                    w.pool, w.desc2, w.tile_ctr + 1, 1, w.hot0, w.hot1);
-  }
+  const int ie = obj_launch(P.fid)->insert(P, w, bmax * kids, st);
+  if (ie) return ie;
   if (hook) hook->end(5, st);
   LAUNCH_OK;
 }
