@@ -60,8 +60,8 @@ int ib_num_functions(void);
 typedef struct {
     int d;            /* variables partitioned per iteration, the variable-cycling
                          chunk (§3.2) [min(n, 16)], 1 <= d <= 20
-                         (bench.py: d = 20 at n = 10,000, m^d >= 148 SMs x 2048
-                         threads, the occupancy rule of §3.2) */
+                         (bench.py: d = 18 at n = 10,000, m^d close to 148 SMs x
+                         2048 threads, the occupancy rule of §3.2) */
     int m;            /* pieces per partitioned variable, uniform partition
                          Eq. (10)-(11) generalised [2 = bisection], 2 <= m <= 8,
                          m^d <= 2^24, d*m <= 64 */
@@ -79,6 +79,18 @@ typedef struct {
     int64_t max_iter; /* iteration limit [1,000,000] */
     int64_t pool_cap; /* capacity of the list L in records [derived from workspace] */
     int64_t arch_cap; /* capacity of the archive of selected regions [derived] */
+    void* gub_shared; /* multi-GPU (north_star: the incumbent shared "each
+                         iteration" over NVLink): device address of ONE 64-bit
+                         word, the same word on every rank (one rank's memory,
+                         mapped into the others with ib_ipc_open), holding the
+                         incumbent GUB as an ordered integer (initialise to
+                         ~0).  Every iteration of the deep-dive kernel
+                         atomically lowers it to the rank's GUB and takes the
+                         minimum back (one NVLink atomic, overlapped with the
+                         children); NULL [default]: not shared.  The value is
+                         only ever a rigorous upper bound of f at a feasible
+                         point of the whole domain, so sharing never affects
+                         rigour, only how early regions are ruled out. */
 } ib_options;
 
 typedef struct {
@@ -245,6 +257,14 @@ int ib_compact_le(const double* keys, int64_t n, double thr, int64_t* out_idx, i
 int ib_select(const double* lb, int64_t n, double gub, int64_t bmax, int64_t* sel_idx, int64_t* keep_idx,
               int64_t* n_sel, int64_t* n_keep, void* ws, size_t ws_bytes, void* stream);
 size_t ib_select_workspace_size(int64_t n);
+
+/* Inter-process handle of a device allocation (cudaIpcGetMemHandle): 64
+ * bytes into handle.  ib_ipc_open maps a handle of another process (same or
+ * peer GPU, NVLink) and returns the device address; ib_ipc_close unmaps it.
+ * For ib_options.gub_shared across ranks (bench.py --mode partition). */
+int ib_ipc_get_handle(const void* dptr, void* handle);
+int ib_ipc_open(const void* handle, void** dptr);
+int ib_ipc_close(void* dptr);
 
 #ifdef __cplusplus
 }

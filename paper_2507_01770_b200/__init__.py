@@ -36,6 +36,7 @@ class IbOptions(ctypes.Structure):
     _fields_ = [
         ("d", ctypes.c_int), ("m", ctypes.c_int), ("mono", ctypes.c_int), ("profile", ctypes.c_int),
         ("search", ctypes.c_int), ("reserved", ctypes.c_int), ("bmax", _i64), ("max_iter", _i64), ("pool_cap", _i64), ("arch_cap", _i64),
+        ("gub_shared", ctypes.c_void_p),
     ]
 
 
@@ -78,6 +79,9 @@ EXPORTS = {
     "ib_search": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, _vp,
                                  ctypes.c_size_t, _vp]),
     "ib_compact_le": (ctypes.c_int, [_vp, _i64, ctypes.c_double, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
+    "ib_ipc_get_handle": (ctypes.c_int, [_vp, _vp]),
+    "ib_ipc_open": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_void_p)]),
+    "ib_ipc_close": (ctypes.c_int, [_vp]),
     "ib_select_workspace_size": (ctypes.c_size_t, [_i64]),
     "ib_select": (ctypes.c_int, [_vp, _i64, ctypes.c_double, _i64, _vp, _vp, ctypes.POINTER(_i64),
                                  ctypes.POINTER(_i64), _vp, ctypes.c_size_t, _vp]),
@@ -402,3 +406,25 @@ def ib_select(lb, gub: float, bmax: int, stream=None):
     _check(lib().ib_select(_ptr(lb), n, float(gub), int(bmax), _ptr(sel), _ptr(keep), ctypes.byref(ns),
                            ctypes.byref(nk), _ptr(ws), int(wsb), _stream(stream)), "ib_select")
     return sel[: ns.value], keep[: nk.value]
+
+
+# ---------------------------------------------------------------- multi-GPU incumbent word
+def ib_ipc_get_handle(t) -> bytes:
+    """64-byte inter-process handle of the device allocation holding tensor t."""
+    _torch()
+    h = ctypes.create_string_buffer(64)
+    _check(lib().ib_ipc_get_handle(ctypes.c_void_p(t.data_ptr()), ctypes.cast(h, ctypes.c_void_p)), "ib_ipc_get_handle")
+    return h.raw
+
+
+def ib_ipc_open(handle: bytes) -> int:
+    """Device address of another process's allocation (ib_ipc_get_handle)."""
+    _torch()
+    p = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(bytes(handle), 64)
+    _check(lib().ib_ipc_open(ctypes.cast(buf, ctypes.c_void_p), ctypes.byref(p)), "ib_ipc_open")
+    return int(p.value)
+
+
+def ib_ipc_close(ptr: int) -> None:
+    _check(lib().ib_ipc_close(ctypes.c_void_p(ptr)), "ib_ipc_close")

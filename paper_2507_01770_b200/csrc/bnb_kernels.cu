@@ -3081,10 +3081,7 @@ int launch_fused(const Problem& P, const IterBufs& w, int iters, long bmax, cuda
 // launch, one block per SM, the block slices of the region in dynamic shared
 // memory (2 * per doubles)
 int launch_chain(const Problem& P, const IterBufs& w, const ChainBufs& cb, int iters, cudaStream_t st) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return obj_launch(P.fid)->chain(P, w, cb, iters, (unsigned)sms, st);
+  return obj_launch(P.fid)->chain(P, w, cb, iters, (unsigned)cb.grid, st);
 }
 
 size_t chainc_smem(int per) {

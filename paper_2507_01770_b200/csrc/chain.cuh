@@ -556,9 +556,14 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     const int cn = (c + d) % n;
     const double gub0 = okey_inv(gub_key);
     // ================= phase 1
+    unsigned long long shared_old = ~0ull;
     if (blk == 0 && t == 0) {  // slot of the next iteration (last read before the previous barrier)
       cb.cnt[(k + 1) % 3] = 0ull;
       cb.gacc[(k + 1) % 3] = ~0ull;
+      // multi-GPU: lower the shared incumbent word to this rank's GUB and
+      // take the other ranks' back (one NVLink atomic; its value is needed
+      // only at the end of the phase)
+      if (cb.gshared) shared_old = atomicMin(cb.gshared, gub_key);
     }
     // (a) children: a thread owns the 2^H children of a code whose H low bits
     // are clear (enough groups for every thread of the grid, H <= 3)
@@ -585,7 +590,8 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     }
     // (c) entries of chunk c' (unchanged in every child of R)
     chain_chunk_entries<F>(P, s_lo, s_hi, i0, i1, cn, cb.tabn + (size_t)((k + 1) & 1) * DM_MAX * ENT);
-    // (d) this block's midpoint minimum
+    // (d) this block's midpoint minimum; block 0 also brings in the incumbent
+    // shared with the other ranks (issued at the iteration start)
     {
       __shared__ double s_m[TPB / 32];
       best = warp_min(best);
@@ -594,6 +600,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
       if (t == 0) {
         for (int q = 1; q < TPB / 32; ++q) best = fmin(best, s_m[q]);
         if (best < CUDART_INF) atomicMin(&cb.gacc[sl], (unsigned long long)okey(best));
+        if (shared_old != ~0ull) atomicMin(&cb.gacc[sl], shared_old);
       }
     }
     CH_TICK(27)

@@ -151,8 +151,9 @@ struct ChainBufs {
   unsigned long long* exits;  // [8] why launches left the chain (trace statistics): 0 no survivor,
                               // 1 several survivors, 2 > PCAP potential candidates, 3 stop test,
                               // 4 iteration limit, 5 launch budget, 6 nothing to chain at entry
+  unsigned long long* gshared;  // multi-GPU: the incumbent word shared by every rank (or nullptr)
   int per;                   // variables per block slice
-  int pad;
+  int grid;                  // k_chain blocks (one per SM, IBNB_CHAIN_GRID caps it)
 };
 
 // host callbacks around the kernel classes of an iteration: profiling

@@ -314,6 +314,7 @@ static int chain_grid() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (const char* e = std::getenv("IBNB_CHAIN_GRID")) sms = std::max(16, std::min(sms, std::atoi(e)));
   return sms;
 }
 static int chain_per(int n) { return (n + chain_grid() - 1) / chain_grid(); }
@@ -364,6 +365,7 @@ static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
   w.chain.tabn = A.take<double>((size_t)2 * DM_MAX * ENT);
   w.chain.exits = A.take<unsigned long long>(8);
   w.chain.per = chain_per(n);
+  w.chain.grid = chain_grid();
   w.root_out = A.take<double>(2);
   w.f_search = A.take<double>(1);
   w.search_rounds = A.take<int32_t>(1);
@@ -655,7 +657,8 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   unsigned long long pcount = 1, free_top = hc.free_top, peak = 1;
   long fused_iters = 0, chain_iters = 0, iter_prev = 0, chain_launches = 0;
   const bool use_chain = chain_applies(P);
-  const bool use_chainc = use_chain && chainc_applies(P);
+  w.chain.gshared = opt ? reinterpret_cast<unsigned long long*>(opt->gub_shared) : nullptr;
+  const bool use_chainc = use_chain && chainc_applies(P) && !w.chain.gshared;
   ChainBufs cbc = w.chain;
   cbc.per = (n + chain_cs() - 1) / chain_cs();
   // iterations per chain launch: the host reads the control block between
@@ -995,7 +998,32 @@ using namespace ib;
 
 extern "C" {
 
-const char* ib_version(void) { return "ibnb 0.2.0 (sm_100a, fp64 directed rounding, device-driven iteration)"; }
+const char* ib_version(void) { return "ibnb 0.3.0 (sm_100a, fp64 directed rounding, device-driven iteration)"; }
+
+int ib_ipc_get_handle(const void* dptr, void* handle) {
+  if (!dptr || !handle) return fail(IB_EINVAL, "ib_ipc_get_handle: NULL argument");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(dptr));
+  if (e != cudaSuccess) return fail((int)e, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  std::memcpy(handle, &h, sizeof h);
+  return 0;
+}
+
+int ib_ipc_open(const void* handle, void** dptr) {
+  if (!dptr || !handle) return fail(IB_EINVAL, "ib_ipc_open: NULL argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  cudaError_t e = cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail((int)e, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+int ib_ipc_close(void* dptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(dptr);
+  if (e != cudaSuccess) return fail((int)e, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+  return 0;
+}
 const char* ib_last_error(void) { return g_err.c_str(); }
 int ib_num_functions(void) { return 11; }
 

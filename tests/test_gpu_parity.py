@@ -820,3 +820,71 @@ def test_search_matches_oracle_mid_sizes(pb, fid, n):
     assert abs(f - fo) <= t, (f, fo)
     ev = oracle.eval_point(fid, x.cpu().numpy())
     assert ev[0] <= f + t and f <= ev[1] + t
+
+
+# ------------------------------------------------------------ multi-GPU: the shared incumbent word
+def _slab(l, u, cut):
+    a, b = l.copy(), u.copy()
+    c, d = l.copy(), u.copy()
+    b[0] = cut
+    c[0] = cut
+    return (a, b), (c, d)
+
+
+def test_shared_incumbent_word_prunes_the_other_slab(pb):
+    """ib_options.gub_shared: the deep-dive kernel lowers the shared word to
+    its GUB every iteration and takes the minimum back.  Rastrigin n = 2000
+    cut at x_1 = 0.25: the slab with the minimiser encloses f* = 0 and leaves
+    its GUB in the word; the other slab, solved with the same word, is ruled
+    out at once (status 2, far fewer iterations than alone) and reports the
+    shared incumbent; the union enclosure is the eps-enclosure of 0."""
+    fid, n = 7, 2000
+    l, u = workloads.bounds(fid, n)
+    (l0, u0), (l1, u1) = _slab(l, u, 0.25)
+    word = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    o = pb.options(d=16, gub_shared=word.data_ptr())
+    r0 = pb.ib_solve_dev(fid, cuda(l0), cuda(u0), 1e-6, 1e-6, o)
+    assert r0.status == 0 and r0.f_lo <= 0.0 <= r0.f_hi and r0.f_hi - r0.f_lo <= 1e-6
+    alone = pb.ib_solve_dev(fid, cuda(l1), cuda(u1), 1e-6, 1e-6, pb.options(d=16))
+    r1 = pb.ib_solve_dev(fid, cuda(l1), cuda(u1), 1e-6, 1e-6, o)
+    assert r1.status == 2, r1.status  # every region of the slab ruled out by the shared GUB
+    assert r1.iters < alone.iters // 10
+    assert r1.f_hi <= r0.f_hi
+    assert min(r0.f_lo, r1.f_lo) <= 0.0 <= min(r0.f_hi, r1.f_hi) <= 1e-6
+
+
+def _ipc_child(handle, q):
+    import torch as _t
+
+    import paper_2507_01770_b200 as _pb
+    import workloads as _w
+    _t.cuda.set_device(0)
+    l, u = _w.bounds(7, 2000)
+    _, (l1, u1) = _slab(l, u, 0.25)
+    ptr = _pb.ib_ipc_open(handle)
+    r = _pb.ib_solve_dev(7, _t.tensor(l1, device="cuda"), _t.tensor(u1, device="cuda"), 1e-6, 1e-6,
+                         _pb.options(d=16, gub_shared=ptr))
+    _pb.ib_ipc_close(ptr)
+    q.put((r.status, r.iters, r.f_lo, r.f_hi))
+
+
+def test_shared_incumbent_word_across_processes(pb):
+    """The same through an inter-process handle (the bench's multi-GPU
+    partition mode maps rank 0's word into every rank with ib_ipc_open): a
+    second process on this GPU solves the other slab with the word this
+    process filled."""
+    import multiprocessing as mp
+
+    fid, n = 7, 2000
+    l, u = workloads.bounds(fid, n)
+    (l0, u0), _ = _slab(l, u, 0.25)
+    word = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    r0 = pb.ib_solve_dev(fid, cuda(l0), cuda(u0), 1e-6, 1e-6, pb.options(d=16, gub_shared=word.data_ptr()))
+    assert r0.status == 0
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_ipc_child, args=(pb.ib_ipc_get_handle(word), q))
+    p.start()
+    status, iters, f_lo, f_hi = q.get(timeout=240)
+    p.join(timeout=60)
+    assert status == 2 and f_hi <= r0.f_hi
