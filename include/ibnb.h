@@ -87,7 +87,9 @@ typedef struct {
                          ~0).  Every iteration of the deep-dive kernel
                          atomically lowers it to the rank's GUB and takes the
                          minimum back (one NVLink atomic, overlapped with the
-                         children); NULL [default]: not shared.  The value is
+                         children); the batch paths do the same before every
+                         chunk of <= 64 iterations; NULL [default]: not
+                         shared.  The value is
                          only ever a rigorous upper bound of f at a feasible
                          point of the whole domain, so sharing never affects
                          rigour, only how early regions are ruled out. */

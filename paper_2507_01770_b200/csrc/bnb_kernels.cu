@@ -823,7 +823,8 @@ __device__ __forceinline__ void child_eval_dev(const Problem& P, Ctl* __restrict
                                                const double* __restrict__ tab, int tab_stride,
                                                double* __restrict__ clb, uint64_t* zero_a, uint64_t* zero_b,
                                                long nzero, uint32_t* zero_ctr, unsigned int* zero_hist,
-                                               uint32_t* pot = nullptr, const double* __restrict__ ppart = nullptr) {
+                                               uint32_t* pot = nullptr, const double* __restrict__ ppart = nullptr,
+                                               uint64_t* __restrict__ pbits = nullptr) {
   if (ctl->done) return;
   if (zero_a) {  // descriptors and tickets of the following k_cand / k_emit,
                  // histograms and accumulators of the next k_list
@@ -887,7 +888,10 @@ __device__ __forceinline__ void child_eval_dev(const Problem& P, Ctl* __restrict
         Tsh = &s_tab[0][0];
       }
     }
-    if (gi >= ngroups) continue;
+    // potential-candidate bits of this thread's G children (lb <= GUB_old):
+    // the bitmap of the sparse insertion (graph path, G = 8 only)
+    uint32_t pm = 0;
+    if (gi < ngroups) {
     const int b = P.mbits ? (int)(gi >> (P.kbits - h * P.mbits)) : (int)(gi / gpp);
     const uint32_t hcode = P.mbits ? (uint32_t)gi & (uint32_t)(gpp - 1) : (uint32_t)(gi % gpp);
     const double* __restrict__ T = Tsh ? Tsh + (size_t)(b - b0) * TS : tab + (size_t)b * tab_stride;
@@ -962,6 +966,23 @@ __device__ __forceinline__ void child_eval_dev(const Problem& P, Ctl* __restrict
         clb[gi * G + q] = lbq;
         if (lbq <= gub0) best = fmin(best, outer_hi<F>(Bm, n));
         if (pot) pot_append(ctl, pot, lbq <= gub0, (uint32_t)(gi * G + q));
+        if (lbq <= gub0) pm |= 1u << q;
+      }
+    }
+    }  // gi < ngroups
+    if constexpr (GT == 8) {
+      if (pbits) {
+        // a warp's 32 groups are 256 consecutive children = 4 words; every
+        // word below ceil(B m^d / 64) is written (zeros included), so the
+        // bitmap needs no clearing between iterations
+        const int lane = threadIdx.x & 31;
+        unsigned long long v = (unsigned long long)pm << (8 * (lane & 7));
+        v |= __shfl_xor_sync(0xffffffffu, v, 1);
+        v |= __shfl_xor_sync(0xffffffffu, v, 2);
+        v |= __shfl_xor_sync(0xffffffffu, v, 4);
+        if ((lane & 7) == 0 && gi < ngroups) pbits[gi >> 3] = v;
+        const unsigned np = __reduce_add_sync(0xffffffffu, (unsigned)__popc(pm));
+        if (lane == 0 && np) atomicAdd(&ctl->npot, (unsigned long long)np);
       }
     }
   }
@@ -980,8 +1001,10 @@ __global__ void __launch_bounds__(TPB, 4) k_child_eval(Problem P, Ctl* __restric
                                                                const double* __restrict__ tab, int tab_stride,
                                                                double* __restrict__ clb, uint64_t* zero_a,
                                                                uint64_t* zero_b, long nzero, uint32_t* zero_ctr,
-                                                               unsigned int* zero_hist, const double* ppart) {
-  child_eval_dev<F, GT>(P, ctl, tab, tab_stride, clb, zero_a, zero_b, nzero, zero_ctr, zero_hist, nullptr, ppart);
+                                                               unsigned int* zero_hist, const double* ppart,
+                                                               uint64_t* pbits) {
+  child_eval_dev<F, GT>(P, ctl, tab, tab_stride, clb, zero_a, zero_b, nzero, zero_ctr, zero_hist, nullptr, ppart,
+                        pbits);
 }
 
 // Pass 2a: stable compaction of the candidates (children with lb <= GUB,
@@ -1047,11 +1070,12 @@ __device__ void mono_dev(const Problem& P, const Ctl* __restrict__ ctl, const do
 __device__ void iter_end_dev(Ctl* ctl, long kids);
 // the next k_fused list phase may take the single-block path: every live
 // record is in the hot index (tau = ~0) and, with this iteration's survivors,
-// it has at most min(bmax, TPB) entries (decided here, before the barrier,
+// it has at most min(bmax, LSMAX * TPB) entries (decided here, before the barrier,
 // so that every block reads the same flag)
 __device__ __forceinline__ void set_list_fast(Ctl* ctl, unsigned long long nsurv_hot) {
   const unsigned long long nh = ctl->nhot + nsurv_hot;
-  ctl->list_fast = ctl->hot_valid && ctl->tau_key == ~0ull && nh <= ctl->bmax && nh <= (unsigned long long)TPB;
+  ctl->list_fast =
+      ctl->hot_valid && ctl->tau_key == ~0ull && nh <= ctl->bmax && nh <= (unsigned long long)(LSMAX * TPB);
 }
 // MONO: the first-order test of each candidate is evaluated here (fused
 // kernel) instead of being read from ok[] (k_mono)
@@ -1515,6 +1539,144 @@ __global__ void __launch_bounds__(TPB, 4) k_mono(Problem P, const Ctl* __restric
 //      survivors are counted per tile (integer atomics);
 //  (C) grid barrier; every block scans the tile survivor counts and
 //      compacts its tiles' survivors into L at their stable positions.
+// Sparse insertion (graph path, bisection with G = 8, at most SCAP potential
+// candidates): the same candidates, first-order test and stable compaction
+// as cand_emit_dev, but a tile covers SP_WORDS words of the potential bitmap
+// written by k_child_eval (32,768 children) and only the children whose bit
+// is set (lb <= GUB at the iteration start, a superset of the candidates
+// lb <= GUB, line 140) are read: 32x fewer tiles in the look-back chain and
+// 1/64 of the bytes.  Same survivors in the same order (bit-identical L).
+constexpr int SP_WORDS = 64;       // 64-bit bitmap words per tile (4,096 children: a few candidates per tile,
+                                   // one warp each -- the first-order tests spread over the grid)
+constexpr int SCAP = 4096;         // potential candidates of one iteration
+template <class F>
+__device__ void cand_emit_sparse_dev(const Problem& P, Ctl* __restrict__ ctl, const double* __restrict__ tab,
+                                     int tab_stride, const double* __restrict__ clb,
+                                     const int32_t* __restrict__ new_slot, Pool out, const uint64_t* pbits,
+                                     uint64_t* desc, uint32_t* hot0, uint32_t* hot1) {
+  __shared__ uint32_t s_idx[SCAP];
+  __shared__ uint8_t s_f[SCAP];
+  __shared__ uint32_t s_cnt[3];
+  uint32_t* hot = ctl->hsel ? hot1 : hot0;
+  const unsigned long long tau = ctl->tau_key;
+  const double gub = okey_inv(ctl->gub_key);
+  const long total = (long)ctl->B * P.kids;
+  const long nwords = (total + 63) / 64;
+  const long ntiles = (nwords + SP_WORDS - 1) / SP_WORDS;
+  const int t = threadIdx.x;
+  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    // (1) the potential candidates of the tile, in child order
+    const long w0 = tile * SP_WORDS + 2 * t;
+    const bool mine = 2 * t < SP_WORDS;
+    const uint64_t a = mine && w0 < nwords ? __ldcg(&pbits[w0]) : 0ull;
+    const uint64_t b = mine && w0 + 1 < nwords ? __ldcg(&pbits[w0 + 1]) : 0ull;
+    uint32_t c1[1] = {(uint32_t)(__popcll(a) + __popcll(b))}, ex1[1], tot1[1];
+    block_exclusive_scan<1, TPB>(c1, ex1, tot1);
+    {
+      uint32_t pos = ex1[0];
+      for (uint64_t v = a; v; v &= v - 1) s_idx[pos++] = (uint32_t)(w0 * 64 + __ffsll((long long)v) - 1);
+      for (uint64_t v = b; v; v &= v - 1) s_idx[pos++] = (uint32_t)((w0 + 1) * 64 + __ffsll((long long)v) - 1);
+    }
+    const int np = (int)tot1[0];
+    if (t < 3) s_cnt[t] = 0;
+    __syncthreads();
+    // (2) candidates (lb <= GUB), a thread each
+    {
+      uint32_t nc = 0;
+      for (int k = t; k < np; k += TPB) {
+        const uint8_t f = clb[s_idx[k]] <= gub ? 1 : 0;
+        s_f[k] = f;
+        nc += f;
+      }
+      nc = __reduce_add_sync(0xffffffffu, nc);
+      if ((t & 31) == 0 && nc) atomicAdd(&s_cnt[0], nc);
+    }
+    __syncthreads();
+    // (3) the first-order test (lines 142-144): a warp per candidate (a lane
+    // per split variable) when the tile has few, else a thread per candidate
+    const int lane = t & 31;
+    if (s_cnt[0] <= 4u * (TPB / 32)) {  // uniform
+      for (int k = t >> 5; k < np; k += TPB / 32) {
+        if (!(s_f[k] & 1)) continue;  // warp-uniform
+        const uint32_t g = s_idx[k];
+        ChildIdx ci = child_of(g, P);
+        const double* T = tab + (size_t)ci.b * tab_stride;
+        bool ok = true;
+        if (P.mono) {
+          if constexpr (F::SEP) {
+            bool bad = false;
+            if (lane < P.d)
+              bad = T[HDR + (size_t)(lane * P.m + piece(ci.code, lane, P)) * ENT + E_T + 4 * F::K + 2 * F::KG] != 0.0;
+            ok = __ballot_sync(0xffffffffu, bad) == 0u;
+          } else {
+            ok = child_mono_ok_warp<F>(P, T, ci.code);
+          }
+        }
+        if (lane == 0 && ok) s_f[k] |= okey(clb[g]) < tau ? 6 : 2;
+      }
+    } else {
+      for (int k = t; k < np; k += TPB) {
+        if (!(s_f[k] & 1)) continue;
+        const uint32_t g = s_idx[k];
+        ChildIdx ci = child_of(g, P);
+        if (!P.mono || child_mono_ok<F>(P, tab + (size_t)ci.b * tab_stride, ci.code))
+          s_f[k] |= okey(clb[g]) < tau ? 6 : 2;
+      }
+    }
+    __syncthreads();
+    {
+      uint32_t my1 = 0, my2 = 0;
+      for (int k = t; k < np; k += TPB) {
+        my1 += (s_f[k] >> 1) & 1;
+        my2 += (s_f[k] >> 2) & 1;
+      }
+      my1 = __reduce_add_sync(0xffffffffu, my1);
+      my2 = __reduce_add_sync(0xffffffffu, my2);
+      if (lane == 0 && my1) atomicAdd(&s_cnt[1], my1);
+      if (lane == 0 && my2) atomicAdd(&s_cnt[2], my2);
+    }
+    __syncthreads();
+    uint32_t tot[3] = {s_cnt[0], s_cnt[1], s_cnt[2]};
+    uint64_t pfx[3];
+    dl_lookback<3>(desc, (uint32_t)tile, tot, pfx);
+    // (3) stable compaction of the survivors into L (and the hot index)
+    const uint64_t base = ctl->pcount, cap = ctl->pool_cap, hbase = ctl->nhot;
+    uint64_t run = 0, hrun = 0;
+    for (int k0 = 0; k0 < np; k0 += TPB) {
+      const int k = k0 + t;
+      const uint8_t f = k < np ? s_f[k] : 0;
+      uint32_t c2[2] = {(uint32_t)((f >> 1) & 1), (uint32_t)((f >> 2) & 1)}, ex[2], tt[2];
+      block_exclusive_scan<2, TPB>(c2, ex, tt);
+      if (f & 2) {
+        const uint64_t pos = base + pfx[1] + run + ex[0];
+        if (pos < cap) {
+          const uint32_t g = s_idx[k];
+          ChildIdx ci = child_of(g, P);
+          out.lb[pos] = clb[g];
+          out.w[pos] = child_width(P, tab + (size_t)ci.b * tab_stride, ci.code);
+          out.slot[pos] = new_slot[ci.b];
+          out.code[pos] = ci.code;
+          if (f & 4) hot[hbase + pfx[2] + hrun + ex[1]] = (uint32_t)pos;
+        }
+      }
+      run += tt[0];
+      hrun += tt[1];
+    }
+    if (tile == ntiles - 1 && t == 0) {
+      ctl->ncand = pfx[0] + tot[0];
+      ctl->nsurv = pfx[1] + tot[1];
+      ctl->nsurv_hot = pfx[2] + tot[2];
+      if (base + pfx[1] + tot[1] > cap) {
+        ctl->err = -2;  // IB_ENOSPACE
+        ctl->done = 4;
+      }
+      ctl->pending_end = 1;
+      set_list_fast(ctl, pfx[2] + tot[2]);
+    }
+    __syncthreads();  // shared arrays are reused by the next tile
+  }
+}
+
 // insertion in one pass (a5 + a6): candidates lb <= GUB, the first-order
 // test, stable compaction of the survivors into L -- k_cand + k_mono + k_emit
 // of the explicit-batch path as one cooperative kernel (static tiles with
@@ -1524,6 +1686,21 @@ __global__ void __launch_bounds__(TPB, 4) k_mono(Problem P, const Ctl* __restric
 template <class F>
 __global__ void __launch_bounds__(TPB) k_insert(Problem P, IterBufs w) {
   if (w.ctl->done) return;
+  if constexpr (!F::CHAIN) {
+    // uniform: the potential bitmap exists (k_child_eval's G = 8 path) and
+    // the potential candidates fit one tile's list
+    const bool sparse = w.pbits && P.m == 2 && P.G == 8 && w.ctl->npot <= (unsigned long long)SCAP;
+    if (w.tstamp && blockIdx.x == 0 && threadIdx.x == 0) {  // trace statistics
+      atomicAdd(&w.tstamp[22], 1ull);
+      atomicAdd(&w.tstamp[23], sparse ? 1ull : 0ull);
+      atomicAdd(&w.tstamp[24], w.ctl->npot);
+    }
+    if (sparse) {
+      cand_emit_sparse_dev<F>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.new_slot, w.pool, w.pbits, w.desc2, w.hot0,
+                              w.hot1);
+      return;
+    }
+  }
   cand_emit_dev<F>(P, w.ctl, w.tab, w.tab_stride, w.clb, w.new_slot, w.pool, w.desc2, w.hot0, w.hot1);
 }
 #ifndef IBNB_OBJ_TU
@@ -2119,7 +2296,7 @@ __device__ __noinline__ void hot_select_dev(const Pool& p, const uint32_t* __res
 // again by k_child_eval); the acc_* fields likewise.
 // Single-block list phase (k_fused, when ctl->list_fast): the same decisions
 // as list_dev when every live record is in a hot index of at most
-// min(bmax, TPB) entries -- then live <= bmax, the selection takes every live
+// min(bmax, LSMAX * TPB) entries -- then live <= bmax, the selection takes every live
 // entry in list order and no radix pass is needed.  Block 0 only.
 __device__ void list_small_dev(const Pool& p, Ctl* ctl, uint32_t* hot0, uint32_t* hot1, int32_t* sel_slot,
                                uint32_t* sel_code, long kids) {
@@ -2141,43 +2318,65 @@ __device__ void list_small_dev(const Pool& p, Ctl* ctl, uint32_t* hot0, uint32_t
   const long nh = (long)ctl->nhot;
   const uint32_t* hin = hsel ? hot1 : hot0;
   const int t = threadIdx.x;
-  uint32_t r = 0;
-  double lb = CUDART_INF, wv = 0.0;
-  bool live = false;
-  if (t < nh) {
-    r = hin[t];
-    lb = p.lb[r];
-    wv = p.w[r];
-    live = lb <= gub;
+  // thread t owns the hot entries t * ls .. t * ls + ls - 1 (list order),
+  // ls <= LSMAX (set_list_fast)
+  const int ls = (int)((nh + TPB - 1) / TPB);
+  uint32_t r[LSMAX];
+  double lbv[LSMAX], wv[LSMAX];
+  bool live[LSMAX];
+  uint32_t cnt = 0;
+  unsigned long long mk = ~0ull;
+#pragma unroll
+  for (int j = 0; j < LSMAX; ++j) {
+    const long e = (long)t * ls + j;
+    r[j] = 0;
+    lbv[j] = CUDART_INF;
+    wv[j] = 0.0;
+    live[j] = false;
+    if (j < ls && e < nh) {
+      r[j] = hin[e];
+      lbv[j] = p.lb[r[j]];
+      wv[j] = p.w[r[j]];
+      live[j] = lbv[j] <= gub;
+    }
+    if (live[j]) {
+      ++cnt;
+      const unsigned long long key = okey(lbv[j]);
+      mk = key < mk ? key : mk;
+    }
   }
-  const unsigned long long key = live ? okey(lb) : ~0ull;
   // live count (exclusive scan = selection position) and min key
-  const unsigned bal = __ballot_sync(0xffffffffu, live);
   const int lane = t & 31, wid = t >> 5;
-  unsigned long long mk = key;
+  uint32_t inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     unsigned long long q = __shfl_xor_sync(0xffffffffu, mk, o);
     mk = q < mk ? q : mk;
   }
-  if (lane == 0) {
-    s_scan[wid] = __popc(bal);
-    if (mk != ~0ull) atomicMin(&s_min, mk);
-  }
+  if (lane == 31) s_scan[wid] = inc;
+  if (lane == 0 && mk != ~0ull) atomicMin(&s_min, mk);
   __syncthreads();
   uint32_t before = 0, total = 0;
   for (int w2 = 0; w2 < TPB / 32; ++w2) {
     if (w2 < wid) before += s_scan[w2];
     total += s_scan[w2];
   }
-  const uint32_t pos = before + __popc(bal & ((1u << lane) - 1u));
+  const uint32_t pos0 = before + inc - cnt;
   const unsigned long long nlive = total, minkey = s_min;
   unsigned long long bytes = 12ull * nh;
   int done = 0;
   if (nlive == 0) {
     done = 3;
   } else if (__dsub_ru(gub, okey_inv(minkey)) <= ctl->eps_f) {
-    double mw = live ? wv : 0.0;
+    double mw = 0.0;
+#pragma unroll
+    for (int j = 0; j < LSMAX; ++j)
+      if (live[j]) mw = fmax(mw, wv[j]);
     mw = warp_max(mw);
     if (lane == 0) atomicMax((unsigned long long*)&s_w, (unsigned long long)__double_as_longlong(mw));
     __syncthreads();
@@ -2205,10 +2404,17 @@ __device__ void list_small_dev(const Pool& p, Ctl* ctl, uint32_t* hot0, uint32_t
     return;
   }
   // selection (line 130): every live entry, in list order; L loses them
-  if (live) {
-    sel_slot[pos] = p.slot[r];
-    sel_code[pos] = p.code[r];
-    p.lb[r] = CUDART_INF;
+  {
+    uint32_t pos = pos0;
+#pragma unroll
+    for (int j = 0; j < LSMAX; ++j) {
+      if (live[j]) {
+        sel_slot[pos] = p.slot[r[j]];
+        sel_code[pos] = p.code[r[j]];
+        p.lb[r[j]] = CUDART_INF;
+        ++pos;
+      }
+    }
   }
   bytes += 16ull * nh;
   __syncthreads();
@@ -2390,6 +2596,9 @@ __device__ __noinline__ void list_dev(const Pool& p, Ctl* ctl, unsigned int* his
 __global__ void __launch_bounds__(TPB) k_list(Pool p, Ctl* ctl, unsigned int* hists, int32_t* sel_slot,
                                               uint32_t* sel_code, uint64_t* desc, uint64_t* desc2, uint32_t* tile_ctr,
                                               uint32_t* hot0, uint32_t* hot1, long kids) {
+  // potential-candidate count of this iteration's k_child_eval (read by
+  // k_insert before this kernel runs again)
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->npot = 0ull;
   if (ctl->list_fast) {  // uniform: set by the previous insertion (emit)
     if (blockIdx.x == 0) list_small_dev(p, ctl, hot0, hot1, sel_slot, sel_code, kids);
     return;
@@ -2854,12 +3063,12 @@ static void launch_eval_t(const Problem& P, const IterBufs& w, long nkids, cudaS
   if constexpr (!F::CHAIN) {  // the Levy chain never takes the G = 8 path
     if (P.m == 2 && P.G == 8) {
       k_child_eval<F, 8><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr, w.hist,
-                                             w.ppart);
+                                             w.ppart, zero ? w.pbits : nullptr);
       return;
     }
   }
   k_child_eval<F, 0><<<g, TPB, 0, st>>>(P, w.ctl, w.tab, w.tab_stride, w.clb, za, zb, nz, w.tile_ctr, w.hist,
-                                         w.ppart);
+                                         w.ppart, nullptr);
 }
 
 // k_list blocks for ~hint records: a power of two in [8, g_max]
@@ -2917,19 +3126,26 @@ struct ObjImpl {
   }
   // deep-dive chain (chain.cuh): one cooperative launch, one block per SM,
   // the block slices in dynamic shared memory (2 * per doubles)
-  static int chain(const Problem& P, const IterBufs& w, const ChainBufs& cb, int iters, unsigned sms,
+  static int chain(const Problem& P, const IterBufs& w, const ChainBufs& cb0, int iters, unsigned sms,
                    cudaStream_t st) {
     if constexpr (!F::CHAIN) {
-      const size_t smem = sizeof(MitmTabs) + sizeof(double) * 2 * (size_t)cb.per;
-      static size_t attr = 0;  // dynamic shared memory opted in so far (per instantiation)
-      if (smem > attr) {
-        cudaError_t e = cudaFuncSetAttribute((const void*)k_chain<F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+      // the slice (2 doubles per variable) and, when it fits, its term cache
+      // (4K doubles per variable)
+      ChainBufs cb = cb0;
+      const size_t tcb = sizeof(double) * 4 * F::K * (size_t)cb.per;
+      cb.tcache = sizeof(double) * 2 * (size_t)cb.per + tcb <= 110u * 1024u ? 1 : 0;
+      if (const char* e = std::getenv("IBNB_TCACHE"))
+        if (std::atoi(e) == 0) cb.tcache = 0;
+      const size_t smem = sizeof(MitmTabs) + sizeof(double) * 2 * (size_t)cb.per + (cb.tcache ? tcb : 0);
+      static size_t attr[2] = {0, 0};  // dynamic shared memory opted in so far (per instantiation)
+      const void* fn = P.mitm ? (const void*)k_chain<F, true> : (const void*)k_chain<F, false>;
+      if (smem > attr[P.mitm ? 1 : 0]) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return (int)e;
-        attr = smem;
+        attr[P.mitm ? 1 : 0] = smem;
       }
       void* argv[] = {(void*)&P, (void*)&w, (void*)&cb, (void*)&iters};
-      return (int)cudaLaunchCooperativeKernel((const void*)k_chain<F>, dim3(sms), dim3(TPB), argv, smem, st);
+      return (int)cudaLaunchCooperativeKernel(fn, dim3(sms), dim3(TPB), argv, smem, st);
     } else {
       return (int)cudaErrorInvalidValue;
     }

@@ -56,7 +56,7 @@ __device__ __forceinline__ bool in_chunk(int i, int c, int d, int n) { return ((
 
 // warp-aggregated append of (code, lb) to the iteration's candidate list
 __device__ __forceinline__ void chain_append(unsigned long long* cnt, uint32_t* pc, double* pl, bool cond,
-                                             uint32_t code, double lb) {
+                                             uint32_t code, double lb, double* pw = nullptr, double wv = 0.0) {
   const unsigned am = __activemask();
   const unsigned mk = __ballot_sync(am, cond);
   if (!mk) return;
@@ -69,6 +69,7 @@ __device__ __forceinline__ void chain_append(unsigned long long* cnt, uint32_t* 
     if (idx < (unsigned long long)PCAP) {
       pc[idx] = code;
       pl[idx] = lb;
+      if (pw) pw[idx] = wv;
     }
   }
 }
@@ -118,6 +119,50 @@ __device__ __forceinline__ void chain_slice_partial(const Problem& P, const doub
   }
 }
 
+// the same partial from the per-variable term cache s_tc (box terms then
+// midpoint terms of each slice variable, 4K doubles: F::terms of the current
+// values, written when a variable changes) -- the same combinations in the
+// same order as chain_slice_partial, so the same bits, without evaluating
+// any term
+template <class F>
+__device__ __forceinline__ void chain_slice_partial_cached(const Problem& P, const double* s_lo, const double* s_hi,
+                                                           const double* s_tc, int i0, int i1, int c1, int c2,
+                                                           double* part, double* keep) {
+  const int n = P.n, d = P.d;
+  constexpr int TC = 4 * F::K;
+  Iv acc[2], accm[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) acc[k] = accm[k] = iv(0.0);
+#pragma unroll
+  for (int k = 0; k < F::K; ++k) acc[k] = accm[k] = acc_ident<F>(k);
+  double wmax = 0.0;
+  constexpr int HB = TPB / 2;
+  const int hv = threadIdx.x % HB, half = threadIdx.x / HB;
+  for (int i = i0 + hv; i < i1; i += HB) {
+    if (in_chunk(i, c1, d, n) || (c2 >= 0 && in_chunk(i, c2, d, n))) continue;
+    const double* tc = s_tc + (size_t)(i - i0) * TC;
+    if (half == 0) {
+      wmax = fmax(wmax, __dsub_rn(s_hi[i - i0], s_lo[i - i0]));
+#pragma unroll
+      for (int k = 0; k < F::K; ++k) acc[k] = acc_comb<F>(k, acc[k], get(tc + 2 * k));
+    } else {
+#pragma unroll
+      for (int k = 0; k < F::K; ++k) accm[k] = acc_comb<F>(k, accm[k], get(tc + 2 * F::K + 2 * k));
+    }
+  }
+  block_reduce_prep<F, TPB>(acc, accm, wmax);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 2; ++k) {
+      put(part + 2 * k, acc[k]);
+      put(part + 4 + 2 * k, accm[k]);
+      put(keep + 2 * k, acc[k]);
+      put(keep + 4 + 2 * k, accm[k]);
+    }
+    part[8] = keep[8] = wmax;
+    part[9] = keep[9] = 0.0;
+  }
+}
+
 // first-order test of child `code` of the bisection table T (one thread):
 // separable objectives read the per-entry flags, the others take
 // child_mono_ok (bit-identical to the warp version of the other paths)
@@ -130,6 +175,48 @@ __device__ __forceinline__ bool chain_fo_ok(const Problem& P, const double* T, u
   } else {
     return child_mono_ok<F>(P, T, code);
   }
+}
+
+// i / per without an integer division (rper = 1 / per as float, corrected)
+__device__ __forceinline__ int blk_of(int i, int per, float rper) {
+  int q = __float2int_rz(__int2float_rn(i) * rper);
+  if ((q + 1) * per <= i) ++q;
+  if (q * per > i) --q;
+  return q;
+}
+
+// chain_child_rank for slices of per >= d variables (every chunk meets at
+// most two slices: those of its first and last variable), registers only
+__device__ __forceinline__ int chain_child_rank_fast(int blk, int G, int per, float rper, int n, int d, int c,
+                                                     int cn, int cprev, bool with_prev, int& nrank) {
+  int bs[6];
+  const int st[3] = {c, cn, with_prev ? cprev : c};
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    int e = st[q] + d - 1;
+    if (e >= n) e -= n;
+    bs[2 * q] = blk_of(st[q], per, rper);
+    bs[2 * q + 1] = blk_of(e, per, rper);
+  }
+  int busy = 0, before = 0;
+  bool me = false;
+#pragma unroll
+  for (int a = 0; a < 6; ++a) {
+    bool dup = false;
+#pragma unroll
+    for (int z = 0; z < a; ++z) dup |= bs[z] == bs[a];
+    if (!dup) {
+      ++busy;
+      before += bs[a] < blk ? 1 : 0;
+      me |= bs[a] == blk;
+    }
+  }
+  nrank = G - busy;
+  if (2 * nrank < G) {  // degenerate (tiny grid): every block shares the children
+    nrank = G;
+    return blk;
+  }
+  return me ? -1 : blk - before;
 }
 
 // rank of block `blk` among the blocks whose slices (per variables each) meet
@@ -184,6 +271,8 @@ struct ChainOut {
   double* pl;
   double* clb;
   bool all;
+  unsigned long long* npot = nullptr;  // (IBNB_TRACE) children with lb <= GUB at the iteration start
+  double* pw = nullptr;                // max width of each listed child (k_chain's phase 2 reads it)
 };
 
 
@@ -208,22 +297,41 @@ __device__ __forceinline__ void chain_leaf(const Problem& P, const double* T, do
   }
   const bool pot = valid && lb <= gub0;
   bool keep = pot;
+  double wv = 0.0;
   if (pot) {
     o.clb[code] = lb;
-    Iv Bm[2];
+    // midpoint accumulators: rest + the d chunk terms as four interleaved
+    // partial sums (a short dependence chain; another association of the
+    // natural extension's sum, R10)
+    Iv Bm[4][2];
 #pragma unroll
-    for (int q = 0; q < F::K; ++q) Bm[q] = get(T + H_RESTM + 2 * q);
-    for (int jj = 0; jj < P.d; ++jj) {
-      const double* e = T + HDR + (size_t)(2 * jj + ((code >> jj) & 1u)) * ENT + E_T + 2 * F::K;
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int q = 0; q < F::K; ++q) Bm[q] = acc_comb<F>(q, Bm[q], get(e + 2 * q));
+      for (int q = 0; q < F::K; ++q) Bm[u][q] = u == 0 ? get(T + H_RESTM + 2 * q) : acc_ident<F>(q);
+    for (int jj = 0; jj < P.d; jj += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (jj + u < P.d) {
+          const double* e = T + HDR + (size_t)(2 * (jj + u) + ((code >> (jj + u)) & 1u)) * ENT;
+#pragma unroll
+          for (int q = 0; q < F::K; ++q) Bm[u][q] = acc_comb<F>(q, Bm[u][q], get(e + E_T + 2 * F::K + 2 * q));
+          wv = fmax(wv, __dsub_rn(e[E_HI], e[E_LO]));
+        }
+      }
     }
-    best = fmin(best, outer_hi<F>(Bm, P.n));
+#pragma unroll
+    for (int q = 0; q < F::K; ++q)
+      Bm[0][q] = acc_comb<F>(q, acc_comb<F>(q, Bm[0][q], Bm[1][q]), acc_comb<F>(q, Bm[2][q], Bm[3][q]));
+    best = fmin(best, outer_hi<F>(Bm[0], P.n));
     // the first-order test does not depend on GUB: taken here, so the list
     // holds only children it keeps
     if (P.mono) keep = chain_fo_ok<F>(P, T, code);
   }
-  chain_append(o.cnt, o.pc, o.pl, keep, code, lb);
+  if (o.npot) {  // trace statistics, one atomic per warp
+    const unsigned am = __activemask(), pm = __ballot_sync(am, pot);
+    if (pm && (threadIdx.x & 31) == __ffs(am) - 1) atomicAdd(o.npot, (unsigned long long)__popc(pm));
+  }
+  chain_append(o.cnt, o.pc, o.pl, keep, code, lb, o.pw, wv);
 }
 
 // lower bounds of the 2^J children below accumulators A into lbs[idx ..]:
@@ -451,20 +559,21 @@ __device__ __forceinline__ void chain_combine(const double* part, int G, Iv* acc
   wmax = rw;
 }
 
-template <class F>
+// MITM: the children by meet in the middle (d > 16) -- a template parameter so
+// that each kernel holds only its own children code (instruction cache)
+template <class F, bool MITM>
 __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBufs cb, int iters) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double s_dyn[];
   constexpr int TS = HDR + 2 * D_MAX * ENT;  // bisection tables (m = 2, d <= 16)
   __shared__ double s_T[2][TS];
-  __shared__ uint32_t s_pc[PCAP];
-  __shared__ double s_pl[PCAP];
   __shared__ Iv s_ra[TPB / 32][2], s_rm[TPB / 32][2];
   __shared__ double s_rw[TPB / 32];
   __shared__ double s_my[CH_PART];  // this block's last published slice partial
   __shared__ uint32_t s_code;
   __shared__ double s_lb, s_wsurv;
-  __shared__ unsigned int s_nc, s_ns;
+  __shared__ unsigned int s_ns[2];
+  __shared__ double s_m[TPB / 32];
   Ctl* ctl = w.ctl;
   const int n = P.n, d = P.d, t = threadIdx.x, blk = blockIdx.x, G = gridDim.x;
   const int lane = t & 31;
@@ -472,6 +581,8 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
   MitmTabs& M = *reinterpret_cast<MitmTabs*>(s_dyn);  // d >= 17: meet-in-the-middle tables
   double* s_lo = s_dyn + sizeof(MitmTabs) / sizeof(double);
   double* s_hi = s_lo + cb.per;
+  double* s_tc = s_hi + cb.per;  // term cache (cb.tcache): 4K doubles per slice variable
+  const bool tcache = cb.tcache != 0;
   const int i0 = blk * cb.per, i1 = min(n, i0 + cb.per);
 
   // ---- entry: list phase (block 0) -- the host launches k_chain only when
@@ -511,6 +622,21 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     }
   }
   __syncthreads();
+  if (tcache) {  // the terms of every slice variable (box and midpoint), once
+    for (int i = i0 + t; i < i1; i += TPB) {
+      const double a = s_lo[i - i0], bb = s_hi[i - i0];
+      Iv tb[2], tm[2];
+      F::terms(Iv{a, bb}, i, n, tb);
+      const double xm = midpt(a, bb);
+      F::terms(Iv{xm, xm}, i, n, tm);
+      double* tc = s_tc + (size_t)(i - i0) * 4 * F::K;
+#pragma unroll
+      for (int q = 0; q < F::K; ++q) {
+        put(tc + 2 * q, tb[q]);
+        put(tc + 2 * F::K + 2 * q, tm[q]);
+      }
+    }
+  }
   // rest accumulators of R0 (variables outside chunk c) and its chunk entries
   chain_slice_partial<F>(P, s_lo, s_hi, i0, i1, c, -1, cb.part + ((size_t)1 * G + blk) * CH_PART, s_my);
   chain_chunk_entries<F>(P, s_lo, s_hi, i0, i1, c, cb.tabn);
@@ -549,6 +675,19 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     ts[slot] += tn - tb;                   \
     tb = tn;                               \
   }
+  // header of the current table in registers of every thread (the same bits
+  // in every thread of every block; also in s_T for the rare readers)
+  Iv hrest[2], hrestm[2];
+  double hw;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    hrest[q] = get(s_T[0] + H_REST + 2 * q);
+    hrestm[q] = get(s_T[0] + H_RESTM + 2 * q);
+  }
+  hw = s_T[0][H_WREST];
+  if (t == 0) s_ns[0] = s_ns[1] = 0u;  // read after the first phase-2 barrier
+  const float rper = 1.0f / (float)cb.per;
+  const bool fast_rank = cb.per >= d;
   for (;; ++k) {
     const int sl = k % 3;
     double* T = s_T[k & 1];
@@ -556,6 +695,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     const int cn = (c + d) % n;
     const double gub0 = okey_inv(gub_key);
     // ================= phase 1
+    const unsigned long long tp1 = (w.tstamp && t == 0) ? gtimer() : 0ull;  // per-role phase-1 times (trace)
     unsigned long long shared_old = ~0ull;
     if (blk == 0 && t == 0) {  // slot of the next iteration (last read before the previous barrier)
       cb.cnt[(k + 1) % 3] = 0ull;
@@ -568,12 +708,14 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     // (a) children: a thread owns the 2^H children of a code whose H low bits
     // are clear (enough groups for every thread of the grid, H <= 3)
     double best = CUDART_INF;
+    int nrank = G;
+    const int rank = fast_rank ? chain_child_rank_fast(blk, G, cb.per, rper, n, d, c, cn, cprev, k > 0, nrank)
+                               : chain_child_rank(blk, G, cb.per, n, d, c, cn, cprev, k > 0, nrank);
     {
-      ChainOut o{cb.cnt + sl, cb.pcode + (size_t)sl * PCAP, cb.plb + (size_t)sl * PCAP, w.clb, false};
-      int nrank = G;
-      const int rank = chain_child_rank(blk, G, cb.per, n, d, c, cn, cprev, k > 0, nrank);
+      ChainOut o{cb.cnt + sl, cb.pcode + (size_t)sl * PCAP, cb.plb + (size_t)sl * PCAP, w.clb, false,
+                 w.tstamp ? cb.exits + 7 : nullptr, cb.pw + (size_t)sl * PCAP};
       if (rank >= 0) {
-        if (!P.mitm) best = chain_children<F, 1>(P, T, gub0, o, rank, nrank);
+        if constexpr (!MITM) best = chain_children<F, 1>(P, T, gub0, o, rank, nrank);
         else best = chain_children_mitm<F>(P, T, M, gub0, o, rank, nrank);
       }
     }
@@ -583,17 +725,22 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     // republishes the bits of its previous partial (the full slice sum)
     {
       double* dst = cb.part + ((size_t)(k & 1) * G + blk) * CH_PART;
-      if (meets(i0, i1, c, d, n) || meets(i0, i1, cn, d, n) || (k > 0 && meets(i0, i1, cprev, d, n)))
-        chain_slice_partial<F>(P, s_lo, s_hi, i0, i1, c, cn, dst, s_my);
-      else if (t < CH_PART)
+      if (meets(i0, i1, c, d, n) || meets(i0, i1, cn, d, n) || (k > 0 && meets(i0, i1, cprev, d, n))) {
+        __syncthreads();  // the slice update of the last phase 2 (uniform: an owner block)
+        if (tcache) chain_slice_partial_cached<F>(P, s_lo, s_hi, s_tc, i0, i1, c, cn, dst, s_my);
+        else chain_slice_partial<F>(P, s_lo, s_hi, i0, i1, c, cn, dst, s_my);
+      } else if (t < CH_PART) {
         dst[t] = s_my[t];
+      }
     }
     // (c) entries of chunk c' (unchanged in every child of R)
     chain_chunk_entries<F>(P, s_lo, s_hi, i0, i1, cn, cb.tabn + (size_t)((k + 1) & 1) * DM_MAX * ENT);
-    // (d) this block's midpoint minimum; block 0 also brings in the incumbent
-    // shared with the other ranks (issued at the iteration start)
+    // (d) this block's midpoint minimum, ONE atomic per block (one word takes
+    // every block's: per-warp atomics queue 8x as many at its L2 slice, and
+    // the phase-2 load of the word waits behind them); block 0 also brings in
+    // the incumbent shared with the other ranks (issued at the iteration
+    // start).  The block barrier costs little: the grid barrier starts with one.
     {
-      __shared__ double s_m[TPB / 32];
       best = warp_min(best);
       if (lane == 0) s_m[t >> 5] = best;
       __syncthreads();
@@ -602,6 +749,11 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
         if (best < CUDART_INF) atomicMin(&cb.gacc[sl], (unsigned long long)okey(best));
         if (shared_old != ~0ull) atomicMin(&cb.gacc[sl], shared_old);
       }
+    }
+    if (w.tstamp && t == 0) {  // phase-1 time by role: 16/17 blocks with slice work, 18/19 children only
+      const int role = rank < 0 ? 16 : 18;
+      atomicAdd(&w.tstamp[role], gtimer() - tp1);
+      atomicAdd(&w.tstamp[role + 1], 1ull);
     }
     CH_TICK(27)
     grid.sync();
@@ -613,10 +765,11 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     const unsigned long long np = __ldcg(&cb.cnt[sl]);
     const unsigned long long gk = __ldcg(&cb.gacc[sl]);
     uint32_t my_pc = 0;
-    double my_pl = CUDART_INF;
+    double my_pl = CUDART_INF, my_pw = 0.0;
     if (t < PCAP) {
       my_pc = __ldcg(&cb.pcode[(size_t)sl * PCAP + t]);
       my_pl = __ldcg(&cb.plb[(size_t)sl * PCAP + t]);
+      my_pw = __ldcg(&cb.pw[(size_t)sl * PCAP + t]);
     }
     Iv ra[2], rm[2];
     double rw = 0.0;
@@ -644,104 +797,108 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     const int npi = fits ? (int)np : 0;
     // warp level of the (fixed-order) reduction of the slice partials
     warp_reduce_prep<F>(ra, rm, rw);
-    {
-      if (lane == 0) {
+    if (lane == 0) {
 #pragma unroll
-        for (int q = 0; q < F::K; ++q) {
-          s_ra[t >> 5][q] = ra[q];
-          s_rm[t >> 5][q] = rm[q];
-        }
-        s_rw[t >> 5] = rw;
+      for (int q = 0; q < F::K; ++q) {
+        s_ra[t >> 5][q] = ra[q];
+        s_rm[t >> 5][q] = rm[q];
       }
-      if (t < npi) {
-        s_pc[t] = my_pc;
-        s_pl[t] = my_pl;
-      }
-      if (t == 0) {
-        s_nc = 0;
-        s_ns = 0;
-      }
+      s_rw[t >> 5] = rw;
     }
-    __syncthreads();
-    // candidates (lb <= GUB; the first-order test was taken in phase 1): the
-    // survivors and their widths, a warp each
-    for (int q = t >> 5; q < npi; q += TPB / 32) {
-      if (!(s_pl[q] <= gub)) continue;  // warp-uniform
-      const uint32_t code = s_pc[q];
-      double wl = 0.0;
-      if (lane < d) {
-        const double* e = T + HDR + (size_t)(2 * lane + ((code >> lane) & 1u)) * ENT;
-        wl = __dsub_rn(e[E_HI], e[E_LO]);
-      }
-      wl = warp_max(wl);
-      if (lane == 0) {
-        atomicAdd(&s_nc, 1u);
-        atomicAdd(&s_ns, 1u);
-        s_code = code;  // the survivor when it is the only one
-        s_lb = s_pl[q];
-        s_wsurv = fmax(T[H_WREST], wl);
-      }
+    // candidates (lb <= GUB; the first-order test and the widths were taken
+    // in phase 1), a thread each: the survivors are counted, the survivor's
+    // code, bound and width are read back only when it is the only one
+    if (t == 0) s_ns[(k + 1) & 1] = 0u;  // last read before this iteration's grid barrier
+    if (t < npi && my_pl <= gub) {
+      atomicAdd(&s_ns[k & 1], 1u);
+      s_code = my_pc;
+      s_lb = my_pl;
+      s_wsurv = my_pw;
     }
-    __syncthreads();
+    __syncthreads();  // the only block barrier of phase 2
+    const unsigned ns = s_ns[k & 1];
+    const uint32_t scode = s_code;
+    const double slb = s_lb, swid = s_wsurv;
     bool cont = fits;
     why = 2;
     if (cont) {
-      const unsigned ns = s_ns;
       cont = ns == 1;
       why = ns == 0 ? 0 : 1;
       if (cont) {
         // the next list phase on the single live record (list_small_dev's
         // decisions): stop test (lines 148-150), iteration limit, budget
-        if (__dsub_ru(gub, s_lb) <= eps_f) {
+        if (__dsub_ru(gub, slb) <= eps_f) {
           nwidth += 1;
-          if (s_wsurv <= eps_x) cont = false, why = 3;
+          if (fmax(hw, swid) <= eps_x) cont = false, why = 3;
         }
         if (cont && iter0 + (unsigned long long)k + 1 >= max_iter) cont = false, why = 4;
         if (cont && k + 1 >= iters) cont = false, why = 5;
       }
-      if (cont) sum_cand += s_nc;
+      if (cont) sum_cand += ns;
     }
     CH_TICK(29)
     if (!cont) break;  // uniform: every block took the same decisions
-    // ---- continue: the survivor R' becomes the selected region
-    const uint32_t scode = s_code;
-    if (t == 0) {
-      // block level of the partials' reduction (block_reduce_prep's order),
-      // then rest(R') = S_excl + terms of R' in chunk c (not in c', n >= 2d)
-      for (int wq = 1; wq < TPB / 32; ++wq) {
+    // ---- continue: the survivor R' becomes the selected region.  Every
+    // warp builds the header of R' itself, lanes in parallel: lane l < 8
+    // holds warp l's partial of S_excl, lane j < d the terms of R' in chunk c
+    // (not in c', n >= 2d); an xor butterfly leaves the same bits in every
+    // lane of every warp of every block (commutative combinations): rest(R')
+    // = S_excl + the chunk-c terms of R'
+    {
+      Iv A[2], Am[2];
+      double W = 0.0;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) A[q] = Am[q] = iv(0.0);
+#pragma unroll
+      for (int q = 0; q < F::K; ++q) {
+        A[q] = lane < TPB / 32 ? s_ra[lane][q] : acc_ident<F>(q);
+        Am[q] = lane < TPB / 32 ? s_rm[lane][q] : acc_ident<F>(q);
+      }
+      if (lane < TPB / 32) W = s_rw[lane];
+      if (lane < d) {
+        const double* e = T + HDR + (size_t)(2 * lane + ((scode >> lane) & 1u)) * ENT;
 #pragma unroll
         for (int q = 0; q < F::K; ++q) {
-          ra[q] = acc_comb<F>(q, ra[q], s_ra[wq][q]);
-          rm[q] = acc_comb<F>(q, rm[q], s_rm[wq][q]);
+          A[q] = acc_comb<F>(q, A[q], get(e + E_T + 2 * q));
+          Am[q] = acc_comb<F>(q, Am[q], get(e + E_T + 2 * F::K + 2 * q));
         }
-        rw = fmax(rw, s_rw[wq]);
+        W = fmax(W, __dsub_rn(e[E_HI], e[E_LO]));
       }
-      for (int j = 0; j < d; ++j) {
-        const double* e = T + HDR + (size_t)(2 * j + ((scode >> j) & 1u)) * ENT;
+      warp_reduce_prep<F>(A, Am, W);
 #pragma unroll
-        for (int q = 0; q < F::K; ++q) {
-          ra[q] = acc_comb<F>(q, ra[q], get(e + E_T + 2 * q));
-          rm[q] = acc_comb<F>(q, rm[q], get(e + E_T + 2 * F::K + 2 * q));
-        }
-        rw = fmax(rw, __dsub_rn(e[E_HI], e[E_LO]));
-      }
       for (int q = 0; q < 2; ++q) {
-        put(Tn + H_REST + 2 * q, ra[q]);
-        put(Tn + H_RESTM + 2 * q, rm[q]);
+        hrest[q] = A[q];
+        hrestm[q] = Am[q];
       }
-      Tn[H_WREST] = rw;
-      Tn[H_CHUNK] = (double)cn;
+      hw = W;
+      // the header also in s_T for the readers of the table (children, the
+      // first-order test, the exit path): every warp writes the same bits
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          put(Tn + H_REST + 2 * q, hrest[q]);
+          put(Tn + H_RESTM + 2 * q, hrestm[q]);
+        }
+        Tn[H_WREST] = hw;
+        Tn[H_CHUNK] = (double)cn;
+      }
+      __syncwarp();
     }
-    // slice update: chunk c variables take the survivor's pieces
+    // slice update: chunk c variables take the survivor's pieces (read by
+    // this block's next slice partial after its barrier)
     for (int j = t; j < d; j += TPB) {
       const int i = (c + j) % n;
       if (i >= i0 && i < i1) {
         const double* e = T + HDR + (size_t)(2 * j + ((scode >> j) & 1u)) * ENT;
         s_lo[i - i0] = e[E_LO];
         s_hi[i - i0] = e[E_HI];
+        if (tcache) {  // the piece's terms are the entry's (piece_entry: same F::terms, same arguments)
+          double* tc = s_tc + (size_t)(i - i0) * 4 * F::K;
+#pragma unroll
+          for (int q = 0; q < 4 * F::K; ++q) tc[q] = e[E_T + q];
+        }
       }
     }
-    __syncthreads();
     cprev = c;
     c = cn;
     CH_TICK(30)
@@ -790,7 +947,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     const long nz = 3 * (((long)P.kids + TILE - 1) / TILE + 1);
     for (long q = (long)blk * TPB + t; q < nz; q += (long)G * TPB) w.desc2[q] = 0;
     ChainOut o{nullptr, nullptr, nullptr, w.clb, true};
-    if (!P.mitm) chain_children<F, 1>(P, T, 0.0, o);
+    if constexpr (!MITM) chain_children<F, 1>(P, T, 0.0, o);
     else chain_children_mitm<F>(P, T, M, 0.0, o);
   }
   grid.sync();

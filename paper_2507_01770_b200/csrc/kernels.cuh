@@ -15,6 +15,7 @@ constexpr int ENT = 24;                         // doubles per (variable, piece)
 constexpr int TPB = 256;                        // threads per block (all kernels)
 constexpr int IPT = 4;                          // items per thread in scans
 constexpr int TILE = TPB * IPT;
+constexpr int LSMAX = 4;                        // hot entries per thread of the single-block list phase
 constexpr int PCAP = 256;                       // k_fused: potential candidates handled by one block
 
 // header offsets (doubles)
@@ -137,6 +138,7 @@ struct IterBufs {
   unsigned int* pticket;   // k_prep per-parent arrival tickets [bmax] (zero between launches)
   unsigned long long* tstamp;  // k_fused phase timer (trace only; nullptr otherwise)
   uint32_t* pot;               // k_fused: potential candidates (child indices), PCAP entries
+  uint64_t* pbits;             // graph path: potential-candidate bitmap of the children (k_child_eval -> k_insert)
 };
 
 // buffers of the deep-dive chain kernel (chain.cuh)
@@ -146,6 +148,7 @@ struct ChainBufs {
   unsigned long long* gacc;  // [3] midpoint minima (ordered keys) per slot
   uint32_t* pcode;           // [3][PCAP] potential candidates (child codes)
   double* plb;               // [3][PCAP] their lower bounds
+  double* pw;                // [3][PCAP] their max widths
   double* part;              // [2][grid][CH_PART] slice partials
   double* tabn;              // [2][DM_MAX * ENT] entries of the next chunk
   unsigned long long* exits;  // [8] why launches left the chain (trace statistics): 0 no survivor,
@@ -153,6 +156,7 @@ struct ChainBufs {
                               // 4 iteration limit, 5 launch budget, 6 nothing to chain at entry
   unsigned long long* gshared;  // multi-GPU: the incumbent word shared by every rank (or nullptr)
   int per;                   // variables per block slice
+  int tcache;                // k_chain keeps the slice's term cache in shared memory (set by the launcher)
   int grid;                  // k_chain blocks (one per SM, IBNB_CHAIN_GRID caps it)
 };
 

@@ -82,6 +82,14 @@ __global__ void k_root(const double* root_out, double w0, Pool p, Ctl* ctl) {
   ctl->pcount = 1;
 }
 // after a compaction of L: new record count, positions changed -> rebuild the hot index
+// multi-GPU incumbent word (ib_options.gub_shared): lower it to this rank's
+// GUB and take the other ranks' value back -- before every chunk, so the
+// batch paths (k_fused, the iteration graph) prune with it too; k_chain also
+// does this every iteration
+__global__ void k_gub_shared(Ctl* ctl, unsigned long long* word) {
+  const unsigned long long old = atomicMin(word, ctl->gub_key);
+  if (old < ctl->gub_key) ctl->gub_key = old;
+}
 __global__ void k_set_pcount(Ctl* ctl, const uint64_t* c) {
   ctl->pcount = *c;
   ctl->hot_valid = 0;
@@ -306,6 +314,7 @@ struct SolveWs {
   double* ppart;
   unsigned int* pticket;
   uint32_t* pot;
+  uint64_t* pbits;
   ChainBufs chain;
 };
 
@@ -357,10 +366,12 @@ static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {
   w.ppart = A.take<double>((size_t)o.bmax * prep_slices(n, o.bmax) * 10);
   w.pticket = A.take<unsigned int>(o.bmax);
   w.pot = A.take<uint32_t>(PCAP);
+  w.pbits = A.take<uint64_t>((size_t)(kids_tot + 63) / 64 + 8);
   w.chain.cnt = A.take<unsigned long long>(3);
   w.chain.gacc = A.take<unsigned long long>(3);
   w.chain.pcode = A.take<uint32_t>(3 * PCAP);
   w.chain.plb = A.take<double>(3 * PCAP);
+  w.chain.pw = A.take<double>(3 * PCAP);
   w.chain.part = A.take<double>((size_t)2 * chain_grid() * CH_PART);
   w.chain.tabn = A.take<double>((size_t)2 * DM_MAX * ENT);
   w.chain.exits = A.take<unsigned long long>(8);
@@ -471,6 +482,7 @@ struct GraphKey {
   long bound;
   long list_hint;  // k_list grid size class
   long bmax, pool_cap, arch_cap;  // workspace layout
+  const void* tstamp;              // trace counters (IBNB_TRACE) baked into the kernels' arguments
 };
 static bool same_problem(const Problem& a, const Problem& b) { return std::memcmp(&a, &b, sizeof(Problem)) == 0; }
 
@@ -488,7 +500,7 @@ struct ThreadCache {
   cudaGraphExec_t find(const GraphKey& k, long need_bound) {
     for (auto& e : graphs)
       if (same_problem(e.k.P, k.P) && e.k.pool == k.pool && e.k.ws == k.ws && e.k.bmax == k.bmax &&
-          e.k.list_hint == k.list_hint &&
+          e.k.list_hint == k.list_hint && e.k.tstamp == k.tstamp &&
           e.k.pool_cap == k.pool_cap && e.k.arch_cap == k.arch_cap && e.k.bound >= need_bound)
         return e.ge;
     return nullptr;
@@ -631,6 +643,9 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   ib.ppart = w.ppart;
   ib.pticket = w.pticket;
   ib.pot = w.pot;
+  ib.pbits = w.pbits;
+  if (const char* e = std::getenv("IBNB_SPARSE"))  // 0: always the dense insertion (A/B measurements)
+    if (std::atoi(e) == 0) ib.pbits = nullptr;
   unsigned long long* tstamp = nullptr;
   if (trace) {
     CK(cudaMalloc(&tstamp, 32 * sizeof(unsigned long long)));
@@ -697,6 +712,10 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
       chunk = std::max(1L, std::min(chunk, (long)free_top / o.bmax));
     }
     ib.pool = w.pa;
+    if (w.chain.gshared) {
+      k_gub_shared<<<1, 1, 0, st>>>(w.ctl, w.chain.gshared);
+      nk += 1;
+    }
     const long pool_bound = (long)pcount + chunk * per_it;
     // k_list grid class from the records L holds now: two classes, so that
     // the cached iteration graphs do not multiply
@@ -722,7 +741,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
       // one captured iteration per (problem, buffers, grid bound), cached per
       // thread and replayed; re-captured when its grid bound is exceeded
       GraphKey key{P, ib.pool.lb, ws, graph_bound_for(pool_bound, pcount, per_it, o.pool_cap), list_hint, o.bmax,
-                   o.pool_cap, o.arch_cap};
+                   o.pool_cap, o.arch_cap, ib.tstamp};
       cudaGraphExec_t ge = tc.find(key, pool_bound);
       if (!ge) {
         CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
@@ -907,6 +926,13 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
               tsh[28] / 1e3 / tsh[31], tsh[29] / 1e3 / tsh[31], tsh[30] / 1e3 / tsh[31]);
     fprintf(stderr, "\n[ibnb] chain launches %ld, exits:", chain_launches);
     for (int k = 0; k < 7; ++k) fprintf(stderr, " %s=%llu", why[k], ex[k]);
+    if (tsh[31]) fprintf(stderr, " potential_children_per_iter=%.2f", (double)ex[7] / tsh[31]);
+    if (tsh[17] + tsh[19])
+      fprintf(stderr, "\n[ibnb] chain phase 1 per block (us): slice/entry blocks %.2f (%llu), children blocks %.2f (%llu)",
+              tsh[16] / 1e3 / std::max(1ull, tsh[17]), tsh[17], tsh[18] / 1e3 / std::max(1ull, tsh[19]), tsh[19]);
+    if (tsh[22])
+      fprintf(stderr, "\n[ibnb] k_insert launches %llu, sparse %llu, potential candidates per launch %.1f", tsh[22],
+              tsh[23], (double)tsh[24] / (double)tsh[22]);
     fprintf(stderr, "\n");
   }
   // exact max width of the remaining regions for the result
@@ -919,7 +945,7 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
   switch (c.done) {
     case 1: status = IB_STATUS_CONVERGED; break;
     case 2: status = IB_STATUS_MAX_ITER; break;
-    default: status = xfn ? IB_STATUS_EMPTY : IB_EEMPTY; break;
+    default: status = (xfn || w.chain.gshared) ? IB_STATUS_EMPTY : IB_EEMPTY; break;
   }
   if (status == IB_EEMPTY) return fail(IB_EEMPTY, "list L became empty after %llu iterations", c.iter);
   // output (line 150): GLB, GUB and the live regions of L, in list order

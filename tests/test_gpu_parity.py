@@ -836,8 +836,10 @@ def test_shared_incumbent_word_prunes_the_other_slab(pb):
     its GUB every iteration and takes the minimum back.  Rastrigin n = 2000
     cut at x_1 = 0.25: the slab with the minimiser encloses f* = 0 and leaves
     its GUB in the word; the other slab, solved with the same word, is ruled
-    out at once (status 2, far fewer iterations than alone) and reports the
-    shared incumbent; the union enclosure is the eps-enclosure of 0."""
+    out at once (status 2 after a few iterations; alone, its list L outgrows
+    2^26 records: its best point has f ~ 1) and reports the shared incumbent;
+    the union enclosure is the eps-enclosure of 0.  The word is taken before
+    every chunk of the batch paths too, not only by the deep-dive kernel."""
     fid, n = 7, 2000
     l, u = workloads.bounds(fid, n)
     (l0, u0), (l1, u1) = _slab(l, u, 0.25)
@@ -845,10 +847,9 @@ def test_shared_incumbent_word_prunes_the_other_slab(pb):
     o = pb.options(d=16, gub_shared=word.data_ptr())
     r0 = pb.ib_solve_dev(fid, cuda(l0), cuda(u0), 1e-6, 1e-6, o)
     assert r0.status == 0 and r0.f_lo <= 0.0 <= r0.f_hi and r0.f_hi - r0.f_lo <= 1e-6
-    alone = pb.ib_solve_dev(fid, cuda(l1), cuda(u1), 1e-6, 1e-6, pb.options(d=16))
     r1 = pb.ib_solve_dev(fid, cuda(l1), cuda(u1), 1e-6, 1e-6, o)
     assert r1.status == 2, r1.status  # every region of the slab ruled out by the shared GUB
-    assert r1.iters < alone.iters // 10
+    assert r1.iters <= 4, r1.iters
     assert r1.f_hi <= r0.f_hi
     assert min(r0.f_lo, r1.f_lo) <= 0.0 <= min(r0.f_hi, r1.f_hi) <= 1e-6
 
