@@ -114,8 +114,19 @@ def roofline(prof, prof_ms, fid, d=16):
         peak, src = fp64_peak()
         units = pd["units"] / max(1, pd["launches"])
         ach = per_unit * units / avg_s / 1e12 if per_unit else None
-        roof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": peak, "unit": "T FP64-pipe instr/s",
-                "frac": (ach / peak) if ach else None, "traffic": ops.get("dram_bytes_per_launch"),
+        # algorithmic work: the lower bound of every child box, Eq. (3)
+        # as tabulated here -- d lower-end additions of the split variables'
+        # terms onto the rest + the outer function -- per child box, x 2^d
+        # children per deep-dive iteration
+        kids_per_unit = {"chain": 2 ** d, "fused": 2 ** d, "child_eval": 1}.get(dom)
+        algo = kids_per_unit * (d + 1) if kids_per_unit else None
+        ach_algo = algo * units / avg_s / 1e12 if algo else None
+        roof = {"bound": "alu", "kernel": dom, "achieved": ach_algo, "peak": peak, "unit": "T FP64-pipe instr/s",
+                "frac": (ach_algo / peak) if ach_algo else None,
+                "algorithmic_fp64_per_unit": algo,
+                "algorithmic_def": "lower bound of every child: d lower-end additions + the outer function (Eq. 3)",
+                "achieved_executed": ach, "frac_executed": (ach / peak) if ach else None,
+                "traffic": ops.get("dram_bytes_per_launch"),
                 "fp64_inst_per_unit": per_unit, "unit_of_work": ops.get("unit"), "units_per_launch": units,
                 "issue_active_pct_ncu": ops.get("issue_active_pct"), "fp64_pipe_pct_ncu": ops.get("fp64_pipe_pct"),
                 "peak_source": src, "counts_source": "ncu sm__sass_thread_inst_executed_op_{dadd,dmul,dfma} "

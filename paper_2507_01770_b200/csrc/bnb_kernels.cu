@@ -3128,27 +3128,24 @@ struct ObjImpl {
   // the block slices in dynamic shared memory (2 * per doubles)
   static int chain(const Problem& P, const IterBufs& w, const ChainBufs& cb0, int iters, unsigned sms,
                    cudaStream_t st) {
-    if constexpr (!F::CHAIN) {
-      // the slice (2 doubles per variable) and, when it fits, its term cache
-      // (4K doubles per variable)
-      ChainBufs cb = cb0;
-      const size_t tcb = sizeof(double) * 4 * F::K * (size_t)cb.per;
-      cb.tcache = sizeof(double) * 2 * (size_t)cb.per + tcb <= 110u * 1024u ? 1 : 0;
-      if (const char* e = std::getenv("IBNB_TCACHE"))
-        if (std::atoi(e) == 0) cb.tcache = 0;
-      const size_t smem = sizeof(MitmTabs) + sizeof(double) * 2 * (size_t)cb.per + (cb.tcache ? tcb : 0);
-      static size_t attr[2] = {0, 0};  // dynamic shared memory opted in so far (per instantiation)
-      const void* fn = P.mitm ? (const void*)k_chain<F, true> : (const void*)k_chain<F, false>;
-      if (smem > attr[P.mitm ? 1 : 0]) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return (int)e;
-        attr[P.mitm ? 1 : 0] = smem;
-      }
-      void* argv[] = {(void*)&P, (void*)&w, (void*)&cb, (void*)&iters};
-      return (int)cudaLaunchCooperativeKernel(fn, dim3(sms), dim3(TPB), argv, smem, st);
-    } else {
-      return (int)cudaErrorInvalidValue;
+    // the slice (2 doubles per variable) and, when it fits, its term cache
+    // (4K doubles per variable; not for the Levy chain sum)
+    ChainBufs cb = cb0;
+    const size_t tcb = sizeof(double) * 4 * F::K * (size_t)cb.per;
+    cb.tcache = !F::CHAIN && sizeof(double) * 2 * (size_t)cb.per + tcb <= 110u * 1024u ? 1 : 0;
+    if (const char* e = std::getenv("IBNB_TCACHE"))
+      if (std::atoi(e) == 0) cb.tcache = 0;
+    const size_t smem = sizeof(MitmTabs) + sizeof(double) * 2 * (size_t)cb.per + (cb.tcache ? tcb : 0);
+    const bool mitm = P.mitm && !F::CHAIN;  // Levy: a thread per child at any d
+    static size_t attr[2] = {0, 0};  // dynamic shared memory opted in so far (per instantiation)
+    const void* fn = mitm ? (const void*)k_chain<F, !F::CHAIN> : (const void*)k_chain<F, false>;
+    if (smem > attr[mitm ? 1 : 0]) {
+      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return (int)e;
+      attr[mitm ? 1 : 0] = smem;
     }
+    void* argv[] = {(void*)&P, (void*)&w, (void*)&cb, (void*)&iters};
+    return (int)cudaLaunchCooperativeKernel(fn, dim3(sms), dim3(TPB), argv, smem, st);
   }
   template <int CS>
   static int chainc_cs(const Problem& P, const IterBufs& w, const ChainBufs& cb, int iters, cudaStream_t st) {

@@ -54,6 +54,130 @@ IB_NS_BEGIN
 
 __device__ __forceinline__ bool in_chunk(int i, int c, int d, int n) { return ((i - c + n) % n) < d; }
 
+// accumulator identity / combination for every objective (Levy, R11: one
+// plain sum of chain terms)
+template <class F>
+__device__ __forceinline__ Iv ch_ident(int k) {
+  if constexpr (F::CHAIN) return iv(0.0);
+  else return acc_ident<F>(k);
+}
+template <class F>
+__device__ __forceinline__ Iv ch_comb(int k, Iv a, Iv b) {
+  if constexpr (F::CHAIN) return a + b;
+  else return acc_comb<F>(k, a, b);
+}
+
+// ------------------------------------------------------------------ Levy
+// Levy (A11-A12, reading R11) in the chain: term i couples x_i and x_{i+1},
+// so the chunk's table lists the affected chain terms (levy_desc, as k_prep
+// writes them) and the child sums are taken over that list; a block's slice
+// partial covers the pairs (i, i + 1) with i in its slice -- the value of
+// x_{i1} (the next slice's first variable) is kept as a halo.
+// Where the chunk's two neighbour variables live in the tables of the
+// iteration buffers (tabn): the L slot at entry only, the R slot always.
+constexpr int LEVY_TABN_L = DM_MAX * ENT - 16, LEVY_TABN_R = DM_MAX * ENT - 8;
+
+// descriptors of the chain terms affected by chunk c (k_prep's list)
+__device__ __forceinline__ void levy_desc(int c, int d, int n, double* T) {
+  LevyChunk q = levy_chunk(c, d, n);
+  int nt = 0;
+  double* td = T + H_LEVY_T;
+  if (q.inJ(0)) td[nt++] = (double)(0 * 65536 + q.local(0) * 256);
+  const int ncand = d < n ? d + 1 : n;
+  for (int t = 0; t < ncand; ++t) {
+    const int i = d < n ? (c - 1 + t + n) % n : t;
+    if (i > n - 2) continue;
+    if (q.inJ(i) || q.inJ(i + 1)) td[nt++] = (double)(1 * 65536 + q.local(i) * 256 + q.local(i + 1));
+  }
+  if (q.inJ(n - 1)) td[nt++] = (double)(2 * 65536 + q.local(n - 1) * 256);
+  T[H_LEVY_NT] = (double)nt;
+  T[H_LEVY_LR] = (double)q.L;
+  T[H_LEVY_LR + 1] = (double)q.R;
+  T[H_CHUNK] = (double)c;
+}
+
+// value of descriptor dsc for the child `code` (mid: at the midpoint values)
+__device__ __forceinline__ Iv levy_term(const double* T, int dsc, uint32_t code, int d, bool mid) {
+  const int kind = dsc >> 16, li = (dsc >> 8) & 255, lj = dsc & 255;
+  auto ent = [&](int l) { return T + HDR + (size_t)(2 * l + ((code >> l) & 1u)) * ENT; };
+  auto u = [&](int l) {
+    return l < d ? get(ent(l) + (mid ? 12 : 2)) : get(T + H_LEVY_NB + 8 * (l - d) + (mid ? 4 : 0));
+  };
+  auto v = [&](int l) {
+    return l < d ? get(ent(l) + (mid ? 14 : 4)) : get(T + H_LEVY_NB + 8 * (l - d) + (mid ? 6 : 2));
+  };
+  if (kind == 0) return get(ent(li) + (mid ? 16 : 6));
+  if (kind == 1) return mulpos(u(li), v(lj));  // u >= 0, v >= 1
+  return u(li);
+}
+
+// the child's chain sum: rest + the affected terms (list order, as LevyView)
+__device__ __forceinline__ Iv levy_child_acc(const double* T, uint32_t code, int d, bool mid) {
+  Iv a = get(T + (mid ? H_RESTM : H_REST));
+  const int nt = (int)T[H_LEVY_NT];
+  for (int t = 0; t < nt; ++t) a = a + levy_term(T, (int)T[H_LEVY_T + t], code, d, mid);
+  return a;
+}
+
+// slice partial: the chain terms of the slice [i0, i1) that involve no
+// variable of chunk c1 nor of chunk c2 (c2 < 0: none) -- pairs (i, i + 1),
+// s0(x_0), u(x_{n-1}) -- box and midpoint, and the max width outside the
+// chunks; (hlo, hhi): x_{i1} (halo, i1 < n)
+template <class F>
+__device__ __forceinline__ void chain_levy_partial(const Problem& P, const double* s_lo, const double* s_hi,
+                                                   double hlo, double hhi, int i0, int i1, int c1, int c2,
+                                                   double* part, double* keep) {
+  const int n = P.n, d = P.d;
+  Iv acc[2], accm[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) acc[k] = accm[k] = iv(0.0);
+  double wmax = 0.0;
+  constexpr int HB = TPB / 2;
+  const int hv = threadIdx.x % HB, half = threadIdx.x / HB;
+  auto inC = [&](int i) { return in_chunk(i, c1, d, n) || (c2 >= 0 && in_chunk(i, c2, d, n)); };
+  for (int i = i0 + hv; i < i1; i += HB) {
+    const bool ci = inC(i);
+    double a = s_lo[i - i0], bb = s_hi[i - i0];
+    if (half == 1) a = bb = midpt(a, bb);
+    const LevyVals v = ObjLevy::vals(Iv{a, bb});
+    Iv r = iv(0.0);
+    if (!ci) {
+      if (half == 0) wmax = fmax(wmax, __dsub_rn(s_hi[i - i0], s_lo[i - i0]));
+      if (i == 0) r = r + v.s0;
+      if (i == n - 1) r = r + v.u;
+    }
+    if (i <= n - 2 && !ci && !inC(i + 1)) {
+      double a1 = i + 1 < i1 ? s_lo[i + 1 - i0] : hlo, b1 = i + 1 < i1 ? s_hi[i + 1 - i0] : hhi;
+      if (half == 1) a1 = b1 = midpt(a1, b1);
+      r = r + mulpos(v.u, ObjLevy::vals(Iv{a1, b1}).v);
+    }
+    if (half == 0) acc[0] = acc[0] + r;
+    else accm[0] = accm[0] + r;
+  }
+  block_reduce_prep<F, TPB>(acc, accm, wmax);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 2; ++k) {
+      put(part + 2 * k, acc[k]);
+      put(part + 4 + 2 * k, accm[k]);
+      put(keep + 2 * k, acc[k]);
+      put(keep + 4 + 2 * k, accm[k]);
+    }
+    part[8] = keep[8] = wmax;
+    part[9] = keep[9] = 0.0;
+  }
+}
+
+// the Levy values of variable x (box and midpoint: u v um vm) -> 8 doubles
+__device__ __forceinline__ void levy_nb_vals(double a, double bb, double* out) {
+  const LevyVals v = ObjLevy::vals(Iv{a, bb});
+  const double xm = midpt(a, bb);
+  const LevyVals vm = ObjLevy::vals(Iv{xm, xm});
+  put(out + 0, v.u);
+  put(out + 2, v.v);
+  put(out + 4, vm.u);
+  put(out + 6, vm.v);
+}
+
 // warp-aggregated append of (code, lb) to the iteration's candidate list
 __device__ __forceinline__ void chain_append(unsigned long long* cnt, uint32_t* pc, double* pl, bool cond,
                                              uint32_t code, double lb, double* pw = nullptr, double wv = 0.0) {
@@ -414,6 +538,52 @@ __device__ __forceinline__ double chain_children(const Problem& P, const double*
   return best;
 }
 
+// Levy children (R11): a thread per child, the chain sum over the affected
+// terms (levy_child_acc); for a potential candidate the midpoint sum, the
+// first-order test (child_mono_ok, k_prep's table layout) and the width
+template <class F>
+__device__ __forceinline__ double chain_children_levy(const Problem& P, const double* T, double gub0, const ChainOut& o,
+                                                      int rank = -1, int nrank = 0) {
+  if (rank < 0) {
+    rank = blockIdx.x;
+    nrank = gridDim.x;
+  }
+  const int d = P.d, n = P.n;
+  const long nk = 1L << d;
+  const long per = (nk + nrank - 1) / nrank;
+  const long cb = (long)rank * per, ce = min(nk, cb + per);
+  double best = CUDART_INF;
+  for (long c0 = cb; c0 < ce; c0 += blockDim.x) {  // warp-uniform trip count
+    const long ci = c0 + threadIdx.x;
+    const bool valid = ci < ce;
+    const uint32_t code = (uint32_t)(valid ? ci : cb);
+    const double lb = canon_lb(ObjLevy::outer(levy_child_acc(T, code, d, false), n).lo);
+    if (o.all) {
+      if (valid) o.clb[code] = lb;
+      continue;
+    }
+    const bool pot = valid && lb <= gub0;
+    if (!__any_sync(0xffffffffu, pot)) continue;  // rare: a potential candidate in the warp
+    bool keep = pot;
+    double wv = 0.0;
+    if (pot) {
+      o.clb[code] = lb;
+      best = fmin(best, ObjLevy::outer(levy_child_acc(T, code, d, true), n).hi);
+      if (P.mono) keep = child_mono_ok<F>(P, T, code);
+      for (int j = 0; j < d; ++j) {
+        const double* e = T + HDR + (size_t)(2 * j + ((code >> j) & 1u)) * ENT;
+        wv = fmax(wv, __dsub_rn(e[E_HI], e[E_LO]));
+      }
+    }
+    if (o.npot) {  // trace statistics, one atomic per warp
+      const unsigned pm = __ballot_sync(0xffffffffu, pot);
+      if ((threadIdx.x & 31) == 0) atomicAdd(o.npot, (unsigned long long)__popc(pm));
+    }
+    chain_append(o.cnt, o.pc, o.pl, keep, code, lb, o.pw, wv);
+  }
+  return best;
+}
+
 // Meet in the middle (d >= 17): with the split variables cut into a low half
 // (bits 0 .. dl-1 of the child code) and a high half (dl .. d-1), every
 // child's accumulators are ONE combination  RH[h] (+) LO[l]  of two tables
@@ -518,7 +688,7 @@ __device__ __forceinline__ double chain_children_mitm(const Problem& P, const do
 // block's slice -> ent (global, d * m entries of ENT doubles)
 template <class F>
 __device__ __forceinline__ void chain_chunk_entries(const Problem& P, const double* s_lo, const double* s_hi, int i0,
-                                                    int i1, int c, double* ent) {
+                                                    int i1, int c, double* ent, bool with_left = false) {
   const int n = P.n, d = P.d, m = P.m;
   for (int t = threadIdx.x; t < 3 * d * m; t += TPB) {
     const int e = t % (d * m), part = t / (d * m);
@@ -527,7 +697,35 @@ __device__ __forceinline__ void chain_chunk_entries(const Problem& P, const doub
     if (i < i0 || i >= i1) continue;
     const double a = s_lo[i - i0], bb = s_hi[i - i0];
     const double pa = part_point(a, bb, m, p), pb = part_point(a, bb, m, p + 1);
-    piece_entry<F>(P, pa, pb, midpt(pa, pb), i, part, ent + (size_t)e * ENT);
+    if constexpr (F::CHAIN) {  // k_prep's Levy entry layout
+      double* en = ent + (size_t)e * ENT;
+      if (part == 0) {
+        const LevyVals v = ObjLevy::vals(Iv{pa, pb});
+        en[E_LO] = pa;
+        en[E_HI] = pb;
+        put(en + 2, v.u);
+        put(en + 4, v.v);
+        put(en + 6, v.s0);
+        put(en + 8, v.du);
+        put(en + 10, v.sg);
+      } else if (part == 1) {
+        const double xm = midpt(pa, pb);
+        const LevyVals vm = ObjLevy::vals(Iv{xm, xm});
+        put(en + 12, vm.u);
+        put(en + 14, vm.v);
+        put(en + 16, vm.s0);
+      }
+    } else {
+      piece_entry<F>(P, pa, pb, midpt(pa, pb), i, part, ent + (size_t)e * ENT);
+    }
+  }
+  if constexpr (F::CHAIN) {
+    // the chunk's right neighbour (and, with_left, its left one): the owner
+    // of the variable writes its Levy values (k_prep's neighbour slots)
+    const LevyChunk q = levy_chunk(c, d, n);
+    if (threadIdx.x == 0 && q.R >= i0 && q.R < i1) levy_nb_vals(s_lo[q.R - i0], s_hi[q.R - i0], ent + LEVY_TABN_R);
+    if (with_left && threadIdx.x == 0 && q.L >= i0 && q.L < i1)
+      levy_nb_vals(s_lo[q.L - i0], s_hi[q.L - i0], ent + LEVY_TABN_L);
   }
 }
 
@@ -541,13 +739,13 @@ __device__ __forceinline__ void chain_combine(const double* part, int G, Iv* acc
 #pragma unroll
   for (int k = 0; k < 2; ++k) ra[k] = rm[k] = iv(0.0);
 #pragma unroll
-  for (int k = 0; k < F::K; ++k) ra[k] = rm[k] = acc_ident<F>(k);
+  for (int k = 0; k < F::K; ++k) ra[k] = rm[k] = ch_ident<F>(k);
   for (int q = threadIdx.x; q < G; q += TPB) {
     const double* pt = part + (size_t)q * CH_PART;
 #pragma unroll
     for (int k = 0; k < F::K; ++k) {
-      ra[k] = acc_comb<F>(k, ra[k], Iv{__ldcg(pt + 2 * k), __ldcg(pt + 2 * k + 1)});
-      rm[k] = acc_comb<F>(k, rm[k], Iv{__ldcg(pt + 4 + 2 * k), __ldcg(pt + 5 + 2 * k)});
+      ra[k] = ch_comb<F>(k, ra[k], Iv{__ldcg(pt + 2 * k), __ldcg(pt + 2 * k + 1)});
+      rm[k] = ch_comb<F>(k, rm[k], Iv{__ldcg(pt + 4 + 2 * k), __ldcg(pt + 5 + 2 * k)});
     }
     rw = fmax(rw, __ldcg(pt + 8));
   }
@@ -599,6 +797,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
   unsigned long long gub_key = __ldcg(&ctl->gub_key);
   // the selected region R0: materialise this block's slice (Eq. 8-11)
   int c;
+  double hlo = 0.0, hhi = 0.0;  // Levy: x_{i1}, the first variable of the next slice
   {
     const int src = __ldcg(&w.sel_slot[0]);
     const uint32_t code = __ldcg(&w.sel_code[0]);
@@ -620,8 +819,24 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
       s_lo[i - i0] = a;
       s_hi[i - i0] = bb;
     }
+    if constexpr (F::CHAIN) {  // Levy: x_{i1}, the halo (every thread, same bits)
+      if (i1 < n) {
+        hlo = __ldcg(&slo[i1]);
+        hhi = __ldcg(&shi[i1]);
+        if (code != CODE_WHOLE) {
+          const int jj = (i1 - psc + n) % n;
+          if (jj < d) {
+            const int p = digit(code, jj, P.m);
+            const double a2 = part_point(hlo, hhi, P.m, p), b2 = part_point(hlo, hhi, P.m, p + 1);
+            hlo = a2;
+            hhi = b2;
+          }
+        }
+      }
+    }
   }
   __syncthreads();
+  if constexpr (!F::CHAIN)
   if (tcache) {  // the terms of every slice variable (box and midpoint), once
     for (int i = i0 + t; i < i1; i += TPB) {
       const double a = s_lo[i - i0], bb = s_hi[i - i0];
@@ -638,8 +853,11 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     }
   }
   // rest accumulators of R0 (variables outside chunk c) and its chunk entries
-  chain_slice_partial<F>(P, s_lo, s_hi, i0, i1, c, -1, cb.part + ((size_t)1 * G + blk) * CH_PART, s_my);
-  chain_chunk_entries<F>(P, s_lo, s_hi, i0, i1, c, cb.tabn);
+  if constexpr (F::CHAIN)
+    chain_levy_partial<F>(P, s_lo, s_hi, hlo, hhi, i0, i1, c, -1, cb.part + ((size_t)1 * G + blk) * CH_PART, s_my);
+  else
+    chain_slice_partial<F>(P, s_lo, s_hi, i0, i1, c, -1, cb.part + ((size_t)1 * G + blk) * CH_PART, s_my);
+  chain_chunk_entries<F>(P, s_lo, s_hi, i0, i1, c, cb.tabn, true);
   if (blk == 0 && t == 0) {
     for (int q = 0; q < 3; ++q) {
       cb.cnt[q] = 0ull;
@@ -659,8 +877,11 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
       }
       T[H_WREST] = rw;
       T[H_CHUNK] = (double)c;
+      if constexpr (F::CHAIN) levy_desc(c, d, n, T);
     }
     for (int q = t; q < tabw; q += TPB) T[HDR + q] = __ldcg(&cb.tabn[q]);
+    if constexpr (F::CHAIN)
+      if (t < 16) T[H_LEVY_NB + t] = __ldcg(&cb.tabn[LEVY_TABN_L + t]);  // L then R slot
   }
   __syncthreads();
 
@@ -715,7 +936,8 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
       ChainOut o{cb.cnt + sl, cb.pcode + (size_t)sl * PCAP, cb.plb + (size_t)sl * PCAP, w.clb, false,
                  w.tstamp ? cb.exits + 7 : nullptr, cb.pw + (size_t)sl * PCAP};
       if (rank >= 0) {
-        if constexpr (!MITM) best = chain_children<F, 1>(P, T, gub0, o, rank, nrank);
+        if constexpr (F::CHAIN) best = chain_children_levy<F>(P, T, gub0, o, rank, nrank);
+        else if constexpr (!MITM) best = chain_children<F, 1>(P, T, gub0, o, rank, nrank);
         else best = chain_children_mitm<F>(P, T, M, gub0, o, rank, nrank);
       }
     }
@@ -725,9 +947,12 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     // republishes the bits of its previous partial (the full slice sum)
     {
       double* dst = cb.part + ((size_t)(k & 1) * G + blk) * CH_PART;
-      if (meets(i0, i1, c, d, n) || meets(i0, i1, cn, d, n) || (k > 0 && meets(i0, i1, cprev, d, n))) {
+      // (Levy: the slice's last pair reaches x_{i1}, so the halo counts)
+      const int i1x = F::CHAIN ? min(n, i1 + 1) : i1;
+      if (meets(i0, i1x, c, d, n) || meets(i0, i1x, cn, d, n) || (k > 0 && meets(i0, i1x, cprev, d, n))) {
         __syncthreads();  // the slice update of the last phase 2 (uniform: an owner block)
-        if (tcache) chain_slice_partial_cached<F>(P, s_lo, s_hi, s_tc, i0, i1, c, cn, dst, s_my);
+        if constexpr (F::CHAIN) chain_levy_partial<F>(P, s_lo, s_hi, hlo, hhi, i0, i1, c, cn, dst, s_my);
+        else if (tcache) chain_slice_partial_cached<F>(P, s_lo, s_hi, s_tc, i0, i1, c, cn, dst, s_my);
         else chain_slice_partial<F>(P, s_lo, s_hi, i0, i1, c, cn, dst, s_my);
       } else if (t < CH_PART) {
         dst[t] = s_my[t];
@@ -777,19 +1002,21 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
 #pragma unroll
       for (int q = 0; q < 2; ++q) ra[q] = rm[q] = iv(0.0);
 #pragma unroll
-      for (int q = 0; q < F::K; ++q) ra[q] = rm[q] = acc_ident<F>(q);
+      for (int q = 0; q < F::K; ++q) ra[q] = rm[q] = ch_ident<F>(q);
       const double* part = cb.part + (size_t)(k & 1) * G * CH_PART;
       for (int q = t; q < G; q += TPB) {  // G <= TPB: one partial per thread
         const double* pt = part + (size_t)q * CH_PART;
 #pragma unroll
         for (int kk = 0; kk < F::K; ++kk) {
-          ra[kk] = acc_comb<F>(kk, ra[kk], Iv{__ldcg(pt + 2 * kk), __ldcg(pt + 2 * kk + 1)});
-          rm[kk] = acc_comb<F>(kk, rm[kk], Iv{__ldcg(pt + 4 + 2 * kk), __ldcg(pt + 5 + 2 * kk)});
+          ra[kk] = ch_comb<F>(kk, ra[kk], Iv{__ldcg(pt + 2 * kk), __ldcg(pt + 2 * kk + 1)});
+          rm[kk] = ch_comb<F>(kk, rm[kk], Iv{__ldcg(pt + 4 + 2 * kk), __ldcg(pt + 5 + 2 * kk)});
         }
         rw = fmax(rw, __ldcg(pt + 8));
       }
       const double* en = cb.tabn + (size_t)((k + 1) & 1) * DM_MAX * ENT;
       for (int q = t; q < tabw; q += TPB) Tn[HDR + q] = __ldcg(&en[q]);
+      if constexpr (F::CHAIN)
+        if (t < 8) Tn[H_LEVY_NB + 8 + t] = __ldcg(&en[LEVY_TABN_R + t]);  // R slot of chunk c'
     }
     if (gk < gub_key) gub_key = gk;
     const double gub = okey_inv(gub_key);
@@ -851,11 +1078,26 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
       for (int q = 0; q < 2; ++q) A[q] = Am[q] = iv(0.0);
 #pragma unroll
       for (int q = 0; q < F::K; ++q) {
-        A[q] = lane < TPB / 32 ? s_ra[lane][q] : acc_ident<F>(q);
-        Am[q] = lane < TPB / 32 ? s_rm[lane][q] : acc_ident<F>(q);
+        A[q] = lane < TPB / 32 ? s_ra[lane][q] : ch_ident<F>(q);
+        Am[q] = lane < TPB / 32 ? s_rm[lane][q] : ch_ident<F>(q);
       }
       if (lane < TPB / 32) W = s_rw[lane];
-      if (lane < d) {
+      if constexpr (F::CHAIN) {
+        // Levy: the terms of chunk c at the survivor, except the pair that
+        // reaches into chunk c' (x_{c+d-1} x_{c+d}: the R neighbour)
+        const int nt = (int)T[H_LEVY_NT];
+        if (lane < nt) {
+          const int dsc = (int)T[H_LEVY_T + lane];
+          if (!((dsc >> 16) == 1 && (dsc & 255) == d + 1)) {
+            A[0] = A[0] + levy_term(T, dsc, scode, d, false);
+            Am[0] = Am[0] + levy_term(T, dsc, scode, d, true);
+          }
+        }
+        if (lane < d) {
+          const double* e = T + HDR + (size_t)(2 * lane + ((scode >> lane) & 1u)) * ENT;
+          W = fmax(W, __dsub_rn(e[E_HI], e[E_LO]));
+        }
+      } else if (lane < d) {
         const double* e = T + HDR + (size_t)(2 * lane + ((scode >> lane) & 1u)) * ENT;
 #pragma unroll
         for (int q = 0; q < F::K; ++q) {
@@ -881,6 +1123,16 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
         }
         Tn[H_WREST] = hw;
         Tn[H_CHUNK] = (double)cn;
+        if constexpr (F::CHAIN) {
+          // the term list of chunk c' and its left neighbour x_{c+d-1} (the
+          // survivor's last piece); the right one came from its owner
+          levy_desc(cn, d, n, Tn);
+          const double* e = T + HDR + (size_t)(2 * (d - 1) + ((scode >> (d - 1)) & 1u)) * ENT;
+          put(Tn + H_LEVY_NB + 0, get(e + 2));
+          put(Tn + H_LEVY_NB + 2, get(e + 4));
+          put(Tn + H_LEVY_NB + 4, get(e + 12));
+          put(Tn + H_LEVY_NB + 6, get(e + 14));
+        }
       }
       __syncwarp();
     }
@@ -897,6 +1149,14 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
 #pragma unroll
           for (int q = 0; q < 4 * F::K; ++q) tc[q] = e[E_T + q];
         }
+      }
+    }
+    if constexpr (F::CHAIN) {  // the halo x_{i1} (every thread)
+      if (i1 < n && in_chunk(i1, c, d, n)) {
+        const int j = (i1 - c + n) % n;
+        const double* e = T + HDR + (size_t)(2 * j + ((scode >> j) & 1u)) * ENT;
+        hlo = e[E_LO];
+        hhi = e[E_HI];
       }
     }
     cprev = c;
@@ -947,7 +1207,8 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     const long nz = 3 * (((long)P.kids + TILE - 1) / TILE + 1);
     for (long q = (long)blk * TPB + t; q < nz; q += (long)G * TPB) w.desc2[q] = 0;
     ChainOut o{nullptr, nullptr, nullptr, w.clb, true};
-    if constexpr (!MITM) chain_children<F, 1>(P, T, 0.0, o);
+    if constexpr (F::CHAIN) chain_children_levy<F>(P, T, 0.0, o);
+    else if constexpr (!MITM) chain_children<F, 1>(P, T, 0.0, o);
     else chain_children_mitm<F>(P, T, M, 0.0, o);
   }
   grid.sync();

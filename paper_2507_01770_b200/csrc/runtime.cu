@@ -336,7 +336,7 @@ static int chain_cs() {
 }
 static bool chainc_applies(const Problem& P) {
   const char* e = std::getenv("IBNB_CHAIN");
-  if (!e || std::atoi(e) != 2) return false;  // opt-in (IBNB_CHAIN=2)
+  if (!e || std::atoi(e) != 2 || P.fid == 6) return false;  // opt-in (IBNB_CHAIN=2); not the Levy chain sum
   const int cs = chain_cs();
   const int per = (P.n + cs - 1) / cs;
   return chainc_smem(per) <= 185u * 1024u;
@@ -346,7 +346,10 @@ static bool chainc_applies(const Problem& P) {
 static bool chain_applies(const Problem& P) {
   if (const char* e = std::getenv("IBNB_CHAIN"))
     if (std::atoi(e) == 0) return false;
-  return P.m == 2 && P.fid != 6 && P.n >= 2 * P.d && P.d >= 2 && 16L * chain_per(P.n) <= 110L * 1024;
+  // Levy (fid 6, a chain sum, R11): n >= 3d + 2 keeps the chunk's neighbours
+  // out of the next and the previous chunk
+  const long nmin = P.fid == 6 ? 3L * P.d + 2 : 2L * P.d;
+  return P.m == 2 && P.n >= nmin && P.d >= 2 && 16L * chain_per(P.n) <= 110L * 1024;
 }
 
 static size_t layout(const Opts& o, int n, Arena& A, SolveWs& w) {

@@ -723,12 +723,15 @@ def test_solve_parity_at_headline_chunk_sizes(pb, monkeypatch, fid, n, d, eps, s
 @pytest.mark.parametrize("fid,n,d,eps,search", [(7, 24, 8, 1e-6, 32), (1, 30, 8, 1e-6, 32), (5, 27, 8, 1e-6, 32),
                                                 (10, 24, 8, 1e-6, 32), (9, 27, 8, 1e-6, 32), (8, 40, 8, 1e-6, 32),
                                                 (3, 25, 8, 1e-6, 32), (4, 24, 8, 1e-6, 32), (2, 26, 8, 1e-6, 32),
-                                                (7, 24, 8, 1e-6, 0), (1, 24, 8, 1e-4, 0)])
+                                                (7, 24, 8, 1e-6, 0), (1, 24, 8, 1e-4, 0),
+                                                (6, 27, 8, 1e-6, 32), (6, 32, 8, 1e-6, 32), (6, 26, 8, 1e-6, 0)])
 @pytest.mark.parametrize("chain", ["1", "1m", "2"])
 def test_chain_solve_parity(pb, monkeypatch, fid, n, d, eps, search, chain):
     """Whole solves through the deep-dive chain kernels (n >= 2 d: k_chain on
     the whole grid with the children by pairs, 1, or by meet in the middle --
-    the d > 16 path --, 1m; k_chainc on one thread-block cluster, 2), with the R9
+    the d > 16 path --, 1m; k_chainc on one thread-block cluster, 2; Levy, fid
+    6, always takes k_chain's chain-sum path, R11: n % d != 0 makes chunks
+    wrap around x_n -> x_1), with the R9
     search on (one region live per iteration) or off (many potential
     candidates: the static-tile exit path): iterations, evaluations and every
     surviving region bit for bit against the oracle, the enclosure within the
