@@ -96,6 +96,30 @@ __device__ __forceinline__ void levy_desc(int c, int d, int n, double* T) {
   T[H_CHUNK] = (double)c;
 }
 
+// the chunk is interior (x_1 and x_n outside it, both neighbours exist): its
+// term list is L-pair, the d - 1 inner pairs, R-pair (levy_desc's result)
+__device__ __forceinline__ bool levy_interior(int c, int d, int n) { return c >= 1 && c + d <= n - 1; }
+
+// levy_desc by the lanes of a warp (same bits as levy_desc; interior chunks
+// in parallel, the others on lane 0); __syncwarp before other lanes read
+__device__ __forceinline__ void levy_desc_warp(int c, int d, int n, double* T) {
+  const int lane = threadIdx.x & 31;
+  if (levy_interior(c, d, n)) {
+    if (lane <= d) {
+      const int li = lane == 0 ? d : lane - 1, lj = lane == 0 ? 0 : (lane == d ? d + 1 : lane);
+      T[H_LEVY_T + lane] = (double)(1 * 65536 + li * 256 + lj);
+    }
+    if (lane == 0) {
+      T[H_LEVY_NT] = (double)(d + 1);
+      T[H_LEVY_LR] = (double)(c - 1);
+      T[H_LEVY_LR + 1] = (double)(c + d);
+      T[H_CHUNK] = (double)c;
+    }
+  } else if (lane == 0) {
+    levy_desc(c, d, n, T);
+  }
+}
+
 // value of descriptor dsc for the child `code` (mid: at the midpoint values)
 __device__ __forceinline__ Iv levy_term(const double* T, int dsc, uint32_t code, int d, bool mid) {
   const int kind = dsc >> 16, li = (dsc >> 8) & 255, lj = dsc & 255;
@@ -447,10 +471,13 @@ __device__ __forceinline__ void chain_leaf(const Problem& P, const double* T, do
     for (int q = 0; q < F::K; ++q)
       Bm[0][q] = acc_comb<F>(q, acc_comb<F>(q, Bm[0][q], Bm[1][q]), acc_comb<F>(q, Bm[2][q], Bm[3][q]));
     best = fmin(best, outer_hi<F>(Bm[0], P.n));
-    // the first-order test does not depend on GUB: taken here, so the list
-    // holds only children it keeps
-    if (P.mono) keep = chain_fo_ok<F>(P, T, code);
   }
+  // the iteration's GUB will be <= every midpoint value of this warp: a
+  // child above the warp's smallest cannot be a candidate (never lists one
+  // that phase 2 would keep); then the first-order test, which does not
+  // depend on GUB, so the list holds only children it keeps
+  keep = pot && lb <= warp_min(best);
+  if (keep && P.mono) keep = chain_fo_ok<F>(P, T, code);
   if (o.npot) {  // trace statistics, one atomic per warp
     const unsigned am = __activemask(), pm = __ballot_sync(am, pot);
     if (pm && (threadIdx.x & 31) == __ffs(am) - 1) atomicAdd(o.npot, (unsigned long long)__popc(pm));
@@ -553,23 +580,59 @@ __device__ __forceinline__ double chain_children_levy(const Problem& P, const do
   const long per = (nk + nrank - 1) / nrank;
   const long cb = (long)rank * per, ce = min(nk, cb + per);
   double best = CUDART_INF;
+  // interior chunk: the d + 1 terms of every child tabulated per warp (the
+  // same products in the same order as levy_child_acc: same bits)
+  __shared__ Iv s_pair[TPB / 32][D_MAX + 1][4];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool interior = levy_interior((int)T[H_CHUNK], d, n);
+  if (interior) {
+    for (int q = lane; q < 4 * (d + 1); q += 32) {
+      const int tt = q >> 2, b = q & 3;
+      Iv uu, vv;
+      if (tt == 0) {  // x_{c-1} x_c: combo b = b_0 (b < 2)
+        uu = get(T + H_LEVY_NB + 0);
+        vv = get(T + HDR + (size_t)(b & 1) * ENT + 4);
+      } else if (tt == d) {  // x_{c+d-1} x_{c+d}: combo b = b_{d-1}
+        uu = get(T + HDR + (size_t)(2 * (d - 1) + (b & 1)) * ENT + 2);
+        vv = get(T + H_LEVY_NB + 8 + 2);
+      } else {  // x_{c+tt-1} x_{c+tt}: combo b = b_{tt-1} + 2 b_tt
+        uu = get(T + HDR + (size_t)(2 * (tt - 1) + (b & 1)) * ENT + 2);
+        vv = get(T + HDR + (size_t)(2 * tt + (b >> 1)) * ENT + 4);
+      }
+      s_pair[w][tt][b] = mulpos(uu, vv);
+    }
+    __syncwarp();
+  }
   for (long c0 = cb; c0 < ce; c0 += blockDim.x) {  // warp-uniform trip count
     const long ci = c0 + threadIdx.x;
     const bool valid = ci < ce;
     const uint32_t code = (uint32_t)(valid ? ci : cb);
-    const double lb = canon_lb(ObjLevy::outer(levy_child_acc(T, code, d, false), n).lo);
+    Iv acc;
+    if (interior) {
+      acc = get(T + H_REST);
+      acc = acc + s_pair[w][0][code & 1u];
+      for (int tt = 1; tt < d; ++tt) acc = acc + s_pair[w][tt][((code >> (tt - 1)) & 1u) | (((code >> tt) & 1u) << 1)];
+      acc = acc + s_pair[w][d][(code >> (d - 1)) & 1u];
+    } else {
+      acc = levy_child_acc(T, code, d, false);
+    }
+    const double lb = canon_lb(ObjLevy::outer(acc, n).lo);
     if (o.all) {
       if (valid) o.clb[code] = lb;
       continue;
     }
     const bool pot = valid && lb <= gub0;
     if (!__any_sync(0xffffffffu, pot)) continue;  // rare: a potential candidate in the warp
-    bool keep = pot;
     double wv = 0.0;
     if (pot) {
       o.clb[code] = lb;
       best = fmin(best, ObjLevy::outer(levy_child_acc(T, code, d, true), n).hi);
-      if (P.mono) keep = child_mono_ok<F>(P, T, code);
+    }
+    // as chain_leaf: below the warp's smallest midpoint value, then the
+    // first-order test
+    bool keep = pot && lb <= warp_min(best);
+    if (keep && P.mono) keep = child_mono_ok<F>(P, T, code);
+    if (keep) {
       for (int j = 0; j < d; ++j) {
         const double* e = T + HDR + (size_t)(2 * j + ((code >> j) & 1u)) * ENT;
         wv = fmax(wv, __dsub_rn(e[E_HI], e[E_LO]));
@@ -1020,6 +1083,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     }
     if (gk < gub_key) gub_key = gk;
     const double gub = okey_inv(gub_key);
+    if (ts) ts[25] += np;  // trace: potential candidates kept (first-order test passed) per iteration
     const bool fits = np <= (unsigned long long)PCAP;
     const int npi = fits ? (int)np : 0;
     // warp level of the (fixed-order) reduction of the slice partials
@@ -1126,7 +1190,6 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
         if constexpr (F::CHAIN) {
           // the term list of chunk c' and its left neighbour x_{c+d-1} (the
           // survivor's last piece); the right one came from its owner
-          levy_desc(cn, d, n, Tn);
           const double* e = T + HDR + (size_t)(2 * (d - 1) + ((scode >> (d - 1)) & 1u)) * ENT;
           put(Tn + H_LEVY_NB + 0, get(e + 2));
           put(Tn + H_LEVY_NB + 2, get(e + 4));
@@ -1134,6 +1197,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
           put(Tn + H_LEVY_NB + 6, get(e + 14));
         }
       }
+      if constexpr (F::CHAIN) levy_desc_warp(cn, d, n, Tn);
       __syncwarp();
     }
     // slice update: chunk c variables take the survivor's pieces (read by

@@ -929,7 +929,8 @@ static int solve_impl(int fid, int n, const double* l_dev, const double* u_dev, 
               tsh[28] / 1e3 / tsh[31], tsh[29] / 1e3 / tsh[31], tsh[30] / 1e3 / tsh[31]);
     fprintf(stderr, "\n[ibnb] chain launches %ld, exits:", chain_launches);
     for (int k = 0; k < 7; ++k) fprintf(stderr, " %s=%llu", why[k], ex[k]);
-    if (tsh[31]) fprintf(stderr, " potential_children_per_iter=%.2f", (double)ex[7] / tsh[31]);
+    if (tsh[31]) fprintf(stderr, " potential_children_per_iter=%.2f listed_per_iter=%.2f", (double)ex[7] / tsh[31],
+                         (double)tsh[25] / tsh[31]);
     if (tsh[17] + tsh[19])
       fprintf(stderr, "\n[ibnb] chain phase 1 per block (us): slice/entry blocks %.2f (%llu), children blocks %.2f (%llu)",
               tsh[16] / 1e3 / std::max(1ull, tsh[17]), tsh[17], tsh[18] / 1e3 / std::max(1ull, tsh[19]), tsh[19]);
