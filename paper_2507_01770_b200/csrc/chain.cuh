@@ -476,7 +476,8 @@ __device__ __forceinline__ void chain_leaf(const Problem& P, const double* T, do
   // child above the warp's smallest cannot be a candidate (never lists one
   // that phase 2 would keep); then the first-order test, which does not
   // depend on GUB, so the list holds only children it keeps
-  keep = pot && lb <= warp_min(best);
+  const double wmin = warp_min(best);  // every lane (a full-warp shuffle: not inside the && below)
+  keep = pot && lb <= wmin;
   if (keep && P.mono) keep = chain_fo_ok<F>(P, T, code);
   if (o.npot) {  // trace statistics, one atomic per warp
     const unsigned am = __activemask(), pm = __ballot_sync(am, pot);
@@ -630,7 +631,8 @@ __device__ __forceinline__ double chain_children_levy(const Problem& P, const do
     }
     // as chain_leaf: below the warp's smallest midpoint value, then the
     // first-order test
-    bool keep = pot && lb <= warp_min(best);
+    const double wmin = warp_min(best);  // every lane (a full-warp shuffle)
+    bool keep = pot && lb <= wmin;
     if (keep && P.mono) keep = child_mono_ok<F>(P, T, code);
     if (keep) {
       for (int j = 0; j < d; ++j) {
