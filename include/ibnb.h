@@ -263,7 +263,9 @@ size_t ib_select_workspace_size(int64_t n);
 /* Inter-process handle of a device allocation (cudaIpcGetMemHandle): 64
  * bytes into handle.  ib_ipc_open maps a handle of another process (same or
  * peer GPU, NVLink) and returns the device address; ib_ipc_close unmaps it.
- * For ib_options.gub_shared across ranks (bench.py --mode partition). */
+ * For ib_options.gub_shared across processes (tested with two processes on
+ * one GPU; bench.py --mode partition exchanges the incumbent with NCCL per
+ * chunk instead).  Return 0 or a CUDA error code. */
 int ib_ipc_get_handle(const void* dptr, void* handle);
 int ib_ipc_open(const void* handle, void** dptr);
 int ib_ipc_close(void* dptr);

@@ -471,14 +471,11 @@ __device__ __forceinline__ void chain_leaf(const Problem& P, const double* T, do
     for (int q = 0; q < F::K; ++q)
       Bm[0][q] = acc_comb<F>(q, acc_comb<F>(q, Bm[0][q], Bm[1][q]), acc_comb<F>(q, Bm[2][q], Bm[3][q]));
     best = fmin(best, outer_hi<F>(Bm[0], P.n));
+    // the first-order test does not depend on GUB: taken here, so the list
+    // holds only children it keeps (filtering first by the warp's smallest
+    // midpoint value was measured slower: a 5-level shuffle per call)
+    if (P.mono) keep = chain_fo_ok<F>(P, T, code);
   }
-  // the iteration's GUB will be <= every midpoint value of this warp: a
-  // child above the warp's smallest cannot be a candidate (never lists one
-  // that phase 2 would keep); then the first-order test, which does not
-  // depend on GUB, so the list holds only children it keeps
-  const double wmin = warp_min(best);  // every lane (a full-warp shuffle: not inside the && below)
-  keep = pot && lb <= wmin;
-  if (keep && P.mono) keep = chain_fo_ok<F>(P, T, code);
   if (o.npot) {  // trace statistics, one atomic per warp
     const unsigned am = __activemask(), pm = __ballot_sync(am, pot);
     if (pm && (threadIdx.x & 31) == __ffs(am) - 1) atomicAdd(o.npot, (unsigned long long)__popc(pm));
@@ -625,15 +622,12 @@ __device__ __forceinline__ double chain_children_levy(const Problem& P, const do
     const bool pot = valid && lb <= gub0;
     if (!__any_sync(0xffffffffu, pot)) continue;  // rare: a potential candidate in the warp
     double wv = 0.0;
+    bool keep = pot;
     if (pot) {
       o.clb[code] = lb;
       best = fmin(best, ObjLevy::outer(levy_child_acc(T, code, d, true), n).hi);
+      if (P.mono) keep = child_mono_ok<F>(P, T, code);
     }
-    // as chain_leaf: below the warp's smallest midpoint value, then the
-    // first-order test
-    const double wmin = warp_min(best);  // every lane (a full-warp shuffle)
-    bool keep = pot && lb <= wmin;
-    if (keep && P.mono) keep = child_mono_ok<F>(P, T, code);
     if (keep) {
       for (int j = 0; j < d; ++j) {
         const double* e = T + HDR + (size_t)(2 * j + ((code >> j) & 1u)) * ENT;
