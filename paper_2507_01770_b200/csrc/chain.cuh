@@ -652,12 +652,24 @@ __device__ __forceinline__ double chain_children_levy(const Problem& P, const do
 // association: rigorous, equal to the oracle's left-to-right evaluation up
 // to rounding (tests/tol.py).  A block builds LO in full and RH for the h of
 // its own children only.
-constexpr int MITM_BITS = D_MAX / 2;        // bits of one half (d <= D_MAX)
-constexpr int MITM_MAX = 1 << MITM_BITS;    // entries of one half
+constexpr int MITM_BITS = 16;               // tree slots of one half (d - dl <= 16)
+constexpr int MITM_MAX = 1024;              // entries of one table
 struct MitmTabs {
   Iv lo[2][MITM_MAX];  // [accumulator][l]: consecutive l in consecutive lanes
-  Iv rh[2][MITM_MAX];
+  Iv rh[2][MITM_MAX];  // [accumulator][h - h0]: this block's high halves only
 };
+
+// split of the d bits: the low half is built by every block in full (2^dl
+// entries), the high half only for the block's own children (~per / 2^dl):
+// 2^dl ~ sqrt(per) minimises the table work per iteration (d = 18 on 145
+// blocks: 64 + 29 entries instead of 512 + 4 with dl = d / 2)
+__device__ __forceinline__ int mitm_dl(int d, long per) {
+  int dl = 0;
+  while ((1L << (2 * (dl + 1))) <= per) ++dl;
+  dl = max(dl, d - MITM_BITS);
+  dl = min(dl, min(10, d - 1));
+  return max(dl, 1);
+}
 
 // tree (+) of the terms of split variables j0 .. j0 + nb - 1, chosen by the
 // bits of `bits` (identity-padded balanced tree over MITM_BITS slots)
@@ -695,9 +707,12 @@ __device__ __forceinline__ double chain_children_mitm(const Problem& P, const do
     rank = blockIdx.x;
     nrank = gridDim.x;
   }
-  const int d = P.d, dl = d / 2, dh = d - dl;
+  const int d = P.d;
   const long nk = 1L << d;
   const long per = (nk + nrank - 1) / nrank;
+  // the split depends on d and the grid only (the exit path's recomputation
+  // over all blocks takes the same association)
+  const int dl = mitm_dl(d, (nk + gridDim.x - 1) / gridDim.x), dh = d - dl;
   const long cb = (long)rank * per, ce = min(nk, cb + per);
   const uint32_t lmask = (1u << dl) - 1u;
   const int h0 = (int)(cb >> dl), h1 = ce > cb ? (int)((ce - 1) >> dl) : h0 - 1;
@@ -713,7 +728,7 @@ __device__ __forceinline__ double chain_children_mitm(const Problem& P, const do
       const int h = h0 + (q - nlo);
       mitm_tree<F>(T, dl, dh, (uint32_t)h, A);
 #pragma unroll
-      for (int k = 0; k < F::K; ++k) M.rh[k][h] = acc_comb<F>(k, get(T + H_REST + 2 * k), A[k]);
+      for (int k = 0; k < F::K; ++k) M.rh[k][h - h0] = acc_comb<F>(k, get(T + H_REST + 2 * k), A[k]);
     }
   }
   __syncthreads();
@@ -729,7 +744,7 @@ __device__ __forceinline__ double chain_children_mitm(const Problem& P, const do
       const uint32_t h = code >> dl, l = code & lmask;
       Iv B[2];
 #pragma unroll
-      for (int k = 0; k < F::K; ++k) B[k] = acc_comb<F>(k, M.rh[k][h], M.lo[k][l]);
+      for (int k = 0; k < F::K; ++k) B[k] = acc_comb<F>(k, M.rh[k][h - h0], M.lo[k][l]);
       lbs[u] = chain_lb<F>(P, B);
       any |= ci < ce && lbs[u] <= gub0;
     }
