@@ -553,12 +553,25 @@ __device__ __forceinline__ double chain_children(const Problem& P, const double*
     for (int q = 0; q < F::K; ++q) A[q] = acc_comb<F>(q, get(T + H_REST + 2 * q), tt[0][q]);
     double lbs[1 << H];
     ChainTree<F, H>::run(P, T, A, lbs, 0);
-    bool any = o.all;
+    if (o.all) {
 #pragma unroll
-    for (int q = 0; q < (1 << H); ++q) any |= valid && lbs[q] <= gub0;
-    if (__any_sync(0xffffffffu, any))  // rare: a potential candidate in the warp
+      for (int q = 0; q < (1 << H); ++q)
+        if (valid) o.clb[code0 | (uint32_t)q] = lbs[q];
+      continue;
+    }
+    // potential candidates of this thread; the warp visits them one per
+    // lane and round (usually one round) instead of every child slot
+    uint32_t pm = 0;
 #pragma unroll
-      for (int q = 0; q < (1 << H); ++q) chain_leaf<F>(P, T, gub0, o, code0 | (uint32_t)q, lbs[q], valid, best);
+    for (int q = 0; q < (1 << H); ++q) pm |= (valid && lbs[q] <= gub0) ? 1u << q : 0u;
+    while (__any_sync(0xffffffffu, pm != 0)) {  // rare: a potential candidate in the warp
+      const int q = pm ? __ffs(pm) - 1 : 0;
+      double lq = lbs[0];
+#pragma unroll
+      for (int z = 1; z < (1 << H); ++z) lq = q == z ? lbs[z] : lq;
+      chain_leaf<F>(P, T, gub0, o, code0 | (uint32_t)q, lq, pm != 0, best);
+      pm &= pm - 1;
+    }
   }
   return best;
 }
@@ -748,12 +761,31 @@ __device__ __forceinline__ double chain_children_mitm(const Problem& P, const do
       lbs[u] = chain_lb<F>(P, B);
       any |= ci < ce && lbs[u] <= gub0;
     }
-    if (__any_sync(0xffffffffu, any))  // rare: a potential candidate in the warp
+    if (o.all) {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const long ci = c0 + threadIdx.x + (long)u * blockDim.x;
-        chain_leaf<F>(P, T, gub0, o, (uint32_t)(ci < ce ? ci : cb), lbs[u], ci < ce, best);
+        if (ci < ce) o.clb[ci] = lbs[u];
       }
+      continue;
+    }
+    // potential candidates of this thread, visited one per lane and round
+    uint32_t pm = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long ci = c0 + threadIdx.x + (long)u * blockDim.x;
+      pm |= (ci < ce && lbs[u] <= gub0) ? 1u << u : 0u;
+    }
+    (void)any;
+    while (__any_sync(0xffffffffu, pm != 0)) {  // rare: a potential candidate in the warp
+      const int u = pm ? __ffs(pm) - 1 : 0;
+      double lu = lbs[0];
+#pragma unroll
+      for (int z = 1; z < U; ++z) lu = u == z ? lbs[z] : lu;
+      const long ci = c0 + threadIdx.x + (long)u * blockDim.x;
+      chain_leaf<F>(P, T, gub0, o, (uint32_t)(pm ? ci : cb), lu, pm != 0, best);
+      pm &= pm - 1;
+    }
   }
   return best;
 }
