@@ -311,6 +311,68 @@ __device__ __forceinline__ void chain_slice_partial_cached(const Problem& P, con
   }
 }
 
+// the cached partial on warps 0..3 only (named barrier 1), so that warps
+// 4..7 of an owner block tabulate the next chunk meanwhile (another thread
+// mapping than chain_slice_partial_cached: another association, R10)
+template <class F>
+__device__ __forceinline__ void chain_slice_partial_cached128(const Problem& P, const double* s_lo,
+                                                              const double* s_hi, const double* s_tc, int i0, int i1,
+                                                              int c1, int c2, double* part, double* keep) {
+  const int n = P.n, d = P.d;
+  constexpr int TC = 4 * F::K;
+  Iv acc[2], accm[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) acc[k] = accm[k] = iv(0.0);
+#pragma unroll
+  for (int k = 0; k < F::K; ++k) acc[k] = accm[k] = acc_ident<F>(k);
+  double wmax = 0.0;
+  constexpr int HB = 64;
+  const int hv = threadIdx.x % HB, half = threadIdx.x / HB;
+  for (int i = i0 + hv; i < i1; i += HB) {
+    if (in_chunk(i, c1, d, n) || (c2 >= 0 && in_chunk(i, c2, d, n))) continue;
+    const double* tc = s_tc + (size_t)(i - i0) * TC;
+    if (half == 0) {
+      wmax = fmax(wmax, __dsub_rn(s_hi[i - i0], s_lo[i - i0]));
+#pragma unroll
+      for (int k = 0; k < F::K; ++k) acc[k] = acc_comb<F>(k, acc[k], get(tc + 2 * k));
+    } else {
+#pragma unroll
+      for (int k = 0; k < F::K; ++k) accm[k] = acc_comb<F>(k, accm[k], get(tc + 2 * F::K + 2 * k));
+    }
+  }
+  warp_reduce_prep<F>(acc, accm, wmax);
+  __shared__ Iv s_a[4][2], s_b[4][2];
+  __shared__ double s_w[4];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < F::K; ++k) {
+      s_a[wid][k] = acc[k];
+      s_b[wid][k] = accm[k];
+    }
+    s_w[wid] = wmax;
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 4; ++w) {
+#pragma unroll
+      for (int k = 0; k < F::K; ++k) {
+        acc[k] = acc_comb<F>(k, acc[k], s_a[w][k]);
+        accm[k] = acc_comb<F>(k, accm[k], s_b[w][k]);
+      }
+      wmax = fmax(wmax, s_w[w]);
+    }
+    for (int k = 0; k < 2; ++k) {
+      put(part + 2 * k, acc[k]);
+      put(part + 4 + 2 * k, accm[k]);
+      put(keep + 2 * k, acc[k]);
+      put(keep + 4 + 2 * k, accm[k]);
+    }
+    part[8] = keep[8] = wmax;
+    part[9] = keep[9] = 0.0;
+  }
+}
+
 // first-order test of child `code` of the bisection table T (one thread):
 // separable objectives read the per-entry flags, the others take
 // child_mono_ok (bit-identical to the warp version of the other paths)
@@ -587,9 +649,9 @@ __device__ __forceinline__ double chain_children_levy(const Problem& P, const do
     nrank = gridDim.x;
   }
   const int d = P.d, n = P.n;
-  const long nk = 1L << d;
-  const long per = (nk + nrank - 1) / nrank;
-  const long cb = (long)rank * per, ce = min(nk, cb + per);
+  const int nk = 1 << d;  // d <= 20: 32-bit division
+  const int per = (nk + nrank - 1) / nrank;
+  const long cb = (long)rank * per, ce = min((long)nk, cb + per);
   double best = CUDART_INF;
   // interior chunk: the d + 1 terms of every child tabulated per warp (the
   // same products in the same order as levy_child_acc: same bits)
@@ -676,9 +738,8 @@ struct MitmTabs {
 // entries), the high half only for the block's own children (~per / 2^dl):
 // 2^dl ~ sqrt(per) minimises the table work per iteration (d = 18 on 145
 // blocks: 64 + 29 entries instead of 512 + 4 with dl = d / 2)
-__device__ __forceinline__ int mitm_dl(int d, long per) {
-  int dl = 0;
-  while ((1L << (2 * (dl + 1))) <= per) ++dl;
+__device__ __forceinline__ int mitm_dl(int d, int per) {
+  int dl = (31 - __clz(max(per, 1))) / 2;  // largest dl with 4^dl <= per
   dl = max(dl, d - MITM_BITS);
   dl = min(dl, min(10, d - 1));
   return max(dl, 1);
@@ -721,12 +782,12 @@ __device__ __forceinline__ double chain_children_mitm(const Problem& P, const do
     nrank = gridDim.x;
   }
   const int d = P.d;
-  const long nk = 1L << d;
-  const long per = (nk + nrank - 1) / nrank;
+  const int nk = 1 << d;  // d <= 20: 32-bit arithmetic (a 64-bit division per thread was 4 % of the samples)
+  const int per = (nk + nrank - 1) / nrank;
   // the split depends on d and the grid only (the exit path's recomputation
   // over all blocks takes the same association)
-  const int dl = mitm_dl(d, (nk + gridDim.x - 1) / gridDim.x), dh = d - dl;
-  const long cb = (long)rank * per, ce = min(nk, cb + per);
+  const int dl = mitm_dl(d, (nk + (int)gridDim.x - 1) / (int)gridDim.x), dh = d - dl;
+  const long cb = (long)rank * per, ce = min((long)nk, cb + per);
   const uint32_t lmask = (1u << dl) - 1u;
   const int h0 = (int)(cb >> dl), h1 = ce > cb ? (int)((ce - 1) >> dl) : h0 - 1;
   const int nlo = 1 << dl, nrh = h1 - h0 + 1;
@@ -794,9 +855,11 @@ __device__ __forceinline__ double chain_children_mitm(const Problem& P, const do
 // block's slice -> ent (global, d * m entries of ENT doubles)
 template <class F>
 __device__ __forceinline__ void chain_chunk_entries(const Problem& P, const double* s_lo, const double* s_hi, int i0,
-                                                    int i1, int c, double* ent, bool with_left = false) {
+                                                    int i1, int c, double* ent, bool with_left = false,
+                                                    int tid = -1, int nth = TPB) {
   const int n = P.n, d = P.d, m = P.m;
-  for (int t = threadIdx.x; t < 3 * d * m; t += TPB) {
+  if (tid < 0) tid = threadIdx.x;
+  for (int t = tid; t < 3 * d * m; t += nth) {
     const int e = t % (d * m), part = t / (d * m);
     const int j = e / m, p = e % m;
     const int i = (c + j) % n;
@@ -829,8 +892,8 @@ __device__ __forceinline__ void chain_chunk_entries(const Problem& P, const doub
     // the chunk's right neighbour (and, with_left, its left one): the owner
     // of the variable writes its Levy values (k_prep's neighbour slots)
     const LevyChunk q = levy_chunk(c, d, n);
-    if (threadIdx.x == 0 && q.R >= i0 && q.R < i1) levy_nb_vals(s_lo[q.R - i0], s_hi[q.R - i0], ent + LEVY_TABN_R);
-    if (with_left && threadIdx.x == 0 && q.L >= i0 && q.L < i1)
+    if (tid == 0 && q.R >= i0 && q.R < i1) levy_nb_vals(s_lo[q.R - i0], s_hi[q.R - i0], ent + LEVY_TABN_R);
+    if (with_left && tid == 0 && q.L >= i0 && q.L < i1)
       levy_nb_vals(s_lo[q.L - i0], s_hi[q.L - i0], ent + LEVY_TABN_L);
   }
 }
@@ -1051,21 +1114,32 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     // (b) S_excl of R over this block's slice, outside chunks c and c'; a
     // slice that meets none of them (nor the chunk the last iteration changed)
     // republishes the bits of its previous partial (the full slice sum)
+    bool ent_done = false;
     {
       double* dst = cb.part + ((size_t)(k & 1) * G + blk) * CH_PART;
       // (Levy: the slice's last pair reaches x_{i1}, so the halo counts)
       const int i1x = F::CHAIN ? min(n, i1 + 1) : i1;
       if (meets(i0, i1x, c, d, n) || meets(i0, i1x, cn, d, n) || (k > 0 && meets(i0, i1x, cprev, d, n))) {
         __syncthreads();  // the slice update of the last phase 2 (uniform: an owner block)
-        if constexpr (F::CHAIN) chain_levy_partial<F>(P, s_lo, s_hi, hlo, hhi, i0, i1, c, cn, dst, s_my);
-        else if (tcache) chain_slice_partial_cached<F>(P, s_lo, s_hi, s_tc, i0, i1, c, cn, dst, s_my);
-        else chain_slice_partial<F>(P, s_lo, s_hi, i0, i1, c, cn, dst, s_my);
+        if constexpr (F::CHAIN) {
+          chain_levy_partial<F>(P, s_lo, s_hi, hlo, hhi, i0, i1, c, cn, dst, s_my);
+        } else if (tcache) {
+          // warps 0..3 the partial, warps 4..7 the entries of chunk c'
+          if (t < 128)
+            chain_slice_partial_cached128<F>(P, s_lo, s_hi, s_tc, i0, i1, c, cn, dst, s_my);
+          else
+            chain_chunk_entries<F>(P, s_lo, s_hi, i0, i1, cn, cb.tabn + (size_t)((k + 1) & 1) * DM_MAX * ENT, false,
+                                   t - 128, TPB - 128);
+          ent_done = true;
+        } else {
+          chain_slice_partial<F>(P, s_lo, s_hi, i0, i1, c, cn, dst, s_my);
+        }
       } else if (t < CH_PART) {
         dst[t] = s_my[t];
       }
     }
     // (c) entries of chunk c' (unchanged in every child of R)
-    chain_chunk_entries<F>(P, s_lo, s_hi, i0, i1, cn, cb.tabn + (size_t)((k + 1) & 1) * DM_MAX * ENT);
+    if (!ent_done) chain_chunk_entries<F>(P, s_lo, s_hi, i0, i1, cn, cb.tabn + (size_t)((k + 1) & 1) * DM_MAX * ENT);
     // (d) this block's midpoint minimum, ONE atomic per block (one word takes
     // every block's: per-warp atomics queue 8x as many at its L2 slice, and
     // the phase-2 load of the word waits behind them); block 0 also brings in
@@ -1097,7 +1171,9 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     const unsigned long long gk = __ldcg(&cb.gacc[sl]);
     uint32_t my_pc = 0;
     double my_pl = CUDART_INF, my_pw = 0.0;
-    if (t < PCAP) {
+    // the first 32 list slots with the other loads (one child is listed per
+    // iteration in the deep dive); the rest only when the count says so
+    if (t < 32) {
       my_pc = __ldcg(&cb.pcode[(size_t)sl * PCAP + t]);
       my_pl = __ldcg(&cb.plb[(size_t)sl * PCAP + t]);
       my_pw = __ldcg(&cb.pw[(size_t)sl * PCAP + t]);
@@ -1129,6 +1205,11 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     if (ts) ts[25] += np;  // trace: potential candidates kept (first-order test passed) per iteration
     const bool fits = np <= (unsigned long long)PCAP;
     const int npi = fits ? (int)np : 0;
+    if (npi > 32 && t >= 32 && t < npi) {  // uniform per block (np is the same everywhere)
+      my_pc = __ldcg(&cb.pcode[(size_t)sl * PCAP + t]);
+      my_pl = __ldcg(&cb.plb[(size_t)sl * PCAP + t]);
+      my_pw = __ldcg(&cb.pw[(size_t)sl * PCAP + t]);
+    }
     // warp level of the (fixed-order) reduction of the slice partials
     warp_reduce_prep<F>(ra, rm, rw);
     if (lane == 0) {
