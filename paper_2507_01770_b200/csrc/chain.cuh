@@ -67,6 +67,24 @@ __device__ __forceinline__ Iv ch_comb(int k, Iv a, Iv b) {
   else return acc_comb<F>(k, a, b);
 }
 
+// doubles of a table entry that any reader of a chain table uses: bounds,
+// box and midpoint terms, derivative ingredients, the separable flag (Levy:
+// k_prep's layout up to s0 of the midpoint) -- phase 2 copies only these
+// (every block reads the entries of the next chunk: L2 broadcast traffic)
+template <class F>
+__device__ __forceinline__ constexpr int ent_used() {
+  if constexpr (F::CHAIN) return 18;
+  else return E_T + 4 * F::K + 2 * F::KG + 1;
+}
+template <class F>
+__device__ __forceinline__ void copy_entries(double* dst, const double* src, int dm) {
+  constexpr int EU = ent_used<F>();
+  for (int q = threadIdx.x; q < dm * EU; q += TPB) {
+    const int j = q / EU, f = q - j * EU;
+    dst[(size_t)j * ENT + f] = __ldcg(&src[(size_t)j * ENT + f]);
+  }
+}
+
 // ------------------------------------------------------------------ Levy
 // Levy (A11-A12, reading R11) in the chain: term i couples x_i and x_{i+1},
 // so the chunk's table lists the affected chain terms (levy_desc, as k_prep
@@ -944,7 +962,6 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
   Ctl* ctl = w.ctl;
   const int n = P.n, d = P.d, t = threadIdx.x, blk = blockIdx.x, G = gridDim.x;
   const int lane = t & 31;
-  const int tabw = d * P.m * ENT;  // doubles of the entries
   MitmTabs& M = *reinterpret_cast<MitmTabs*>(s_dyn);  // d >= 17: meet-in-the-middle tables
   double* s_lo = s_dyn + sizeof(MitmTabs) / sizeof(double);
   double* s_hi = s_lo + cb.per;
@@ -1048,7 +1065,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
       T[H_CHUNK] = (double)c;
       if constexpr (F::CHAIN) levy_desc(c, d, n, T);
     }
-    for (int q = t; q < tabw; q += TPB) T[HDR + q] = __ldcg(&cb.tabn[q]);
+    copy_entries<F>(T + HDR, cb.tabn, d * P.m);
     if constexpr (F::CHAIN)
       if (t < 16) T[H_LEVY_NB + t] = __ldcg(&cb.tabn[LEVY_TABN_L + t]);  // L then R slot
   }
@@ -1196,7 +1213,7 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
         rw = fmax(rw, __ldcg(pt + 8));
       }
       const double* en = cb.tabn + (size_t)((k + 1) & 1) * DM_MAX * ENT;
-      for (int q = t; q < tabw; q += TPB) Tn[HDR + q] = __ldcg(&en[q]);
+      copy_entries<F>(Tn + HDR, en, d * P.m);
       if constexpr (F::CHAIN)
         if (t < 8) Tn[H_LEVY_NB + 8 + t] = __ldcg(&en[LEVY_TABN_R + t]);  // R slot of chunk c'
     }
