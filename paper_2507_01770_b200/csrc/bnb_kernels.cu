@@ -3131,8 +3131,9 @@ struct ObjImpl {
     // the slice (2 doubles per variable) and, when it fits, its term cache
     // (4K doubles per variable; not for the Levy chain sum)
     ChainBufs cb = cb0;
-    const size_t tcb = sizeof(double) * 4 * F::K * (size_t)cb.per;
-    cb.tcache = !F::CHAIN && sizeof(double) * 2 * (size_t)cb.per + tcb <= 110u * 1024u ? 1 : 0;
+    // (Levy: u, v, s0 of the box and of the midpoint, 12 doubles per variable)
+    const size_t tcb = sizeof(double) * (F::CHAIN ? 12 : 4 * F::K) * (size_t)cb.per;
+    cb.tcache = sizeof(double) * 2 * (size_t)cb.per + tcb <= 110u * 1024u ? 1 : 0;
     if (const char* e = std::getenv("IBNB_TCACHE"))
       if (std::atoi(e) == 0) cb.tcache = 0;
     const size_t smem = sizeof(MitmTabs) + sizeof(double) * 2 * (size_t)cb.per + (cb.tcache ? tcb : 0);

@@ -209,6 +209,67 @@ __device__ __forceinline__ void chain_levy_partial(const Problem& P, const doubl
   }
 }
 
+// chain_levy_partial from the Levy value cache s_lc (u, v, s0 of the box,
+// then of the midpoint, 12 doubles per slice variable: ObjLevy::vals of the
+// current values, written when a variable changes) and the halo's v (box,
+// midpoint) -- on warps 0..3 (named barrier 1) while warps 4..7 tabulate
+// the next chunk; the same terms as chain_levy_partial (another thread
+// mapping: another association, R10)
+template <class F>
+__device__ __forceinline__ void chain_levy_partial_cached128(const Problem& P, const double* s_lo, const double* s_hi,
+                                                             const double* s_lc, Iv hvb, Iv hvm, int i0, int i1,
+                                                             int c1, int c2, double* part, double* keep) {
+  const int n = P.n, d = P.d;
+  Iv acc = iv(0.0), accm = iv(0.0);
+  double wmax = 0.0;
+  constexpr int HB = 64;
+  const int hv = threadIdx.x % HB, half = threadIdx.x / HB;
+  auto inC = [&](int i) { return in_chunk(i, c1, d, n) || (c2 >= 0 && in_chunk(i, c2, d, n)); };
+  const int o = half == 0 ? 0 : 6;
+  for (int i = i0 + hv; i < i1; i += HB) {
+    const bool ci = inC(i);
+    const double* lc = s_lc + (size_t)(i - i0) * 12 + o;
+    Iv r = iv(0.0);
+    if (!ci) {
+      if (half == 0) wmax = fmax(wmax, __dsub_rn(s_hi[i - i0], s_lo[i - i0]));
+      if (i == 0) r = r + get(lc + 4);
+      if (i == n - 1) r = r + get(lc + 0);
+    }
+    if (i <= n - 2 && !ci && !inC(i + 1)) {
+      const Iv v1 = i + 1 < i1 ? get(s_lc + (size_t)(i + 1 - i0) * 12 + o + 2) : (half == 0 ? hvb : hvm);
+      r = r + mulpos(get(lc + 0), v1);
+    }
+    if (half == 0) acc = acc + r;
+    else accm = accm + r;
+  }
+  Iv A[2] = {acc, iv(0.0)}, Am[2] = {accm, iv(0.0)};
+  warp_reduce_prep<F>(A, Am, wmax);
+  __shared__ Iv s_a[4], s_b[4];
+  __shared__ double s_w[4];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    s_a[wid] = A[0];
+    s_b[wid] = Am[0];
+    s_w[wid] = wmax;
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 4; ++w) {
+      A[0] = A[0] + s_a[w];
+      Am[0] = Am[0] + s_b[w];
+      wmax = fmax(wmax, s_w[w]);
+    }
+    for (int k = 0; k < 2; ++k) {
+      put(part + 2 * k, A[k]);
+      put(part + 4 + 2 * k, Am[k]);
+      put(keep + 2 * k, A[k]);
+      put(keep + 4 + 2 * k, Am[k]);
+    }
+    part[8] = keep[8] = wmax;
+    part[9] = keep[9] = 0.0;
+  }
+}
+
 // the Levy values of variable x (box and midpoint: u v um vm) -> 8 doubles
 __device__ __forceinline__ void levy_nb_vals(double a, double bb, double* out) {
   const LevyVals v = ObjLevy::vals(Iv{a, bb});
@@ -1022,6 +1083,27 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
     }
   }
   __syncthreads();
+  Iv hvb = iv(1.0), hvm = iv(1.0);  // Levy: v of the halo x_{i1} (box, midpoint), every thread
+  if constexpr (F::CHAIN) {
+    if (tcache) {  // the Levy values of every slice variable (box and midpoint), once
+      for (int i = i0 + t; i < i1; i += TPB) {
+        const double a = s_lo[i - i0], bb = s_hi[i - i0], xm = midpt(a, bb);
+        const LevyVals v = ObjLevy::vals(Iv{a, bb}), vm = ObjLevy::vals(Iv{xm, xm});
+        double* lc = s_tc + (size_t)(i - i0) * 12;
+        put(lc + 0, v.u);
+        put(lc + 2, v.v);
+        put(lc + 4, v.s0);
+        put(lc + 6, vm.u);
+        put(lc + 8, vm.v);
+        put(lc + 10, vm.s0);
+      }
+      if (i1 < n) {
+        const double xm = midpt(hlo, hhi);
+        hvb = ObjLevy::vals(Iv{hlo, hhi}).v;
+        hvm = ObjLevy::vals(Iv{xm, xm}).v;
+      }
+    }
+  }
   if constexpr (!F::CHAIN)
   if (tcache) {  // the terms of every slice variable (box and midpoint), once
     for (int i = i0 + t; i < i1; i += TPB) {
@@ -1139,7 +1221,16 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
       if (meets(i0, i1x, c, d, n) || meets(i0, i1x, cn, d, n) || (k > 0 && meets(i0, i1x, cprev, d, n))) {
         __syncthreads();  // the slice update of the last phase 2 (uniform: an owner block)
         if constexpr (F::CHAIN) {
-          chain_levy_partial<F>(P, s_lo, s_hi, hlo, hhi, i0, i1, c, cn, dst, s_my);
+          if (tcache) {  // warps 0..3 the partial from the value cache, warps 4..7 the entries of chunk c'
+            if (t < 128)
+              chain_levy_partial_cached128<F>(P, s_lo, s_hi, s_tc, hvb, hvm, i0, i1, c, cn, dst, s_my);
+            else
+              chain_chunk_entries<F>(P, s_lo, s_hi, i0, i1, cn, cb.tabn + (size_t)((k + 1) & 1) * DM_MAX * ENT,
+                                     false, t - 128, TPB - 128);
+            ent_done = true;
+          } else {
+            chain_levy_partial<F>(P, s_lo, s_hi, hlo, hhi, i0, i1, c, cn, dst, s_my);
+          }
         } else if (tcache) {
           // warps 0..3 the partial, warps 4..7 the entries of chunk c'
           if (t < 128)
@@ -1349,10 +1440,19 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
         const double* e = T + HDR + (size_t)(2 * j + ((scode >> j) & 1u)) * ENT;
         s_lo[i - i0] = e[E_LO];
         s_hi[i - i0] = e[E_HI];
-        if (tcache) {  // the piece's terms are the entry's (piece_entry: same F::terms, same arguments)
-          double* tc = s_tc + (size_t)(i - i0) * 4 * F::K;
+        if (tcache) {
+          if constexpr (F::CHAIN) {  // the entry's Levy values (k_prep's layout: ObjLevy::vals of the piece)
+            double* lc = s_tc + (size_t)(i - i0) * 12;
 #pragma unroll
-          for (int q = 0; q < 4 * F::K; ++q) tc[q] = e[E_T + q];
+            for (int q = 0; q < 6; ++q) {
+              lc[q] = e[2 + q];       // u v s0 of the box
+              lc[6 + q] = e[12 + q];  // u v s0 of the midpoint
+            }
+          } else {  // the piece's terms are the entry's (piece_entry: same F::terms, same arguments)
+            double* tc = s_tc + (size_t)(i - i0) * 4 * F::K;
+#pragma unroll
+            for (int q = 0; q < 4 * F::K; ++q) tc[q] = e[E_T + q];
+          }
         }
       }
     }
@@ -1362,6 +1462,8 @@ __global__ void __launch_bounds__(TPB, 1) k_chain(Problem P, IterBufs w, ChainBu
         const double* e = T + HDR + (size_t)(2 * j + ((scode >> j) & 1u)) * ENT;
         hlo = e[E_LO];
         hhi = e[E_HI];
+        hvb = get(e + 4);
+        hvm = get(e + 14);
       }
     }
     cprev = c;
