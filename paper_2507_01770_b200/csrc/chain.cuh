@@ -775,24 +775,34 @@ __device__ __forceinline__ double chain_children_levy(const Problem& P, const do
     }
     const bool pot = valid && lb <= gub0;
     if (!__any_sync(0xffffffffu, pot)) continue;  // rare: a potential candidate in the warp
-    double wv = 0.0;
-    bool keep = pot;
-    if (pot) {
-      o.clb[code] = lb;
-      best = fmin(best, ObjLevy::outer(levy_child_acc(T, code, d, true), n).hi);
-      if (P.mono) keep = child_mono_ok<F>(P, T, code);
-    }
-    if (keep) {
-      for (int j = 0; j < d; ++j) {
-        const double* e = T + HDR + (size_t)(2 * j + ((code >> j) & 1u)) * ENT;
-        wv = fmax(wv, __dsub_rn(e[E_HI], e[E_LO]));
-      }
-    }
     if (o.npot) {  // trace statistics, one atomic per warp
-      const unsigned pm = __ballot_sync(0xffffffffu, pot);
-      if ((threadIdx.x & 31) == 0) atomicAdd(o.npot, (unsigned long long)__popc(pm));
+      const unsigned pmk = __ballot_sync(0xffffffffu, pot);
+      if ((threadIdx.x & 31) == 0) atomicAdd(o.npot, (unsigned long long)__popc(pmk));
     }
-    chain_append(o.cnt, o.pc, o.pl, keep, code, lb, o.pw, wv);
+    // the warp's potential candidates one at a time: the midpoint sample on
+    // the owning lane, the first-order test with a lane per split variable
+    // (child_mono_ok_warp: the decisions of child_mono_ok) -- the serial
+    // test of a chain objective made the survivor's block the last at the
+    // grid barrier
+    unsigned pmask = __ballot_sync(0xffffffffu, pot);
+    while (pmask) {
+      const int src = __ffs(pmask) - 1;
+      pmask &= pmask - 1;
+      const uint32_t pc = __shfl_sync(0xffffffffu, code, src);
+      const double plb = __shfl_sync(0xffffffffu, lb, src);
+      const bool keep = !P.mono || child_mono_ok_warp<F>(P, T, pc);
+      if (lane == src) {
+        o.clb[pc] = plb;
+        best = fmin(best, ObjLevy::outer(levy_child_acc(T, pc, d, true), n).hi);
+      }
+      double wv = 0.0;
+      if (lane < d) {
+        const double* e = T + HDR + (size_t)(2 * lane + ((pc >> lane) & 1u)) * ENT;
+        wv = __dsub_rn(e[E_HI], e[E_LO]);
+      }
+      wv = warp_max(wv);
+      chain_append(o.cnt, o.pc, o.pl, keep && lane == src, pc, plb, o.pw, wv);
+    }
   }
   return best;
 }
