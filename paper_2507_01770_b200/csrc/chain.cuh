@@ -615,7 +615,34 @@ __device__ __forceinline__ void chain_leaf(const Problem& P, const double* T, do
     // the first-order test does not depend on GUB: taken here, so the list
     // holds only children it keeps (filtering first by the warp's smallest
     // midpoint value was measured slower: a 5-level shuffle per call)
-    if (P.mono) keep = chain_fo_ok<F>(P, T, code);
+    if constexpr (F::SEP)
+      if (P.mono) keep = chain_fo_ok<F>(P, T, code);
+  }
+  if constexpr (!F::SEP) {
+    // non-separable objectives: the warp's potential candidates one at a
+    // time, a lane per split variable (child_mono_ok_warp, the decisions of
+    // child_mono_ok): a serial test on one lane made its block the last at
+    // the grid barrier (Levy: 0.32 -> 0.20 s)
+    // Only when the warp has few of them: with many (Styblinski: ~7 per warp)
+    // or product accumulators (Griewank, Zabinsky) the per-lane tests in
+    // parallel are faster (measured: Griewank 0.38 s vs 1.75 s warp-only)
+    if (P.mono) {
+      const int lane = threadIdx.x & 31;
+      unsigned pmask = __ballot_sync(0xffffffffu, pot);
+      if (!F::HASPROD && __popc(pmask) <= 2) {
+        bool ok_me = true;
+        while (pmask) {
+          const int src = __ffs(pmask) - 1;
+          pmask &= pmask - 1;
+          const uint32_t pc = __shfl_sync(0xffffffffu, code, src);
+          const bool ok = child_mono_ok_warp<F>(P, T, pc);
+          if (lane == src) ok_me = ok;
+        }
+        keep = pot && ok_me;
+      } else if (pot) {
+        keep = chain_fo_ok<F>(P, T, code);
+      }
+    }
   }
   if (o.npot) {  // trace statistics, one atomic per warp
     const unsigned am = __activemask(), pm = __ballot_sync(am, pot);
